@@ -1,0 +1,196 @@
+/*
+ * ettg.h — C-ABI of the B200-native Euler-tour pipeline (arXiv 2103.15217).
+ *
+ * Drop-in boundary for the reference library's hot-path entry points
+ * (namespace ett, /root/reference/proj/core/include/ett/):
+ *
+ *   ett::inlabel_build(const RootedTree&)            lca.hpp:26      -> ettg_lca_build
+ *   ett::answer_batch(inlabel_lca, queries, batch)   lca.hpp:50-65   -> ettg_lca_query
+ *   ett::rmq_lca_build / rmq_lca                     lca.hpp:46-47   -> ettg_lca_build(.., ETTG_ENGINE_RMQ)
+ *                                                                       + ettg_lca_query_engine
+ *   ett::node_stats(linearize(...))                  euler.hpp:55    -> ettg_lca_stats
+ *   InlabelIndex fields                              lca.hpp:17-24   -> ettg_lca_inlabel_index
+ *   ett::tv_bridges(const AdjacencyIndex&, PhaseTimes*) bridges.hpp:55 -> ettg_bridges
+ *   ett::list_rank(const LinkedListArray&)           primitives.hpp:68 -> ettg_list_rank_dev
+ *   ett::exclusive_scan(values, +, 0)                primitives.hpp:29 -> ettg_exclusive_scan_dev
+ *   generators.hpp (grasp_tree, permute_labels, sample_queries, ...) -> ettg_gen_*
+ *
+ * Conventions
+ *  - Ids are int64 at the host boundary (the reference's i64); kNone = -1.
+ *    Device-resident variants (*_dev) take uint32 ids; 0xFFFFFFFF = none.
+ *  - Host buffers are caller-owned.  A handle owns its device memory.
+ *  - Host-buffer calls are synchronous.  *_dev calls enqueue on `stream`
+ *    (a cudaStream_t, NULL = legacy default stream) and return immediately
+ *    unless documented otherwise.
+ *  - A handle may not be used from two host threads at once; distinct
+ *    handles are independent.
+ *  - Every function returns ETTG_OK or an error code; ettg_last_error()
+ *    returns the message of the last failure on the calling thread.
+ *    Error codes mirror the reference's exceptions:
+ *      ETTG_EINVAL  <- std::invalid_argument (bad tree, disconnected graph,
+ *                      batch < 1, n or m too large, not a list)
+ *      ETTG_ERANGE  <- std::out_of_range / out-of-range query ids
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with ETTG_ECUDA.
+ */
+#ifndef ETTG_H_
+#define ETTG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ETTG_OK 0
+#define ETTG_EINVAL 1
+#define ETTG_ERANGE 2
+#define ETTG_ECUDA 3
+#define ETTG_ENOMEM 4
+#define ETTG_EINTERNAL 5
+
+#define ETTG_ENGINE_INLABEL 1u /* Schieber-Vishkin inlabel (core/src/lca.cpp:20-109) */
+#define ETTG_ENGINE_RMQ 2u     /* RMQ over the Euler tour (core/src/lca.cpp:128-157) */
+
+typedef struct ettg_lca ettg_lca;
+
+/* Per-phase device times of one bridges call, named as the reference's
+ * PhaseTimes (core/src/bridges.cpp:292-314). */
+typedef struct ettg_phase_times {
+  double spanning_ms; /* connected-components spanning forest      */
+  double euler_ms;    /* tree CSR, Euler tour, list rank, preorder   */
+  double lowhigh_ms;  /* low/high, subtree RMQ, classification       */
+  double total_ms;    /* device time of the whole call              */
+} ettg_phase_times;
+
+const char* ettg_last_error(void);
+int ettg_version(void);
+/* Number of CUDA devices visible (0 on a machine without a GPU). */
+int ettg_device_count(int* count);
+
+/* ---------------------------------------------------------------- LCA -- */
+
+/* inlabel_build (core/src/lca.cpp:20): parent[root] == -1, every other
+ * parent in [0,n).  `engines` is a bit set of ETTG_ENGINE_*; 0 means
+ * ETTG_ENGINE_INLABEL.  Rejects non-trees with ETTG_EINVAL exactly where
+ * validate_tree (core/src/graph.cpp:175-206) throws. */
+int ettg_lca_build(const int64_t* parent, int64_t n, int64_t root, int device,
+                   unsigned engines, ettg_lca** out);
+/* Same, from a device-resident uint32 parent array (0xFFFFFFFF = root).
+ * Synchronises `stream` before returning (the index is complete). */
+int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root,
+                       int device, unsigned engines, void* stream,
+                       ettg_lca** out);
+void ettg_lca_free(ettg_lca* h);
+
+int ettg_lca_size(const ettg_lca* h, int64_t* n);
+/* Device time of the last build (ms), measured with CUDA events. */
+int ettg_lca_build_ms(const ettg_lca* h, double* ms);
+
+/* answer_batch(inlabel_lca, pairs, batch) (core/include/ett/lca.hpp:50-65):
+ * pairs = x0,y0,x1,y1,... (2q int64), answers = q int64.  batch < 1 ->
+ * ETTG_EINVAL; answers do not depend on batch.  Ids outside [0,n) give
+ * ETTG_ERANGE (the reference leaves them undefined).  Host copies are
+ * pipelined with the query kernel on two streams. */
+int ettg_lca_query(const ettg_lca* h, const int64_t* pairs, int64_t q,
+                   int64_t batch, int64_t* answers);
+int ettg_lca_query_engine(const ettg_lca* h, unsigned engine,
+                          const int64_t* pairs, int64_t q, int64_t batch,
+                          int64_t* answers);
+/* Device-resident batch: d_pairs = 2q uint32, d_answers = q uint32.
+ * Out-of-range ids answer 0xFFFFFFFF. */
+int ettg_lca_query_dev(const ettg_lca* h, unsigned engine,
+                       const uint32_t* d_pairs, int64_t q, uint32_t* d_answers,
+                       void* stream);
+
+/* NodeStats of the Euler tour (core/src/euler.cpp:119-155): 1-based
+ * preorder, subtree size, level, parent (-1 at the root).  Any pointer may
+ * be NULL.  Bit-identical to the reference (same DCEL child order). */
+int ettg_lca_stats(const ettg_lca* h, int64_t* preorder, int64_t* size,
+                   int64_t* level, int64_t* parent);
+/* InlabelIndex fields (core/include/ett/lca.hpp:17-24): inlabel[n],
+ * ascendant[n], head[n+1] (-1 where unused), level[n], parent[n]. */
+int ettg_lca_inlabel_index(const ettg_lca* h, int64_t* inlabel,
+                           uint64_t* ascendant, int64_t* head, int64_t* level,
+                           int64_t* parent);
+
+/* Multi-GPU replication of the inlabel index (query batches shard; the
+ * index is broadcast once, e.g. with ncclBroadcast over NVLink).
+ * index_bytes: size of the packed index; export copies it into a device
+ * buffer of that size on the handle's device; attach builds a query-only
+ * handle on `device` from such a buffer (copied). */
+int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes);
+int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream);
+int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device,
+                              void* stream, ettg_lca** out);
+
+/* ------------------------------------------------------------ bridges -- */
+
+/* tv_bridges (core/src/bridges.cpp:311-316) on the undirected simple graph
+ * edges = u0,v0,u1,v1,... (2m int64, ids in [0,n)).  is_bridge[m] gets 1
+ * for bridges, 0 otherwise, indexed by input edge id.  Disconnected input
+ * -> ETTG_EINVAL.  times may be NULL. */
+int ettg_bridges(const int64_t* edges, int64_t n, int64_t m, int device,
+                 uint8_t* is_bridge, ettg_phase_times* times);
+/* Device-resident: d_edges = 2m uint32, d_is_bridge = m bytes.  Returns
+ * after the stream has completed (connectivity is checked on the host). */
+int ettg_bridges_dev(const uint32_t* d_edges, int64_t n, int64_t m, int device,
+                     uint8_t* d_is_bridge, void* stream,
+                     ettg_phase_times* times);
+
+/* --------------------------------------------------------- primitives -- */
+
+/* list_rank (core/src/primitives.cpp:145): rank[i] = links from head to i.
+ * d_succ[k] uint32 with 0xFFFFFFFF as the tail.  Cycles / uncovered
+ * elements -> ETTG_EINVAL.  Synchronous. */
+int ettg_list_rank_dev(const uint32_t* d_succ, int64_t k, int64_t head,
+                       uint32_t* d_rank, int device, void* stream);
+/* exclusive_scan(values, +, 0) (core/include/ett/primitives.hpp:29-66)
+ * over uint32 (sums modulo 2^32). */
+int ettg_exclusive_scan_dev(const uint32_t* d_in, int64_t n, uint32_t* d_out,
+                            int device, void* stream);
+/* Stable sort of (key, value) uint32 pairs by key (LSD radix). */
+int ettg_sort_pairs_dev(const uint32_t* d_keys, const uint32_t* d_vals,
+                        int64_t n, uint32_t* d_keys_out, uint32_t* d_vals_out,
+                        int device, void* stream);
+
+/* --------------------------------------------------------- generators -- */
+/* Bit-identical to core/src/generators.cpp (SplitMix64, core/include/ett/rng.hpp). */
+int ettg_gen_grasp_tree(int64_t n, uint64_t gamma, uint64_t seed,
+                        int64_t* parent);
+int ettg_gen_barabasi_tree(int64_t n, uint64_t seed, int64_t* parent);
+int ettg_gen_permute_labels(int64_t n, const int64_t* parent, int64_t root,
+                            uint64_t seed, int64_t* parent_out,
+                            int64_t* root_out);
+int ettg_gen_sample_queries(int64_t n, int64_t q, uint64_t seed,
+                            int64_t* pairs);
+int ettg_gen_random_connected_graph(int64_t n, int64_t m, uint64_t seed,
+                                    int64_t* edges);
+/* sample_queries on the device in counter mode: query i of the stream
+ * (offset + i) is SplitMix64 draws 2(offset+i)+1 and 2(offset+i)+2.
+ * *rejected is set non-zero if any Lemire rejection occurred (the counter
+ * replay is then invalid and the host generator must be used).
+ * Synchronous. */
+int ettg_gen_queries_dev(int64_t n, int64_t q, uint64_t seed, int64_t offset,
+                         uint32_t* d_pairs, int* rejected, int device,
+                         void* stream);
+/* New generators for the bridge configs; truth[m] gets
+ * the planted bridge mask, which is the exact answer by construction. */
+int ettg_gen_planted_bridge_graph(int64_t n, int64_t m, int64_t b,
+                                  uint64_t seed, int64_t* edges,
+                                  uint8_t* truth);
+/* Road-like: W x H lattice (row-major ids), grid edges + `extra` random
+ * edges per node inside Chebyshev radius r, plus `pendant` pendant nodes
+ * whose attaching edges are the planted bridges.  n = W*H + pendant,
+ * m = ettg_road_like_edge_count(...). */
+int64_t ettg_road_like_edge_count(int64_t W, int64_t H, int64_t extra,
+                                  int64_t r, int64_t pendant);
+int ettg_gen_road_like_graph(int64_t W, int64_t H, int64_t extra, int64_t r,
+                             int64_t pendant, uint64_t seed, int64_t* edges,
+                             uint8_t* truth);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ETTG_H_ */

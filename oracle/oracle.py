@@ -1,0 +1,215 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes loaders for the CPU oracles.
+
+* ``ref()``  -> oracle/_ref/libett_ref.so : the unmodified reference core/
+  compiled by oracle/Makefile (plus our extern "C" wrapper ref_capi.cpp).
+* ``port()`` -> oracle/_build/libettg_oracle.so : the plain-C restatement
+  (oracle/ettg_oracle.c), pinned against the reference's golden vectors and
+  against ``ref()`` in tests/test_oracle.py.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libett_ref.so")
+PORT_SO = os.path.join(HERE, "_build", "libettg_oracle.so")
+
+_ref = None
+_port = None
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{msg} (code {code})")
+        self.code = code
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def have_port() -> bool:
+    return os.path.exists(PORT_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not have_ref():
+            raise RuntimeError(f"reference oracle not built: {REF_SO}")
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_inlabel_new.restype = C.c_void_p
+        _ref = L
+    return _ref
+
+
+def port():
+    global _port
+    if _port is None:
+        if not have_port():
+            raise RuntimeError(f"oracle restatement not built: {PORT_SO}")
+        L = C.CDLL(PORT_SO)
+        L.orc_last_error.restype = C.c_char_p
+        _port = L
+    return _port
+
+
+def _rc(L, rc, err_fn):
+    if rc != 0:
+        raise OracleError(rc, getattr(L, err_fn)().decode())
+
+
+i64 = C.c_int64
+u64 = C.c_uint64
+
+
+# ------------------------------------------------------------- reference
+class Ref:
+    """The compiled reference library (oracle/_ref)."""
+
+    @staticmethod
+    def set_workers(w: int):
+        ref().ref_set_workers(C.c_int(w))
+
+    @staticmethod
+    def workers() -> int:
+        return ref().ref_workers()
+
+    @staticmethod
+    def grasp_tree(n, gamma, seed):
+        out = np.empty(n, np.int64)
+        _rc(ref(), ref().ref_grasp_tree(i64(n), u64(gamma), u64(seed), _p(out)), "ref_last_error")
+        return out
+
+    @staticmethod
+    def barabasi_tree(n, seed):
+        out = np.empty(n, np.int64)
+        _rc(ref(), ref().ref_barabasi_tree(i64(n), u64(seed), _p(out)), "ref_last_error")
+        return out
+
+    @staticmethod
+    def permute_labels(parent, root, seed):
+        n = len(parent)
+        out = np.empty(n, np.int64)
+        r = C.c_int64()
+        _rc(ref(), ref().ref_permute_labels(i64(n), _p(parent), i64(root), u64(seed), _p(out),
+                                            C.byref(r)), "ref_last_error")
+        return out, r.value
+
+    @staticmethod
+    def sample_queries(n, q, seed):
+        out = np.empty((q, 2), np.int64)
+        _rc(ref(), ref().ref_sample_queries(i64(n), i64(q), u64(seed), _p(out)), "ref_last_error")
+        return out
+
+    @staticmethod
+    def random_connected_graph(n, m, seed):
+        out = np.empty((m, 2), np.int64)
+        _rc(ref(), ref().ref_random_connected_graph(i64(n), i64(m), u64(seed), _p(out)),
+            "ref_last_error")
+        return out
+
+    @staticmethod
+    def list_rank(succ, head):
+        succ = np.ascontiguousarray(succ, np.int64)
+        out = np.empty(len(succ), np.int64)
+        _rc(ref(), ref().ref_list_rank(i64(len(succ)), _p(succ), i64(head), _p(out)),
+            "ref_last_error")
+        return out
+
+    @staticmethod
+    def exclusive_scan_sum(values):
+        v = np.ascontiguousarray(values, np.int64)
+        out = np.empty(len(v), np.int64)
+        _rc(ref(), ref().ref_exclusive_scan_sum(i64(len(v)), _p(v), _p(out)), "ref_last_error")
+        return out
+
+    @staticmethod
+    def euler_tour(parent, root):
+        n = len(parent)
+        k = 2 * (n - 1)
+        s = np.empty(max(k, 1), np.int64)
+        d = np.empty(max(k, 1), np.int64)
+        _rc(ref(), ref().ref_euler_tour(i64(n), _p(parent), i64(root), _p(s), _p(d)),
+            "ref_last_error")
+        return s[:k], d[:k]
+
+    @staticmethod
+    def node_stats(parent, root):
+        n = len(parent)
+        a = [np.empty(n, np.int64) for _ in range(4)]
+        _rc(ref(), ref().ref_node_stats(i64(n), _p(parent), i64(root), *[_p(x) for x in a]),
+            "ref_last_error")
+        return a
+
+    @staticmethod
+    def inlabel_index(parent, root):
+        n = len(parent)
+        inl = np.empty(n, np.int64)
+        asc = np.empty(n, np.uint64)
+        head = np.empty(n + 1, np.int64)
+        lev = np.empty(n, np.int64)
+        par = np.empty(n, np.int64)
+        _rc(ref(), ref().ref_inlabel_index(i64(n), _p(parent), i64(root), _p(inl), _p(asc),
+                                           _p(head), _p(lev), _p(par)), "ref_last_error")
+        return inl, asc, head, lev, par
+
+    @staticmethod
+    def lca(engine, parent, root, pairs, batch=None):
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        q = pairs.shape[0]
+        out = np.empty(q, np.int64)
+        _rc(ref(), ref().ref_lca(engine.encode(), i64(len(parent)), _p(parent), i64(root),
+                                 _p(pairs), i64(q), i64(batch or max(q, 1)), _p(out)),
+            "ref_last_error")
+        return out
+
+    @staticmethod
+    def bridges(engine, n, edges):
+        edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+        m = edges.shape[0]
+        mask = np.empty(m, np.uint8)
+        ph = np.zeros(4, np.int64)
+        _rc(ref(), ref().ref_bridges(engine.encode(), i64(n), i64(m), _p(edges), _p(mask),
+                                     _p(ph)), "ref_last_error")
+        return mask, ph
+
+
+class RefInlabel:
+    """Built reference InlabelIndex for timing build and queries apart."""
+
+    def __init__(self, parent, root):
+        L = ref()
+        bn = C.c_int64()
+        self.h = L.ref_inlabel_new(i64(len(parent)), _p(np.ascontiguousarray(parent, np.int64)),
+                                   i64(root), C.byref(bn))
+        if not self.h:
+            raise OracleError(1, L.ref_last_error().decode())
+        self.build_ns = bn.value
+
+    def answer(self, pairs, batch=None):
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        q = pairs.shape[0]
+        out = np.empty(q, np.int64)
+        ns = C.c_int64()
+        L = ref()
+        _rc(L, L.ref_inlabel_answer(C.c_void_p(self.h), _p(pairs), i64(q),
+                                    i64(batch or max(q, 1)), _p(out), C.byref(ns)),
+            "ref_last_error")
+        return out, ns.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_inlabel_free(C.c_void_p(self.h))
+            self.h = None

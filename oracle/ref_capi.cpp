@@ -1,0 +1,290 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" face of the *unmodified* reference library (eulertools core/),
+// compiled straight from /root/reference/proj/core/src/*.cpp by
+// oracle/Makefile into oracle/_ref/libett_ref.so.  Tests use it to pin the
+// C restatement (oracle/ettg_oracle.c) and the CUDA path; bench.py uses it as
+// the "reference" CPU arm (cpu_baseline.kind = "reference").
+//
+// Every function returns 0 on success, 1 for std::invalid_argument,
+// 2 for std::out_of_range, 3 for anything else; ref_last_error() holds the
+// exception text.  Ids cross the boundary as int64 (the reference's i64).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ett/bridges.hpp"
+#include "ett/euler.hpp"
+#include "ett/generators.hpp"
+#include "ett/graph.hpp"
+#include "ett/lca.hpp"
+#include "ett/primitives.hpp"
+
+using namespace ett;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+RootedTree make_tree(int64_t n, const int64_t* parent, int64_t root) {
+  RootedTree t;
+  t.n = n;
+  t.root = root;
+  t.parent.assign(parent, parent + n);
+  return t;
+}
+
+EdgeList make_edges(int64_t n, int64_t m, const int64_t* edges) {
+  EdgeList g;
+  g.n = n;
+  g.edges.resize(m);
+  for (int64_t i = 0; i < m; ++i) g.edges[i] = {edges[2 * i], edges[2 * i + 1]};
+  return g;
+}
+
+std::vector<std::pair<i64, i64>> make_pairs(const int64_t* pairs, int64_t q) {
+  std::vector<std::pair<i64, i64>> out(q);
+  for (int64_t i = 0; i < q; ++i) out[i] = {pairs[2 * i], pairs[2 * i + 1]};
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_set_workers(int w) { set_worker_count(w); }
+int ref_workers() { return worker_count(); }
+
+// ---- generators (core/src/generators.cpp) ---------------------------------
+int ref_grasp_tree(int64_t n, uint64_t gamma, uint64_t seed, int64_t* parent) {
+  return guard([&] {
+    RootedTree t = grasp_tree({n, gamma, seed});
+    std::memcpy(parent, t.parent.data(), n * sizeof(int64_t));
+  });
+}
+
+int ref_barabasi_tree(int64_t n, uint64_t seed, int64_t* parent) {
+  return guard([&] {
+    RootedTree t = barabasi_tree(n, seed);
+    std::memcpy(parent, t.parent.data(), n * sizeof(int64_t));
+  });
+}
+
+int ref_permute_labels(int64_t n, const int64_t* parent, int64_t root,
+                       uint64_t seed, int64_t* parent_out, int64_t* root_out) {
+  return guard([&] {
+    RootedTree t = permute_labels(make_tree(n, parent, root), seed);
+    std::memcpy(parent_out, t.parent.data(), n * sizeof(int64_t));
+    *root_out = t.root;
+  });
+}
+
+int ref_sample_queries(int64_t n, int64_t q, uint64_t seed, int64_t* pairs) {
+  return guard([&] {
+    auto qs = sample_queries(n, q, seed);
+    for (int64_t i = 0; i < q; ++i) {
+      pairs[2 * i] = qs[i].first;
+      pairs[2 * i + 1] = qs[i].second;
+    }
+  });
+}
+
+int ref_random_connected_graph(int64_t n, int64_t m, uint64_t seed,
+                               int64_t* edges) {
+  return guard([&] {
+    EdgeList g = random_connected_graph(n, m, seed);
+    for (int64_t i = 0; i < m; ++i) {
+      edges[2 * i] = g.edges[i].first;
+      edges[2 * i + 1] = g.edges[i].second;
+    }
+  });
+}
+
+// ---- primitives (core/src/primitives.cpp) ---------------------------------
+int ref_list_rank(int64_t k, const int64_t* succ, int64_t head, int64_t* out) {
+  return guard([&] {
+    LinkedListArray l;
+    l.succ.assign(succ, succ + k);
+    l.head = head;
+    auto r = list_rank(l);
+    std::memcpy(out, r.data(), k * sizeof(int64_t));
+  });
+}
+
+int ref_exclusive_scan_sum(int64_t n, const int64_t* in, int64_t* out) {
+  return guard([&] {
+    auto r = exclusive_scan(std::span<const i64>(in, n),
+                            [](i64 a, i64 b) { return a + b; }, 0);
+    std::memcpy(out, r.data(), n * sizeof(int64_t));
+  });
+}
+
+// ---- Euler tour (core/src/euler.cpp) --------------------------------------
+// Tour of the tree given by `parent`, as (src,dst) pairs in tour order,
+// 2(n-1) of them; plus node_stats.
+int ref_euler_tour(int64_t n, const int64_t* parent, int64_t root,
+                   int64_t* tour_src, int64_t* tour_dst) {
+  return guard([&] {
+    RootedTree t = make_tree(n, parent, root);
+    validate_tree(t);
+    EulerTour tour = linearize(build_half_edges(tree_edges(t), true), root);
+    const auto& h = tour.structure;
+    for (size_t i = 0; i < tour.order.size(); ++i) {
+      tour_src[i] = h.src[tour.order[i]];
+      tour_dst[i] = h.dst[tour.order[i]];
+    }
+  });
+}
+
+int ref_node_stats(int64_t n, const int64_t* parent, int64_t root,
+                   int64_t* preorder, int64_t* size, int64_t* level,
+                   int64_t* par) {
+  return guard([&] {
+    RootedTree t = make_tree(n, parent, root);
+    validate_tree(t);
+    NodeStats s =
+        node_stats(linearize(build_half_edges(tree_edges(t), true), root));
+    std::memcpy(preorder, s.preorder.data(), n * sizeof(int64_t));
+    std::memcpy(size, s.size.data(), n * sizeof(int64_t));
+    std::memcpy(level, s.level.data(), n * sizeof(int64_t));
+    std::memcpy(par, s.parent.data(), n * sizeof(int64_t));
+  });
+}
+
+// ---- LCA (core/src/lca.cpp) -----------------------------------------------
+int ref_inlabel_index(int64_t n, const int64_t* parent, int64_t root,
+                      int64_t* inlabel, uint64_t* ascendant, int64_t* head,
+                      int64_t* level, int64_t* par) {
+  return guard([&] {
+    InlabelIndex idx = inlabel_build(make_tree(n, parent, root));
+    std::memcpy(inlabel, idx.inlabel.data(), n * sizeof(int64_t));
+    std::memcpy(ascendant, idx.ascendant.data(), n * sizeof(uint64_t));
+    std::memcpy(head, idx.head.data(), (n + 1) * sizeof(int64_t));
+    std::memcpy(level, idx.level.data(), n * sizeof(int64_t));
+    std::memcpy(par, idx.parent.data(), n * sizeof(int64_t));
+  });
+}
+
+// Opaque index handles so the bench can time build and query separately,
+// exactly as tools/ett_bench.cpp:136-150 does.
+void* ref_inlabel_new(int64_t n, const int64_t* parent, int64_t root,
+                      int64_t* build_ns) {
+  InlabelIndex* out = nullptr;
+  int rc = guard([&] {
+    RootedTree t = make_tree(n, parent, root);
+    int64_t t0 = now_ns();
+    out = new InlabelIndex(inlabel_build(t));
+    if (build_ns) *build_ns = now_ns() - t0;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+void ref_inlabel_free(void* h) { delete static_cast<InlabelIndex*>(h); }
+
+// answer_batch(inlabel_lca) over caller pairs; query_ns excludes the
+// int64 pair marshalling.
+int ref_inlabel_answer(void* h, const int64_t* pairs, int64_t q, int64_t batch,
+                       int64_t* answers, int64_t* query_ns) {
+  return guard([&] {
+    const InlabelIndex& idx = *static_cast<InlabelIndex*>(h);
+    auto qs = make_pairs(pairs, q);
+    int64_t t0 = now_ns();
+    auto a = answer_batch([&](i64 x, i64 y) { return inlabel_lca(idx, x, y); },
+                          qs, batch);
+    if (query_ns) *query_ns = now_ns() - t0;
+    std::memcpy(answers, a.data(), q * sizeof(int64_t));
+  });
+}
+
+int ref_lca(const char* engine, int64_t n, const int64_t* parent, int64_t root,
+            const int64_t* pairs, int64_t q, int64_t batch, int64_t* answers) {
+  return guard([&] {
+    RootedTree t = make_tree(n, parent, root);
+    auto qs = make_pairs(pairs, q);
+    std::vector<i64> a;
+    std::string e(engine);
+    if (e == "inlabel") {
+      InlabelIndex idx = inlabel_build(t);
+      a = answer_batch([&](i64 x, i64 y) { return inlabel_lca(idx, x, y); },
+                       qs, batch);
+    } else if (e == "rmq") {
+      RmqLcaIndex idx = rmq_lca_build(t);
+      a = answer_batch([&](i64 x, i64 y) { return rmq_lca(idx, x, y); }, qs,
+                       batch);
+    } else if (e == "naive") {
+      NaiveIndex idx = naive_build(t);
+      a = answer_batch([&](i64 x, i64 y) { return naive_lca(idx, x, y); }, qs,
+                       batch);
+    } else {
+      throw std::runtime_error("unknown engine " + e);
+    }
+    std::memcpy(answers, a.data(), q * sizeof(int64_t));
+  });
+}
+
+// ---- bridges (core/src/bridges.cpp) ----------------------------------------
+// engine: "tv" | "dfs" | "ck" | "hybrid" | "brute".  build_adjacency is
+// excluded from phase_ns exactly as tools/ett_bench.cpp:310-317 excludes it.
+// phase_ns receives up to 4 entries (tv: spanning, euler, lowhigh; total last).
+int ref_bridges(const char* engine, int64_t n, int64_t m, const int64_t* edges,
+                uint8_t* is_bridge, int64_t* phase_ns) {
+  return guard([&] {
+    AdjacencyIndex adj = build_adjacency(make_edges(n, m, edges));
+    std::string e(engine);
+    PhaseTimes pt;
+    BridgeMask mask;
+    int64_t t0 = now_ns();
+    if (e == "tv") mask = tv_bridges(adj, &pt);
+    else if (e == "dfs") mask = dfs_bridges(adj, &pt);
+    else if (e == "ck") mask = ck_bridges(adj, &pt);
+    else if (e == "hybrid") mask = hybrid_bridges(adj, &pt);
+    else if (e == "brute") mask = brute_force_bridges(adj);
+    else throw std::runtime_error("unknown engine " + e);
+    int64_t total = now_ns() - t0;
+    for (int64_t i = 0; i < m; ++i) is_bridge[i] = mask.is_bridge[i] ? 1 : 0;
+    if (phase_ns) {
+      for (int i = 0; i < 4; ++i) phase_ns[i] = 0;
+      for (size_t i = 0; i < pt.nanos.size() && i < 3; ++i)
+        phase_ns[i] = pt.nanos[i].second;
+      phase_ns[3] = total;
+    }
+  });
+}
+
+// Spanning tree of the reference's deterministic hooking + its rooting,
+// so low/high can be compared on an identical tree.
+int ref_spanning_tree_hooking(int64_t n, int64_t m, const int64_t* edges,
+                              uint8_t* tree_mask) {
+  return guard([&] {
+    AdjacencyIndex adj = build_adjacency(make_edges(n, m, edges));
+    auto mask = spanning_tree_hooking(adj);
+    for (int64_t i = 0; i < m; ++i) tree_mask[i] = mask[i] ? 1 : 0;
+  });
+}
+
+}  // extern "C"

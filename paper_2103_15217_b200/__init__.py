@@ -1,0 +1,17 @@
+"""B200-native Euler-tour graph pipeline (arXiv 2103.15217): LCA and bridges.
+
+Public surface mirrors the reference's ``ett`` namespace; see ``ett.py`` and
+include/ettg.h for the C-ABI underneath.
+"""
+from . import _lib
+from .ett import *  # noqa: F401,F403
+from .ett import (BridgeMask, EdgeList, InlabelIndex, NodeStats, RmqLcaIndex, RootedTree,
+                  answer_batch, inlabel_build, inlabel_lca, node_stats, rmq_lca, rmq_lca_build,
+                  tv_bridges)
+from ._lib import InvalidArgument, OutOfRange, lib
+
+__all__ = [
+    "BridgeMask", "EdgeList", "InlabelIndex", "NodeStats", "RmqLcaIndex", "RootedTree",
+    "answer_batch", "inlabel_build", "inlabel_lca", "node_stats", "rmq_lca", "rmq_lca_build",
+    "tv_bridges", "InvalidArgument", "OutOfRange", "lib",
+]

@@ -1,0 +1,549 @@
+// Bridges on B200: Tarjan-Vishkin over a GPU spanning forest.
+//
+// Reference path (core/src/bridges.cpp, all CPU):
+//   tv_bridges                 :311-316
+//     spanning_tree_hooking    :105-158   min-(component, edge) hooking rounds
+//     euler_root_tree          :160-196   sequential O(m) endpoint recovery,
+//                                         build_half_edges + linearize + node_stats
+//     low_high                 :251-287   2m-slot segmented min/max + 2 segment trees
+//     classify                 :301-306   bridge iff low >= pre && high < pre + size
+//
+// Device pipeline (input: COO edge list, u32 ids; no CSR of the graph is built):
+//   spanning  k_cc_hook        lock-free union-find (min-id roots, ECL-CC style
+//                              hooking); a successful CAS joins two trees, so
+//                              its edge is a spanning-forest edge
+//   euler     scan             tree-edge compaction (decoupled look-back); the
+//                              count is the connectivity check (n-1 tree edges)
+//             k_tree_he        2(n-1) half-edges keyed by source vertex
+//             sort_pairs       stable radix sort -> per-vertex rotation
+//             k_tree_succ      succ(e) = next(twin(e)); cut before first(0)
+//             list_rank_core   ranks of the tour rooted at vertex 0
+//             k_tour_flags     position -> (tree edge, is-down)
+//             scan + functor   #downs before each position => preorder, size and
+//                              parent edge, written preorder-indexed
+//   lowhigh   k_lowhigh_init / k_lowhigh_edges (one atomicMin + one atomicMax
+//             per non-tree edge: the reference's other two updates are provably
+//             no-ops because each slot is seeded with its own preorder),
+//             block-sparse min/max table over preorder, k_classify writes the
+//             bridge mask by input edge id.
+//
+// The spanning forest may differ from the reference's; bridges are a graph
+// property, so the mask cannot (core/include/ett/bridges.hpp:56-58).
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "api_internal.cuh"
+#include "common.cuh"
+#include "listrank.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+namespace ettg {
+
+__global__ void k_edges_from_i64(const longlong2* __restrict__ in, u32 m, u32 n,
+                                 uint2* __restrict__ out, u32* flags) {
+  u32 bad = 0;
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const longlong2 v = in[e];
+    const bool ok = v.x >= 0 && v.y >= 0 && v.x < n && v.y < n;
+    bad |= !ok;
+    out[e] = ok ? make_uint2(static_cast<u32>(v.x), static_cast<u32>(v.y)) : make_uint2(0, 0);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+__global__ void k_edges_check(const uint2* __restrict__ e2, u32 m, u32 n, u32* flags) {
+  u32 bad = 0;
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint2 v = e2[e];
+    bad |= (v.x >= n) | (v.y >= n);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+__global__ void k_iota(u32* __restrict__ a, u32 n) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+// Representative with path halving; parents always point to smaller ids,
+// so the root of a tree is its minimum vertex.
+__device__ __forceinline__ u32 uf_find(u32* par, u32 x) {
+  u32 cur = par[x];
+  if (cur != x) {
+    u32 prev = x, next;
+    while (cur > (next = par[cur])) {
+      par[prev] = next;  // benign race: only ever shortens paths
+      prev = cur;
+      cur = next;
+    }
+  }
+  return cur;
+}
+
+// One pass over the edges.  Hooking root a (> b) under b with CAS; on
+// failure retry from the value found.  Each successful CAS unions two
+// distinct trees (a is the minimum of its own tree and b < a), so exactly
+// n - #components edges are marked.
+__global__ void __launch_bounds__(256)
+    k_cc_hook(const uint2* __restrict__ edges, u32 m, u32* par, uint8_t* __restrict__ tree) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint2 uv = edges[e];
+    u32 a = uf_find(par, uv.x);
+    u32 b = uf_find(par, uv.y);
+    uint8_t t = 0;
+    while (a != b) {
+      if (a < b) {
+        const u32 tmp = a;
+        a = b;
+        b = tmp;
+      }
+      const u32 old = atomicCAS(&par[a], a, b);
+      if (old == a) {
+        t = 1;
+        break;
+      }
+      a = uf_find(par, old);
+      b = uf_find(par, b);
+    }
+    tree[e] = t;
+  }
+}
+
+// Tree-edge compaction functors: tedge[t] = e for the t-th tree edge.
+struct TreeIn {
+  const uint8_t* tree;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return tree[i]; }
+};
+struct TreeOut {
+  const uint8_t* tree;
+  u32* tedge;
+  u32 cap;
+  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
+    if (tree[i] && excl < cap) tedge[excl] = static_cast<u32>(i);
+  }
+};
+
+// Half-edges of the spanning tree: 2t = (u -> v), 2t+1 = (v -> u).
+__global__ void k_tree_he(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
+                          u32* __restrict__ keys, u32* __restrict__ vals) {
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    const uint2 uv = edges[tedge[t]];
+    keys[2 * t] = uv.x;
+    vals[2 * t] = 2 * t;
+    keys[2 * t + 1] = uv.y;
+    vals[2 * t + 1] = 2 * t + 1;
+  }
+}
+
+__global__ void k_vertex_ranges(const u32* __restrict__ skey, u32 k, uint2* __restrict__ crange) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < k; s += gridDim.x * blockDim.x) {
+    const u32 y = skey[s];
+    if (s == 0 || skey[s - 1] != y) crange[y].x = s;
+    if (s + 1 == k || skey[s + 1] != y) crange[y].y = s + 1;
+  }
+}
+
+__global__ void k_inverse(const u32* __restrict__ sval, u32 k, u32* __restrict__ slot_of) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < k; s += gridDim.x * blockDim.x)
+    slot_of[sval[s]] = s;
+}
+
+// succ(e) = next(twin(e)) in the cyclic rotation of twin(e)'s source
+// (core/src/euler.cpp:85-88, :105).
+__global__ void k_tree_succ(const u32* __restrict__ skey, const u32* __restrict__ sval,
+                            const u32* __restrict__ slot_of, const uint2* __restrict__ crange,
+                            u32 k, u32* __restrict__ succ) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    const u32 s = slot_of[e ^ 1u];
+    const uint2 r = crange[skey[s]];
+    const u32 ns = (s + 1 < r.y) ? s + 1 : r.x;
+    succ[e] = sval[ns];
+  }
+}
+
+// Cut the cycle just before first(root) (core/src/euler.cpp:104-110).
+__global__ void k_tree_cut(const u32* __restrict__ sval, const uint2* __restrict__ crange,
+                           u32 root, u32* __restrict__ succ, u32* head) {
+  const uint2 r = crange[root];
+  const u32 last = sval[r.y - 1];
+  succ[last ^ 1u] = kNone;
+  *head = sval[r.x];
+}
+
+// flags[pos] = (t << 1) | is_down for the half-edge at tour position pos.
+// A half-edge is down iff it precedes its twin (core/src/euler.cpp:134-139).
+__global__ void k_tour_flags(Lr0View lr, u32 T, u32* __restrict__ flags) {
+  const u32 S1 = *lr.d_S1;
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    u32 r0, r1, d;
+    lr.get(2 * t, S1, r0, d);
+    lr.get(2 * t + 1, S1, r1, d);
+    const u32 k = 2 * T;
+    if (r0 < k) flags[r0] = (t << 1) | (r0 < r1 ? 1u : 0u);
+    if (r1 < k) flags[r1] = (t << 1) | (r1 < r0 ? 1u : 0u);
+  }
+}
+
+struct DownIn {
+  const u32* flags;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return flags[i] & 1u; }
+};
+
+// Epilogue of the #downs scan: at a down half-edge (p -> c) at position pos
+// with D downs before it, preorder(c) = D + 2, size(c) = (pos(twin) - pos + 1)/2
+// (node_stats, core/src/euler.cpp:144-153).  Outputs are preorder-indexed
+// (index = preorder - 1) so low/high and classification stream over them.
+struct StatsOut {
+  const u32* flags;
+  const u32* tedge;
+  const uint2* edges;
+  Lr0View lr;
+  u32 n;
+  u32* pre_of;         // [n]   node -> preorder
+  u32* size_by_pre;    // [n]
+  u32* pedge_by_pre;   // [n]   input edge id to the parent
+  __device__ __forceinline__ void operator()(u64 pos, u32 dbefore) const {
+    const u32 f = flags[pos];
+    if (!(f & 1u)) return;
+    const u32 t = f >> 1;
+    const u32 S1 = *lr.d_S1;
+    u32 r0, r1, d;
+    lr.get(2 * t, S1, r0, d);
+    lr.get(2 * t + 1, S1, r1, d);
+    const u32 e = tedge[t];
+    const uint2 uv = edges[e];
+    const bool first_is_down = r0 < r1;           // half-edge 2t = (u -> v)
+    const u32 child = first_is_down ? uv.y : uv.x;
+    const u32 pos_up = first_is_down ? r1 : r0;
+    const u32 pre = dbefore + 2;
+    if (child < n && pre <= n) {
+      pre_of[child] = pre;
+      size_by_pre[pre - 1] = (pos_up - static_cast<u32>(pos) + 1) >> 1;
+      pedge_by_pre[pre - 1] = e;
+    }
+  }
+};
+
+__global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32* pedge_by_pre) {
+  pre_of[root] = 1;
+  size_by_pre[0] = n;
+  pedge_by_pre[0] = kNone;
+}
+
+// lh[i] = (low seed, high seed) = (i + 1, i + 1): each node's own preorder.
+__global__ void k_lowhigh_init(uint2* __restrict__ lh, u32 n) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    lh[i] = make_uint2(i + 1, i + 1);
+}
+
+// Non-tree edge {u, v} with pre(u) < pre(v): low(v) <- min(., pre(u)) and
+// high(u) <- max(., pre(v)).  (core/src/bridges.cpp:256-273)
+__global__ void __launch_bounds__(256)
+    k_lowhigh_edges(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
+                    const u32* __restrict__ pre_of, uint2* lh) {
+  u32* w = reinterpret_cast<u32*>(lh);
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    if (tree[e]) continue;
+    const uint2 uv = edges[e];
+    u32 a = __ldg(pre_of + uv.x), b = __ldg(pre_of + uv.y);
+    if (a == b) continue;  // self-loop
+    if (a > b) {
+      const u32 t = a;
+      a = b;
+      b = t;
+    }
+    // slot index = preorder - 1; .x = low, .y = high
+    if (w[2 * (b - 1)] > a) atomicMin(&w[2 * (b - 1)], a);
+    if (w[2 * (a - 1) + 1] < b) atomicMax(&w[2 * (a - 1) + 1], b);
+  }
+}
+
+__device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
+  return make_uint2(min(a.x, b.x), max(a.y, b.y));
+}
+
+// Block-sparse (min low, max high) table: level 0 = 32-entry block extrema.
+__global__ void k_lh_block(const uint2* __restrict__ lh, u32 n, u32 nb, uint2* __restrict__ sp0) {
+  const u32 lane = threadIdx.x & 31;
+  const u32 warps = (gridDim.x * blockDim.x) >> 5;
+  for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const u32 i = b * 32 + lane;
+    uint2 v = i < n ? lh[i] : make_uint2(0xFFFFFFFFu, 0u);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      uint2 o;
+      o.x = __shfl_xor_sync(0xffffffffu, v.x, d);
+      o.y = __shfl_xor_sync(0xffffffffu, v.y, d);
+      v = lh_merge(v, o);
+    }
+    if (lane == 0) sp0[b] = v;
+  }
+}
+
+__global__ void k_lh_level(const uint2* __restrict__ prev, uint2* __restrict__ cur, u32 nb,
+                           u32 half) {
+  for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
+       b += gridDim.x * blockDim.x)
+    cur[b] = lh_merge(prev[b], prev[b + half]);
+}
+
+// Subtree range [i, i + size - 1] in preorder -> (low, high) -> bridge test
+// (core/src/bridges.cpp:280-285, :301-306).
+__global__ void __launch_bounds__(256)
+    k_classify(const uint2* __restrict__ lh, const uint2* __restrict__ sp, u32 nb, u32 n,
+               const u32* __restrict__ size_by_pre, const u32* __restrict__ pedge_by_pre,
+               uint8_t* __restrict__ mask, u32 m) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i == 0) continue;  // the root has no parent edge
+    const u32 sz = size_by_pre[i];
+    const u32 a = i, b = min(i + sz - 1, n - 1);
+    uint2 acc = lh[a];
+    if (b - a < 64) {
+      for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+    } else {
+      const u32 la = a >> 5, lb = b >> 5;
+      for (u32 j = a + 1; j < (la + 1) * 32; ++j) acc = lh_merge(acc, __ldg(lh + j));
+      for (u32 j = lb * 32; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+      if (lb > la + 1) {
+        const u32 cnt = lb - la - 1;
+        const int k = hb32(cnt);
+        const uint2* row = sp + static_cast<u64>(k) * nb;
+        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << k)]));
+      }
+    }
+    const u32 pre = i + 1;
+    const bool inside = acc.x >= pre && acc.y < pre + sz;
+    const u32 e = pedge_by_pre[i];
+    if (e < m) mask[e] = inside ? 1 : 0;
+  }
+}
+
+struct BridgeWs {
+  longlong2* e64 = nullptr;
+  uint2* edges = nullptr;
+  u32* par = nullptr;
+  uint8_t* tree = nullptr;
+  u64* scan_m = nullptr;
+  u32* tedge = nullptr;
+  u32 *keys = nullptr, *vals = nullptr, *skey = nullptr, *sval = nullptr;
+  SortWs sort;
+  uint2* crange = nullptr;
+  u32* slot_of = nullptr;
+  u32* succ = nullptr;
+  ListRankWs lr;
+  u32* flags = nullptr;
+  u64* scan_k = nullptr;
+  u32* pre_of = nullptr;
+  u32* size_by_pre = nullptr;
+  u32* pedge_by_pre = nullptr;
+  uint2* lh = nullptr;
+  uint2* sp = nullptr;
+  u32 nb = 0, levels = 0;
+  u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
+  void carve(Carver& c, u32 n, u32 m, bool host_i64) {
+    const u32 k = 2 * (n - 1);
+    if (host_i64) {
+      e64 = c.take<longlong2>(m);
+      edges = c.take<uint2>(m);
+    }
+    par = c.take<u32>(n);
+    tree = c.take<uint8_t>(m + 16);
+    scan_m = c.take<u64>(scan_ws_words(m));
+    tedge = c.take<u32>(n);
+    keys = c.take<u32>(k + 1);
+    vals = c.take<u32>(k + 1);
+    skey = c.take<u32>(k + 1);
+    sval = c.take<u32>(k + 1);
+    sort.carve(c, k + 1);
+    crange = c.take<uint2>(n);
+    slot_of = c.take<u32>(k + 1);
+    succ = c.take<u32>(k + 1);
+    lr.carve(c, k > 0 ? k : 1);
+    flags = c.take<u32>(k + 1);
+    scan_k = c.take<u64>(scan_ws_words(k + 1));
+    pre_of = c.take<u32>(n);
+    size_by_pre = c.take<u32>(n);
+    pedge_by_pre = c.take<u32>(n);
+    lh = c.take<uint2>(n);
+    nb = (n + 31) / 32;
+    levels = 32 - __builtin_clz(nb);
+    sp = c.take<uint2>(static_cast<u64>(levels) * nb);
+    words = c.take<u32>(16);
+  }
+};
+
+void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int device,
+                 uint8_t* d_mask_user, uint8_t* h_mask, cudaStream_t st_in,
+                 ettg_phase_times* times) {
+  if (n64 <= 0) einval("empty graph");
+  if (n64 >= (i64(1) << 31) || m64 >= (i64(1) << 31) || m64 < 0)
+    einval("graph too large for packed hooking keys");
+  const u32 n = static_cast<u32>(n64), m = static_cast<u32>(m64);
+  const int sms = sm_count(device);
+  const unsigned g = sms * 8;
+  cudaStream_t own = nullptr;
+  if (!st_in) CK(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+  cudaStream_t st = st_in ? st_in : own;
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      if (s) cudaStreamDestroy(s);
+    }
+  } sg{own};
+
+  BridgeWs ws;
+  Carver c;
+  ws.carve(c, n, m, host_i64);
+  uint8_t* d_mask = d_mask_user;
+  if (!d_mask) d_mask = c.take<uint8_t>(m + 16);
+  Lease lease(device, st, c.off);
+  c = Carver{lease.base()};
+  ws.carve(c, n, m, host_i64);
+  if (!d_mask_user) d_mask = c.take<uint8_t>(m + 16);
+
+  cudaEvent_t ev[4];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  } eg{ev};
+
+  CK(cudaEventRecord(ev[0], st));
+  CK(cudaMemsetAsync(ws.words, 0, 16 * sizeof(u32), st));
+  const uint2* edges;
+  if (host_i64) {
+    if (m) {
+      CK(cudaMemcpyAsync(ws.e64, edges_in, static_cast<u64>(m) * 16, cudaMemcpyHostToDevice, st));
+      k_edges_from_i64<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.e64, m, n, ws.edges,
+                                                                        ws.words);
+      CK_LAUNCH();
+    }
+    edges = ws.edges;
+  } else {
+    edges = static_cast<const uint2*>(edges_in);
+    if (m) {
+      k_edges_check<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
+      CK_LAUNCH();
+    }
+  }
+  if (m) CK(cudaMemsetAsync(d_mask, 0, m, st));
+
+  // ---- spanning forest --------------------------------------------------
+  k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+  CK_LAUNCH();
+  if (m) {
+    k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, ws.par, ws.tree);
+    CK_LAUNCH();
+  }
+  CK(cudaEventRecord(ev[1], st));
+
+  // ---- Euler tour of the forest, rooted at 0 -----------------------------
+  scan_exclusive(TreeIn{ws.tree}, TreeOut{ws.tree, ws.tedge, n}, m, ws.scan_m, ws.words + 1, st);
+  u32 w[2];
+  CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (w[0]) einval("edge endpoint out of range");
+  const u32 T = w[1];
+  if (T != n - 1) einval("disconnected graph; extract the largest component first");
+
+  if (n > 1) {
+    const u32 k = 2 * T;
+    k_tree_he<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, ws.keys,
+                                                               ws.vals);
+    CK_LAUNCH();
+    sort_pairs(ws.keys, ws.vals, ws.skey, ws.sval, k, bits_for(n - 1), ws.sort, st);
+    CK(cudaMemsetAsync(ws.crange, 0, static_cast<u64>(n) * sizeof(uint2), st));
+    k_vertex_ranges<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.skey, k, ws.crange);
+    CK_LAUNCH();
+    k_inverse<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.sval, k, ws.slot_of);
+    CK_LAUNCH();
+    k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.skey, ws.sval, ws.slot_of,
+                                                                 ws.crange, k, ws.succ);
+    CK_LAUNCH();
+    k_tree_cut<<<1, 1, 0, st>>>(ws.sval, ws.crange, 0, ws.succ, ws.words + 2);
+    CK_LAUNCH();
+    u32 head = 0;
+    CK(cudaMemcpyAsync(&head, ws.words + 2, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    list_rank_core(ws.succ, k, head, NoDown{}, ws.lr, st, sms);
+    const Lr0View lv = lr0_view(ws.lr);
+    k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
+    CK_LAUNCH();
+    scan_exclusive(DownIn{ws.flags},
+                   StatsOut{ws.flags, ws.tedge, edges, lv, n, ws.pre_of, ws.size_by_pre,
+                            ws.pedge_by_pre},
+                   k, ws.scan_k, nullptr, st);
+  }
+  k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre);
+  CK_LAUNCH();
+  CK(cudaEventRecord(ev[2], st));
+
+  // ---- low / high + classification ---------------------------------------
+  k_lowhigh_init<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.lh, n);
+  CK_LAUNCH();
+  if (m) {
+    k_lowhigh_edges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m,
+                                                                     ws.pre_of, ws.lh);
+    CK_LAUNCH();
+  }
+  k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,
+                                                                            ws.sp);
+  CK_LAUNCH();
+  for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
+    k_lh_level<<<std::min(g, blocks_for(ws.nb, 256)), 256, 0, st>>>(
+        ws.sp + static_cast<u64>(lvl - 1) * ws.nb, ws.sp + static_cast<u64>(lvl) * ws.nb, ws.nb,
+        1u << (lvl - 1));
+    CK_LAUNCH();
+  }
+  k_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+      ws.lh, ws.sp, ws.nb, n, ws.size_by_pre, ws.pedge_by_pre, d_mask, m);
+  CK_LAUNCH();
+  CK(cudaEventRecord(ev[3], st));
+  if (h_mask && m) CK(cudaMemcpyAsync(h_mask, d_mask, m, cudaMemcpyDeviceToHost, st));
+  u32 lerr = 0;
+  if (n > 1) CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4,
+                                cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (lerr) throw Error(ETTG_EINTERNAL, "bridges: spanning-tree tour ranking failed");
+  if (times) {
+    float a = 0, b = 0, d = 0, tot = 0;
+    CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    CK(cudaEventElapsedTime(&d, ev[2], ev[3]));
+    CK(cudaEventElapsedTime(&tot, ev[0], ev[3]));
+    times->spanning_ms = a;
+    times->euler_ms = b;
+    times->lowhigh_ms = d;
+    times->total_ms = tot;
+  }
+}
+
+}  // namespace ettg
+
+using namespace ettg;
+
+extern "C" {
+
+int ettg_bridges(const int64_t* edges, int64_t n, int64_t m, int device, uint8_t* is_bridge,
+                 ettg_phase_times* times) {
+  return guard([&] {
+    if ((!edges || !is_bridge) && m > 0) einval("null argument");
+    DeviceScope ds(device);
+    run_bridges(edges, true, n, m, device, nullptr, is_bridge, nullptr, times);
+  });
+}
+
+int ettg_bridges_dev(const uint32_t* d_edges, int64_t n, int64_t m, int device,
+                     uint8_t* d_is_bridge, void* stream, ettg_phase_times* times) {
+  return guard([&] {
+    if ((!d_edges || !d_is_bridge) && m > 0) einval("null argument");
+    DeviceScope ds(device);
+    run_bridges(d_edges, false, n, m, device, d_is_bridge, nullptr,
+                static_cast<cudaStream_t>(stream), times);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// Shared device helpers for the sm_100a Euler-tour pipeline.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace ettg {
+
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = int64_t;
+
+constexpr u32 kNone = 0xFFFFFFFFu;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs (queried at run time too)
+
+// ---- error plumbing (host) -----------------------------------------------
+// Exceptions are caught at the C-ABI boundary (capi.cu) and turned into
+// ETTG_* codes; they never cross extern "C".
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file,
+                       int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line,
+             cudaGetErrorString(e));
+    throw Error(e == cudaErrorMemoryAllocation ? 4 : 3, buf);
+  }
+}
+#define CK(x) ::ettg::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::ettg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+inline unsigned blocks_for(u64 n, unsigned threads, unsigned cap = 148u * 64u) {
+  u64 b = (n + threads - 1) / threads;
+  if (b == 0) b = 1;
+  return b > cap ? cap : static_cast<unsigned>(b);
+}
+
+// ---- bit helpers (device) -------------------------------------------------
+__device__ __forceinline__ int hb32(u32 x) { return 31 - __clz(x); }  // x != 0
+__device__ __forceinline__ int tz32(u32 x) { return __ffs(x) - 1; }   // x != 0
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Read-only, L1-no-allocate gathers for index records (random, never reused
+// within a CTA): one 32-B sector per record.
+__device__ __forceinline__ uint4 ldg_nc_na(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_nc_na(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+// Streaming loads/stores (read once / write once).
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.cs.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(u32* p, u32 v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
+// Device-scope acquire/release for look-back status words.
+__device__ __forceinline__ u64 ld_acquire(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_volatile_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// 32-bit avalanche (murmur3 finaliser) used for splitter sampling.
+__device__ __forceinline__ u32 mix32(u32 x) {
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+
+// ---- workspace carving -----------------------------------------------------
+// Pipelines lay out their scratch with a Carver twice: once with base ==
+// nullptr to measure, once on the leased arena to hand out pointers.
+struct Carver {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+// Grow-only per-device scratch arena (capi.cu).  A Lease serialises users of
+// the arena across host threads and orders reuse across streams.
+class Lease {
+ public:
+  Lease(int device, cudaStream_t stream, size_t bytes);
+  ~Lease();
+  char* base() const { return base_; }
+  Lease(const Lease&) = delete;
+  Lease& operator=(const Lease&) = delete;
+
+ private:
+  int device_;
+  cudaStream_t stream_;
+  char* base_;
+};
+
+int sm_count(int device);
+
+// Copy `count` words device->host on `stream` and wait (used for counters
+// and error flags; a handful of bytes).
+inline void read_back(void* host, const void* dev, size_t bytes,
+                      cudaStream_t stream) {
+  CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+}
+
+}  // namespace ettg

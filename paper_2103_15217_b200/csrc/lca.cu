@@ -1,0 +1,833 @@
+// LCA on B200: Euler-tour index build + batched inlabel / RMQ query kernels.
+//
+// Reference path (all CPU, OpenMP):
+//   inlabel_build            core/src/lca.cpp:20-82
+//     validate_tree          core/src/graph.cpp:175-206   (sequential chain walks)
+//     tree_edges             core/src/graph.cpp:208-217
+//     build_half_edges       core/src/euler.cpp:38-90     (2 sequential counting passes)
+//     linearize / list_rank  core/src/euler.cpp:92-117, primitives.cpp:26-115
+//     node_stats             core/src/euler.cpp:119-155   (2 scans)
+//     inlabel / head / ascendant fix-point  core/src/lca.cpp:35-80
+//   inlabel_lca              core/src/lca.cpp:84-109
+//   rmq_lca_build / rmq_lca  core/src/lca.cpp:128-157 (segment tree, O(log n))
+//
+// Device pipeline (u32 ids, n < 2^31):
+//   k_tree_validate   parent -> (key=parent, val=child) pairs, root/range flags
+//   sort_pairs        stable radix sort => children of each node in ascending
+//                     id, i.e. exactly the reference's sorted half-edge order
+//   k_child_ranges    [start,end) of each node's child slice
+//   k_node_succ       succ(down(y)); j(y) = #children < parent(y)
+//   k_slot_succ       succ(up(c)) by the DCEL rotation rule
+//   list_rank_core    2n-element tour list (down(root) ... up(root)), weight
+//                     "is down", giving rank and #downs before each half-edge
+//   k_tree_stats      preorder / level / size / inlabel / first position
+//                     (+ RMQ tour keys) in one pass per node
+//   k_head            head, label record {parent(head), level}, up-label
+//   k_path_asc        ascendant per label by a <= 31-hop chain walk
+//   k_pack            16-B node record {inlabel, ascendant, level, 0}
+//
+// Half-edge ids: down(v) = 2v (parent -> v), up(v) = 2v+1 (v -> parent); the
+// root's pair is the virtual start/end of the tour, so the tour list has
+// exactly 2n elements and rank r(down(v)) equals the reference's tour step of
+// v's first occurrence (rmq tour_nodes, core/src/lca.cpp:135-146).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "api_internal.cuh"
+#include "common.cuh"
+#include "listrank.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+namespace ettg {
+
+// validation flags (bit set)
+constexpr u32 kVRootParent = 1u;  // parent[root] != none
+constexpr u32 kVRange = 2u;       // parent id out of range
+constexpr u32 kVRoots = 4u;       // more than one root
+
+template <class P>
+__device__ __forceinline__ bool parent_is_none(P p);
+template <>
+__device__ __forceinline__ bool parent_is_none<int64_t>(int64_t p) { return p == -1; }
+template <>
+__device__ __forceinline__ bool parent_is_none<u32>(u32 p) { return p == kNone; }
+
+template <class P>
+__global__ void k_tree_validate(const P* __restrict__ parent, u32 n, u32 root,
+                                u32* __restrict__ par, u32* __restrict__ keys,
+                                u32* __restrict__ vals, u32* flags) {
+  u32 f = 0;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const P p = parent[v];
+    u32 pu;
+    if (parent_is_none<P>(p)) {
+      pu = kNone;
+      if (v != root) f |= kVRoots;
+    } else if (static_cast<u64>(static_cast<int64_t>(p)) >= n) {  // negative wraps high
+      pu = kNone;
+      f |= kVRange;
+      if (v == root) f |= kVRootParent;
+    } else {
+      pu = static_cast<u32>(p);
+      if (v == root) f |= kVRootParent;
+    }
+    par[v] = pu;
+    if (v != root) {
+      const u32 idx = v < root ? v : v - 1;
+      keys[idx] = pu == kNone ? 0u : pu;  // keep the sort well-formed on bad input
+      vals[idx] = v;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+// crange[y] = [first slot, end slot) of y's children in the sorted arrays.
+__global__ void k_child_ranges(const u32* __restrict__ pkey, u32 m, uint2* __restrict__ crange) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
+    const u32 y = pkey[s];
+    if (s == 0 || pkey[s - 1] != y) crange[y].x = s;
+    if (s + 1 == m || pkey[s + 1] != y) crange[y].y = s + 1;
+  }
+}
+
+__global__ void k_node_succ(const uint2* __restrict__ crange, const u32* __restrict__ child,
+                            const u32* __restrict__ par, u32 n, u32 root,
+                            u32* __restrict__ jj, u32* __restrict__ succ) {
+  for (u32 y = blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+    const uint2 r = crange[y];
+    const u32 deg = r.y - r.x;
+    u32 j = 0;
+    if (y == root) {
+      succ[2 * y + 1] = kNone;  // up(root) is the tail
+    } else if (deg > 0) {
+      // lower_bound of parent(y) among y's sorted children: the rotation at y
+      // starts just after the entering half-edge (euler.cpp:85-88).
+      const u32 p = par[y];
+      u32 lo = 0, hi = deg;
+      while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (child[r.x + mid] < p) lo = mid + 1;
+        else hi = mid;
+      }
+      j = lo == deg ? 0u : lo;
+    }
+    jj[y] = j;
+    succ[2 * y] = deg > 0 ? 2 * child[r.x + j] : 2 * y + 1;
+  }
+}
+
+__global__ void k_slot_succ(const uint2* __restrict__ crange, const u32* __restrict__ child,
+                            const u32* __restrict__ pkey, const u32* __restrict__ jj, u32 m,
+                            u32 root, u32* __restrict__ succ) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
+    const u32 c = child[s];
+    const u32 y = pkey[s];
+    const uint2 r = crange[y];
+    const u32 deg = r.y - r.x;
+    const u32 i = s - r.x;
+    u32 nxt;
+    if (y == root) {
+      nxt = (i + 1 == deg) ? 2 * y + 1 : 2 * child[s + 1];
+    } else {
+      const u32 i2 = (i + 1 == deg) ? 0u : i + 1;
+      nxt = (i2 == jj[y]) ? 2 * y + 1 : 2 * child[r.x + i2];
+    }
+    succ[2 * c + 1] = nxt;
+  }
+}
+
+// preorder (1-based), level, size, inlabel, first tour step per node
+// (node_stats core/src/euler.cpp:144-153 + inlabel core/src/lca.cpp:35-44).
+__global__ void k_tree_stats(Lr0View lr, u32 n, const u32* __restrict__ par,
+                             u32* __restrict__ pre, u32* __restrict__ size,
+                             u32* __restrict__ level, u32* __restrict__ inlabel,
+                             u32* __restrict__ first, u64* __restrict__ tour_key) {
+  const u32 S1 = *lr.d_S1;
+  const u32 steps = 2 * n - 1;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    u32 rd, dd, ru, du;
+    lr.get(2 * v, S1, rd, dd);
+    lr.get(2 * v + 1, S1, ru, du);
+    const u32 p = dd + 1;
+    const u32 lev = 2 * dd - rd;
+    const u32 sz = (ru - rd + 1) >> 1;
+    const u32 r = p + sz - 1;
+    const u32 in = (p == r) ? p : (r & ~((1u << hb32((p - 1) ^ r)) - 1u));
+    pre[v] = p;
+    size[v] = sz;
+    level[v] = lev;
+    inlabel[v] = in;
+    first[v] = rd;
+    if (tour_key) {
+      if (rd < steps) tour_key[rd] = (static_cast<u64>(lev) << 32) | v;
+      const u32 pv = par[v];
+      if (pv != kNone && ru < steps) tour_key[ru] = (static_cast<u64>(lev - 1) << 32) | pv;
+    }
+  }
+}
+
+// head / label record / up-label (core/src/lca.cpp:49-53 and the fix-point
+// input of :59-78).  lab[L] = {parent(head(L)), level(parent(head(L)))}.
+__global__ void k_head(const u32* __restrict__ inlabel, const u32* __restrict__ par,
+                       const u32* __restrict__ level, u32 n, u32* __restrict__ head,
+                       uint2* __restrict__ lab, u32* __restrict__ up) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const u32 L = inlabel[v];
+    if (L == 0 || L > n) continue;  // malformed input, already rejected
+    const u32 p = par[v];
+    const u32 pl = p == kNone ? 0u : inlabel[p];
+    if (p == kNone || pl != L) {
+      head[L] = v;
+      lab[L] = make_uint2(p, p == kNone ? kNone : level[v] - 1);
+      up[L] = p == kNone ? 0u : pl;
+    }
+  }
+}
+
+// ascendant(L) = OR of 2^tz over the label chain to the root's label.  Each
+// hop strictly raises tz, so <= 31 hops (replaces the log-n global rounds of
+// core/src/lca.cpp:59-78 with one independent walk per label).
+__global__ void k_path_asc(const u32* __restrict__ up, u32 n, u32* __restrict__ asc) {
+  for (u32 L = blockIdx.x * blockDim.x + threadIdx.x + 1; L <= n; L += gridDim.x * blockDim.x) {
+    u32 u = up[L];
+    if (u == kNone) continue;
+    u32 a = 1u << tz32(L);
+    for (int hop = 0; hop < 32 && u != 0u && u <= n; ++hop) {
+      a |= 1u << tz32(u);
+      u = up[u];
+    }
+    asc[L] = a;
+  }
+}
+
+__global__ void k_pack(const u32* __restrict__ inlabel, const u32* __restrict__ level,
+                       const u32* __restrict__ asc, u32 n, uint4* __restrict__ node) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const u32 L = inlabel[v];
+    node[v] = make_uint4(L, (L >= 1 && L <= n) ? asc[L] : 0u, level[v], 0u);
+  }
+}
+
+// ---- RMQ over the tour (block-sparse table, 32-step blocks) ---------------
+// Keys (level << 32 | node) make the minimum's low word the LCA itself.
+__global__ void k_rmq_block(const u64* __restrict__ key, u32 steps, u32 nb,
+                            u64* __restrict__ pre_in, u64* __restrict__ suf_in,
+                            u64* __restrict__ sp0) {
+  const u32 lane = threadIdx.x & 31;
+  const u32 warps = (gridDim.x * blockDim.x) >> 5;
+  for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const u32 t = b * 32 + lane;
+    const u64 k = t < steps ? key[t] : ~0ull;
+    u64 f = k, g = k;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u64 a = __shfl_up_sync(0xffffffffu, f, d);
+      if (lane >= static_cast<u32>(d)) f = min(f, a);
+      u64 c = __shfl_down_sync(0xffffffffu, g, d);
+      if (lane + d < 32) g = min(g, c);
+    }
+    if (t < steps) {
+      pre_in[t] = f;
+      suf_in[t] = g;
+    }
+    if (lane == 31) sp0[b] = f;
+  }
+}
+
+__global__ void k_rmq_level(const u64* __restrict__ prev, u64* __restrict__ cur, u32 nb,
+                            u32 half) {
+  for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
+       b += gridDim.x * blockDim.x)
+    cur[b] = min(prev[b], prev[b + half]);
+}
+
+// ---- queries ---------------------------------------------------------------
+struct PairsU32 {
+  const uint2* p;
+  __device__ __forceinline__ void get(u64 i, u32& x, u32& y) const {
+    const uint2 v = ld_stream(p + i);
+    x = v.x;
+    y = v.y;
+  }
+};
+struct PairsI64 {
+  const longlong2* p;
+  __device__ __forceinline__ void get(u64 i, u32& x, u32& y) const {
+    const longlong2 v = p[i];
+    // ids outside [0, 2^32) map to kNone, which the range check rejects
+    x = (v.x < 0 || v.x > 0xFFFFFFFFll) ? kNone : static_cast<u32>(v.x);
+    y = (v.y < 0 || v.y > 0xFFFFFFFFll) ? kNone : static_cast<u32>(v.y);
+  }
+};
+struct AnsU32 {
+  u32* p;
+  __device__ __forceinline__ void put(u64 i, u32 a) const { st_stream(p + i, a); }
+};
+struct AnsI64 {
+  long long* p;
+  __device__ __forceinline__ void put(u64 i, u32 a) const {
+    p[i] = a == kNone ? -1ll : static_cast<long long>(a);
+  }
+};
+
+constexpr int kQThreads = 256;
+constexpr int kQPer = 4;  // independent queries per thread (memory-level parallelism)
+
+// inlabel_lca (core/src/lca.cpp:84-109), four queries in flight per thread:
+// two 16-B node-record gathers, then at most two 8-B label-record gathers.
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads)
+    k_lca_inlabel(const uint4* __restrict__ node, const uint2* __restrict__ lab, u32 n, In in,
+                  Out out, u64 q, u32* err) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
+  u32 bad_any = 0;
+  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
+       base += stride) {
+    u32 x[kQPer], y[kQPer];
+    bool ok[kQPer], bad[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      const u64 i = base + static_cast<u64>(j) * kQThreads;
+      ok[j] = i < q;
+      x[j] = y[j] = 0;
+      if (ok[j]) in.get(i, x[j], y[j]);
+      bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
+      if (bad[j]) x[j] = y[j] = 0;
+    }
+    uint4 A[kQPer], B[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      A[j] = ldg_nc_na(node + x[j]);
+      B[j] = ldg_nc_na(node + y[j]);
+    }
+    u32 ans[kQPer], wx[kQPer], wy[kQPer];
+    bool lx[kQPer], ly[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      lx[j] = ly[j] = false;
+      wx[j] = wy[j] = 0;
+      if (A[j].x == B[j].x) {
+        ans[j] = A[j].z <= B[j].z ? x[j] : y[j];
+      } else {
+        const int i = hb32(A[j].x ^ B[j].x);
+        const u32 common = A[j].y & B[j].y & ~((1u << i) - 1u);
+        const int jb = tz32(common);
+        const u32 target = (A[j].x & ~((2u << jb) - 1u)) | (1u << jb);
+        const u32 lowmask = (1u << jb) - 1u;
+        if (A[j].x != target) {
+          const int kx = hb32(A[j].y & lowmask);
+          wx[j] = min((A[j].x & ~((2u << kx) - 1u)) | (1u << kx), n);
+          lx[j] = true;
+        }
+        if (B[j].x != target) {
+          const int ky = hb32(B[j].y & lowmask);
+          wy[j] = min((B[j].x & ~((2u << ky) - 1u)) | (1u << ky), n);
+          ly[j] = true;
+        }
+      }
+    }
+    uint2 LX[kQPer], LY[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      LX[j] = lx[j] ? ldg_nc_na(lab + wx[j]) : make_uint2(x[j], A[j].z);
+      LY[j] = ly[j] ? ldg_nc_na(lab + wy[j]) : make_uint2(y[j], B[j].z);
+    }
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      if (A[j].x != B[j].x) ans[j] = LX[j].y <= LY[j].y ? LX[j].x : LY[j].x;
+      if (ok[j]) out.put(base + static_cast<u64>(j) * kQThreads, bad[j] ? kNone : ans[j]);
+      bad_any |= bad[j];
+    }
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+struct RmqView {
+  const u64* key;
+  const u64* pre_in;
+  const u64* suf_in;
+  const u64* sp;
+  const u32* first;
+  u32 nb;
+  __device__ __forceinline__ u32 query(u32 x, u32 y) const {
+    u32 l = __ldg(first + x), r = __ldg(first + y);
+    if (l > r) {
+      const u32 t = l;
+      l = r;
+      r = t;
+    }
+    const u32 lb = l >> 5, rb = r >> 5;
+    u64 m;
+    if (lb == rb) {
+      m = ~0ull;
+      for (u32 t = l; t <= r; ++t) m = min(m, __ldg(key + t));
+    } else {
+      m = min(__ldg(suf_in + l), __ldg(pre_in + r));
+      if (rb > lb + 1) {
+        const int k = hb32(rb - lb - 1);
+        const u64* row = sp + static_cast<u64>(k) * nb;
+        m = min(m, min(__ldg(row + lb + 1), __ldg(row + rb - (1u << k))));
+      }
+    }
+    return static_cast<u32>(m);
+  }
+};
+
+// rmq_lca (core/src/lca.cpp:151-157) with O(1) block-sparse lookups.
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads)
+    k_lca_rmq(RmqView rv, u32 n, In in, Out out, u64 q, u32* err) {
+  u32 bad_any = 0;
+  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
+       i += static_cast<u64>(gridDim.x) * kQThreads) {
+    u32 x, y;
+    in.get(i, x, y);
+    const bool bad = x >= n || y >= n;
+    bad_any |= bad;
+    out.put(i, bad ? kNone : rv.query(x, y));
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+}  // namespace ettg
+
+// ============================================================================
+// Handle and C-ABI
+// ============================================================================
+using namespace ettg;
+
+struct ettg_lca {
+  int device = 0;
+  u32 n = 0;
+  u32 root = 0;
+  unsigned engines = 0;
+  bool full = false;  // built here (stats available) vs attached replica
+  cudaStream_t stream = nullptr;
+  cudaStream_t qs[2] = {nullptr, nullptr};
+  char* mem = nullptr;
+  uint4* node = nullptr;
+  uint2* lab = nullptr;
+  u32 *par = nullptr, *pre = nullptr, *size = nullptr, *level = nullptr, *inlabel = nullptr,
+      *first = nullptr, *head = nullptr;
+  // rmq
+  u64 *tkey = nullptr, *pre_in = nullptr, *suf_in = nullptr, *sp = nullptr;
+  u32 nb = 0, levels = 0;
+  // host-query staging (lazy)
+  char* qmem = nullptr;
+  u64 qchunk = 0;
+  u32* qerr = nullptr;
+  double build_ms = 0;
+
+  void carve(Carver& c) {
+    node = c.take<uint4>(n);
+    lab = c.take<uint2>(static_cast<u64>(n) + 1);
+    if (!full) return;
+    par = c.take<u32>(n);
+    pre = c.take<u32>(n);
+    size = c.take<u32>(n);
+    level = c.take<u32>(n);
+    inlabel = c.take<u32>(n);
+    first = c.take<u32>(n);
+    head = c.take<u32>(static_cast<u64>(n) + 1);
+    if (engines & ETTG_ENGINE_RMQ) {
+      const u32 steps = 2 * n - 1;
+      nb = (steps + 31) / 32;
+      levels = 32 - __builtin_clz(nb);
+      tkey = c.take<u64>(steps);
+      pre_in = c.take<u64>(steps);
+      suf_in = c.take<u64>(steps);
+      sp = c.take<u64>(static_cast<u64>(levels) * nb);
+    }
+  }
+  ~ettg_lca() {
+    if (mem) cudaFree(mem);
+    if (qmem) cudaFree(qmem);
+    for (auto s : qs)
+      if (s) cudaStreamDestroy(s);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+struct BuildWs {
+  int64_t* par64 = nullptr;
+  u32 *keys = nullptr, *vals = nullptr, *pkey = nullptr, *child = nullptr;
+  SortWs sort;
+  uint2* crange = nullptr;
+  u32* jj = nullptr;
+  u32* succ = nullptr;
+  ListRankWs lr;
+  u32* up = nullptr;
+  u32* asc = nullptr;
+  u32* flags = nullptr;
+  void carve(Carver& c, u32 n, bool host_i64) {
+    if (host_i64) par64 = c.take<int64_t>(n);
+    const u32 m = n - 1;
+    keys = c.take<u32>(m + 1);
+    vals = c.take<u32>(m + 1);
+    pkey = c.take<u32>(m + 1);
+    child = c.take<u32>(m + 1);
+    sort.carve(c, m + 1);
+    crange = c.take<uint2>(n);
+    jj = c.take<u32>(n);
+    succ = c.take<u32>(2ull * n);
+    lr.carve(c, 2 * n);
+    up = c.take<u32>(static_cast<u64>(n) + 1);
+    asc = c.take<u32>(static_cast<u64>(n) + 1);
+    flags = c.take<u32>(8);
+  }
+};
+
+void launch_stats_rmq(ettg_lca* h, cudaStream_t st, int sms) {
+  const u32 n = h->n;
+  const u32 steps = 2 * n - 1;
+  const unsigned g = sms * 8;
+  k_rmq_block<<<blocks_for(static_cast<u64>(h->nb) * 32, 256), 256, 0, st>>>(
+      h->tkey, steps, h->nb, h->pre_in, h->suf_in, h->sp);
+  CK_LAUNCH();
+  for (u32 k = 1; k < h->levels; ++k) {
+    k_rmq_level<<<std::min<unsigned>(g, blocks_for(h->nb, 256)), 256, 0, st>>>(
+        h->sp + static_cast<u64>(k - 1) * h->nb, h->sp + static_cast<u64>(k) * h->nb, h->nb,
+        1u << (k - 1));
+    CK_LAUNCH();
+  }
+}
+
+ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
+                      int64_t root64, int device, unsigned engines, cudaStream_t user_st) {
+  if (n64 <= 0) einval("parent array size mismatch");
+  if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
+  if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
+  if (engines == 0) engines = ETTG_ENGINE_INLABEL;
+  const u32 n = static_cast<u32>(n64), root = static_cast<u32>(root64);
+  const int sms = sm_count(device);
+
+  auto h = std::make_unique<ettg_lca>();
+  h->device = device;
+  h->n = n;
+  h->root = root;
+  h->engines = engines;
+  h->full = true;
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  cudaStream_t st = user_st ? user_st : h->stream;
+
+  Carver hc;
+  h->carve(hc);
+  CK(cudaMalloc(&h->mem, hc.off));
+  hc = Carver{h->mem};
+  h->carve(hc);
+
+  Carver wc;
+  BuildWs ws;
+  ws.carve(wc, n, host_i64);
+  Lease lease(device, st, wc.off);
+  wc = Carver{lease.base()};
+  ws.carve(wc, n, host_i64);
+
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+
+  const u32 m = n - 1;
+  const unsigned g = sms * 8;
+  CK(cudaMemsetAsync(ws.flags, 0, 8 * sizeof(u32), st));
+  if (host_i64) {
+    CK(cudaMemcpyAsync(ws.par64, parent, static_cast<u64>(n) * 8, cudaMemcpyHostToDevice, st));
+    k_tree_validate<int64_t><<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+        ws.par64, n, root, h->par, ws.keys, ws.vals, ws.flags);
+  } else {
+    (void)dev_u32;
+    k_tree_validate<u32><<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+        static_cast<const u32*>(parent), n, root, h->par, ws.keys, ws.vals, ws.flags);
+  }
+  CK_LAUNCH();
+  sort_pairs(ws.keys, ws.vals, ws.pkey, ws.child, m, bits_for(n - 1), ws.sort, st);
+  CK(cudaMemsetAsync(ws.crange, 0, static_cast<u64>(n) * sizeof(uint2), st));
+  if (m > 0) {
+    k_child_ranges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.pkey, m, ws.crange);
+    CK_LAUNCH();
+  }
+  k_node_succ<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.crange, ws.child, h->par, n,
+                                                              root, ws.jj, ws.succ);
+  CK_LAUNCH();
+  if (m > 0) {
+    k_slot_succ<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.crange, ws.child, ws.pkey,
+                                                                ws.jj, m, root, ws.succ);
+    CK_LAUNCH();
+  }
+  list_rank_core(ws.succ, 2 * n, 2 * root, EvenIsDown{}, ws.lr, st, sms);
+  k_tree_stats<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+      lr0_view(ws.lr), n, h->par, h->pre, h->size, h->level, h->inlabel, h->first,
+      (engines & ETTG_ENGINE_RMQ) ? h->tkey : nullptr);
+  CK_LAUNCH();
+
+  // Validation verdict before building the rest (bad input -> no index).
+  u32 vflags[8], lerr;
+  CK(cudaMemcpyAsync(vflags, ws.flags, sizeof vflags, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, sizeof lerr,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (vflags[0] & kVRootParent) einval("root has no kNone parent entry");
+  if (vflags[0] & kVRange) einval("parent id out of range");
+  if (vflags[0] & kVRoots) einval("tree must have exactly one root");
+  if (lerr & kErrStructure) einval("cycle in parent array");
+  if (lerr & kErrCapacity) throw Error(ETTG_EINTERNAL, "list ranking: splitter capacity exceeded");
+
+  CK(cudaMemsetAsync(h->head, 0xFF, (static_cast<u64>(n) + 1) * 4, st));
+  CK(cudaMemsetAsync(h->lab, 0xFF, (static_cast<u64>(n) + 1) * 8, st));
+  CK(cudaMemsetAsync(ws.up, 0xFF, (static_cast<u64>(n) + 1) * 4, st));
+  k_head<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->par, h->level, n,
+                                                         h->head, h->lab, ws.up);
+  CK_LAUNCH();
+  k_path_asc<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.up, n, ws.asc);
+  CK_LAUNCH();
+  k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, ws.asc, n,
+                                                         h->node);
+  CK_LAUNCH();
+  if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  h->build_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return h.release();
+}
+
+void ensure_qbuf(ettg_lca* h, u64 chunk) {
+  if (h->qmem && h->qchunk >= chunk) return;
+  if (h->qmem) CK(cudaFree(h->qmem));
+  h->qmem = nullptr;
+  // per stream: pairs (16 B/query) + answers (8 B/query); + 2 error words
+  chunk = (chunk + 1) & ~u64(1);
+  CK(cudaMalloc(&h->qmem, 2 * chunk * 24 + 256));
+  h->qchunk = chunk;
+  h->qerr = reinterpret_cast<u32*>(h->qmem + 2 * chunk * 24);
+  for (auto& s : h->qs)
+    if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+}
+
+template <class In, class Out>
+void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32* err,
+                  cudaStream_t st) {
+  if (q == 0) return;
+  const int sms = sm_count(h->device);
+  if (engine == ETTG_ENGINE_RMQ) {
+    if (!(h->engines & ETTG_ENGINE_RMQ) || !h->tkey)
+      einval("index was built without the RMQ engine");
+    RmqView rv{h->tkey, h->pre_in, h->suf_in, h->sp, h->first, h->nb};
+    unsigned blocks = std::min<u64>((q + kQThreads - 1) / kQThreads, u64(sms) * 16);
+    k_lca_rmq<In, Out><<<blocks, kQThreads, 0, st>>>(rv, h->n, in, out, q, err);
+  } else {
+    const u64 per = u64(kQThreads) * kQPer;
+    unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * 16);
+    k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->lab, h->n, in, out, q, err);
+  }
+  CK_LAUNCH();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ettg_lca_build(const int64_t* parent, int64_t n, int64_t root, int device, unsigned engines,
+                   ettg_lca** out) {
+  return guard([&] {
+    if (!out || (!parent && n > 0)) einval("null argument");
+    *out = nullptr;
+    DeviceScope ds(device);
+    *out = build_index(parent, true, false, n, root, device, engines, nullptr);
+  });
+}
+
+int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root, int device,
+                       unsigned engines, void* stream, ettg_lca** out) {
+  return guard([&] {
+    if (!out || !d_parent) einval("null argument");
+    *out = nullptr;
+    DeviceScope ds(device);
+    *out = build_index(d_parent, false, true, n, root, device, engines,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+void ettg_lca_free(ettg_lca* h) {
+  if (!h) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  delete h;
+  cudaSetDevice(prev);
+}
+
+int ettg_lca_size(const ettg_lca* h, int64_t* n) {
+  return guard([&] {
+    if (!h || !n) einval("null argument");
+    *n = h->n;
+  });
+}
+
+int ettg_lca_build_ms(const ettg_lca* h, double* ms) {
+  return guard([&] {
+    if (!h || !ms) einval("null argument");
+    *ms = h->build_ms;
+  });
+}
+
+int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pairs, int64_t q,
+                          int64_t batch, int64_t* answers) {
+  return guard([&] {
+    if (!hc) einval("null handle");
+    if (batch < 1) einval("batch_size must be >= 1");
+    if (q < 0) einval("negative query count");
+    if (q == 0) return;
+    if (!pairs || !answers) einval("null argument");
+    ettg_lca* h = const_cast<ettg_lca*>(hc);
+    DeviceScope ds(h->device);
+    const u64 chunk = std::min<u64>(static_cast<u64>(q), u64(1) << 22);
+    ensure_qbuf(h, chunk);
+    CK(cudaMemsetAsync(h->qerr, 0, 8, h->qs[0]));
+    CK(cudaStreamSynchronize(h->qs[0]));
+    u64 done = 0;
+    int c = 0;
+    while (done < static_cast<u64>(q)) {
+      const u64 cnt = std::min<u64>(chunk, static_cast<u64>(q) - done);
+      const int s = c & 1;
+      cudaStream_t st = h->qs[s];
+      const u64 qc = h->qchunk;  // even (or a single chunk): keeps 16-B alignment
+      longlong2* dp = reinterpret_cast<longlong2*>(h->qmem + s * qc * 24);
+      long long* da = reinterpret_cast<long long*>(h->qmem + s * qc * 24 + qc * 16);
+      CK(cudaMemcpyAsync(dp, pairs + 2 * done, cnt * 16, cudaMemcpyHostToDevice, st));
+      launch_query(h, engine, PairsI64{dp}, AnsI64{da}, cnt, h->qerr + s, st);
+      CK(cudaMemcpyAsync(answers + done, da, cnt * 8, cudaMemcpyDeviceToHost, st));
+      done += cnt;
+      ++c;
+    }
+    u32 errs[2] = {0, 0};
+    CK(cudaStreamSynchronize(h->qs[1]));
+    CK(cudaMemcpyAsync(errs, h->qerr, sizeof errs, cudaMemcpyDeviceToHost, h->qs[0]));
+    CK(cudaStreamSynchronize(h->qs[0]));
+    if (errs[0] | errs[1]) throw Error(ETTG_ERANGE, "query node id out of range");
+  });
+}
+
+int ettg_lca_query(const ettg_lca* h, const int64_t* pairs, int64_t q, int64_t batch,
+                   int64_t* answers) {
+  return ettg_lca_query_engine(h, ETTG_ENGINE_INLABEL, pairs, q, batch, answers);
+}
+
+int ettg_lca_query_dev(const ettg_lca* h, unsigned engine, const uint32_t* d_pairs, int64_t q,
+                       uint32_t* d_answers, void* stream) {
+  return guard([&] {
+    if (!h) einval("null handle");
+    if (q < 0) einval("negative query count");
+    if (q == 0) return;
+    if (!d_pairs || !d_answers) einval("null argument");
+    DeviceScope ds(h->device);
+    static thread_local u32* dummy_err[64] = {nullptr};
+    u32*& err = dummy_err[h->device & 63];
+    if (!err) CK(cudaMalloc(&err, 256));
+    launch_query(h, engine ? engine : ETTG_ENGINE_INLABEL,
+                 PairsU32{reinterpret_cast<const uint2*>(d_pairs)}, AnsU32{d_answers},
+                 static_cast<u64>(q), err, static_cast<cudaStream_t>(stream));
+  });
+}
+
+namespace {
+void copy_widen(int64_t* dst, const u32* src, u64 count, cudaStream_t st) {
+  if (!dst) return;
+  std::vector<u32> tmp(count);
+  CK(cudaMemcpyAsync(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (u64 i = 0; i < count; ++i) dst[i] = tmp[i] == kNone ? -1 : static_cast<int64_t>(tmp[i]);
+}
+}  // namespace
+
+int ettg_lca_stats(const ettg_lca* h, int64_t* preorder, int64_t* size, int64_t* level,
+                   int64_t* parent) {
+  return guard([&] {
+    if (!h) einval("null handle");
+    if (!h->full) einval("attached replica has no node statistics");
+    DeviceScope ds(h->device);
+    copy_widen(preorder, h->pre, h->n, h->stream);
+    copy_widen(size, h->size, h->n, h->stream);
+    copy_widen(level, h->level, h->n, h->stream);
+    copy_widen(parent, h->par, h->n, h->stream);
+  });
+}
+
+int ettg_lca_inlabel_index(const ettg_lca* h, int64_t* inlabel, uint64_t* ascendant,
+                           int64_t* head, int64_t* level, int64_t* parent) {
+  return guard([&] {
+    if (!h) einval("null handle");
+    if (!h->full) einval("attached replica has no exportable index fields");
+    DeviceScope ds(h->device);
+    copy_widen(inlabel, h->inlabel, h->n, h->stream);
+    copy_widen(head, h->head, static_cast<u64>(h->n) + 1, h->stream);
+    copy_widen(level, h->level, h->n, h->stream);
+    copy_widen(parent, h->par, h->n, h->stream);
+    if (ascendant) {
+      std::vector<uint4> rec(h->n);
+      CK(cudaMemcpyAsync(rec.data(), h->node, static_cast<u64>(h->n) * 16,
+                         cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      for (u32 v = 0; v < h->n; ++v) ascendant[v] = rec[v].y;
+    }
+  });
+}
+
+int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes) {
+  return guard([&] {
+    if (!h || !bytes) einval("null argument");
+    *bytes = static_cast<int64_t>(h->n) * 16 + (static_cast<int64_t>(h->n) + 1) * 8;
+  });
+}
+
+int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
+  return guard([&] {
+    if (!h || !d_dst) einval("null argument");
+    DeviceScope ds(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* dst = static_cast<char*>(d_dst);
+    CK(cudaMemcpyAsync(dst, h->node, static_cast<u64>(h->n) * 16, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(dst + static_cast<u64>(h->n) * 16, h->lab,
+                       (static_cast<u64>(h->n) + 1) * 8, cudaMemcpyDeviceToDevice, st));
+  });
+}
+
+int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* stream,
+                              ettg_lca** out) {
+  return guard([&] {
+    if (!d_src || !out) einval("null argument");
+    if (n <= 0 || n >= (int64_t(1) << 31)) einval("bad node count");
+    *out = nullptr;
+    DeviceScope ds(device);
+    auto h = std::make_unique<ettg_lca>();
+    h->device = device;
+    h->n = static_cast<u32>(n);
+    h->engines = ETTG_ENGINE_INLABEL;
+    h->full = false;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    Carver c;
+    h->carve(c);
+    CK(cudaMalloc(&h->mem, c.off));
+    c = Carver{h->mem};
+    h->carve(c);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const char* src = static_cast<const char*>(d_src);
+    CK(cudaMemcpyAsync(h->node, src, static_cast<u64>(n) * 16, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(h->lab, src + static_cast<u64>(n) * 16, (static_cast<u64>(n) + 1) * 8,
+                       cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    *out = h.release();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,518 @@
+// Weighted list ranking, Wei-JaJa style, for sm_100a.
+//
+// Replaces list_prefix (core/src/primitives.cpp:26-115).  The reference
+// samples ~k/1024 splitters with SplitMix64, walks the sublists with one
+// OpenMP thread each, stitches the sublists *sequentially*, then adds
+// offsets.  On the GPU:
+//
+//  level 0  splitters = head + every element whose mixed id has its low
+//           log2(L0) bits clear (hash sampling: O(1), no memory reads, no
+//           duplicates, robust to any layout); compacted in order with the
+//           decoupled look-back scan.  Walkers run in persistent warps that
+//           refill idle lanes from a work ticket, so the geometric sublist
+//           lengths do not leave lanes idle.  One dependent 4-B gather
+//           (succ) and one 8-B store (rec) per element.  Each element's
+//           record packs (local rank : 16 | local weight : 16 | sublist : 32);
+//           a walker that reaches 2^16-1 steps opens a fresh sublist id, so
+//           the packing never overflows.
+//  level l  the sublists form a list of S_l elements with u64 weights
+//           (weight-sum << 32 | length); the same walk recurses until the
+//           expected size fits one CTA.
+//  final    <= 8192 elements: pointer jumping (Wyllie) in shared memory by
+//           one 1024-thread CTA.  It also proves the structure: every chain
+//           must reach the tail (no cycles) and the head's total length must
+//           equal k (every element covered) -- the checks the reference makes
+//           with "cycle" / "does not cover all elements" (primitives.cpp:59-113).
+//
+// Weights: each element contributes rank 1 and a 0/1 "down" weight supplied
+// by a functor; prefix(e) = (#elements before e, sum of down weights before e).
+// The Euler tour uses down = "half-edge goes away from the root", which
+// yields preorder and level straight from the walk (no tour-order array and
+// no second scan, unlike node_stats in core/src/euler.cpp:134-142).
+#pragma once
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace ettg {
+namespace {  // kernels defined in headers: internal linkage per TU
+
+constexpr u32 kLrFinalMax = 8192;
+constexpr int kLrFinalThreads = 1024;
+constexpr size_t kLrFinalSmem = kLrFinalMax * (sizeof(uint64_t) + sizeof(uint32_t));
+constexpr u32 kLrL0 = 8;    // level-0 mean sublist length (power of two)
+constexpr u32 kLrL = 16;    // deeper levels
+constexpr u32 kLrCapStep = 0xFFFFu;
+
+// error bits
+constexpr u32 kErrStructure = 1u;  // cycle / uncovered / bad successor
+constexpr u32 kErrCapacity = 2u;   // splitter capacity exceeded (internal)
+
+struct NoDown {
+  __device__ __forceinline__ u32 operator()(u32) const { return 0u; }
+};
+struct EvenIsDown {  // Euler tour of a rooted tree: 2v = down(v), 2v+1 = up(v)
+  __device__ __forceinline__ u32 operator()(u32 e) const { return (~e) & 1u; }
+};
+
+__device__ __forceinline__ bool lr_is_splitter(u32 e, u32 head, u32 seed, u32 mask) {
+  return e == head || (mix32(e ^ seed) & mask) == 0u;
+}
+
+// ---- splitter compaction via the look-back scan ---------------------------
+struct SplIn {
+  u32 head, seed, mask;
+  __device__ __forceinline__ u32 operator()(u64 i) const {
+    return lr_is_splitter(static_cast<u32>(i), head, seed, mask) ? 1u : 0u;
+  }
+};
+struct SplOut {
+  u32 head, seed, mask, cap;
+  u32* spl;
+  u32* err;
+  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
+    if (lr_is_splitter(static_cast<u32>(i), head, seed, mask)) {
+      if (excl < cap) spl[excl] = static_cast<u32>(i);
+      else atomicOr(err, kErrCapacity);
+    }
+  }
+};
+// Level >= 1: head and size live in device memory; the scan runs over the
+// level's capacity and ignores ids >= S.
+struct SplInDev {
+  const u32* head;
+  const u32* S;
+  u32 seed, mask;
+  __device__ __forceinline__ u32 operator()(u64 i) const {
+    return (i < *S && lr_is_splitter(static_cast<u32>(i), *head, seed, mask)) ? 1u : 0u;
+  }
+};
+struct SplOutDev {
+  const u32* head;
+  const u32* S;
+  u32 seed, mask, cap;
+  u32* spl;
+  u32* err;
+  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
+    if (i < *S && lr_is_splitter(static_cast<u32>(i), *head, seed, mask)) {
+      if (excl < cap) spl[excl] = static_cast<u32>(i);
+      else atomicOr(err, kErrCapacity);
+    }
+  }
+};
+
+// Counters block (u32 words) shared by one ranking.
+struct LrCounters {
+  enum { kTicket0 = 0, kSubTotal0 = 1, kErr = 2, kNspl = 3, kLevelBase = 8 };
+  // level l >= 1 uses words kLevelBase + 4*l + {0: ticket, 1: nspl, 2: head}
+};
+
+// ---- level-0 walk -----------------------------------------------------------
+template <class Down>
+__global__ void __launch_bounds__(256)
+    k_lr_walk0(const u32* __restrict__ succ, u32 k, u32 head, u32 seed, u32 mask,
+               const u32* __restrict__ spl, u32* counters, u32 sub_cap,
+               u64* __restrict__ rec, u32* __restrict__ sub_next,
+               u64* __restrict__ sub_w, Down down) {
+  const int lane = threadIdx.x & 31;
+  const u32 lt = lanemask_lt();
+  const u32 nspl = min(counters[LrCounters::kNspl], sub_cap);
+  bool active = false, retired = false;
+  u32 sid = 0, cur = 0, acc = 0, steps = 0;
+  while (true) {
+    const u32 need = __ballot_sync(0xffffffffu, !active && !retired);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      u32 base = 0;
+      if (lane == leader) base = atomicAdd(&counters[LrCounters::kTicket0], __popc(need));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!active && !retired) {
+        const u32 idx = base + __popc(need & lt);
+        if (idx < nspl) {
+          sid = idx;
+          cur = spl[idx];
+          acc = 0;
+          active = true;
+        } else {
+          retired = true;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+    if (active) {
+      rec[cur] = (static_cast<u64>(acc) << 32) | sid;
+      acc += 1u + (down(cur) << 16);
+      const u32 nxt = succ[cur];
+      ++steps;
+      const bool bad = (nxt != kNone && nxt >= k) || steps > k;
+      const bool stop = bad || nxt == kNone || lr_is_splitter(nxt, head, seed, mask);
+      if (stop || (acc & 0xFFFFu) == kLrCapStep) {
+        sub_next[sid] = bad ? kNone : nxt;
+        sub_w[sid] = (static_cast<u64>(acc >> 16) << 32) | (acc & 0xFFFFu);
+        if (bad) atomicOr(&counters[LrCounters::kErr], kErrStructure);
+        if (stop) {
+          active = false;
+        } else {
+          const u32 ns = atomicAdd(&counters[LrCounters::kSubTotal0], 1u);
+          if (ns >= sub_cap) {
+            atomicOr(&counters[LrCounters::kErr], kErrCapacity);
+            active = false;
+          } else {
+            sid = ns;
+            acc = 0;
+            cur = nxt;
+          }
+        }
+      } else {
+        cur = nxt;
+      }
+    }
+  }
+}
+
+// ---- level >= 1 walk (explicit u64 weights) ---------------------------------
+__global__ void __launch_bounds__(256)
+    k_lr_walk(const u32* __restrict__ succ, const u64* __restrict__ w,
+              const u32* d_S, const u32* d_head, u32 seed, u32 mask,
+              const u32* __restrict__ spl, const u32* d_nspl, u32* ticket,
+              u32* __restrict__ rec_sid, u64* __restrict__ rec_loc,
+              u32* __restrict__ sub_next, u64* __restrict__ sub_w, u32* err) {
+  const int lane = threadIdx.x & 31;
+  const u32 lt = lanemask_lt();
+  const u32 S = *d_S, head = *d_head, nspl = *d_nspl;
+  bool active = false, retired = false;
+  u32 sid = 0, cur = 0, steps = 0;
+  u64 acc = 0;
+  while (true) {
+    const u32 need = __ballot_sync(0xffffffffu, !active && !retired);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      u32 base = 0;
+      if (lane == leader) base = atomicAdd(ticket, __popc(need));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!active && !retired) {
+        const u32 idx = base + __popc(need & lt);
+        if (idx < nspl) {
+          sid = idx;
+          cur = spl[idx];
+          acc = 0;
+          active = true;
+        } else {
+          retired = true;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+    if (active) {
+      rec_sid[cur] = sid;
+      rec_loc[cur] = acc;
+      acc += w[cur];
+      const u32 nxt = succ[cur];
+      ++steps;
+      const bool bad = (nxt != kNone && nxt >= S) || steps > S;
+      if (bad || nxt == kNone || lr_is_splitter(nxt, head, seed, mask)) {
+        sub_next[sid] = bad ? kNone : nxt;
+        sub_w[sid] = acc;
+        if (bad) atomicOr(err, kErrStructure);
+        active = false;
+      } else {
+        cur = nxt;
+      }
+    }
+  }
+}
+
+// Clamp a device count to a capacity (flags the overflow) so every later
+// kernel indexes within its arrays even for malformed input.
+__global__ void k_lr_clamp(u32* count, u32 cap, u32* err) {
+  if (*count > cap) {
+    *count = cap;
+    atomicOr(err, kErrCapacity);
+  }
+}
+
+// Next-level list: succ'[sid] = sublist of the element after sublist sid.
+// Level-0 records are packed (local<<32 | sid).
+__global__ void k_lr_next_level0(const u64* __restrict__ rec, const u32* __restrict__ sub_next,
+                                 const u64* __restrict__ sub_w, const u32* d_S, u32 head,
+                                 u32* __restrict__ succ2, u64* __restrict__ w2, u32* d_head2) {
+  const u32 S = *d_S;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const u32 ne = sub_next[i];
+    succ2[i] = ne == kNone ? kNone : static_cast<u32>(rec[ne]);
+    w2[i] = sub_w[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_head2 = static_cast<u32>(rec[head]);
+}
+
+__global__ void k_lr_next_level(const u32* __restrict__ rec_sid, const u32* __restrict__ sub_next,
+                                const u64* __restrict__ sub_w, const u32* d_S, const u32* d_head,
+                                u32* __restrict__ succ2, u64* __restrict__ w2, u32* d_head2) {
+  const u32 S = *d_S;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const u32 ne = sub_next[i];
+    succ2[i] = ne == kNone ? kNone : rec_sid[ne];
+    w2[i] = sub_w[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_head2 = rec_sid[*d_head];
+}
+
+// prefix_l[e] = prefix_{l+1}[rec_sid[e]] + rec_loc[e]
+__global__ void k_lr_expand(const u32* __restrict__ rec_sid, const u64* __restrict__ rec_loc,
+                            const u64* __restrict__ pnext, const u32* d_S, const u32* d_Snext,
+                            u64* __restrict__ prefix) {
+  const u32 S = *d_S, Sn = *d_Snext;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    u32 sid = rec_sid[i];
+    if (sid >= Sn) sid = 0;  // unreached element of a malformed list (already flagged)
+    prefix[i] = pnext[sid] + rec_loc[i];
+  }
+}
+
+// Final level: Wyllie pointer jumping in shared memory, one CTA.
+// total_rank_expect: the head chain must have this many level-0 elements.
+__global__ void __launch_bounds__(kLrFinalThreads)
+    k_lr_final(const u32* __restrict__ succ, const u64* __restrict__ w, const u32* d_S,
+               const u32* d_head, u64* __restrict__ prefix, u32 total_rank_expect,
+               u32* err) {
+  extern __shared__ u64 s_dyn[];  // kLrFinalMax u64 values, then u32 links
+  u64* s_val = s_dyn;
+  u32* s_nxt = reinterpret_cast<u32*>(s_dyn + kLrFinalMax);
+  const u32 S = *d_S;
+  if (S > kLrFinalMax) {
+    if (threadIdx.x == 0) atomicOr(err, kErrCapacity);
+    return;
+  }
+  constexpr int kPer = kLrFinalMax / kLrFinalThreads;
+  for (u32 i = threadIdx.x; i < S; i += kLrFinalThreads) {
+    u32 nx = succ[i];
+    if (nx != kNone && nx >= S) {
+      atomicOr(err, kErrStructure);
+      nx = kNone;
+    }
+    s_nxt[i] = nx;
+    s_val[i] = w[i];
+  }
+  __syncthreads();
+  for (int round = 0; round < 15; ++round) {
+    u32 nn[kPer];
+    u64 nv[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const u32 i = threadIdx.x + j * kLrFinalThreads;
+      nn[j] = kNone;
+      nv[j] = 0;
+      if (i < S) {
+        const u32 nx = s_nxt[i];
+        nv[j] = s_val[i];
+        if (nx != kNone) {
+          nv[j] += s_val[nx];
+          nn[j] = s_nxt[nx];
+        }
+      }
+    }
+    __syncthreads();
+    int live = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const u32 i = threadIdx.x + j * kLrFinalThreads;
+      if (i < S) {
+        s_nxt[i] = nn[j];
+        s_val[i] = nv[j];
+        live |= nn[j] != kNone;
+      }
+    }
+    if (!__syncthreads_or(live)) break;
+  }
+  // s_val[i] = inclusive suffix sum; prefix = total - suffix + own weight.
+  const u32 head = *d_head;
+  const u64 total = s_val[head];
+  for (u32 i = threadIdx.x; i < S; i += kLrFinalThreads) {
+    if (s_nxt[i] != kNone) atomicOr(err, kErrStructure);  // cycle
+    prefix[i] = total - s_val[i];
+  }
+  if (threadIdx.x == 0 && static_cast<u32>(total) != total_rank_expect)
+    atomicOr(err, kErrStructure);  // head chain does not cover every element
+}
+
+// ---- orchestration ---------------------------------------------------------
+struct LrLevel {
+  u32 cap = 0;            // capacity of this level's element arrays
+  u32* succ = nullptr;    // level >= 1
+  u64* w = nullptr;       // level >= 1
+  u32* rec_sid = nullptr; // level >= 1
+  u64* rec_loc = nullptr; // level >= 1
+  u64* prefix = nullptr;  // level >= 1
+  u32* spl = nullptr;     // splitters of this level (cap = next level cap)
+  u32* sub_next = nullptr;
+  u64* sub_w = nullptr;
+  u64* scan_status = nullptr;
+};
+
+struct ListRankWs {
+  static constexpr int kMaxLevels = 8;
+  u32 k = 0;
+  int levels = 0;  // number of walk levels (>= 1); final Wyllie after the last
+  LrLevel lv[kMaxLevels + 1];
+  u64* rec0 = nullptr;  // level-0 records, k entries
+  u32* counters = nullptr;
+  u64* prefix1 = nullptr;  // == lv[1].prefix: exclusive prefix per level-0 sublist
+
+  static u32 next_cap(u64 S, u32 L) {
+    double mu = static_cast<double>(S) / L;
+    u64 c = static_cast<u64>(mu + 8.0 * __builtin_sqrt(mu + 1.0) + 1024.0);
+    return static_cast<u32>(c > S + 1 ? S + 1 : c);
+  }
+
+  void carve(Carver& c, u32 k_) {
+    k = k_;
+    rec0 = c.take<u64>(k);
+    counters = c.take<u32>(64);
+    // level 0 caps
+    u32 cap1 = next_cap(k, kLrL0) + k / kLrCapStep + 2;
+    lv[0].cap = k;
+    lv[0].spl = c.take<u32>(cap1);
+    lv[0].sub_next = c.take<u32>(cap1);
+    lv[0].sub_w = c.take<u64>(cap1);
+    lv[0].scan_status = c.take<u64>(scan_ws_words(k));
+    int l = 1;
+    u32 cap = cap1;
+    double expect = static_cast<double>(k) / kLrL0;
+    while (true) {
+      LrLevel& L = lv[l];
+      L.cap = cap;
+      L.succ = c.take<u32>(cap);
+      L.w = c.take<u64>(cap);
+      L.prefix = c.take<u64>(cap);
+      if (expect <= 2048.0 || l == kMaxLevels) break;  // final Wyllie level
+      L.rec_sid = c.take<u32>(cap);
+      L.rec_loc = c.take<u64>(cap);
+      u32 capn = next_cap(cap, kLrL);
+      L.spl = c.take<u32>(capn);
+      L.sub_next = c.take<u32>(capn);
+      L.sub_w = c.take<u64>(capn);
+      L.scan_status = c.take<u64>(scan_ws_words(cap));
+      cap = capn;
+      expect /= kLrL;
+      ++l;
+    }
+    levels = l;  // walk levels 0..l-1, Wyllie on level l
+    prefix1 = lv[1].prefix;
+  }
+};
+
+inline u32 lr_seed(int level) { return 0x65746b5fu ^ (0x9e3779b9u * (level + 1)); }
+
+// Runs the ranking up to the per-sublist prefixes of level 0 (ws.prefix1).
+// Callers finish with their own fused per-element kernel (lr_prefix0).
+// No host synchronisation; errors accumulate in counters[kErr].
+template <class Down>
+void list_rank_core(const u32* succ, u32 k, u32 head, Down down, ListRankWs& ws,
+                    cudaStream_t st, int sms) {
+  CK(cudaMemsetAsync(ws.counters, 0, 64 * sizeof(u32), st));
+  u32* cnt = ws.counters;
+  const u32 mask0 = kLrL0 - 1;
+  const u32 seed0 = lr_seed(0);
+  const u32 cap1 = ws.lv[1].cap;
+  // level 0 splitters -> counters[kNspl]; sublists beyond come from cap splits
+  scan_exclusive(SplIn{head, seed0, mask0},
+                 SplOut{head, seed0, mask0, cap1, ws.lv[0].spl, cnt + LrCounters::kErr}, k,
+                 ws.lv[0].scan_status, cnt + LrCounters::kNspl, st);
+  CK(cudaMemcpyAsync(cnt + LrCounters::kSubTotal0, cnt + LrCounters::kNspl, sizeof(u32),
+                     cudaMemcpyDeviceToDevice, st));
+  const unsigned walk_blocks = sms * 8;  // 2048 threads / SM resident
+  k_lr_walk0<Down><<<walk_blocks, 256, 0, st>>>(succ, k, head, seed0, mask0, ws.lv[0].spl,
+                                                cnt, cap1, ws.rec0, ws.lv[0].sub_next,
+                                                ws.lv[0].sub_w, down);
+  CK_LAUNCH();
+  // level-1 list
+  u32* S1 = cnt + LrCounters::kSubTotal0;
+  k_lr_clamp<<<1, 1, 0, st>>>(S1, cap1, cnt + LrCounters::kErr);
+  u32* head1 = cnt + LrCounters::kLevelBase + 4 * 1 + 2;
+  k_lr_next_level0<<<blocks_for(cap1, 256), 256, 0, st>>>(
+      ws.rec0, ws.lv[0].sub_next, ws.lv[0].sub_w, S1, head, ws.lv[1].succ, ws.lv[1].w, head1);
+  CK_LAUNCH();
+  // deeper levels
+  const u32* S_l = S1;
+  for (int l = 1; l < ws.levels; ++l) {
+    LrLevel& L = ws.lv[l];
+    LrLevel& N = ws.lv[l + 1];
+    u32* tick = cnt + LrCounters::kLevelBase + 4 * l + 0;
+    u32* nspl = cnt + LrCounters::kLevelBase + 4 * l + 1;
+    u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
+    u32* hd_next = cnt + LrCounters::kLevelBase + 4 * (l + 1) + 2;
+    const u32 seed = lr_seed(l), mask = kLrL - 1;
+    scan_exclusive(SplInDev{hd, S_l, seed, mask},
+                   SplOutDev{hd, S_l, seed, mask, N.cap, L.spl, cnt + LrCounters::kErr}, L.cap,
+                   L.scan_status, nspl, st);
+    k_lr_clamp<<<1, 1, 0, st>>>(nspl, N.cap, cnt + LrCounters::kErr);
+    k_lr_walk<<<walk_blocks, 256, 0, st>>>(L.succ, L.w, S_l, hd, seed, mask, L.spl, nspl, tick,
+                                          L.rec_sid, L.rec_loc, L.sub_next, L.sub_w,
+                                          cnt + LrCounters::kErr);
+    CK_LAUNCH();
+    k_lr_next_level<<<blocks_for(N.cap, 256), 256, 0, st>>>(L.rec_sid, L.sub_next, L.sub_w, nspl,
+                                                            hd, N.succ, N.w, hd_next);
+    CK_LAUNCH();
+    S_l = nspl;
+  }
+  // final level
+  {
+    const int l = ws.levels;
+    LrLevel& F = ws.lv[l];
+    const u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
+    static bool attr_set = false;  // per process; same value for every device
+    if (!attr_set) {
+      CK(cudaFuncSetAttribute(k_lr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kLrFinalSmem));
+      attr_set = true;
+    }
+    k_lr_final<<<1, kLrFinalThreads, kLrFinalSmem, st>>>(F.succ, F.w, S_l, hd, F.prefix, k,
+                                              cnt + LrCounters::kErr);
+    CK_LAUNCH();
+  }
+  // expand back down to level 1
+  for (int l = ws.levels - 1; l >= 1; --l) {
+    LrLevel& L = ws.lv[l];
+    const u32* S = (l == 1) ? (cnt + LrCounters::kSubTotal0)
+                            : (cnt + LrCounters::kLevelBase + 4 * (l - 1) + 1);
+    const u32* Sn = cnt + LrCounters::kLevelBase + 4 * l + 1;
+    k_lr_expand<<<blocks_for(L.cap, 256), 256, 0, st>>>(L.rec_sid, L.rec_loc, ws.lv[l + 1].prefix,
+                                                        S, Sn, L.prefix);
+    CK_LAUNCH();
+  }
+}
+
+// Level-0 element prefix: (rank, down-weight sum) of everything before e.
+// Records of elements no walker reached are stale; the sublist id is
+// clamped so a malformed input can never index out of bounds (the ranking
+// has already flagged kErrStructure in that case).
+struct Lr0View {
+  const u64* rec0;
+  const u64* prefix1;
+  const u32* d_S1;  // number of level-0 sublists (device)
+  __device__ __forceinline__ void get(u32 e, u32 S1, u32& rank, u32& dsum) const {
+    const u64 r = rec0[e];
+    u32 sid = static_cast<u32>(r);
+    if (sid >= S1) sid = 0;
+    const u64 p = prefix1[sid];
+    const u32 loc = static_cast<u32>(r >> 32);
+    rank = static_cast<u32>(p) + (loc & 0xFFFFu);
+    dsum = static_cast<u32>(p >> 32) + (loc >> 16);
+  }
+};
+
+inline Lr0View lr0_view(const ListRankWs& ws) {
+  return Lr0View{ws.rec0, ws.prefix1, ws.counters + LrCounters::kSubTotal0};
+}
+
+__global__ void k_lr_rank_out(Lr0View v, u32 k, u32* __restrict__ rank) {
+  const u32 S1 = *v.d_S1;
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    u32 r, d;
+    v.get(e, S1, r, d);
+    rank[e] = r;
+  }
+}
+
+}  // namespace
+}  // namespace ettg

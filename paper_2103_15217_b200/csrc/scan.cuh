@@ -1,0 +1,163 @@
+// Single-pass exclusive +scan with decoupled look-back (Merrill & Garland).
+//
+// Replaces ett::exclusive_scan (core/include/ett/primitives.hpp:29-66), whose
+// CPU version is a chunked two-pass scan with a sequential carry.  Here one
+// kernel reads every element once and writes it once: a 4096-item tile per
+// 256-thread CTA (16 items/thread), warp-shuffle scans inside the tile, and a
+// windowed 32-tile look-back by warp 0 over per-tile status words.  Tiles are
+// numbered by an atomic ticket so every predecessor is already resident
+// (forward progress without cooperative launch).
+//
+// In  : functor  u32 operator()(u64 i) const          (called for i < n)
+// Out : functor  void operator()(u64 i, u32 excl) const
+#pragma once
+
+#include "common.cuh"
+
+namespace ettg {
+namespace {  // kernels defined in headers: internal linkage per TU
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr u32 kScanTile = kScanThreads * kScanItems;  // 4096
+
+constexpr u64 kFlagAgg = 1ull << 62;
+constexpr u64 kFlagInc = 2ull << 62;
+constexpr u64 kFlagMask = 3ull << 62;
+
+struct ArrayIn {
+  const u32* p;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return p[i]; }
+};
+struct ArrayOut {
+  u32* p;
+  __device__ __forceinline__ void operator()(u64 i, u32 v) const { p[i] = v; }
+};
+
+__device__ __forceinline__ u32 warp_incl_scan(u32 v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    u32 t = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+
+__device__ __forceinline__ u32 warp_sum(u32 v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Look-back by warp 0: returns the exclusive prefix of `tile` (all lanes).
+__device__ __forceinline__ u32 tile_lookback(u64* status, u32 tile, u32 agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(&status[0], kFlagInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagAgg | agg);
+  u32 prefix = 0;
+  long long end = static_cast<long long>(tile) - 1;
+  while (true) {
+    long long i = end - lane;
+    u64 s = kFlagInc;  // before tile 0: an inclusive zero
+    if (i >= 0) {
+      do {
+        s = ld_acquire(&status[i]);
+      } while ((s & kFlagMask) == 0);
+    }
+    u32 inc = __ballot_sync(0xffffffffu, (s & kFlagMask) == kFlagInc);
+    u32 val = static_cast<u32>(s);
+    if (inc) {
+      int first = __ffs(inc) - 1;
+      prefix += warp_sum(lane <= first ? val : 0u);
+      break;
+    }
+    prefix += warp_sum(val);
+    end -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagInc | (prefix + agg));
+  return prefix;
+}
+
+template <class In, class Out>
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_dlb(In in, Out out, u64 n, u64* status, u32* ticket, u32* total) {
+  constexpr int kPad = kScanTile + kScanTile / 32;
+  __shared__ u32 s_vals[kPad];
+  __shared__ u32 s_warp[kScanThreads / 32];
+  __shared__ u32 s_tile, s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u64 base = static_cast<u64>(tile) * kScanTile;
+
+  // Striped (coalesced) load -> smem -> blocked registers.
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    u32 idx = j * kScanThreads + tid;
+    u64 gi = base + idx;
+    s_vals[idx + (idx >> 5)] = gi < n ? in(gi) : 0u;
+  }
+  __syncthreads();
+  u32 v[kScanItems];
+  u32 run = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    u32 idx = tid * kScanItems + j;
+    v[j] = run;
+    run += s_vals[idx + (idx >> 5)];
+  }
+  u32 incl = warp_incl_scan(run);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u32 w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    u32 wi = warp_incl_scan(w);
+    u32 agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    u32 pre = tile_lookback(status, tile, agg);
+    if (lane == 0) {
+      s_prefix = pre;
+      if (total && base + kScanTile >= n) *total = pre + agg;
+    }
+  }
+  __syncthreads();
+  const u32 off = s_prefix + s_warp[warp] + (incl - run);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    u32 idx = tid * kScanItems + j;
+    s_vals[idx + (idx >> 5)] = off + v[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    u32 idx = j * kScanThreads + tid;
+    u64 gi = base + idx;
+    if (gi < n) out(gi, s_vals[idx + (idx >> 5)]);
+  }
+}
+
+inline size_t scan_ws_words(u64 n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+// status must hold scan_ws_words(n) u64 words (last one doubles as ticket).
+template <class In, class Out>
+void scan_exclusive(In in, Out out, u64 n, u64* status, u32* total,
+                    cudaStream_t st) {
+  if (n == 0) {
+    if (total) CK(cudaMemsetAsync(total, 0, sizeof(u32), st));
+    return;
+  }
+  const u64 tiles = (n + kScanTile - 1) / kScanTile;
+  CK(cudaMemsetAsync(status, 0, (tiles + 1) * sizeof(u64), st));
+  u32* ticket = reinterpret_cast<u32*>(status + tiles);
+  k_scan_dlb<In, Out><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(
+      in, out, n, status, ticket, total);
+  CK_LAUNCH();
+}
+
+}  // namespace
+}  // namespace ettg

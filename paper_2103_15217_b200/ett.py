@@ -1,0 +1,317 @@
+"""Host-side mirror of the reference's ``ett`` namespace for the hot path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/core/include/ett/{graph,lca,bridges,primitives,generators}.hpp,
+backed by the sm_100a kernels in ``libettg.so`` through the C-ABI
+(include/ettg.h).  Arrays are numpy int64 (the reference's i64); device
+variants take torch CUDA tensors.
+
+Exceptions: ``InvalidArgument`` (a ``ValueError``) where the reference
+throws ``std::invalid_argument``; ``OutOfRange`` (an ``IndexError``) for
+``std::out_of_range``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import ENGINE_INLABEL, ENGINE_RMQ, InvalidArgument, OutOfRange, check, lib, ptr
+
+K_NONE = -1
+K_GRASP_INFINITY = (1 << 64) - 1
+
+
+# --------------------------------------------------------------- data model
+@dataclass
+class RootedTree:
+    """core/include/ett/graph.hpp:66-70 -- parent[root] == kNone (-1)."""
+    n: int
+    root: int
+    parent: np.ndarray  # int64[n]
+
+    def __post_init__(self):
+        self.parent = np.ascontiguousarray(self.parent, dtype=np.int64)
+
+
+@dataclass
+class EdgeList:
+    """core/include/ett/graph.hpp:18-23 -- undirected simple graph."""
+    n: int
+    edges: np.ndarray  # int64[m, 2]
+
+    def __post_init__(self):
+        self.edges = np.ascontiguousarray(np.asarray(self.edges, dtype=np.int64).reshape(-1, 2))
+
+    def m(self) -> int:
+        return int(self.edges.shape[0])
+
+
+@dataclass
+class NodeStats:
+    """core/include/ett/euler.hpp:45-53 (preorder is 1-based)."""
+    preorder: np.ndarray
+    size: np.ndarray
+    level: np.ndarray
+    parent: np.ndarray
+
+
+@dataclass
+class BridgeMask:
+    """core/include/ett/bridges.hpp:20-24."""
+    is_bridge: np.ndarray  # uint8[m]
+    phases: dict = field(default_factory=dict)
+
+    def count(self) -> int:
+        return int(self.is_bridge.sum())
+
+
+# -------------------------------------------------------------- LCA indices
+class _LcaHandle:
+    """Owns an ``ettg_lca*``; device memory lives on ``device``."""
+
+    def __init__(self, handle: int, n: int, device: int, engines: int):
+        self._h = C.c_void_p(handle)
+        self.n = n
+        self.device = device
+        self.engines = engines
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().ettg_lca_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def build_ms(self) -> float:
+        v = C.c_double()
+        check(lib().ettg_lca_build_ms(self._h, C.byref(v)))
+        return v.value
+
+    def stats(self) -> NodeStats:
+        n = self.n
+        a = [np.empty(n, np.int64) for _ in range(4)]
+        check(lib().ettg_lca_stats(self._h, *[ptr(x) for x in a]))
+        return NodeStats(*a)
+
+    def query(self, queries, batch_size: int, engine: int) -> np.ndarray:
+        q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64).reshape(-1, 2))
+        out = np.empty(q.shape[0], np.int64)
+        check(lib().ettg_lca_query_engine(self._h, engine, ptr(q), q.shape[0], int(batch_size),
+                                          ptr(out)))
+        return out
+
+    def query_dev(self, d_pairs, d_answers, engine: int, stream: int | None = None) -> None:
+        """Device-resident batch: uint32/int32 torch tensors (2q) -> (q)."""
+        q = d_answers.numel()
+        check(lib().ettg_lca_query_dev(self._h, engine, ptr(d_pairs), q, ptr(d_answers),
+                                       stream))
+
+    def index_bytes(self) -> int:
+        v = C.c_int64()
+        check(lib().ettg_lca_index_bytes(self._h, C.byref(v)))
+        return v.value
+
+    def export_index(self, d_dst, stream: int | None = None) -> None:
+        check(lib().ettg_lca_index_export_dev(self._h, ptr(d_dst), stream))
+
+
+class InlabelIndex(_LcaHandle):
+    """core/include/ett/lca.hpp:13-24; fields are exported on first access."""
+
+    _fields = None
+
+    def _export(self):
+        if self._fields is None:
+            n = self.n
+            inl = np.empty(n, np.int64)
+            asc = np.empty(n, np.uint64)
+            head = np.empty(n + 1, np.int64)
+            lev = np.empty(n, np.int64)
+            par = np.empty(n, np.int64)
+            check(lib().ettg_lca_inlabel_index(self._h, ptr(inl), ptr(asc), ptr(head), ptr(lev),
+                                               ptr(par)))
+            self._fields = (inl, asc, head, lev, par)
+        return self._fields
+
+    inlabel = property(lambda s: s._export()[0])
+    ascendant = property(lambda s: s._export()[1])
+    head = property(lambda s: s._export()[2])
+    level = property(lambda s: s._export()[3])
+    parent = property(lambda s: s._export()[4])
+
+
+class RmqLcaIndex(_LcaHandle):
+    """core/include/ett/lca.hpp:39-44 (block-sparse table on the device)."""
+
+
+def _build(tree: RootedTree, engines: int, device: int):
+    h = C.c_void_p()
+    check(lib().ettg_lca_build(ptr(tree.parent), int(tree.n), int(tree.root), device, engines,
+                               C.byref(h)))
+    return h.value
+
+
+def inlabel_build(tree: RootedTree, device: int = 0, engines: int = ENGINE_INLABEL) -> InlabelIndex:
+    """inlabel_build (core/src/lca.cpp:20)."""
+    if len(tree.parent) != tree.n:
+        raise InvalidArgument("parent array size mismatch")
+    return InlabelIndex(_build(tree, engines, device), tree.n, device, engines)
+
+
+def rmq_lca_build(tree: RootedTree, device: int = 0) -> RmqLcaIndex:
+    """rmq_lca_build (core/src/lca.cpp:128)."""
+    if len(tree.parent) != tree.n:
+        raise InvalidArgument("parent array size mismatch")
+    return RmqLcaIndex(_build(tree, ENGINE_RMQ, device), tree.n, device, ENGINE_RMQ)
+
+
+def attach_index(d_src, n: int, device: int = 0, stream: int | None = None) -> InlabelIndex:
+    """Query-only replica of a packed inlabel index (multi-GPU)."""
+    h = C.c_void_p()
+    check(lib().ettg_lca_index_attach_dev(ptr(d_src), int(n), device, stream, C.byref(h)))
+    return InlabelIndex(h.value, n, device, ENGINE_INLABEL)
+
+
+def answer_batch(index: _LcaHandle, queries, batch_size: int) -> np.ndarray:
+    """answer_batch (core/include/ett/lca.hpp:50-65) for the index's engine."""
+    engine = ENGINE_RMQ if isinstance(index, RmqLcaIndex) else ENGINE_INLABEL
+    return index.query(queries, batch_size, engine)
+
+
+def inlabel_lca(index: InlabelIndex, x: int, y: int) -> int:
+    return int(index.query(np.array([[x, y]], np.int64), 1, ENGINE_INLABEL)[0])
+
+
+def rmq_lca(index: RmqLcaIndex, x: int, y: int) -> int:
+    return int(index.query(np.array([[x, y]], np.int64), 1, ENGINE_RMQ)[0])
+
+
+def node_stats(tree: RootedTree, device: int = 0) -> NodeStats:
+    """node_stats(linearize(build_half_edges(tree_edges(t)), root)) (core/src/euler.cpp)."""
+    return inlabel_build(tree, device).stats()
+
+
+# ------------------------------------------------------------------ bridges
+def tv_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """tv_bridges (core/src/bridges.cpp:311-316); times gets spanning/euler/lowhigh ms."""
+    e = g.edges
+    mask = np.zeros(g.m(), np.uint8)
+    pt = _lib.PhaseTimes()
+    check(lib().ettg_bridges(ptr(e), int(g.n), g.m(), device, ptr(mask), C.byref(pt)))
+    phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "lowhigh": pt.lowhigh_ms,
+              "total": pt.total_ms}
+    if times is not None:
+        times.update(phases)
+    return BridgeMask(mask, phases)
+
+
+# --------------------------------------------------------------- primitives
+def _torch():
+    import torch
+    return torch
+
+
+def list_rank(succ, head: int, device: int = 0) -> np.ndarray:
+    """list_rank (core/src/primitives.cpp:145); succ uses -1 as the tail."""
+    torch = _torch()
+    s = np.asarray(succ, dtype=np.int64)
+    if len(s) == 0:
+        return np.zeros(0, np.int64)
+    if head < 0 or head >= len(s):
+        raise InvalidArgument("list head out of range")
+    d = torch.from_numpy(s.astype(np.uint32)).to(f"cuda:{device}")
+    r = torch.empty_like(d)
+    check(lib().ettg_list_rank_dev(ptr(d), len(s), int(head), ptr(r), device,
+                                   torch.cuda.current_stream(device).cuda_stream))
+    return r.cpu().numpy().astype(np.int64)
+
+
+def exclusive_scan(values, device: int = 0) -> np.ndarray:
+    """exclusive_scan(values, +, 0) over uint32 (core/include/ett/primitives.hpp:29)."""
+    torch = _torch()
+    v = np.asarray(values, dtype=np.uint32)
+    if len(v) == 0:
+        return np.zeros(0, np.int64)
+    d = torch.from_numpy(v).to(f"cuda:{device}")
+    out = torch.empty_like(d)
+    check(lib().ettg_exclusive_scan_dev(ptr(d), len(v), ptr(out), device,
+                                        torch.cuda.current_stream(device).cuda_stream))
+    return out.cpu().numpy().astype(np.int64)
+
+
+def sort_pairs(keys, vals, device: int = 0):
+    torch = _torch()
+    k = torch.from_numpy(np.asarray(keys, dtype=np.uint32)).to(f"cuda:{device}")
+    v = torch.from_numpy(np.asarray(vals, dtype=np.uint32)).to(f"cuda:{device}")
+    ko, vo = torch.empty_like(k), torch.empty_like(v)
+    check(lib().ettg_sort_pairs_dev(ptr(k), ptr(v), k.numel(), ptr(ko), ptr(vo), device,
+                                    torch.cuda.current_stream(device).cuda_stream))
+    return ko.cpu().numpy(), vo.cpu().numpy()
+
+
+# --------------------------------------------------------------- generators
+def grasp_tree(n: int, gamma: int = K_GRASP_INFINITY, seed: int = 0) -> RootedTree:
+    par = np.empty(n, np.int64)
+    check(lib().ettg_gen_grasp_tree(n, gamma & ((1 << 64) - 1), seed, ptr(par)), gen=True)
+    return RootedTree(n, 0, par)
+
+
+def barabasi_tree(n: int, seed: int) -> RootedTree:
+    par = np.empty(n, np.int64)
+    check(lib().ettg_gen_barabasi_tree(n, seed, ptr(par)), gen=True)
+    return RootedTree(n, 0, par)
+
+
+def permute_labels(t: RootedTree, seed: int) -> RootedTree:
+    out = np.empty(t.n, np.int64)
+    root = C.c_int64()
+    check(lib().ettg_gen_permute_labels(t.n, ptr(t.parent), t.root, seed, ptr(out),
+                                        C.byref(root)), gen=True)
+    return RootedTree(t.n, root.value, out)
+
+
+def sample_queries(n: int, q: int, seed: int) -> np.ndarray:
+    out = np.empty((q, 2), np.int64)
+    check(lib().ettg_gen_sample_queries(n, q, seed, ptr(out)), gen=True)
+    return out
+
+
+def random_connected_graph(n: int, m: int, seed: int) -> EdgeList:
+    out = np.empty((m, 2), np.int64)
+    check(lib().ettg_gen_random_connected_graph(n, m, seed, ptr(out)), gen=True)
+    return EdgeList(n, out)
+
+
+def planted_bridge_graph(n: int, m: int, b: int, seed: int):
+    """(EdgeList, truth mask) with exactly b bridges."""
+    out = np.empty((m, 2), np.int64)
+    truth = np.empty(m, np.uint8)
+    check(lib().ettg_gen_planted_bridge_graph(n, m, b, seed, ptr(out), ptr(truth)), gen=True)
+    return EdgeList(n, out), truth
+
+
+def road_like_graph(W: int, H: int, extra: int, r: int, pendant: int, seed: int):
+    """(EdgeList, truth mask): lattice + chords within radius r + pendant bridges."""
+    m = lib().ettg_road_like_edge_count(W, H, extra, r, pendant)
+    if m < 0:
+        raise InvalidArgument("road_like_graph: bad shape")
+    out = np.empty((m, 2), np.int64)
+    truth = np.empty(m, np.uint8)
+    check(lib().ettg_gen_road_like_graph(W, H, extra, r, pendant, seed, ptr(out), ptr(truth)),
+          gen=True)
+    return EdgeList(W * H + pendant, out), truth
+
+
+def gen_queries_dev(n: int, q: int, seed: int, offset: int, d_pairs, device: int = 0,
+                    stream: int | None = None) -> bool:
+    """Counter-mode sample_queries into a uint32 device tensor; False on rejection."""
+    rej = C.c_int()
+    check(lib().ettg_gen_queries_dev(n, q, seed, offset, ptr(d_pairs), C.byref(rej), device,
+                                     stream))
+    return rej.value == 0

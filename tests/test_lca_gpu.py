@@ -1,0 +1,185 @@
+"""LCA parity on the B200: CUDA path (through the C-ABI) vs the CPU oracle.
+
+Bit-exact on everything: answers, and (because the GPU reproduces the DCEL
+child order) every intermediate the reference exposes -- node_stats and the
+InlabelIndex fields.
+"""
+import numpy as np
+import pytest
+
+from util import GRASP_INF, lca_corpus
+
+pytestmark = pytest.mark.gpu
+
+EXAMPLE = np.array([-1, 2, 0, 0, 0, 2], np.int64)  # tests/lca_test.cpp:47-57
+
+
+def test_golden_example_tree(ett):
+    t = ett.RootedTree(6, 0, EXAMPLE)
+    idx = ett.inlabel_build(t)
+    st = idx.stats()
+    # tests/euler_test.cpp:130-139
+    assert st.preorder.tolist() == [1, 3, 2, 5, 6, 4]
+    assert st.level.tolist() == [0, 2, 1, 1, 1, 2]
+    assert st.size[2] == 3 and st.size[0] == 6
+    assert st.parent.tolist() == [-1, 2, 0, 0, 0, 2]
+    # tests/lca_test.cpp:47-74
+    assert idx.inlabel.tolist() == [4, 3, 4, 5, 6, 4]
+    assert idx.head[4] == 0
+    assert ett.inlabel_lca(idx, 1, 5) == 2
+    assert ett.inlabel_lca(idx, 3, 4) == 0
+    for v in range(6):
+        assert ett.inlabel_lca(idx, v, v) == v
+        assert ett.inlabel_lca(idx, 0, v) == 0
+        assert ett.inlabel_lca(idx, v, 0) == 0
+    r = ett.rmq_lca_build(t)
+    assert ett.rmq_lca(r, 1, 5) == 2
+    assert ett.rmq_lca(r, 3, 3) == 3
+
+
+def test_single_node(ett):
+    idx = ett.inlabel_build(ett.RootedTree(1, 0, [-1]))
+    assert idx.inlabel.tolist() == [1]
+    assert idx.ascendant.tolist() == [1]
+    assert ett.inlabel_lca(idx, 0, 0) == 0
+    st = idx.stats()
+    assert st.preorder.tolist() == [1] and st.size.tolist() == [1] and st.level.tolist() == [0]
+
+
+def test_corpus_bit_exact_vs_reference(ett, ref):
+    """acceptance criterion 2 + intermediate parity on 200 corpus trees."""
+    pairs_total = 0
+    for ti, t in enumerate(lca_corpus(ett)):
+        idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.ENGINE_RMQ)
+        pre, size, lev, par = ref.node_stats(t.parent, t.root)
+        st = idx.stats()
+        assert np.array_equal(st.preorder, pre), ti
+        assert np.array_equal(st.size, size), ti
+        assert np.array_equal(st.level, lev), ti
+        assert np.array_equal(st.parent, par), ti
+        inl, asc, head, lev2, par2 = ref.inlabel_index(t.parent, t.root)
+        assert np.array_equal(idx.inlabel, inl), ti
+        assert np.array_equal(idx.ascendant, asc), ti
+        assert np.array_equal(idx.head, head), ti
+        if t.n <= 128:
+            xs, ys = np.meshgrid(np.arange(t.n), np.arange(t.n), indexing="ij")
+            q = np.stack([xs.ravel(), ys.ravel()], 1).astype(np.int64)
+        else:
+            q = ett.sample_queries(t.n, 10_000, t.n)
+        want = ref.lca("inlabel", t.parent, t.root, q)
+        assert np.array_equal(idx.query(q, len(q), ett.ENGINE_INLABEL), want), ti
+        assert np.array_equal(idx.query(q, len(q), ett.ENGINE_RMQ), want), ti
+        pairs_total += len(q)
+    assert pairs_total > 1_000_000
+
+
+@pytest.mark.parametrize("gamma", [1, 2, 64, GRASP_INF])
+def test_medium_trees_vs_reference(ett, ref, gamma):
+    t = ett.permute_labels(ett.grasp_tree(200_003, gamma, 11), 12)
+    q = ett.sample_queries(t.n, 100_000, 13)
+    idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.ENGINE_RMQ)
+    want = ref.lca("rmq", t.parent, t.root, q)
+    assert np.array_equal(ett.answer_batch(idx, q, 4096), want)
+    assert np.array_equal(idx.query(q, len(q), ett.ENGINE_RMQ), want)
+    pre, size, lev, par = ref.node_stats(t.parent, t.root)
+    st = idx.stats()
+    assert np.array_equal(st.preorder, pre) and np.array_equal(st.size, size)
+    assert np.array_equal(st.level, lev) and np.array_equal(st.parent, par)
+
+
+def test_config_a_full_size(ett, ref):
+    """BASELINE config A at full size: 1M-node grasp(inf) tree, 1M queries."""
+    t = ett.permute_labels(ett.grasp_tree(1_000_000, GRASP_INF, 1), 2)
+    q = ett.sample_queries(t.n, 1_000_000, 3)
+    idx = ett.inlabel_build(t)
+    got = ett.answer_batch(idx, q, 1_000_000)
+    want = ref.lca("inlabel", t.parent, t.root, q)
+    assert np.array_equal(got, want)
+    inl, asc, head, lev, par = ref.inlabel_index(t.parent, t.root)
+    assert np.array_equal(idx.inlabel, inl) and np.array_equal(idx.ascendant, asc)
+
+
+def test_barabasi_and_star(ett, ref):
+    for t in [ett.permute_labels(ett.barabasi_tree(300_000, 31), 32),
+              ett.RootedTree(100_000, 7, np.where(np.arange(100_000) == 7, -1, 7))]:
+        q = ett.sample_queries(t.n, 50_000, 5)
+        idx = ett.inlabel_build(t, engines=3)
+        want = ref.lca("inlabel", t.parent, t.root, q)
+        assert np.array_equal(idx.query(q, len(q), 1), want)
+        assert np.array_equal(idx.query(q, len(q), 2), want)
+        inl, asc, head, lev, par = ref.inlabel_index(t.parent, t.root)
+        assert np.array_equal(idx.inlabel, inl)
+
+
+def test_batch_size_invariance_and_errors(ett):
+    t = ett.permute_labels(ett.grasp_tree(300, GRASP_INF, 8), 9)
+    idx = ett.inlabel_build(t)
+    q = ett.sample_queries(t.n, 500, 17)
+    base = ett.answer_batch(idx, q, 1)
+    for b in (7, 500, 10_000):
+        assert np.array_equal(base, ett.answer_batch(idx, q, b))
+    with pytest.raises(ett.InvalidArgument):
+        ett.answer_batch(idx, q, 0)
+    with pytest.raises(ett.OutOfRange):
+        ett.answer_batch(idx, np.array([[0, 300]]), 1)
+    assert len(ett.answer_batch(idx, np.zeros((0, 2), np.int64), 1)) == 0
+
+
+@pytest.mark.parametrize("parent,root,msg", [
+    ([-1, 0, 5], 0, "out of range"),        # parent id out of range
+    ([-1, -1, 0], 0, "exactly one root"),   # two roots
+    ([1, -1, 0], 0, "kNone"),               # root has a parent
+    ([-1, 2, 1], 0, "cycle"),               # 1 <-> 2 cycle off the root
+    ([-1, 1, 0, 3], 0, "cycle"),            # self loop
+])
+def test_invalid_trees(ett, parent, root, msg):
+    with pytest.raises(ett.InvalidArgument, match=msg):
+        ett.inlabel_build(ett.RootedTree(len(parent), root, np.array(parent)))
+
+
+def test_large_cycle_detected(ett):
+    n = 100_000
+    par = np.arange(-1, n - 1, dtype=np.int64)  # path 0 <- 1 <- 2 ...
+    par[50_000] = 99_999                        # detach the tail into a cycle
+    with pytest.raises(ett.InvalidArgument, match="cycle"):
+        ett.inlabel_build(ett.RootedTree(n, 0, par))
+
+
+def test_deep_path_2m(ett, ref):
+    """Config B shape (path, depth n-1) at 2M nodes vs the reference."""
+    t = ett.permute_labels(ett.grasp_tree(2_000_000, 1, 1), 2)
+    q = ett.sample_queries(t.n, 500_000, 3)
+    idx = ett.inlabel_build(t)
+    want = ref.lca("inlabel", t.parent, t.root, q)
+    assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
+
+
+def test_replica_attach_matches(ett):
+    import torch
+    t = ett.permute_labels(ett.grasp_tree(100_000, GRASP_INF, 4), 5)
+    q = ett.sample_queries(t.n, 50_000, 6)
+    idx = ett.inlabel_build(t)
+    buf = torch.empty(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")
+    idx.export_index(buf)
+    torch.cuda.synchronize()
+    rep = ett.attach_index(buf, t.n)
+    assert np.array_equal(ett.answer_batch(rep, q, len(q)), ett.answer_batch(idx, q, len(q)))
+
+
+def test_device_query_and_counter_mode_generator(ett, ref):
+    import torch
+    t = ett.permute_labels(ett.grasp_tree(1 << 20, GRASP_INF, 1), 2)
+    idx = ett.inlabel_build(t)
+    q = 300_001
+    d = torch.empty(2 * q, dtype=torch.int32, device="cuda:0")
+    assert ett.gen_queries_dev(t.n, q, 3, 0, d)
+    host = ett.sample_queries(t.n, q, 3)
+    assert np.array_equal(d.cpu().numpy().astype(np.int64).reshape(-1, 2), host)
+    ans = torch.empty(q, dtype=torch.int32, device="cuda:0")
+    idx.query_dev(d, ans, ett.ENGINE_INLABEL)
+    want = ref.lca("inlabel", t.parent, t.root, host)
+    assert np.array_equal(ans.cpu().numpy().astype(np.int64), want)
+    # an offset window replays the same stream
+    d2 = torch.empty(2 * 1000, dtype=torch.int32, device="cuda:0")
+    assert ett.gen_queries_dev(t.n, 1000, 3, 5000, d2)
+    assert np.array_equal(d2.cpu().numpy().astype(np.int64).reshape(-1, 2), host[5000:6000])
