@@ -213,3 +213,107 @@ class RefInlabel:
         if getattr(self, "h", None):
             ref().ref_inlabel_free(C.c_void_p(self.h))
             self.h = None
+
+
+# ------------------------------------------------------------ C restatement
+class Port:
+    """The plain-C restatement (oracle/ettg_oracle.c)."""
+
+    @staticmethod
+    def _call(fn, *args):
+        _rc(port(), getattr(port(), fn)(*args), "orc_last_error")
+
+    @staticmethod
+    def validate_tree(parent, root):
+        parent = np.ascontiguousarray(parent, np.int64)
+        Port._call("orc_validate_tree", i64(len(parent)), _p(parent), i64(root))
+
+    @staticmethod
+    def list_rank(succ, head):
+        succ = np.ascontiguousarray(succ, np.int64)
+        out = np.empty(len(succ), np.int64)
+        Port._call("orc_list_rank", i64(len(succ)), _p(succ), i64(head), _p(out))
+        return out
+
+    @staticmethod
+    def exclusive_scan(v):
+        v = np.ascontiguousarray(v, np.int64)
+        out = np.empty(len(v), np.int64)
+        Port._call("orc_exclusive_scan", i64(len(v)), _p(v), _p(out))
+        return out
+
+    @staticmethod
+    def euler_tour(parent, root):
+        parent = np.ascontiguousarray(parent, np.int64)
+        k = 2 * (len(parent) - 1)
+        s = np.empty(max(k, 1), np.int64)
+        d = np.empty(max(k, 1), np.int64)
+        Port._call("orc_euler_tour", i64(len(parent)), _p(parent), i64(root), _p(s), _p(d))
+        return s[:k], d[:k]
+
+    @staticmethod
+    def node_stats(parent, root):
+        parent = np.ascontiguousarray(parent, np.int64)
+        n = len(parent)
+        a = [np.empty(n, np.int64) for _ in range(4)]
+        Port._call("orc_node_stats", i64(n), _p(parent), i64(root), *[_p(x) for x in a])
+        return a
+
+    @staticmethod
+    def inlabel_index(parent, root):
+        parent = np.ascontiguousarray(parent, np.int64)
+        n = len(parent)
+        inl = np.empty(n, np.int64)
+        asc = np.empty(n, np.uint64)
+        head = np.empty(n + 1, np.int64)
+        lev = np.empty(n, np.int64)
+        par = np.empty(n, np.int64)
+        Port._call("orc_inlabel_index", i64(n), _p(parent), i64(root), _p(inl), _p(asc),
+                   _p(head), _p(lev), _p(par))
+        return inl, asc, head, lev, par
+
+    @staticmethod
+    def inlabel_query(index, pairs):
+        inl, asc, head, lev, par = index
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        out = np.empty(pairs.shape[0], np.int64)
+        lifts = C.c_int64()
+        Port._call("orc_inlabel_query", i64(len(inl)), _p(inl), _p(asc), _p(head), _p(lev),
+                   _p(par), _p(pairs), i64(pairs.shape[0]), _p(out), C.byref(lifts))
+        return out, lifts.value
+
+    @staticmethod
+    def lca_inlabel(parent, root, pairs):
+        parent = np.ascontiguousarray(parent, np.int64)
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        out = np.empty(pairs.shape[0], np.int64)
+        Port._call("orc_lca_inlabel", i64(len(parent)), _p(parent), i64(root), _p(pairs),
+                   i64(pairs.shape[0]), _p(out))
+        return out
+
+    @staticmethod
+    def lca_rmq(parent, root, pairs):
+        parent = np.ascontiguousarray(parent, np.int64)
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        out = np.empty(pairs.shape[0], np.int64)
+        Port._call("orc_lca_rmq", i64(len(parent)), _p(parent), i64(root), _p(pairs),
+                   i64(pairs.shape[0]), _p(out))
+        return out
+
+    @staticmethod
+    def lca_walk_up(parent, pairs):
+        parent = np.ascontiguousarray(parent, np.int64)
+        pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+        out = np.empty(pairs.shape[0], np.int64)
+        Port._call("orc_lca_walk_up", i64(len(parent)), _p(parent), _p(pairs),
+                   i64(pairs.shape[0]), _p(out))
+        return out
+
+    @staticmethod
+    def bridges(engine, n, edges):
+        edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+        m = edges.shape[0]
+        mask = np.empty(m, np.uint8)
+        fn = {"tv": "orc_tv_bridges", "dfs": "orc_dfs_bridges"}[engine]
+        Port._call(fn, i64(n), i64(m), _p(edges), _p(mask))
+        return mask
