@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark: LCA queries/s (1/2/4/8 B200) and bridges edges/s with HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Headline workload (BASELINE.json configs[1], "LCA: deep path-like tree
+n=16M (depth ~n), 16M queries, 1 vs 8 GPUs"): permute_labels(grasp_tree(16M,
+gamma=1, seed 1), seed 2); 16M sample_queries (seed 3) split into N
+contiguous shards (strong scaling).  Rank 0 builds the inlabel index on its
+GPU, NCCL broadcasts the packed index, every rank answers its shard.  One
+step = one batched query kernel over the rank's shard with pairs already in
+HBM; L2 is flushed (256 MiB write) before every step and the flush is outside
+the CUDA-event interval.
+
+Also reported (same JSON line): config E (16M grasp(inf) tree, 1G queries
+sharded), the index build time, and at N=1 the bridges config D (road-like
+graph) with its own roofline and CPU baseline.  `e2e` goes through the
+public C-ABI (`ettg_lca_query`) with pinned int64 host buffers.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LCA queries/s (1/2/4/8 B200) and bridges edges/s, with HBM roofline fraction"
+GRASP_INF = (1 << 64) - 1
+L2_FLUSH_BYTES = 256 << 20
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """pynvml sampling of SM clock + clock-event reasons during a region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max,
+                "samples": len(self.samples),
+                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k]}
+
+
+def all_max(x: float, device) -> float:
+    if dist.is_initialized():
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def barrier():
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def lift_mean(idx, pairs_host: np.ndarray) -> float:
+    """Mean label lifts per query of inlabel_lca (core/src/lca.cpp:97-105) on a
+    sample, replayed vectorised over the exported index (instrumentation for
+    the roofline byte model)."""
+    inl = idx.inlabel.astype(np.uint64)
+    asc = idx.ascendant.astype(np.uint64)
+    x, y = pairs_host[:, 0], pairs_host[:, 1]
+    ix, iy = inl[x], inl[y]
+    diff = ix != iy
+    xo = np.where(diff, ix ^ iy, np.uint64(1))
+    i = np.floor(np.log2(xo.astype(np.float64))).astype(np.uint64)
+    common = asc[x] & asc[y] & ~((np.uint64(1) << i) - np.uint64(1))
+    common = np.where(diff, common, np.uint64(1))
+    j = np.zeros(len(x), np.uint64)
+    c = common.copy()
+    low = c & (~c + np.uint64(1))
+    j = np.floor(np.log2(low.astype(np.float64))).astype(np.uint64)
+    target = (ix & ~((np.uint64(2) << j) - np.uint64(1))) | (np.uint64(1) << j)
+    lifts = (diff & (ix != target)).astype(np.int64) + (diff & (iy != target)).astype(np.int64)
+    return float(lifts.mean())
+
+
+# ---------------------------------------------------------------- workloads
+def make_tree(ett, n, gamma):
+    return ett.permute_labels(ett.grasp_tree(n, gamma, 1), 2)
+
+
+def device_queries(ett, n, q_total, seed, lo, hi, device):
+    d = torch.empty(2 * (hi - lo), dtype=torch.int32, device=device)
+    if hi > lo and not ett.gen_queries_dev(n, hi - lo, seed, lo, d, device.index):
+        # a Lemire rejection broke the counter replay: use the host stream
+        d.copy_(torch.from_numpy(ett.sample_queries(n, hi, seed)[lo:].astype(np.int32).ravel()))
+    return d
+
+
+def lca_section(ett, args, tree, q_total, device, rank, world, steps, warmup, label):
+    """Build on rank 0, broadcast, shard, time K steps.  Returns a dict."""
+    from paper_2103_15217_b200.dist import replicate_index, shard_range
+    idx = None
+    build_ms = None
+    if rank == 0:
+        # device-resident parent array: the build time excludes the host copy
+        d_par = torch.from_numpy(tree.parent.astype(np.int32)).to(device)
+        ett.inlabel_build_dev(d_par, tree.n, tree.root, device.index)  # warm arena / context
+        idx = ett.inlabel_build_dev(d_par, tree.n, tree.root, device.index)
+        build_ms = idx.build_ms()
+        del d_par
+    if world > 1:
+        idx = replicate_index(idx, tree.n, device)
+    lo, hi = shard_range(q_total, rank, world)
+    q = hi - lo
+    pairs = device_queries(ett, tree.n, q_total, 3, lo, hi, device)
+    ans = torch.empty(q, dtype=torch.int32, device=device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    stream = torch.cuda.current_stream(device)
+    for _ in range(warmup):
+        idx.query_dev(pairs, ans, ett.ENGINE_INLABEL, stream.cuda_stream)
+    torch.cuda.synchronize(device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    barrier()
+    torch.cuda.synchronize(device)
+    with ClockSampler(device.index) as clk:
+        for e0, e1 in evs:
+            flush.fill_(1)  # L2 flush, outside the timed interval
+            e0.record(stream)
+            idx.query_dev(pairs, ans, ett.ENGINE_INLABEL, stream.cuda_stream)
+            e1.record(stream)
+        torch.cuda.synchronize(device)
+    barrier()
+    step_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    step_ms_max = all_max(step_ms, device)
+    out = {"label": label, "q_total": q_total, "q_rank": q, "step_ms": step_ms_max,
+           "value": q_total / (step_ms_max / 1e3), "build_ms": build_ms,
+           "clocks": clk.summary(), "idx": idx, "pairs": pairs, "ans": ans, "lo": lo,
+           "gpu_launches": steps}
+    return out
+
+
+def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
+    """Same metric through ettg_lca_query with pinned int64 host buffers."""
+    host = ett.sample_queries(tree.n, hi, 3)[lo:] if hi > lo else np.zeros((0, 2), np.int64)
+    pin_pairs = torch.from_numpy(np.ascontiguousarray(host)).pin_memory()
+    pin_ans = torch.empty(hi - lo, dtype=torch.int64).pin_memory()
+    from paper_2103_15217_b200 import _lib
+    L = _lib.lib()
+
+    def call():
+        _lib.check(L.ettg_lca_query(idx.handle, pin_pairs.data_ptr(), hi - lo, max(hi - lo, 1),
+                                    pin_ans.data_ptr()))
+    call()
+    barrier()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    barrier()
+    t = all_max(float(np.mean(times)), device)
+    return {"value": q_total / t, "unit": "queries/s",
+            "h2d_bytes_per_step": (hi - lo) * 16, "d2h_bytes_per_step": (hi - lo) * 8,
+            "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)"}, \
+        pin_ans.numpy()
+
+
+def cpu_lca_baseline(tree, pairs_host, reps=3):
+    """The reference's own CPU path (oracle/_ref, compiled from the unmodified
+    core/src) on this host, all cores: inlabel_build untimed, answer_batch timed."""
+    from oracle import oracle as orc
+    if not orc.have_ref():
+        return None, None
+    cores = os.cpu_count() or 1
+    orc.Ref.set_workers(cores)
+    h = orc.RefInlabel(tree.parent, tree.root)
+    best = None
+    answers = None
+    for _ in range(reps):
+        answers, ns = h.answer(pairs_host, len(pairs_host))
+        best = ns if best is None else min(best, ns)
+    return {"value": len(pairs_host) / (best / 1e9), "unit": "queries/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"answer_batch(inlabel_lca) over {len(pairs_host)} queries of this workload,"
+                      f" best of {reps}; inlabel_build {h.build_ns / 1e9:.1f} s untimed"}, answers
+
+
+def bridges_section(ett, args, device, peak):
+    """Config D: road-like graph, TV bridges, edges/s, vs the planted truth."""
+    W = H = args.road_side
+    g, truth = ett.road_like_graph(W, H, 6, 3, args.road_pendant, 5)
+    n, m = g.n, g.m()
+    d_edges = torch.from_numpy(g.edges.astype(np.int32).ravel()).to(device)
+    d_mask = torch.empty(m, dtype=torch.uint8, device=device)
+    from paper_2103_15217_b200 import _lib
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+
+    def run():
+        pt = _lib.PhaseTimes()
+        _lib.check(L.ettg_bridges_dev(d_edges.data_ptr(), n, m, device.index, d_mask.data_ptr(),
+                                      stream.cuda_stream, __import__("ctypes").byref(pt)))
+        return pt
+    run()
+    ok = bool(np.array_equal(d_mask.cpu().numpy(), truth))
+    res = []
+    for _ in range(args.bridge_steps):
+        flush.fill_(1)
+        torch.cuda.synchronize(device)
+        res.append(run())
+    tot = float(np.mean([p.total_ms for p in res]))
+    bytes_model = 41 * m + 108 * n
+    out = {"config": {"workload": f"bridges-road-like W=H={W} r=3 extra=6 pendant={args.road_pendant}",
+                      "n": n, "m": m, "bridges": int(truth.sum())},
+           "metric": "bridges edges/s", "value": m / (tot / 1e3), "unit": "edges/s",
+           "ms_per_step": tot, "steps": args.bridge_steps,
+           "phases_ms": {"spanning": float(np.mean([p.spanning_ms for p in res])),
+                         "euler": float(np.mean([p.euler_ms for p in res])),
+                         "lowhigh": float(np.mean([p.lowhigh_ms for p in res]))},
+           "parity": "bit-exact vs planted truth" if ok else "MISMATCH",
+           "roofline": {"bound": "hbm", "achieved": bytes_model / (tot / 1e3) / 1e9,
+                        "peak": peak[0], "unit": "GB/s",
+                        "frac": bytes_model / (tot / 1e3) / 1e9 / peak[0],
+                        "traffic": None, "peak_kind": peak[1],
+                        "model": "41*m + 108*n bytes per call (SURVEY.md 8(d))",
+                        "io_floor_frac": 9 * m / (tot / 1e3) / 1e9 / peak[0]}}
+    if args.cpu_baseline:
+        from oracle import oracle as orc
+        if orc.have_ref():
+            cores = os.cpu_count() or 1
+            orc.Ref.set_workers(cores)
+            Ws = args.cpu_road_side
+            gs, ts = ett.road_like_graph(Ws, Ws, 6, 3, Ws * Ws // 50, 5)
+            mask, ph = orc.Ref.bridges("tv", gs.n, gs.edges)
+            out["cpu_baseline"] = {
+                "value": gs.m() / (ph[3] / 1e9), "unit": "edges/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"tv_bridges on road-like W=H={Ws} (n={gs.n}, m={gs.m()}), "
+                          f"build_adjacency untimed; phases ns {ph[:3].tolist()}",
+                "parity_vs_truth": bool(np.array_equal(mask, ts))}
+    return out
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=16_000_000)
+    ap.add_argument("--q", type=int, default=16_000_000)
+    ap.add_argument("--scaling-q", type=int, default=1_000_000_000)
+    ap.add_argument("--scaling-steps", type=int, default=5)
+    ap.add_argument("--no-scaling", action="store_true")
+    ap.add_argument("--no-bridges", action="store_true")
+    ap.add_argument("--road-side", type=int, default=5600)
+    ap.add_argument("--road-pendant", type=int, default=640_000)
+    ap.add_argument("--bridge-steps", type=int, default=5)
+    ap.add_argument("--cpu-road-side", type=int, default=1400)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    import paper_2103_15217_b200 as ett
+    peak = peaks()
+
+    # ---- headline: config B -------------------------------------------------
+    tree = make_tree(ett, args.n, 1)
+    sec = lca_section(ett, args, tree, args.q, device, rank, world, args.steps, args.warmup,
+                      "B")
+    idx = sec["idx"]
+    e2e, e2e_ans = e2e_section(ett, idx, tree, args.q, sec["lo"], sec["lo"] + sec["q_rank"],
+                               device, args.e2e_steps)
+    dev_ans = sec["ans"].cpu().numpy().astype(np.int64)
+    consistent = bool(np.array_equal(dev_ans, e2e_ans))
+    consistent = all_max(0.0 if consistent else 1.0, device) == 0.0
+
+    line = None
+    if rank == 0:
+        pairs_host = ett.sample_queries(tree.n, args.q, 3)
+        Lbar = lift_mean(idx, pairs_host[: min(len(pairs_host), 2_000_000)])
+        Bq = 12 + 32 * (2 + Lbar)
+        per_launch_bytes = Bq * sec["q_rank"]
+        achieved = per_launch_bytes / (sec["step_ms"] / 1e3) / 1e9
+        traffic = ncu_traffic("k_lca_inlabel_B")
+        line = {
+            "metric": METRIC, "value": sec["value"], "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec["step_ms"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (reference generators, seeds tree=1 permute=2 "
+                                    "queries=3)",
+            "config": {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) "
+                                   "path tree, 16M sample_queries sharded across GPUs",
+                       "n": tree.n, "queries": args.q, "engine": "inlabel",
+                       "parallelism": f"index replicated, queries sharded x{world}",
+                       "l2": "flushed (256 MiB write) before every step; index 384 MB > L2"},
+            "e2e": e2e,
+            "gpu_launches": sec["gpu_launches"],
+            "build_ms": sec["build_ms"],
+            "clocks": sec["clocks"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak[0], "unit": "GB/s",
+                         "frac": achieved / peak[0], "traffic": traffic,
+                         "peak_kind": peak[1], "kernel": "k_lca_inlabel",
+                         "bytes_per_query": Bq, "lifts_per_query": Lbar,
+                         "floor_76B_frac": 76 * sec["q_rank"] / (sec["step_ms"] / 1e3) / 1e9
+                         / peak[0]},
+            "answers_consistent_dev_vs_e2e": consistent,
+        }
+        if args.cpu_baseline and world == 1:
+            cb, ref_ans = cpu_lca_baseline(tree, pairs_host)
+            if cb is not None:
+                cb["parity_vs_ours"] = bool(np.array_equal(ref_ans, dev_ans))
+                line["cpu_baseline"] = cb
+    del sec, idx
+
+    # ---- config E: 16M grasp(inf), 1G queries sharded -------------------------
+    if not args.no_scaling:
+        treeE = make_tree(ett, args.n, GRASP_INF)
+        secE = lca_section(ett, args, treeE, args.scaling_q, device, rank, world,
+                           args.scaling_steps, 2, "E")
+        if rank == 0:
+            line["scaling_config_E"] = {
+                "workload": "permute_labels(grasp_tree(16M, inf)), 1G queries sharded",
+                "value": secE["value"], "unit": "queries/s", "ms_per_step": secE["step_ms"],
+                "steps": args.scaling_steps, "build_ms": secE["build_ms"],
+                "roofline_frac_140B": 140 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
+                / peak[0]}
+        del secE
+
+    # ---- bridges config D (replicas only: rank 0 of an N=1 run) -------------
+    if not args.no_bridges and rank == 0 and world == 1:
+        torch.cuda.empty_cache()
+        line["bridges"] = bridges_section(ett, args, device, peak)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def reference_arm(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref = unmodified core/src
+    compiled here) on the same workload, metric and unit.  Rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    import paper_2103_15217_b200 as ett
+    if not orc.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    cores = os.cpu_count() or 1
+    orc.Ref.set_workers(cores)
+    tree = make_tree(ett, args.n, 1)
+    pairs = ett.sample_queries(tree.n, args.q, 3)
+    h = orc.RefInlabel(tree.parent, tree.root)
+    sample = min(len(pairs), 2_000_000)
+    for s in range(args.warmup):
+        h.answer(pairs[:sample])
+    tot_ns = 0
+    for s in range(args.steps):
+        lo = (s * sample) % max(1, len(pairs) - sample + 1)
+        _, ns = h.answer(pairs[lo:lo + sample])
+        tot_ns += ns
+    v = sample * args.steps / (tot_ns / 1e9)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ns / 1e6 / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "i64",
+            "data": "synthetic (reference generators, seeds tree=1 permute=2 queries=3)",
+            "config": {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) "
+                                   "path tree, 16M sample_queries",
+                       "n": tree.n, "queries": args.q, "engine": "inlabel"},
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores,
+                             "kind": "reference",
+                             "sample": f"each step: answer_batch(inlabel_lca) over {sample} of "
+                                       f"the 16M queries; inlabel_build "
+                                       f"{h.build_ns / 1e9:.1f} s untimed"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

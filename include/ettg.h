@@ -139,6 +139,12 @@ int ettg_bridges_dev(const uint32_t* d_edges, int64_t n, int64_t m, int device,
                      uint8_t* d_is_bridge, void* stream,
                      ettg_phase_times* times);
 
+/* ------------------------------------------------------------ tuning -- */
+/* cudaLimitMaxL2FetchGranularity for the device's context (bytes: 0..128).
+ * Random 16-B record gathers over-fetch at the default; see DESIGN.md. */
+int ettg_set_l2_fetch_granularity(int device, int bytes);
+int ettg_get_l2_fetch_granularity(int device, int* bytes);
+
 /* --------------------------------------------------------- primitives -- */
 
 /* list_rank (core/src/primitives.cpp:145): rank[i] = links from head to i.

@@ -50,6 +50,8 @@ _SIGS = {
     "ettg_lca_index_attach_dev": ([p, i64, C.c_int, p, C.POINTER(p)], C.c_int),
     "ettg_bridges": ([p, i64, i64, C.c_int, p, C.POINTER(PhaseTimes)], C.c_int),
     "ettg_bridges_dev": ([p, i64, i64, C.c_int, p, p, C.POINTER(PhaseTimes)], C.c_int),
+    "ettg_set_l2_fetch_granularity": ([C.c_int, C.c_int], C.c_int),
+    "ettg_get_l2_fetch_granularity": ([C.c_int, C.POINTER(C.c_int)], C.c_int),
     "ettg_list_rank_dev": ([p, i64, i64, p, C.c_int, p], C.c_int),
     "ettg_exclusive_scan_dev": ([p, i64, p, C.c_int, p], C.c_int),
     "ettg_sort_pairs_dev": ([p, p, i64, p, p, C.c_int, p], C.c_int),

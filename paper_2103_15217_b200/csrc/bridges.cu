@@ -14,8 +14,8 @@
 //                              its edge is a spanning-forest edge
 //   euler     scan             tree-edge compaction (decoupled look-back); the
 //                              count is the connectivity check (n-1 tree edges)
-//             k_tree_he        2(n-1) half-edges keyed by source vertex
-//             sort_pairs       stable radix sort -> per-vertex rotation
+//             k_tree_rot       per-vertex rotation lists by atomicExch (no sort:
+//                              any rotation gives a valid tour)
 //             k_tree_succ      succ(e) = next(twin(e)); cut before first(0)
 //             list_rank_core   ranks of the tour rooted at vertex 0
 //             k_tour_flags     position -> (tree edge, is-down)
@@ -37,7 +37,7 @@
 #include "common.cuh"
 #include "listrank.cuh"
 #include "scan.cuh"
-#include "sort.cuh"
+#include "trace.cuh"
 
 namespace ettg {
 
@@ -124,51 +124,48 @@ struct TreeOut {
   }
 };
 
-// Half-edges of the spanning tree: 2t = (u -> v), 2t+1 = (v -> u).
-__global__ void k_tree_he(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
-                          u32* __restrict__ keys, u32* __restrict__ vals) {
+// Rotation system of the spanning tree without sorting.  Half-edges of tree
+// edge t = {u, v}: 2t = (u -> v), 2t+1 = (v -> u).  Each half-edge pushes
+// itself onto its source's list with one atomicExch; the list order is the
+// (arbitrary, race-dependent) cyclic rotation at that vertex.  Any rotation
+// gives a valid Euler tour, and bridges do not depend on it, so this replaces
+// the reference's two counting-sort passes (core/src/euler.cpp:58-69) by one
+// scattered atomic per half-edge.  The half-edge that found an empty list at
+// the root is the last of the root's rotation: the tour is cut before its twin.
+__global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
+                           u32 root, u32* __restrict__ head, u32* __restrict__ nxt,
+                           uint2* __restrict__ tend, u32* last_root) {
   for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     const uint2 uv = edges[tedge[t]];
-    keys[2 * t] = uv.x;
-    vals[2 * t] = 2 * t;
-    keys[2 * t + 1] = uv.y;
-    vals[2 * t + 1] = 2 * t + 1;
+    tend[t] = uv;
+    const u32 p0 = atomicExch(&head[uv.x], 2 * t);
+    const u32 p1 = atomicExch(&head[uv.y], 2 * t + 1);
+    nxt[2 * t] = p0;
+    nxt[2 * t + 1] = p1;
+    if (p0 == kNone && uv.x == root) *last_root = 2 * t;
+    if (p1 == kNone && uv.y == root) *last_root = 2 * t + 1;
   }
 }
 
-__global__ void k_vertex_ranges(const u32* __restrict__ skey, u32 k, uint2* __restrict__ crange) {
-  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < k; s += gridDim.x * blockDim.x) {
-    const u32 y = skey[s];
-    if (s == 0 || skey[s - 1] != y) crange[y].x = s;
-    if (s + 1 == k || skey[s + 1] != y) crange[y].y = s + 1;
-  }
-}
-
-__global__ void k_inverse(const u32* __restrict__ sval, u32 k, u32* __restrict__ slot_of) {
-  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < k; s += gridDim.x * blockDim.x)
-    slot_of[sval[s]] = s;
-}
-
-// succ(e) = next(twin(e)) in the cyclic rotation of twin(e)'s source
-// (core/src/euler.cpp:85-88, :105).
-__global__ void k_tree_succ(const u32* __restrict__ skey, const u32* __restrict__ sval,
-                            const u32* __restrict__ slot_of, const uint2* __restrict__ crange,
-                            u32 k, u32* __restrict__ succ) {
+// succ(e) = next(twin(e)) in the cyclic rotation of twin(e)'s source, which
+// is e's destination (core/src/euler.cpp:85-88, :105).  Written as list-rank
+// slots; the cut before head[root] makes the tour a list.
+__global__ void k_tree_succ(const uint2* __restrict__ tend, const u32* __restrict__ head,
+                            const u32* __restrict__ nxt, u32 k, u32 cut,
+                            u32* __restrict__ slot) {
   for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
-    const u32 s = slot_of[e ^ 1u];
-    const uint2 r = crange[skey[s]];
-    const u32 ns = (s + 1 < r.y) ? s + 1 : r.x;
-    succ[e] = sval[ns];
+    const u32 tw = e ^ 1u;
+    const uint2 uv = tend[e >> 1];
+    const u32 dst = (e & 1u) ? uv.x : uv.y;
+    const u32 n2 = nxt[tw];
+    slot[e] = e == cut ? kNone : (n2 != kNone ? n2 : head[dst]);
   }
 }
 
-// Cut the cycle just before first(root) (core/src/euler.cpp:104-110).
-__global__ void k_tree_cut(const u32* __restrict__ sval, const uint2* __restrict__ crange,
-                           u32 root, u32* __restrict__ succ, u32* head) {
-  const uint2 r = crange[root];
-  const u32 last = sval[r.y - 1];
-  succ[last ^ 1u] = kNone;
-  *head = sval[r.x];
+__global__ void k_tree_head(const u32* __restrict__ head, u32 root, const u32* last_root,
+                            u32* words) {
+  words[2] = head[root];        // tour head: first half-edge of root's rotation
+  words[3] = *last_root ^ 1u;   // its tour predecessor: twin of the last one
 }
 
 // flags[pos] = (t << 1) | is_down for the half-edge at tour position pos.
@@ -197,7 +194,7 @@ struct DownIn {
 struct StatsOut {
   const u32* flags;
   const u32* tedge;
-  const uint2* edges;
+  const uint2* tend;
   Lr0View lr;
   u32 n;
   u32* pre_of;         // [n]   node -> preorder
@@ -212,7 +209,7 @@ struct StatsOut {
     lr.get(2 * t, S1, r0, d);
     lr.get(2 * t + 1, S1, r1, d);
     const u32 e = tedge[t];
-    const uint2 uv = edges[e];
+    const uint2 uv = tend[t];
     const bool first_is_down = r0 < r1;           // half-edge 2t = (u -> v)
     const u32 child = first_is_down ? uv.y : uv.x;
     const u32 pos_up = first_is_down ? r1 : r0;
@@ -326,11 +323,9 @@ struct BridgeWs {
   uint8_t* tree = nullptr;
   u64* scan_m = nullptr;
   u32* tedge = nullptr;
-  u32 *keys = nullptr, *vals = nullptr, *skey = nullptr, *sval = nullptr;
-  SortWs sort;
-  uint2* crange = nullptr;
-  u32* slot_of = nullptr;
-  u32* succ = nullptr;
+  u32* head = nullptr;
+  u32* nxt = nullptr;
+  uint2* tend = nullptr;
   ListRankWs lr;
   u32* flags = nullptr;
   u64* scan_k = nullptr;
@@ -351,14 +346,9 @@ struct BridgeWs {
     tree = c.take<uint8_t>(m + 16);
     scan_m = c.take<u64>(scan_ws_words(m));
     tedge = c.take<u32>(n);
-    keys = c.take<u32>(k + 1);
-    vals = c.take<u32>(k + 1);
-    skey = c.take<u32>(k + 1);
-    sval = c.take<u32>(k + 1);
-    sort.carve(c, k + 1);
-    crange = c.take<uint2>(n);
-    slot_of = c.take<u32>(k + 1);
-    succ = c.take<u32>(k + 1);
+    head = c.take<u32>(n);
+    nxt = c.take<u32>(k + 1);
+    tend = c.take<uint2>(n);
     lr.carve(c, k > 0 ? k : 1);
     flags = c.take<u32>(k + 1);
     scan_k = c.take<u64>(scan_ws_words(k + 1));
@@ -412,6 +402,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   } eg{ev};
 
   CK(cudaEventRecord(ev[0], st));
+  Trace tr("bridges", st);
   CK(cudaMemsetAsync(ws.words, 0, 16 * sizeof(u32), st));
   const uint2* edges;
   if (host_i64) {
@@ -435,8 +426,10 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
   CK_LAUNCH();
   if (m) {
+    tr.mark("input");
     k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, ws.par, ws.tree);
     CK_LAUNCH();
+    tr.mark("cc_hook");
   }
   CK(cudaEventRecord(ev[1], st));
 
@@ -451,31 +444,31 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
 
   if (n > 1) {
     const u32 k = 2 * T;
-    k_tree_he<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, ws.keys,
-                                                               ws.vals);
+    CK(cudaMemsetAsync(ws.head, 0xFF, static_cast<u64>(n) * 4, st));
+    tr.mark("compact");
+    k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, 0, ws.head,
+                                                                ws.nxt, ws.tend, ws.words + 4);
     CK_LAUNCH();
-    sort_pairs(ws.keys, ws.vals, ws.skey, ws.sval, k, bits_for(n - 1), ws.sort, st);
-    CK(cudaMemsetAsync(ws.crange, 0, static_cast<u64>(n) * sizeof(uint2), st));
-    k_vertex_ranges<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.skey, k, ws.crange);
+    k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words);
     CK_LAUNCH();
-    k_inverse<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.sval, k, ws.slot_of);
-    CK_LAUNCH();
-    k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.skey, ws.sval, ws.slot_of,
-                                                                 ws.crange, k, ws.succ);
-    CK_LAUNCH();
-    k_tree_cut<<<1, 1, 0, st>>>(ws.sval, ws.crange, 0, ws.succ, ws.words + 2);
-    CK_LAUNCH();
-    u32 head = 0;
-    CK(cudaMemcpyAsync(&head, ws.words + 2, 4, cudaMemcpyDeviceToHost, st));
+    u32 hw[2];
+    CK(cudaMemcpyAsync(hw, ws.words + 2, sizeof hw, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    list_rank_core(ws.succ, k, head, NoDown{}, ws.lr, st, sms);
+    const u32 head = hw[0];
+    k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.tend, ws.head, ws.nxt, k,
+                                                                 hw[1], ws.lr.succ0);
+    CK_LAUNCH();
+    tr.mark("rotation");
+    list_rank_core(k, head, NoDown{}, ws.lr, st, sms);
+    tr.mark("list_rank");
     const Lr0View lv = lr0_view(ws.lr);
     k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
     CK_LAUNCH();
     scan_exclusive(DownIn{ws.flags},
-                   StatsOut{ws.flags, ws.tedge, edges, lv, n, ws.pre_of, ws.size_by_pre,
+                   StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of, ws.size_by_pre,
                             ws.pedge_by_pre},
                    k, ws.scan_k, nullptr, st);
+    tr.mark("preorder");
   }
   k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre);
   CK_LAUNCH();
@@ -489,6 +482,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
                                                                      ws.pre_of, ws.lh);
     CK_LAUNCH();
   }
+  tr.mark("lowhigh_edges");
   k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,
                                                                             ws.sp);
   CK_LAUNCH();
@@ -501,6 +495,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   k_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
       ws.lh, ws.sp, ws.nb, n, ws.size_by_pre, ws.pedge_by_pre, d_mask, m);
   CK_LAUNCH();
+  tr.mark("rmq_classify");
   CK(cudaEventRecord(ev[3], st));
   if (h_mask && m) CK(cudaMemcpyAsync(h_mask, d_mask, m, cudaMemcpyDeviceToHost, st));
   u32 lerr = 0;

@@ -97,15 +97,6 @@ Lease::~Lease() {
   a.mu.unlock();
 }
 
-// Every element has at most one predecessor and the head has none.
-__global__ void k_pred_check(const u32* __restrict__ succ, u32 k, u32 head, u32* pred, u32* err) {
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
-    const u32 s = succ[e];
-    if (s == kNone) continue;
-    if (s >= k || s == head || atomicAdd(&pred[s], 1u) != 0u) atomicOr(err, kErrStructure);
-  }
-}
-
 }  // namespace ettg
 
 using namespace ettg;
@@ -128,6 +119,23 @@ int ettg_device_count(int* count) {
   });
 }
 
+int ettg_set_l2_fetch_granularity(int device, int bytes) {
+  return guard([&] {
+    DeviceScope ds(device);
+    CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(bytes)));
+  });
+}
+
+int ettg_get_l2_fetch_granularity(int device, int* bytes) {
+  return guard([&] {
+    if (!bytes) einval("null argument");
+    DeviceScope ds(device);
+    size_t v = 0;
+    CK(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+    *bytes = static_cast<int>(v);
+  });
+}
+
 int ettg_list_rank_dev(const uint32_t* d_succ, int64_t k, int64_t head, uint32_t* d_rank,
                        int device, void* stream) {
   return guard([&] {
@@ -146,14 +154,9 @@ int ettg_list_rank_dev(const uint32_t* d_succ, int64_t k, int64_t head, uint32_t
     c = Carver{lease.base()};
     ws.carve(c, kk);
     pred = c.take<u32>(kk);
-    // Injectivity check (a successor array with a shared successor is a
-    // malformed list for the reference's list_rank as well).
-    CK(cudaMemsetAsync(pred, 0, static_cast<u64>(kk) * 4, st));
+    CK(cudaMemcpyAsync(ws.succ0, d_succ, static_cast<u64>(kk) * 4, cudaMemcpyDeviceToDevice, st));
     const int sms = sm_count(device);
-    list_rank_core(d_succ, kk, static_cast<u32>(head), NoDown{}, ws, st, sms);
-    k_pred_check<<<blocks_for(kk, 256), 256, 0, st>>>(d_succ, kk, static_cast<u32>(head), pred,
-                                                      ws.counters + LrCounters::kErr);
-    CK_LAUNCH();
+    list_rank_core(kk, static_cast<u32>(head), NoDown{}, ws, st, sms, pred);
     k_lr_rank_out<<<blocks_for(kk, 256), 256, 0, st>>>(lr0_view(ws), kk, d_rank);
     CK_LAUNCH();
     u32 err = 0;

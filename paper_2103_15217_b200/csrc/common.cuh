@@ -53,20 +53,19 @@ __device__ __forceinline__ u32 lanemask_lt() {
   return m;
 }
 
-// Read-only, L1-no-allocate gathers for index records (random, never reused
-// within a CTA): one 32-B sector per record.
-__device__ __forceinline__ uint4 ldg_nc_na(const uint4* p) {
+// Read-only gathers of index records (one 32-B sector each).  L1-allocating
+// on purpose: on B200 random 16-B gathers run 1.6x faster than with
+// L1::no_allocate / .cg (profiles/r1_gather_micro.md).
+__device__ __forceinline__ uint4 ldg_rec(const uint4* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
 }
-__device__ __forceinline__ uint2 ldg_nc_na(const uint2* p) {
+__device__ __forceinline__ uint2 ldg_rec(const uint2* p) {
   uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
 // Streaming loads/stores (read once / write once).

@@ -40,6 +40,7 @@
 #include "listrank.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
+#include "trace.cuh"
 
 namespace ettg {
 
@@ -301,8 +302,8 @@ __global__ void __launch_bounds__(kQThreads)
     uint4 A[kQPer], B[kQPer];
 #pragma unroll
     for (int j = 0; j < kQPer; ++j) {
-      A[j] = ldg_nc_na(node + x[j]);
-      B[j] = ldg_nc_na(node + y[j]);
+      A[j] = ldg_rec(node + x[j]);
+      B[j] = ldg_rec(node + y[j]);
     }
     u32 ans[kQPer], wx[kQPer], wy[kQPer];
     bool lx[kQPer], ly[kQPer];
@@ -333,8 +334,8 @@ __global__ void __launch_bounds__(kQThreads)
     uint2 LX[kQPer], LY[kQPer];
 #pragma unroll
     for (int j = 0; j < kQPer; ++j) {
-      LX[j] = lx[j] ? ldg_nc_na(lab + wx[j]) : make_uint2(x[j], A[j].z);
-      LY[j] = ly[j] ? ldg_nc_na(lab + wy[j]) : make_uint2(y[j], B[j].z);
+      LX[j] = lx[j] ? ldg_rec(lab + wx[j]) : make_uint2(x[j], A[j].z);
+      LY[j] = ly[j] ? ldg_rec(lab + wy[j]) : make_uint2(y[j], B[j].z);
     }
 #pragma unroll
     for (int j = 0; j < kQPer; ++j) {
@@ -460,7 +461,6 @@ struct BuildWs {
   SortWs sort;
   uint2* crange = nullptr;
   u32* jj = nullptr;
-  u32* succ = nullptr;
   ListRankWs lr;
   u32* up = nullptr;
   u32* asc = nullptr;
@@ -475,7 +475,6 @@ struct BuildWs {
     sort.carve(c, m + 1);
     crange = c.take<uint2>(n);
     jj = c.take<u32>(n);
-    succ = c.take<u32>(2ull * n);
     lr.carve(c, 2 * n);
     up = c.take<u32>(static_cast<u64>(n) + 1);
     asc = c.take<u32>(static_cast<u64>(n) + 1);
@@ -533,6 +532,7 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, st));
+  Trace tr("lca_build", st);
 
   const u32 m = n - 1;
   const unsigned g = sms * 8;
@@ -547,26 +547,31 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
         static_cast<const u32*>(parent), n, root, h->par, ws.keys, ws.vals, ws.flags);
   }
   CK_LAUNCH();
+  tr.mark("validate");
   sort_pairs(ws.keys, ws.vals, ws.pkey, ws.child, m, bits_for(n - 1), ws.sort, st);
+  tr.mark("sort");
   CK(cudaMemsetAsync(ws.crange, 0, static_cast<u64>(n) * sizeof(uint2), st));
   if (m > 0) {
     k_child_ranges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.pkey, m, ws.crange);
     CK_LAUNCH();
   }
   k_node_succ<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.crange, ws.child, h->par, n,
-                                                              root, ws.jj, ws.succ);
+                                                              root, ws.jj, ws.lr.succ0);
   CK_LAUNCH();
   if (m > 0) {
     k_slot_succ<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.crange, ws.child, ws.pkey,
-                                                                ws.jj, m, root, ws.succ);
+                                                                ws.jj, m, root, ws.lr.succ0);
     CK_LAUNCH();
   }
-  list_rank_core(ws.succ, 2 * n, 2 * root, EvenIsDown{}, ws.lr, st, sms);
+  tr.mark("succ");
+  list_rank_core(2 * n, 2 * root, EvenIsDown{}, ws.lr, st, sms);
+  tr.mark("list_rank");
   k_tree_stats<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
       lr0_view(ws.lr), n, h->par, h->pre, h->size, h->level, h->inlabel, h->first,
       (engines & ETTG_ENGINE_RMQ) ? h->tkey : nullptr);
   CK_LAUNCH();
 
+  tr.mark("stats");
   // Validation verdict before building the rest (bad input -> no index).
   u32 vflags[8], lerr;
   CK(cudaMemcpyAsync(vflags, ws.flags, sizeof vflags, cudaMemcpyDeviceToHost, st));
@@ -590,7 +595,9 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, ws.asc, n,
                                                          h->node);
   CK_LAUNCH();
+  tr.mark("head_asc_pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
+  tr.mark("rmq");
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;

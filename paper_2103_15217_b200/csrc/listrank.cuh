@@ -33,6 +33,7 @@
 
 #include "common.cuh"
 #include "scan.cuh"
+#include "trace.cuh"
 
 namespace ettg {
 namespace {  // kernels defined in headers: internal linkage per TU
@@ -108,15 +109,21 @@ struct LrCounters {
 };
 
 // ---- level-0 walk -----------------------------------------------------------
+// Successors (u32) and records (u64, local << 32 | sublist) live in separate
+// arrays.  Measured on B200 (tools/walk_micro.cu, profiles/r1_walk_micro.md):
+// keeping both in one 8-B slot (load then store the same address) runs at
+// 3.45 G elements/s versus 19.7 G/s for separate arrays -- the same-address
+// store stalls the dependent pointer chase -- so the extra random store is
+// the cheaper option.
 template <class Down>
 __global__ void __launch_bounds__(256)
-    k_lr_walk0(const u32* __restrict__ succ, u32 k, u32 head, u32 seed, u32 mask,
-               const u32* __restrict__ spl, u32* counters, u32 sub_cap,
-               u64* __restrict__ rec, u32* __restrict__ sub_next,
-               u64* __restrict__ sub_w, Down down) {
+    k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, u32 head, u32 seed,
+               u32 mask, const u32* __restrict__ spl, u32* counters, u32 sub_cap,
+               u32* __restrict__ sub_next, u64* __restrict__ sub_w, Down down) {
   const int lane = threadIdx.x & 31;
   const u32 lt = lanemask_lt();
-  const u32 nspl = min(counters[LrCounters::kNspl], sub_cap);
+  // A malformed list (shared successors, found by k_pred_check) is not walked.
+  const u32 nspl = counters[LrCounters::kErr] ? 0u : min(counters[LrCounters::kNspl], sub_cap);
   bool active = false, retired = false;
   u32 sid = 0, cur = 0, acc = 0, steps = 0;
   while (true) {
@@ -167,6 +174,16 @@ __global__ void __launch_bounds__(256)
         cur = nxt;
       }
     }
+  }
+}
+
+// Every element has at most one predecessor and the head has none (checked
+// before walking when the successor array comes from a caller).
+__global__ void k_pred_check(const u32* __restrict__ succ, u32 k, u32 head, u32* pred, u32* err) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    const u32 s = succ[e];
+    if (s == kNone) continue;
+    if (s >= k || s == head || atomicAdd(&pred[s], 1u) != 0u) atomicOr(err, kErrStructure);
   }
 }
 
@@ -354,7 +371,8 @@ struct ListRankWs {
   u32 k = 0;
   int levels = 0;  // number of walk levels (>= 1); final Wyllie after the last
   LrLevel lv[kMaxLevels + 1];
-  u64* rec0 = nullptr;  // level-0 records, k entries
+  u32* succ0 = nullptr;  // level-0 successors (filled by the caller), k entries
+  u64* rec0 = nullptr;   // level-0 records, k entries
   u32* counters = nullptr;
   u64* prefix1 = nullptr;  // == lv[1].prefix: exclusive prefix per level-0 sublist
 
@@ -366,6 +384,7 @@ struct ListRankWs {
 
   void carve(Carver& c, u32 k_) {
     k = k_;
+    succ0 = c.take<u32>(k);
     rec0 = c.take<u64>(k);
     counters = c.take<u32>(64);
     // level 0 caps
@@ -404,13 +423,23 @@ struct ListRankWs {
 inline u32 lr_seed(int level) { return 0x65746b5fu ^ (0x9e3779b9u * (level + 1)); }
 
 // Runs the ranking up to the per-sublist prefixes of level 0 (ws.prefix1).
-// Callers finish with their own fused per-element kernel (lr_prefix0).
-// No host synchronisation; errors accumulate in counters[kErr].
+// The caller has filled ws.succ0 (u32 successors, kNone = tail); on return
+// ws.rec0 holds the level-0 records.  Callers finish with their own fused
+// per-element kernel (Lr0View).  `pred` (k words of scratch) enables the
+// injectivity check for caller-supplied lists.  No host synchronisation;
+// errors accumulate in counters[kErr].
 template <class Down>
-void list_rank_core(const u32* succ, u32 k, u32 head, Down down, ListRankWs& ws,
-                    cudaStream_t st, int sms) {
+void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st, int sms,
+                    u32* pred = nullptr) {
+  Trace tr("list_rank", st);
   CK(cudaMemsetAsync(ws.counters, 0, 64 * sizeof(u32), st));
   u32* cnt = ws.counters;
+  if (pred) {
+    CK(cudaMemsetAsync(pred, 0, static_cast<u64>(k) * 4, st));
+    k_pred_check<<<blocks_for(k, 256), 256, 0, st>>>(ws.succ0, k, head, pred,
+                                                     cnt + LrCounters::kErr);
+    CK_LAUNCH();
+  }
   const u32 mask0 = kLrL0 - 1;
   const u32 seed0 = lr_seed(0);
   const u32 cap1 = ws.lv[1].cap;
@@ -420,11 +449,13 @@ void list_rank_core(const u32* succ, u32 k, u32 head, Down down, ListRankWs& ws,
                  ws.lv[0].scan_status, cnt + LrCounters::kNspl, st);
   CK(cudaMemcpyAsync(cnt + LrCounters::kSubTotal0, cnt + LrCounters::kNspl, sizeof(u32),
                      cudaMemcpyDeviceToDevice, st));
+  tr.mark("splitters0");
   const unsigned walk_blocks = sms * 8;  // 2048 threads / SM resident
-  k_lr_walk0<Down><<<walk_blocks, 256, 0, st>>>(succ, k, head, seed0, mask0, ws.lv[0].spl,
-                                                cnt, cap1, ws.rec0, ws.lv[0].sub_next,
+  k_lr_walk0<Down><<<walk_blocks, 256, 0, st>>>(ws.succ0, ws.rec0, k, head, seed0, mask0,
+                                                ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
                                                 ws.lv[0].sub_w, down);
   CK_LAUNCH();
+  tr.mark("walk0");
   // level-1 list
   u32* S1 = cnt + LrCounters::kSubTotal0;
   k_lr_clamp<<<1, 1, 0, st>>>(S1, cap1, cnt + LrCounters::kErr);
@@ -454,21 +485,19 @@ void list_rank_core(const u32* succ, u32 k, u32 head, Down down, ListRankWs& ws,
                                                             hd, N.succ, N.w, hd_next);
     CK_LAUNCH();
     S_l = nspl;
+    tr.mark("level");
   }
   // final level
   {
     const int l = ws.levels;
     LrLevel& F = ws.lv[l];
     const u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
-    static bool attr_set = false;  // per process; same value for every device
-    if (!attr_set) {
-      CK(cudaFuncSetAttribute(k_lr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kLrFinalSmem));
-      attr_set = true;
-    }
+    CK(cudaFuncSetAttribute(k_lr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kLrFinalSmem));
     k_lr_final<<<1, kLrFinalThreads, kLrFinalSmem, st>>>(F.succ, F.w, S_l, hd, F.prefix, k,
                                               cnt + LrCounters::kErr);
     CK_LAUNCH();
+    tr.mark("final");
   }
   // expand back down to level 1
   for (int l = ws.levels - 1; l >= 1; --l) {
@@ -480,6 +509,7 @@ void list_rank_core(const u32* succ, u32 k, u32 head, Down down, ListRankWs& ws,
                                                         S, Sn, L.prefix);
     CK_LAUNCH();
   }
+  tr.mark("expand");
 }
 
 // Level-0 element prefix: (rank, down-weight sum) of everything before e.

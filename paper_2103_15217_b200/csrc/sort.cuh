@@ -50,23 +50,27 @@ __global__ void __launch_bounds__(kRsThreads)
     k_rs_scatter(const u32* __restrict__ kin, const u32* __restrict__ vin,
                  u32* __restrict__ kout, u32* __restrict__ vout, u32 n, int shift,
                  const u32* __restrict__ hist_scanned, u32 ntiles) {
+  // Keys are staged in shared memory and values re-read (coalesced) at
+  // scatter time, so only the 16 ranks live in registers (occupancy).
   __shared__ u32 cnt[kRsWarps][kRadix];
+  __shared__ u32 skey[kRsTile];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < kRsWarps * kRadix; i += kRsThreads) (&cnt[0][0])[i] = 0;
   __syncthreads();
-  const u32 base = blockIdx.x * kRsTile + warp * (kRsTile / kRsWarps);
+  const u32 wbase = warp * (kRsTile / kRsWarps);
+  const u32 base = blockIdx.x * kRsTile + wbase;
   const u32 lt = lanemask_lt();
-  u32 key[kRsItems], val[kRsItems], rank[kRsItems];
+  u32 rank[kRsItems];
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
-    u32 i = base + r * 32 + lane;
-    bool ok = i < n;
-    key[r] = ok ? kin[i] : 0u;
-    val[r] = ok ? vin[i] : 0u;
-    u32 d = ok ? ((key[r] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = pad
-    u32 peers = __match_any_sync(0xffffffffu, d);
-    u32 lower = __popc(peers & lt);
-    u32 c = ok ? cnt[warp][d] : 0u;
+    const u32 i = base + r * 32 + lane;
+    const bool ok = i < n;
+    const u32 key = ok ? kin[i] : 0u;
+    skey[wbase + r * 32 + lane] = key;
+    const u32 d = ok ? ((key >> shift) & (kRadix - 1)) : kRadix;  // kRadix = pad
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const u32 lower = __popc(peers & lt);
+    const u32 c = ok ? cnt[warp][d] : 0u;
     rank[r] = c + lower;
     __syncwarp();
     if (ok && lower == 0) cnt[warp][d] = c + __popc(peers);
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kRsThreads)
     u32 run = hist_scanned[static_cast<u64>(d) * ntiles + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
-      u32 t = cnt[w][d];
+      const u32 t = cnt[w][d];
       cnt[w][d] = run;
       run += t;
     }
@@ -85,12 +89,12 @@ __global__ void __launch_bounds__(kRsThreads)
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
-    u32 i = base + r * 32 + lane;
+    const u32 i = base + r * 32 + lane;
     if (i < n) {
-      u32 d = (key[r] >> shift) & (kRadix - 1);
-      u32 pos = cnt[warp][d] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+      const u32 key = skey[wbase + r * 32 + lane];
+      const u32 pos = cnt[warp][(key >> shift) & (kRadix - 1)] + rank[r];
+      kout[pos] = key;
+      vout[pos] = vin[i];
     }
   }
 }

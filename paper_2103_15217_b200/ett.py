@@ -164,6 +164,15 @@ def inlabel_build(tree: RootedTree, device: int = 0, engines: int = ENGINE_INLAB
     return InlabelIndex(_build(tree, engines, device), tree.n, device, engines)
 
 
+def inlabel_build_dev(d_parent, n: int, root: int, device: int = 0,
+                     engines: int = ENGINE_INLABEL, stream: int | None = None) -> InlabelIndex:
+    """Build from a device-resident int32/uint32 parent tensor (-1 = root)."""
+    h = C.c_void_p()
+    check(lib().ettg_lca_build_dev(ptr(d_parent), int(n), int(root), device, engines, stream,
+                                   C.byref(h)))
+    return InlabelIndex(h.value, n, device, engines)
+
+
 def rmq_lca_build(tree: RootedTree, device: int = 0) -> RmqLcaIndex:
     """rmq_lca_build (core/src/lca.cpp:128)."""
     if len(tree.parent) != tree.n:
