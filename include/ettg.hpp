@@ -1,0 +1,155 @@
+// ettg.hpp -- header-only C++ shim over the C-ABI (ettg.h) with the
+// reference's signatures and exceptions, so reference-style callers
+// (tools/ett_bench.cpp:93-167, :303-339; tests/acceptance.cpp) can switch by
+// changing the namespace:
+//
+//   ett::inlabel_build(const RootedTree&)        -> ettg::inlabel_build(...)
+//   ett::answer_batch(lambda, queries, batch)    -> ettg::answer_batch(idx, queries, batch)
+//   ett::rmq_lca_build / rmq_lca                 -> ettg::rmq_lca_build / answer_batch
+//   ett::node_stats(linearize(...))              -> ettg::node_stats(tree)
+//   ett::tv_bridges(const AdjacencyIndex&, ...)  -> ettg::tv_bridges(const EdgeList&, ...)
+//
+// Errors: std::invalid_argument / std::out_of_range exactly where the
+// reference throws them (ETTG_EINVAL / ETTG_ERANGE); std::runtime_error for
+// CUDA failures.  Link: -I<repo>/include -L<repo>/paper_2103_15217_b200/_lib -lettg
+#ifndef ETTG_HPP_
+#define ETTG_HPP_
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ettg.h"
+
+namespace ettg {
+
+using i64 = std::int64_t;
+using u64 = std::uint64_t;
+inline constexpr i64 kNone = -1;
+
+inline void check(int rc) {
+  if (rc == ETTG_OK) return;
+  std::string msg = ettg_last_error();
+  if (rc == ETTG_EINVAL) throw std::invalid_argument(msg);
+  if (rc == ETTG_ERANGE) throw std::out_of_range(msg);
+  throw std::runtime_error(msg);
+}
+
+// Same field layout as ett::RootedTree / ett::EdgeList (graph.hpp:18-23, :66-70).
+struct RootedTree {
+  i64 n = 0;
+  i64 root = 0;
+  std::vector<i64> parent;
+};
+
+struct EdgeList {
+  i64 n = 0;
+  std::vector<std::pair<i64, i64>> edges;
+  i64 m() const { return static_cast<i64>(edges.size()); }
+};
+
+struct NodeStats {
+  std::vector<i64> preorder, size, level, parent;
+};
+
+struct BridgeMask {
+  std::vector<char> is_bridge;
+  i64 count() const {
+    i64 c = 0;
+    for (char b : is_bridge) c += b ? 1 : 0;
+    return c;
+  }
+};
+
+struct PhaseTimes {
+  std::vector<std::pair<std::string, double>> ms;  // spanning, euler, lowhigh
+};
+
+// Owns the device index; movable, not copyable.
+class LcaIndex {
+ public:
+  LcaIndex() = default;
+  LcaIndex(ettg_lca* h, unsigned engine) : h_(h, &ettg_lca_free), engine_(engine) {}
+  ettg_lca* get() const { return h_.get(); }
+  unsigned engine() const { return engine_; }
+  i64 n() const {
+    i64 v = 0;
+    check(ettg_lca_size(h_.get(), &v));
+    return v;
+  }
+
+ private:
+  std::unique_ptr<ettg_lca, void (*)(ettg_lca*)> h_{nullptr, &ettg_lca_free};
+  unsigned engine_ = ETTG_ENGINE_INLABEL;
+};
+
+using InlabelIndex = LcaIndex;
+using RmqLcaIndex = LcaIndex;
+
+inline LcaIndex inlabel_build(const RootedTree& t, int device = 0) {
+  if (static_cast<i64>(t.parent.size()) != t.n)
+    throw std::invalid_argument("parent array size mismatch");
+  ettg_lca* h = nullptr;
+  check(ettg_lca_build(t.parent.data(), t.n, t.root, device, ETTG_ENGINE_INLABEL, &h));
+  return LcaIndex(h, ETTG_ENGINE_INLABEL);
+}
+
+inline LcaIndex rmq_lca_build(const RootedTree& t, int device = 0) {
+  if (static_cast<i64>(t.parent.size()) != t.n)
+    throw std::invalid_argument("parent array size mismatch");
+  ettg_lca* h = nullptr;
+  check(ettg_lca_build(t.parent.data(), t.n, t.root, device, ETTG_ENGINE_RMQ, &h));
+  return LcaIndex(h, ETTG_ENGINE_RMQ);
+}
+
+// answer_batch (lca.hpp:50-65): answers in query order; batch < 1 throws.
+inline std::vector<i64> answer_batch(const LcaIndex& idx,
+                                     const std::vector<std::pair<i64, i64>>& queries,
+                                     i64 batch_size) {
+  std::vector<i64> out(queries.size());
+  static_assert(sizeof(std::pair<i64, i64>) == 2 * sizeof(i64), "pair layout");
+  check(ettg_lca_query_engine(idx.get(), idx.engine(),
+                              reinterpret_cast<const int64_t*>(queries.data()),
+                              static_cast<i64>(queries.size()), batch_size, out.data()));
+  return out;
+}
+
+inline i64 inlabel_lca(const LcaIndex& idx, i64 x, i64 y) {
+  return answer_batch(idx, {{x, y}}, 1)[0];
+}
+
+inline NodeStats node_stats(const RootedTree& t, int device = 0) {
+  LcaIndex idx = inlabel_build(t, device);
+  NodeStats s;
+  s.preorder.resize(t.n);
+  s.size.resize(t.n);
+  s.level.resize(t.n);
+  s.parent.resize(t.n);
+  check(ettg_lca_stats(idx.get(), s.preorder.data(), s.size.data(), s.level.data(),
+                       s.parent.data()));
+  return s;
+}
+
+// tv_bridges (bridges.hpp:55).  Takes the EdgeList the reference builds its
+// AdjacencyIndex from (build_adjacency is not needed on the device).
+inline BridgeMask tv_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  std::vector<uint8_t> mask(g.edges.size());
+  ettg_phase_times pt{};
+  check(ettg_bridges(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), device,
+                     mask.data(), &pt));
+  if (times) {
+    times->ms.emplace_back("spanning", pt.spanning_ms);
+    times->ms.emplace_back("euler", pt.euler_ms);
+    times->ms.emplace_back("lowhigh", pt.lowhigh_ms);
+  }
+  BridgeMask out;
+  out.is_bridge.assign(mask.begin(), mask.end());
+  return out;
+}
+
+}  // namespace ettg
+
+#endif  // ETTG_HPP_

@@ -80,8 +80,12 @@ class _LcaHandle:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().ettg_lca_free(h)
+        L = _lib._lib  # may already be torn down at interpreter exit
+        if h is not None and h.value and L is not None:
+            try:
+                L.ettg_lca_free(h)
+            except Exception:
+                pass
             self._h = None
 
     @property

@@ -1,0 +1,48 @@
+// C++ caller through include/ettg.hpp, written like the reference's own tests
+// (tests/lca_test.cpp:47-74, tests/bridges_test.cpp): exits non-zero on failure.
+#include <cstdio>
+#include <stdexcept>
+
+#include "ettg.hpp"
+
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::fprintf(stderr, "CHECK failed: %s (line %d)\n", #c, __LINE__); \
+      return 1;                                                    \
+    }                                                              \
+  } while (0)
+
+int main() {
+  ettg::RootedTree t{6, 0, {-1, 2, 0, 0, 0, 2}};
+  auto idx = ettg::inlabel_build(t);
+  CHECK(ettg::inlabel_lca(idx, 1, 5) == 2);
+  CHECK(ettg::inlabel_lca(idx, 3, 4) == 0);
+  auto ans = ettg::answer_batch(idx, {{1, 5}, {3, 4}, {5, 5}}, 2);
+  CHECK(ans.size() == 3 && ans[0] == 2 && ans[1] == 0 && ans[2] == 5);
+  auto r = ettg::rmq_lca_build(t);
+  CHECK(ettg::answer_batch(r, {{1, 5}}, 1)[0] == 2);
+  auto st = ettg::node_stats(t);
+  CHECK(st.preorder == std::vector<ettg::i64>({1, 3, 2, 5, 6, 4}));
+  bool threw = false;
+  try {
+    ettg::answer_batch(idx, {{0, 1}}, 0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    ettg::inlabel_build(ettg::RootedTree{3, 0, {-1, 2, 1}});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  ettg::EdgeList g{4, {{0, 1}, {1, 2}, {0, 2}, {2, 3}}};
+  ettg::PhaseTimes pt;
+  auto mask = ettg::tv_bridges(g, &pt);
+  CHECK(mask.is_bridge == std::vector<char>({0, 0, 0, 1}));
+  CHECK(mask.count() == 1 && pt.ms.size() == 3 && pt.ms[0].first == "spanning");
+  std::printf("shim ok\n");
+  return 0;
+}
