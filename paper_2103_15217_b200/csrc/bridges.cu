@@ -53,23 +53,13 @@ __global__ void k_edges_from_i64(const longlong2* __restrict__ in, u32 m, u32 n,
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
-__global__ void k_edges_check(const uint2* __restrict__ e2, u32 m, u32 n, u32* flags) {
-  u32 bad = 0;
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    const uint2 v = e2[e];
-    bad |= (v.x >= n) | (v.y >= n);
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
-}
-
 __global__ void k_iota(u32* __restrict__ a, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
 }
 
-// Representative with path halving; parents always point to smaller ids,
-// so the root of a tree is its minimum vertex.
-__device__ __forceinline__ u32 uf_find(u32* par, u32 x) {
-  u32 cur = par[x];
+// Representative with path halving, starting from an already loaded par[x];
+// parents always point to smaller ids, so a tree's root is its minimum vertex.
+__device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
   if (cur != x) {
     u32 prev = x, next;
     while (cur > (next = par[cur])) {
@@ -80,47 +70,96 @@ __device__ __forceinline__ u32 uf_find(u32* par, u32 x) {
   }
   return cur;
 }
+__device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(par, x, par[x]); }
 
-// One pass over the edges.  Hooking root a (> b) under b with CAS; on
-// failure retry from the value found.  Each successful CAS unions two
+// One pass over the edges, kHookE edges per thread: their parent loads and
+// first CAS attempts are issued together (the kernel is bound by dependent
+// L2 latency, profiles/r1_ncu_bridges.md).  Hooking root a (> b) under b with
+// CAS; on failure retry from the value found.  Each successful CAS unions two
 // distinct trees (a is the minimum of its own tree and b < a), so exactly
-// n - #components edges are marked.
+// n - #components edges are marked.  Endpoints are range-checked here (the
+// reference's build_adjacency check, core/src/graph.cpp:141-143) so the edge
+// list is read once.
+constexpr int kHookE = 4;
+
 __global__ void __launch_bounds__(256)
-    k_cc_hook(const uint2* __restrict__ edges, u32 m, u32* par, uint8_t* __restrict__ tree) {
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    const uint2 uv = edges[e];
-    u32 a = uf_find(par, uv.x);
-    u32 b = uf_find(par, uv.y);
-    uint8_t t = 0;
-    while (a != b) {
-      if (a < b) {
-        const u32 tmp = a;
-        a = b;
-        b = tmp;
+    k_cc_hook(const uint2* __restrict__ edges, u32 m, u32 n, u32* par,
+              uint8_t* __restrict__ tree, u32* flags) {
+  u32 bad = 0;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < m;
+       base += stride * kHookE) {
+    uint2 uv[kHookE];
+    bool ok[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      const u64 e = base + j * stride;
+      ok[j] = e < m;
+      uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
+      if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
+        bad = 1;
+        ok[j] = false;
+        tree[e] = 0;
       }
-      const u32 old = atomicCAS(&par[a], a, b);
-      if (old == a) {
-        t = 1;
-        break;
-      }
-      a = uf_find(par, old);
-      b = uf_find(par, b);
+      if (!ok[j]) uv[j] = make_uint2(0, 0);
     }
-    tree[e] = t;
+    u32 a[kHookE], b[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      a[j] = par[uv[j].x];
+      b[j] = par[uv[j].y];
+    }
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      a[j] = uf_find_from(par, uv[j].x, a[j]);
+      b[j] = uf_find_from(par, uv[j].y, b[j]);
+      if (a[j] < b[j]) {
+        const u32 tmp = a[j];
+        a[j] = b[j];
+        b[j] = tmp;
+      }
+    }
+    u32 old[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j)
+      old[j] = (ok[j] && a[j] != b[j]) ? atomicCAS(&par[a[j]], a[j], b[j]) : a[j];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      if (!ok[j]) continue;
+      uint8_t t = 0;
+      if (a[j] != b[j]) {
+        if (old[j] == a[j]) {
+          t = 1;
+        } else {  // another thread re-rooted a: retry from what the CAS found
+          u32 x = uf_find(par, old[j]), y = uf_find(par, b[j]);
+          while (x != y) {
+            if (x < y) {
+              const u32 tmp = x;
+              x = y;
+              y = tmp;
+            }
+            const u32 o = atomicCAS(&par[x], x, y);
+            if (o == x) {
+              t = 1;
+              break;
+            }
+            x = uf_find(par, o);
+            y = uf_find(par, y);
+          }
+        }
+      }
+      tree[base + j * stride] = t;
+    }
   }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
-// Tree-edge compaction functors: tedge[t] = e for the t-th tree edge.
-struct TreeIn {
-  const uint8_t* tree;
-  __device__ __forceinline__ u32 operator()(u64 i) const { return tree[i]; }
-};
+// Tree-edge compaction: tedge[t] = e for the t-th tree edge.
 struct TreeOut {
-  const uint8_t* tree;
   u32* tedge;
   u32 cap;
-  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
-    if (tree[i] && excl < cap) tedge[excl] = static_cast<u32>(i);
+  __device__ __forceinline__ void operator()(u64 i, u32 rank) const {
+    if (rank < cap) tedge[rank] = static_cast<u32>(i);
   }
 };
 
@@ -235,24 +274,47 @@ __global__ void k_lowhigh_init(uint2* __restrict__ lh, u32 n) {
 }
 
 // Non-tree edge {u, v} with pre(u) < pre(v): low(v) <- min(., pre(u)) and
-// high(u) <- max(., pre(v)).  (core/src/bridges.cpp:256-273)
+// high(u) <- max(., pre(v))  (core/src/bridges.cpp:256-273).  kHookE edges per
+// thread so their preorder gathers and extreme reads are in flight together;
+// an atomic is issued only when it can change the slot.
 __global__ void __launch_bounds__(256)
     k_lowhigh_edges(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
                     const u32* __restrict__ pre_of, uint2* lh) {
-  u32* w = reinterpret_cast<u32*>(lh);
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    if (tree[e]) continue;
-    const uint2 uv = edges[e];
-    u32 a = __ldg(pre_of + uv.x), b = __ldg(pre_of + uv.y);
-    if (a == b) continue;  // self-loop
-    if (a > b) {
-      const u32 t = a;
-      a = b;
-      b = t;
+  u32* w = reinterpret_cast<u32*>(lh);  // slot = preorder - 1; .x = low, .y = high
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < m;
+       base += stride * kHookE) {
+    uint2 uv[kHookE];
+    bool nt[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      const u64 e = base + j * stride;
+      nt[j] = e < m && !tree[e];
+      uv[j] = nt[j] ? edges[e] : make_uint2(0, 0);
     }
-    // slot index = preorder - 1; .x = low, .y = high
-    if (w[2 * (b - 1)] > a) atomicMin(&w[2 * (b - 1)], a);
-    if (w[2 * (a - 1) + 1] < b) atomicMax(&w[2 * (a - 1) + 1], b);
+    u32 pa[kHookE], pb[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      pa[j] = nt[j] ? __ldg(pre_of + uv[j].x) : 0u;
+      pb[j] = nt[j] ? __ldg(pre_of + uv[j].y) : 0u;
+    }
+    u32 cl[kHookE], ch[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      if (pa[j] > pb[j]) {
+        const u32 t = pa[j];
+        pa[j] = pb[j];
+        pb[j] = t;
+      }
+      nt[j] = nt[j] && pa[j] != pb[j];  // a self-loop changes nothing
+      cl[j] = nt[j] ? w[2 * (pb[j] - 1)] : 0u;
+      ch[j] = nt[j] ? w[2 * (pa[j] - 1) + 1] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      if (cl[j] > pa[j]) atomicMin(&w[2 * (pb[j] - 1)], pa[j]);
+      if (ch[j] < pb[j]) atomicMax(&w[2 * (pa[j] - 1) + 1], pb[j]);
+    }
   }
 }
 
@@ -414,11 +476,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     }
     edges = ws.edges;
   } else {
-    edges = static_cast<const uint2*>(edges_in);
-    if (m) {
-      k_edges_check<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
-      CK_LAUNCH();
-    }
+    edges = static_cast<const uint2*>(edges_in);  // range-checked inside k_cc_hook
   }
   if (m) CK(cudaMemsetAsync(d_mask, 0, m, st));
 
@@ -427,14 +485,15 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   CK_LAUNCH();
   if (m) {
     tr.mark("input");
-    k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, ws.par, ws.tree);
+    k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.par, ws.tree,
+                                                               ws.words);
     CK_LAUNCH();
     tr.mark("cc_hook");
   }
   CK(cudaEventRecord(ev[1], st));
 
   // ---- Euler tour of the forest, rooted at 0 -----------------------------
-  scan_exclusive(TreeIn{ws.tree}, TreeOut{ws.tree, ws.tedge, n}, m, ws.scan_m, ws.words + 1, st);
+  compact_u8(ws.tree, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
   u32 w[2];
   CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

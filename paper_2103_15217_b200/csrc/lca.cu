@@ -23,7 +23,7 @@
 //   k_tree_stats      preorder / level / size / inlabel / first position
 //                     (+ RMQ tour keys) in one pass per node
 //   k_head            head, label record {parent(head), level}, up-label
-//   k_path_asc        ascendant per label by a <= 31-hop chain walk
+//   k_asc_level       ascendant per label, one pass per trailing-zero level
 //   k_pack            16-B node record {inlabel, ascendant, level, 0}
 //
 // Half-edge ids: down(v) = 2v (parent -> v), up(v) = 2v+1 (v -> parent); the
@@ -189,19 +189,19 @@ __global__ void k_head(const u32* __restrict__ inlabel, const u32* __restrict__ 
   }
 }
 
-// ascendant(L) = OR of 2^tz over the label chain to the root's label.  Each
-// hop strictly raises tz, so <= 31 hops (replaces the log-n global rounds of
-// core/src/lca.cpp:59-78 with one independent walk per label).
-__global__ void k_path_asc(const u32* __restrict__ up, u32 n, u32* __restrict__ asc) {
-  for (u32 L = blockIdx.x * blockDim.x + threadIdx.x + 1; L <= n; L += gridDim.x * blockDim.x) {
-    u32 u = up[L];
-    if (u == kNone) continue;
-    u32 a = 1u << tz32(L);
-    for (int hop = 0; hop < 32 && u != 0u && u <= n; ++hop) {
-      a |= 1u << tz32(u);
-      u = up[u];
-    }
-    asc[L] = a;
+// ascendant(L) = ascendant(up(L)) | 2^tz(L), with up(L) the label of
+// parent(head(L)) and tz(up(L)) > tz(L) (core/src/lca.cpp:55-78).  Instead of
+// the reference's log-n global fix-point rounds, labels are resolved in
+// decreasing tz: labels with tz = t are exactly (2i+1)*2^t, so pass t touches
+// n/2^(t+1) labels and every label costs one gather of its (already final)
+// up-label.  ~25 small launches, n gathers in total.
+__global__ void k_asc_level(const u32* __restrict__ up, u32 n, int t, u32* __restrict__ asc) {
+  const u32 count = ((n >> t) + 1) >> 1;  // #odd multiples of 2^t in [1, n]
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const u32 L = ((2 * i + 1) << t);
+    const u32 u = up[L];
+    if (u == kNone) continue;  // unused label
+    asc[L] = (u == 0u ? 0u : asc[u]) | (1u << t);
   }
 }
 
@@ -590,8 +590,11 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   k_head<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->par, h->level, n,
                                                          h->head, h->lab, ws.up);
   CK_LAUNCH();
-  k_path_asc<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.up, n, ws.asc);
-  CK_LAUNCH();
+  for (int t = 31 - __builtin_clz(n); t >= 0; --t) {
+    const u32 count = ((n >> t) + 1) >> 1;
+    k_asc_level<<<std::min(g, blocks_for(count, 256)), 256, 0, st>>>(ws.up, n, t, ws.asc);
+    CK_LAUNCH();
+  }
   k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, ws.asc, n,
                                                          h->node);
   CK_LAUNCH();

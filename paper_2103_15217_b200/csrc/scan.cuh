@@ -143,6 +143,71 @@ __global__ void __launch_bounds__(kScanThreads)
 
 inline size_t scan_ws_words(u64 n) { return (n + kScanTile - 1) / kScanTile + 1; }
 
+// Stream compaction of a 0/1 byte-flag array: out(i, rank) for every set
+// flag, rank = number of set flags before i.  Each thread loads its 16 flags
+// as one 16-B vector (a warp reads 512 contiguous bytes), sums them with
+// byte arithmetic, and the tile prefix comes from the same look-back.
+// `flags` must be 16-B aligned.
+template <class Out>
+__global__ void __launch_bounds__(kScanThreads)
+    k_compact_u8(const uint8_t* __restrict__ flags, u64 n, Out out, u64* status, u32* ticket,
+                 u32* total) {
+  __shared__ u32 s_warp[kScanThreads / 32];
+  __shared__ u32 s_tile, s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u64 base = static_cast<u64>(tile) * kScanTile + static_cast<u64>(tid) * kScanItems;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (base + kScanItems <= n) {
+    v = *reinterpret_cast<const uint4*>(flags + base);
+  } else if (base < n) {
+    u32 w[4] = {0, 0, 0, 0};
+    for (u64 i = base; i < n; ++i) w[(i - base) >> 2] |= static_cast<u32>(flags[i]) << (8 * ((i - base) & 3));
+    v = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  const u32 cnt = ((v.x * 0x01010101u) >> 24) + ((v.y * 0x01010101u) >> 24) +
+                  ((v.z * 0x01010101u) >> 24) + ((v.w * 0x01010101u) >> 24);
+  const u32 incl = warp_incl_scan(cnt);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    const u32 wi = warp_incl_scan(w);
+    const u32 agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    const u32 pre = tile_lookback(status, tile, agg);
+    if (lane == 0) {
+      s_prefix = pre;
+      if (total && static_cast<u64>(tile + 1) * kScanTile >= n) *total = pre + agg;
+    }
+  }
+  __syncthreads();
+  u32 r = s_prefix + s_warp[warp] + (incl - cnt);
+  if (cnt) {
+    const u32 words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if ((words[j >> 2] >> (8 * (j & 3))) & 0xFFu) out(base + j, r++);
+    }
+  }
+}
+
+template <class Out>
+void compact_u8(const uint8_t* flags, u64 n, Out out, u64* status, u32* total, cudaStream_t st) {
+  if (n == 0) {
+    if (total) CK(cudaMemsetAsync(total, 0, sizeof(u32), st));
+    return;
+  }
+  const u64 tiles = (n + kScanTile - 1) / kScanTile;
+  CK(cudaMemsetAsync(status, 0, (tiles + 1) * sizeof(u64), st));
+  u32* ticket = reinterpret_cast<u32*>(status + tiles);
+  k_compact_u8<Out><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(flags, n, out, status,
+                                                                          ticket, total);
+  CK_LAUNCH();
+}
+
 // status must hold scan_ws_words(n) u64 words (last one doubles as ticket).
 template <class In, class Out>
 void scan_exclusive(In in, Out out, u64 n, u64* status, u32* total,
