@@ -323,6 +323,8 @@ def main():
     ap.add_argument("--cpu-road-side", type=int, default=1400)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--dist-backend", default="nccl")
+    ap.add_argument("--same-device", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -332,10 +334,16 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
+    # --same-device maps every rank to cuda:0 (validation of the N>1 path on
+    # a 1-GPU box; NCCL refuses duplicate devices, so it pairs with gloo).
+    local = 0 if args.same_device else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(args.dist_backend)
     import paper_2103_15217_b200 as ett
     peak = peaks()
 
