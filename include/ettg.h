@@ -52,6 +52,8 @@ extern "C" {
 
 #define ETTG_ENGINE_INLABEL 1u /* Schieber-Vishkin inlabel (core/src/lca.cpp:20-109) */
 #define ETTG_ENGINE_RMQ 2u     /* RMQ over the Euler tour (core/src/lca.cpp:128-157) */
+#define ETTG_ENGINE_NAIVE 4u   /* walk-up over pointer-jumping levels (core/src/lca.cpp:111-126,
+                                  core/src/primitives.cpp:208-241) */
 
 typedef struct ettg_lca ettg_lca;
 
@@ -103,6 +105,11 @@ int ettg_lca_query_engine(const ettg_lca* h, unsigned engine,
 int ettg_lca_query_dev(const ettg_lca* h, unsigned engine,
                        const uint32_t* d_pairs, int64_t q, uint32_t* d_answers,
                        void* stream);
+
+/* ancestor_doubling_levels (core/src/primitives.cpp:208-241): level[n] by
+ * pointer jumping on the device (validates like validate_tree). */
+int ettg_ancestor_levels(const int64_t* parent, int64_t n, int64_t root, int device,
+                         int64_t* level);
 
 /* NodeStats of the Euler tour (core/src/euler.cpp:119-155): 1-based
  * preorder, subtree size, level, parent (-1 at the root).  Any pointer may

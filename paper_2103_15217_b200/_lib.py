@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL = range(6)
 ENGINE_INLABEL = 1
 ENGINE_RMQ = 2
+ENGINE_NAIVE = 4
 
 _lock = threading.Lock()
 _lib = None
@@ -44,6 +45,7 @@ _SIGS = {
     "ettg_lca_query_engine": ([p, C.c_uint, p, i64, i64, p], C.c_int),
     "ettg_lca_query_dev": ([p, C.c_uint, p, i64, p, p], C.c_int),
     "ettg_lca_stats": ([p, p, p, p, p], C.c_int),
+    "ettg_ancestor_levels": ([p, i64, i64, C.c_int, p], C.c_int),
     "ettg_lca_inlabel_index": ([p, p, p, p, p, p], C.c_int),
     "ettg_lca_index_bytes": ([p, i64p], C.c_int),
     "ettg_lca_index_export_dev": ([p, p, p], C.c_int),

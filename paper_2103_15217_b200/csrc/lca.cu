@@ -246,6 +246,44 @@ __global__ void k_rmq_level(const u64* __restrict__ prev, u64* __restrict__ cur,
     cur[b] = min(prev[b], prev[b + half]);
 }
 
+// ---- naive engine: pointer-jumping levels + walk-up queries ----------------
+// ancestor_doubling_levels (core/src/primitives.cpp:208-241) and naive_lca
+// (core/src/lca.cpp:111-126).  State per node: (ancestor, distance); each
+// round doubles the jump (Wyllie), so ceil(log2 depth) rounds; a node whose
+// ancestor is not the root after bits(n)+1 rounds lies on a cycle.
+__global__ void k_dbl_init(const u32* __restrict__ par, u32 n, u32 root, uint2* __restrict__ st) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const u32 p = par[v];
+    st[v] = (v == root || p == kNone) ? make_uint2(v == root ? root : v, 0u) : make_uint2(p, 1u);
+  }
+}
+
+__global__ void k_dbl_round(const uint2* __restrict__ cur, uint2* __restrict__ nxt, u32 n) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint2 s = cur[v];
+    const uint2 a = cur[s.x];
+    nxt[v] = make_uint2(a.x, s.y + a.y);
+  }
+}
+
+// nrec[v] = {parent, level}; flags bit 0 set if some node never reached the root.
+__global__ void k_dbl_finish(const uint2* __restrict__ st, const u32* __restrict__ par, u32 n,
+                             u32 root, uint2* __restrict__ nrec, u32* flags) {
+  u32 bad = 0;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint2 s = st[v];
+    bad |= s.x != root;
+    nrec[v] = make_uint2(v == root ? kNone : par[v], s.y);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+__global__ void k_pack_naive(const u32* __restrict__ par, const u32* __restrict__ level, u32 n,
+                             uint2* __restrict__ nrec) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    nrec[v] = make_uint2(par[v], level[v]);
+}
+
 // ---- queries ---------------------------------------------------------------
 struct PairsU32 {
   const uint2* p;
@@ -347,6 +385,41 @@ __global__ void __launch_bounds__(kQThreads)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// naive_lca (core/src/lca.cpp:118-126): walk the deeper node up, then both.
+// One query per thread; cost is the x-y tree distance (the paper's baseline).
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads)
+    k_lca_naive(const uint2* __restrict__ nrec, u32 n, In in, Out out, u64 q, u32* err) {
+  u32 bad_any = 0;
+  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
+       i += static_cast<u64>(gridDim.x) * kQThreads) {
+    u32 x, y;
+    in.get(i, x, y);
+    if (x >= n || y >= n) {
+      bad_any = 1;
+      out.put(i, kNone);
+      continue;
+    }
+    uint2 rx = __ldg(nrec + x), ry = __ldg(nrec + y);
+    while (rx.y > ry.y) {
+      x = rx.x;
+      rx = __ldg(nrec + x);
+    }
+    while (ry.y > rx.y) {
+      y = ry.x;
+      ry = __ldg(nrec + y);
+    }
+    while (x != y) {
+      x = rx.x;
+      y = ry.x;
+      rx = __ldg(nrec + x);
+      ry = __ldg(nrec + y);
+    }
+    out.put(i, x);
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 struct RmqView {
   const u64* key;
   const u64* pre_in;
@@ -417,6 +490,8 @@ struct ettg_lca {
   // rmq
   u64 *tkey = nullptr, *pre_in = nullptr, *suf_in = nullptr, *sp = nullptr;
   u32 nb = 0, levels = 0;
+  // naive
+  uint2* nrec = nullptr;
   // host-query staging (lazy)
   char* qmem = nullptr;
   u64 qchunk = 0;
@@ -424,8 +499,11 @@ struct ettg_lca {
   double build_ms = 0;
 
   void carve(Carver& c) {
-    node = c.take<uint4>(n);
-    lab = c.take<uint2>(static_cast<u64>(n) + 1);
+    if (engines & ETTG_ENGINE_INLABEL) {
+      node = c.take<uint4>(n);
+      lab = c.take<uint2>(static_cast<u64>(n) + 1);
+    }
+    if (engines & ETTG_ENGINE_NAIVE) nrec = c.take<uint2>(n);
     if (!full) return;
     par = c.take<u32>(n);
     pre = c.take<u32>(n);
@@ -497,12 +575,98 @@ void launch_stats_rmq(ettg_lca* h, cudaStream_t st, int sms) {
   }
 }
 
+// naive_build (core/src/lca.cpp:111-116): validate + pointer-jumping levels.
+ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64_t root64,
+                           int device, cudaStream_t user_st) {
+  const u32 n = static_cast<u32>(n64), root = static_cast<u32>(root64);
+  const int sms = sm_count(device);
+  const unsigned g = sms * 8;
+  auto h = std::make_unique<ettg_lca>();
+  h->device = device;
+  h->n = n;
+  h->root = root;
+  h->engines = ETTG_ENGINE_NAIVE;
+  h->full = false;
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  cudaStream_t st = user_st ? user_st : h->stream;
+  Carver hc;
+  h->carve(hc);
+  CK(cudaMalloc(&h->mem, hc.off));
+  hc = Carver{h->mem};
+  h->carve(hc);
+  struct Ws {
+    int64_t* par64 = nullptr;
+    u32 *par = nullptr, *keys = nullptr, *vals = nullptr, *flags = nullptr;
+    uint2 *s0 = nullptr, *s1 = nullptr;
+    void carve(Carver& c, u32 n, bool h64) {
+      if (h64) par64 = c.take<int64_t>(n);
+      par = c.take<u32>(n);
+      keys = c.take<u32>(n);
+      vals = c.take<u32>(n);
+      s0 = c.take<uint2>(n);
+      s1 = c.take<uint2>(n);
+      flags = c.take<u32>(8);
+    }
+  } ws;
+  Carver wc;
+  ws.carve(wc, n, host_i64);
+  Lease lease(device, st, wc.off);
+  wc = Carver{lease.base()};
+  ws.carve(wc, n, host_i64);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  CK(cudaMemsetAsync(ws.flags, 0, 8 * sizeof(u32), st));
+  const unsigned gb = std::min(g, blocks_for(n, 256));
+  if (host_i64) {
+    CK(cudaMemcpyAsync(ws.par64, parent, static_cast<u64>(n) * 8, cudaMemcpyHostToDevice, st));
+    k_tree_validate<int64_t><<<gb, 256, 0, st>>>(ws.par64, n, root, ws.par, ws.keys, ws.vals,
+                                                 ws.flags);
+  } else {
+    k_tree_validate<u32><<<gb, 256, 0, st>>>(static_cast<const u32*>(parent), n, root, ws.par,
+                                             ws.keys, ws.vals, ws.flags);
+  }
+  CK_LAUNCH();
+  k_dbl_init<<<gb, 256, 0, st>>>(ws.par, n, root, ws.s0);
+  CK_LAUNCH();
+  uint2* cur = ws.s0;
+  uint2* nxt = ws.s1;
+  const int rounds = (32 - __builtin_clz(n)) + 1;
+  for (int r = 0; r < rounds; ++r) {
+    k_dbl_round<<<gb, 256, 0, st>>>(cur, nxt, n);
+    CK_LAUNCH();
+    std::swap(cur, nxt);
+  }
+  k_dbl_finish<<<gb, 256, 0, st>>>(cur, ws.par, n, root, h->nrec, ws.flags + 1);
+  CK_LAUNCH();
+  CK(cudaEventRecord(e1, st));
+  u32 vflags[8];
+  CK(cudaMemcpyAsync(vflags, ws.flags, sizeof vflags, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (vflags[0] & kVRootParent) einval("root has no kNone parent entry");
+  if (vflags[0] & kVRange) einval("parent id out of range");
+  if (vflags[0] & kVRoots) einval("tree must have exactly one root");
+  if (vflags[1]) einval("cycle in parent array");
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  h->build_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return h.release();
+}
+
 ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
                       int64_t root64, int device, unsigned engines, cudaStream_t user_st) {
   if (n64 <= 0) einval("parent array size mismatch");
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
   if (engines == 0) engines = ETTG_ENGINE_INLABEL;
+  if (engines & ~(ETTG_ENGINE_INLABEL | ETTG_ENGINE_RMQ | ETTG_ENGINE_NAIVE))
+    einval("unknown engine flag");
+  if (engines == ETTG_ENGINE_NAIVE)
+    return build_naive_only(parent, host_i64, n64, root64, device, user_st);
+  engines |= ETTG_ENGINE_INLABEL;  // the Euler-tour build yields it for free
   const u32 n = static_cast<u32>(n64), root = static_cast<u32>(root64);
   const int sms = sm_count(device);
 
@@ -601,6 +765,10 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   tr.mark("head_asc_pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
   tr.mark("rmq");
+  if (engines & ETTG_ENGINE_NAIVE) {
+    k_pack_naive<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->par, h->level, n, h->nrec);
+    CK_LAUNCH();
+  }
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -629,13 +797,18 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
                   cudaStream_t st) {
   if (q == 0) return;
   const int sms = sm_count(h->device);
-  if (engine == ETTG_ENGINE_RMQ) {
+  if (engine == ETTG_ENGINE_NAIVE) {
+    if (!h->nrec) einval("index was built without the naive engine");
+    unsigned blocks = std::min<u64>((q + kQThreads - 1) / kQThreads, u64(sms) * 16);
+    k_lca_naive<In, Out><<<blocks, kQThreads, 0, st>>>(h->nrec, h->n, in, out, q, err);
+  } else if (engine == ETTG_ENGINE_RMQ) {
     if (!(h->engines & ETTG_ENGINE_RMQ) || !h->tkey)
       einval("index was built without the RMQ engine");
     RmqView rv{h->tkey, h->pre_in, h->suf_in, h->sp, h->first, h->nb};
     unsigned blocks = std::min<u64>((q + kQThreads - 1) / kQThreads, u64(sms) * 16);
     k_lca_rmq<In, Out><<<blocks, kQThreads, 0, st>>>(rv, h->n, in, out, q, err);
   } else {
+    if (!h->node) einval("index was built without the inlabel engine");
     const u64 per = u64(kQThreads) * kQPer;
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * 16);
     k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->lab, h->n, in, out, q, err);
@@ -764,7 +937,7 @@ int ettg_lca_stats(const ettg_lca* h, int64_t* preorder, int64_t* size, int64_t*
                    int64_t* parent) {
   return guard([&] {
     if (!h) einval("null handle");
-    if (!h->full) einval("attached replica has no node statistics");
+    if (!h->full) einval("index has no Euler-tour statistics (attached replica or naive-only)");
     DeviceScope ds(h->device);
     copy_widen(preorder, h->pre, h->n, h->stream);
     copy_widen(size, h->size, h->n, h->stream);
@@ -777,7 +950,7 @@ int ettg_lca_inlabel_index(const ettg_lca* h, int64_t* inlabel, uint64_t* ascend
                            int64_t* head, int64_t* level, int64_t* parent) {
   return guard([&] {
     if (!h) einval("null handle");
-    if (!h->full) einval("attached replica has no exportable index fields");
+    if (!h->full) einval("index has no exportable inlabel fields (attached replica or naive-only)");
     DeviceScope ds(h->device);
     copy_widen(inlabel, h->inlabel, h->n, h->stream);
     copy_widen(head, h->head, static_cast<u64>(h->n) + 1, h->stream);
@@ -793,9 +966,25 @@ int ettg_lca_inlabel_index(const ettg_lca* h, int64_t* inlabel, uint64_t* ascend
   });
 }
 
+int ettg_ancestor_levels(const int64_t* parent, int64_t n, int64_t root, int device,
+                         int64_t* level) {
+  return guard([&] {
+    if (!parent || !level) einval("null argument");
+    DeviceScope ds(device);
+    std::unique_ptr<ettg_lca> h(
+        build_index(parent, true, false, n, root, device, ETTG_ENGINE_NAIVE, nullptr));
+    std::vector<uint2> rec(h->n);
+    CK(cudaMemcpyAsync(rec.data(), h->nrec, static_cast<u64>(h->n) * 8, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (u32 v = 0; v < h->n; ++v) level[v] = rec[v].y;
+  });
+}
+
 int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes) {
   return guard([&] {
     if (!h || !bytes) einval("null argument");
+    if (!h->node) einval("index has no inlabel engine");
     *bytes = static_cast<int64_t>(h->n) * 16 + (static_cast<int64_t>(h->n) + 1) * 8;
   });
 }
@@ -803,6 +992,7 @@ int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes) {
 int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
   return guard([&] {
     if (!h || !d_dst) einval("null argument");
+    if (!h->node) einval("index has no inlabel engine");
     DeviceScope ds(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char* dst = static_cast<char*>(d_dst);

@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import ENGINE_INLABEL, ENGINE_RMQ, InvalidArgument, OutOfRange, check, lib, ptr
+from ._lib import (ENGINE_INLABEL, ENGINE_NAIVE, ENGINE_RMQ, InvalidArgument, OutOfRange, check,
+                   lib, ptr)
 
 K_NONE = -1
 K_GRASP_INFINITY = (1 << 64) - 1
@@ -154,6 +155,10 @@ class RmqLcaIndex(_LcaHandle):
     """core/include/ett/lca.hpp:39-44 (block-sparse table on the device)."""
 
 
+class NaiveIndex(_LcaHandle):
+    """core/include/ett/lca.hpp:29-35: parent + pointer-jumping levels."""
+
+
 def _build(tree: RootedTree, engines: int, device: int):
     h = C.c_void_p()
     check(lib().ettg_lca_build(ptr(tree.parent), int(tree.n), int(tree.root), device, engines,
@@ -184,6 +189,23 @@ def rmq_lca_build(tree: RootedTree, device: int = 0) -> RmqLcaIndex:
     return RmqLcaIndex(_build(tree, ENGINE_RMQ, device), tree.n, device, ENGINE_RMQ)
 
 
+def naive_build(tree: RootedTree, device: int = 0) -> NaiveIndex:
+    """naive_build (core/src/lca.cpp:111-116): levels by pointer jumping."""
+    if len(tree.parent) != tree.n:
+        raise InvalidArgument("parent array size mismatch")
+    return NaiveIndex(_build(tree, ENGINE_NAIVE, device), tree.n, device, ENGINE_NAIVE)
+
+
+def ancestor_doubling_levels(tree: RootedTree, device: int = 0) -> np.ndarray:
+    """ancestor_doubling_levels (core/src/primitives.cpp:208-241)."""
+    if len(tree.parent) != tree.n:
+        raise InvalidArgument("parent array size mismatch")
+    out = np.empty(tree.n, np.int64)
+    check(lib().ettg_ancestor_levels(ptr(tree.parent), int(tree.n), int(tree.root), device,
+                                     ptr(out)))
+    return out
+
+
 def attach_index(d_src, n: int, device: int = 0, stream: int | None = None) -> InlabelIndex:
     """Query-only replica of a packed inlabel index (multi-GPU)."""
     h = C.c_void_p()
@@ -193,7 +215,8 @@ def attach_index(d_src, n: int, device: int = 0, stream: int | None = None) -> I
 
 def answer_batch(index: _LcaHandle, queries, batch_size: int) -> np.ndarray:
     """answer_batch (core/include/ett/lca.hpp:50-65) for the index's engine."""
-    engine = ENGINE_RMQ if isinstance(index, RmqLcaIndex) else ENGINE_INLABEL
+    engine = (ENGINE_RMQ if isinstance(index, RmqLcaIndex) else
+              ENGINE_NAIVE if isinstance(index, NaiveIndex) else ENGINE_INLABEL)
     return index.query(queries, batch_size, engine)
 
 
@@ -203,6 +226,10 @@ def inlabel_lca(index: InlabelIndex, x: int, y: int) -> int:
 
 def rmq_lca(index: RmqLcaIndex, x: int, y: int) -> int:
     return int(index.query(np.array([[x, y]], np.int64), 1, ENGINE_RMQ)[0])
+
+
+def naive_lca(index: NaiveIndex, x: int, y: int) -> int:
+    return int(index.query(np.array([[x, y]], np.int64), 1, ENGINE_NAIVE)[0])
 
 
 def node_stats(tree: RootedTree, device: int = 0) -> NodeStats:

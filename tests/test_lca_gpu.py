@@ -183,3 +183,55 @@ def test_device_query_and_counter_mode_generator(ett, ref):
     d2 = torch.empty(2 * 1000, dtype=torch.int32, device="cuda:0")
     assert ett.gen_queries_dev(t.n, 1000, 3, 5000, d2)
     assert np.array_equal(d2.cpu().numpy().astype(np.int64).reshape(-1, 2), host[5000:6000])
+
+
+# ------------------------------------------------------------- naive engine
+def test_naive_golden(ett):
+    # tests/lca_test.cpp:76-90
+    t = ett.RootedTree(6, 0, EXAMPLE)
+    idx = ett.naive_build(t)
+    assert ett.naive_lca(idx, 1, 5) == 2
+    assert ett.naive_lca(idx, 4, 4) == 4
+    k = 64
+    path = ett.RootedTree(k, 0, np.arange(-1, k - 1))
+    assert ett.naive_lca(ett.naive_build(path), 0, k - 1) == 0
+
+
+def test_three_engines_agree_on_corpus(ett, ref):
+    """acceptance criterion 2: inlabel == naive == rmq == walk-up oracle."""
+    for ti, t in enumerate(lca_corpus(ett, count=60, seed=2024)):
+        q = ett.sample_queries(t.n, 2000, ti + 1)
+        want = ref.lca("naive", t.parent, t.root, q)
+        nv = ett.naive_build(t)
+        assert np.array_equal(ett.answer_batch(nv, q, 500), want), ti
+        mixed = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.ENGINE_RMQ | ett.ENGINE_NAIVE)
+        for eng in (ett.ENGINE_INLABEL, ett.ENGINE_RMQ, ett.ENGINE_NAIVE):
+            assert np.array_equal(mixed.query(q, len(q), eng), want), (ti, eng)
+
+
+@pytest.mark.parametrize("gamma", [1, 7, GRASP_INF])
+def test_ancestor_doubling_levels(ett, ref, gamma):
+    t = ett.permute_labels(ett.grasp_tree(300_007, gamma, 3), 4)
+    lev = ett.ancestor_doubling_levels(t)
+    _, _, want, _ = ref.node_stats(t.parent, t.root)
+    assert np.array_equal(lev, want)
+
+
+def test_depth_law(ett):
+    """acceptance criterion 5 (tests/acceptance.cpp:221-257): mean grasp depth."""
+    n = 1_000_000
+    for gamma, target in [(GRASP_INF, np.log(n)), (100, n / 101), (1000, n / 1001)]:
+        means = [ett.ancestor_doubling_levels(ett.grasp_tree(n, gamma, s)).mean() for s in range(5)]
+        assert abs(np.mean(means) - target) / target < 0.15, gamma
+
+
+def test_naive_errors(ett):
+    with pytest.raises(ett.InvalidArgument, match="cycle"):
+        ett.naive_build(ett.RootedTree(3, 0, np.array([-1, 2, 1])))
+    with pytest.raises(ett.InvalidArgument, match="out of range"):
+        ett.naive_build(ett.RootedTree(3, 0, np.array([-1, 0, 9])))
+    idx = ett.naive_build(ett.RootedTree(3, 0, np.array([-1, 0, 0])))
+    with pytest.raises(ett.InvalidArgument):
+        idx.query(np.array([[0, 1]]), 1, ett.ENGINE_INLABEL)  # engine not built
+    with pytest.raises(ett.InvalidArgument):
+        idx.stats()
