@@ -60,11 +60,17 @@ typedef struct ettg_lca ettg_lca;
 /* Per-phase device times of one bridges call, named as the reference's
  * PhaseTimes (core/src/bridges.cpp:292-314). */
 typedef struct ettg_phase_times {
-  double spanning_ms; /* connected-components spanning forest      */
-  double euler_ms;    /* tree CSR, Euler tour, list rank, preorder   */
-  double lowhigh_ms;  /* low/high, subtree RMQ, classification       */
-  double total_ms;    /* device time of the whole call              */
+  double spanning_ms; /* spanning tree: CC hooking (tv, hybrid) or BFS (ck) */
+  double euler_ms;    /* Euler tour, list rank, preorder (tv, hybrid)       */
+  double lowhigh_ms;  /* low/high, subtree RMQ, classification (tv)         */
+  double total_ms;    /* device time of the whole call                     */
+  double marking_ms;  /* CK marking + classification (ck, hybrid)          */
 } ettg_phase_times;
+
+/* Bridge engines (core/include/ett/bridges.hpp:55-62). */
+#define ETTG_BRIDGES_TV 0     /* Tarjan-Vishkin (tv_bridges)                  */
+#define ETTG_BRIDGES_CK 1     /* BFS tree + Chaitanya-Kothapalli marking     */
+#define ETTG_BRIDGES_HYBRID 2 /* CC spanning tree + Euler rooting + marking  */
 
 const char* ettg_last_error(void);
 int ettg_version(void);
@@ -145,6 +151,27 @@ int ettg_bridges(const int64_t* edges, int64_t n, int64_t m, int device,
 int ettg_bridges_dev(const uint32_t* d_edges, int64_t n, int64_t m, int device,
                      uint8_t* d_is_bridge, void* stream,
                      ettg_phase_times* times);
+
+/* ck_bridges / hybrid_bridges / tv_bridges by engine id. */
+int ettg_bridges_engine(const int64_t* edges, int64_t n, int64_t m, int device,
+                        int engine, uint8_t* is_bridge, ettg_phase_times* times);
+int ettg_bridges_dev_engine(const uint32_t* d_edges, int64_t n, int64_t m,
+                            int device, int engine, uint8_t* d_is_bridge,
+                            void* stream, ettg_phase_times* times);
+
+/* ---------------------------------------------------------- ingestion -- */
+/* build_adjacency (core/src/graph.cpp:135-173) on the device: offsets[n+1],
+ * neighbors[2m], edge_ids[2m], slices sorted by (neighbor, edge id);
+ * bit-identical to the reference. */
+int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
+                         int64_t* offsets, int64_t* neighbors,
+                         int64_t* edge_ids);
+/* bfs_tree (core/src/bridges.cpp:198-249): tree_mask[m], level[n],
+ * parent[n], parent_edge[n] (-1 at the root); minimum (parent, edge id)
+ * proposals, bit-identical to the reference. */
+int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root,
+                  int device, uint8_t* tree_mask, int64_t* level,
+                  int64_t* parent, int64_t* parent_edge);
 
 /* ------------------------------------------------------------ tuning -- */
 /* cudaLimitMaxL2FetchGranularity for the device's context (bytes: 0..128).

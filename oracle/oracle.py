@@ -186,6 +186,31 @@ class Ref:
         return mask, ph
 
 
+def ref_build_adjacency(n, edges):
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    off = np.empty(n + 1, np.int64)
+    nbr = np.empty(max(2 * m, 1), np.int64)
+    eid = np.empty(max(2 * m, 1), np.int64)
+    _rc(ref(), ref().ref_build_adjacency(i64(n), i64(m), _p(edges), _p(off), _p(nbr), _p(eid)),
+        "ref_last_error")
+    return off, nbr[:2 * m], eid[:2 * m]
+
+
+def ref_bfs_tree(n, edges, root=0):
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    mask = np.empty(max(m, 1), np.uint8)
+    lev, par, pe = (np.empty(n, np.int64) for _ in range(3))
+    _rc(ref(), ref().ref_bfs_tree(i64(n), i64(m), _p(edges), i64(root), _p(mask), _p(lev),
+                                  _p(par), _p(pe)), "ref_last_error")
+    return mask[:m], lev, par, pe
+
+
+Ref.build_adjacency = staticmethod(ref_build_adjacency)
+Ref.bfs_tree = staticmethod(ref_bfs_tree)
+
+
 class RefInlabel:
     """Built reference InlabelIndex for timing build and queries apart."""
 

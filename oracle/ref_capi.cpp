@@ -287,4 +287,28 @@ int ref_spanning_tree_hooking(int64_t n, int64_t m, const int64_t* edges,
   });
 }
 
+// build_adjacency (core/src/graph.cpp:135-173): offsets[n+1], nbr[2m], eid[2m].
+int ref_build_adjacency(int64_t n, int64_t m, const int64_t* edges, int64_t* offsets,
+                        int64_t* neighbors, int64_t* edge_ids) {
+  return guard([&] {
+    AdjacencyIndex a = build_adjacency(make_edges(n, m, edges));
+    std::memcpy(offsets, a.offsets.data(), (n + 1) * sizeof(int64_t));
+    std::memcpy(neighbors, a.neighbors.data(), 2 * m * sizeof(int64_t));
+    std::memcpy(edge_ids, a.edge_ids.data(), 2 * m * sizeof(int64_t));
+  });
+}
+
+// bfs_tree (core/src/bridges.cpp:198-249) from `root`.
+int ref_bfs_tree(int64_t n, int64_t m, const int64_t* edges, int64_t root, uint8_t* tree_mask,
+                 int64_t* level, int64_t* parent, int64_t* parent_edge) {
+  return guard([&] {
+    AdjacencyIndex a = build_adjacency(make_edges(n, m, edges));
+    SpanningTree st = bfs_tree(a, root);
+    for (int64_t e = 0; e < m; ++e) tree_mask[e] = st.is_tree_edge[e] ? 1 : 0;
+    std::memcpy(level, st.level.data(), n * sizeof(int64_t));
+    std::memcpy(parent, st.rooted.parent.data(), n * sizeof(int64_t));
+    std::memcpy(parent_edge, st.parent_edge.data(), n * sizeof(int64_t));
+  });
+}
+
 }  // extern "C"

@@ -5,9 +5,10 @@ include/ettg.h for the C-ABI underneath.
 """
 from . import _lib
 from .ett import *  # noqa: F401,F403
-from .ett import (BridgeMask, EdgeList, InlabelIndex, NodeStats, RmqLcaIndex, RootedTree,
-                  answer_batch, inlabel_build, inlabel_lca, node_stats, rmq_lca, rmq_lca_build,
-                  tv_bridges)
+from .ett import (AdjacencyIndex, BridgeMask, EdgeList, InlabelIndex, NaiveIndex, NodeStats,
+                  RmqLcaIndex, RootedTree, SpanningTree, answer_batch, bfs_tree, build_adjacency,
+                  ck_bridges, hybrid_bridges, inlabel_build, inlabel_lca, naive_build, naive_lca,
+                  node_stats, rmq_lca, rmq_lca_build, tv_bridges)
 from ._lib import InvalidArgument, OutOfRange, lib
 
 __all__ = [

@@ -28,7 +28,11 @@ i64p = C.POINTER(C.c_int64)
 
 class PhaseTimes(C.Structure):
     _fields_ = [("spanning_ms", C.c_double), ("euler_ms", C.c_double),
-                ("lowhigh_ms", C.c_double), ("total_ms", C.c_double)]
+                ("lowhigh_ms", C.c_double), ("total_ms", C.c_double),
+                ("marking_ms", C.c_double)]
+
+
+BRIDGES_TV, BRIDGES_CK, BRIDGES_HYBRID = 0, 1, 2
 
 
 _SIGS = {
@@ -54,6 +58,11 @@ _SIGS = {
     "ettg_bridges_dev": ([p, i64, i64, C.c_int, p, p, C.POINTER(PhaseTimes)], C.c_int),
     "ettg_set_l2_fetch_granularity": ([C.c_int, C.c_int], C.c_int),
     "ettg_get_l2_fetch_granularity": ([C.c_int, C.POINTER(C.c_int)], C.c_int),
+    "ettg_bridges_engine": ([p, i64, i64, C.c_int, C.c_int, p, C.POINTER(PhaseTimes)], C.c_int),
+    "ettg_bridges_dev_engine": ([p, i64, i64, C.c_int, C.c_int, p, p, C.POINTER(PhaseTimes)],
+                                C.c_int),
+    "ettg_build_adjacency": ([p, i64, i64, C.c_int, p, p, p], C.c_int),
+    "ettg_bfs_tree": ([p, i64, i64, i64, C.c_int, p, p, p, p], C.c_int),
     "ettg_list_rank_dev": ([p, i64, i64, p, C.c_int, p], C.c_int),
     "ettg_exclusive_scan_dev": ([p, i64, p, C.c_int, p], C.c_int),
     "ettg_sort_pairs_dev": ([p, p, i64, p, p, C.c_int, p], C.c_int),

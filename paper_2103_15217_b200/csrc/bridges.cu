@@ -37,6 +37,7 @@
 #include "common.cuh"
 #include "listrank.cuh"
 #include "scan.cuh"
+#include "graph.cuh"
 #include "trace.cuh"
 
 namespace ettg {
@@ -154,6 +155,15 @@ __global__ void __launch_bounds__(256)
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
+__global__ void k_cc_range(const uint2* __restrict__ edges, u32 m, u32 n, u32* flags) {
+  u32 bad = 0;
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint2 uv = edges[e];
+    bad |= (uv.x >= n) | (uv.y >= n);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
 // Tree-edge compaction: tedge[t] = e for the t-th tree edge.
 struct TreeOut {
   u32* tedge;
@@ -239,6 +249,8 @@ struct StatsOut {
   u32* pre_of;         // [n]   node -> preorder
   u32* size_by_pre;    // [n]
   u32* pedge_by_pre;   // [n]   input edge id to the parent
+  uint2* rec_of;       // [n]   node -> {parent, level} (hybrid engine), or null
+  u32* pedge_of;       // [n]   node -> parent edge (hybrid engine), or null
   __device__ __forceinline__ void operator()(u64 pos, u32 dbefore) const {
     const u32 f = flags[pos];
     if (!(f & 1u)) return;
@@ -257,14 +269,24 @@ struct StatsOut {
       pre_of[child] = pre;
       size_by_pre[pre - 1] = (pos_up - static_cast<u32>(pos) + 1) >> 1;
       pedge_by_pre[pre - 1] = e;
+      if (rec_of) {  // euler_root_tree's parent / level (core/src/bridges.cpp:184-193)
+        rec_of[child] = make_uint2(first_is_down ? uv.x : uv.y,
+                                   2 * dbefore - static_cast<u32>(pos) + 1);
+        pedge_of[child] = e;
+      }
     }
   }
 };
 
-__global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32* pedge_by_pre) {
+__global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32* pedge_by_pre,
+                             uint2* rec_of, u32* pedge_of) {
   pre_of[root] = 1;
   size_by_pre[0] = n;
   pedge_by_pre[0] = kNone;
+  if (rec_of) {
+    rec_of[root] = make_uint2(kNone, 0u);
+    pedge_of[root] = kNone;
+  }
 }
 
 // lh[i] = (low seed, high seed) = (i + 1, i + 1): each node's own preorder.
@@ -398,8 +420,24 @@ struct BridgeWs {
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
   u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
-  void carve(Carver& c, u32 n, u32 m, bool host_i64) {
+  // CK / hybrid
+  uint2* rec = nullptr;     // {parent, level} per node
+  u32* pedge_of = nullptr;  // parent edge per node
+  uint8_t* marked = nullptr;
+  u32 *blevel = nullptr, *bparent = nullptr;
+  BfsWs bfs;
+  void carve(Carver& c, u32 n, u32 m, bool host_i64, int engine) {
     const u32 k = 2 * (n - 1);
+    if (engine != ETTG_BRIDGES_TV) {
+      rec = c.take<uint2>(n);
+      pedge_of = c.take<u32>(n);
+      marked = c.take<uint8_t>(n + 16);
+    }
+    if (engine == ETTG_BRIDGES_CK) {
+      blevel = c.take<u32>(n);
+      bparent = c.take<u32>(n);
+      bfs.carve(c, n, m);
+    }
     if (host_i64) {
       e64 = c.take<longlong2>(m);
       edges = c.take<uint2>(m);
@@ -427,10 +465,12 @@ struct BridgeWs {
 
 void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int device,
                  uint8_t* d_mask_user, uint8_t* h_mask, cudaStream_t st_in,
-                 ettg_phase_times* times) {
+                 ettg_phase_times* times, int engine) {
   if (n64 <= 0) einval("empty graph");
   if (n64 >= (i64(1) << 31) || m64 >= (i64(1) << 31) || m64 < 0)
     einval("graph too large for packed hooking keys");
+  if (engine != ETTG_BRIDGES_TV && engine != ETTG_BRIDGES_CK && engine != ETTG_BRIDGES_HYBRID)
+    einval("unknown bridges engine");
   const u32 n = static_cast<u32>(n64), m = static_cast<u32>(m64);
   const int sms = sm_count(device);
   const unsigned g = sms * 8;
@@ -446,12 +486,12 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
 
   BridgeWs ws;
   Carver c;
-  ws.carve(c, n, m, host_i64);
+  ws.carve(c, n, m, host_i64, engine);
   uint8_t* d_mask = d_mask_user;
   if (!d_mask) d_mask = c.take<uint8_t>(m + 16);
   Lease lease(device, st, c.off);
   c = Carver{lease.base()};
-  ws.carve(c, n, m, host_i64);
+  ws.carve(c, n, m, host_i64, engine);
   if (!d_mask_user) d_mask = c.take<uint8_t>(m + 16);
 
   cudaEvent_t ev[4];
@@ -476,90 +516,126 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     }
     edges = ws.edges;
   } else {
-    edges = static_cast<const uint2*>(edges_in);  // range-checked inside k_cc_hook
+    edges = static_cast<const uint2*>(edges_in);  // range-checked inside k_cc_hook / below
   }
   if (m) CK(cudaMemsetAsync(d_mask, 0, m, st));
+  tr.mark("input");
+  u32 lerr = 0;
 
-  // ---- spanning forest --------------------------------------------------
-  k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
-  CK_LAUNCH();
-  if (m) {
-    tr.mark("input");
-    k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.par, ws.tree,
-                                                               ws.words);
+  if (engine == ETTG_BRIDGES_CK) {
+    // ---- ck_bridges (core/src/bridges.cpp:477-485): BFS tree + marking ----
+    // BFS indexes vertices straight from the edge list: check the range first
+    if (!host_i64 && m) {
+      k_cc_range<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
+      CK_LAUNCH();
+    }
+    u32 bad = 0;
+    read_back(&bad, ws.words, 4, st);
+    if (bad) einval("edge endpoint out of range");
+    if (m) CK(cudaMemsetAsync(ws.tree, 0, m, st));
+    const u32 reached = run_bfs(edges, n, m, 0, ws.blevel, ws.bparent, ws.pedge_of, ws.tree,
+                                ws.bfs, st, sms);
+    if (reached != n) einval("disconnected graph; extract the largest component first");
+    tr.mark("bfs");
+    CK(cudaEventRecord(ev[1], st));
+    CK(cudaEventRecord(ev[2], st));
+    k_pack_rec<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.bparent, ws.blevel, n, ws.rec);
     CK_LAUNCH();
-    tr.mark("cc_hook");
-  }
-  CK(cudaEventRecord(ev[1], st));
+  } else {
+    // ---- spanning forest --------------------------------------------------
+    k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+    CK_LAUNCH();
+    if (m) {
+      k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.par, ws.tree,
+                                                                 ws.words);
+      CK_LAUNCH();
+      tr.mark("cc_hook");
+    }
+    CK(cudaEventRecord(ev[1], st));
 
-  // ---- Euler tour of the forest, rooted at 0 -----------------------------
-  compact_u8(ws.tree, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
-  u32 w[2];
-  CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (w[0]) einval("edge endpoint out of range");
-  const u32 T = w[1];
-  if (T != n - 1) einval("disconnected graph; extract the largest component first");
-
-  if (n > 1) {
-    const u32 k = 2 * T;
-    CK(cudaMemsetAsync(ws.head, 0xFF, static_cast<u64>(n) * 4, st));
-    tr.mark("compact");
-    k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, 0, ws.head,
-                                                                ws.nxt, ws.tend, ws.words + 4);
-    CK_LAUNCH();
-    k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words);
-    CK_LAUNCH();
-    u32 hw[2];
-    CK(cudaMemcpyAsync(hw, ws.words + 2, sizeof hw, cudaMemcpyDeviceToHost, st));
+    // ---- Euler tour of the forest, rooted at 0 ---------------------------
+    compact_u8(ws.tree, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
+    u32 w[2];
+    CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const u32 head = hw[0];
-    k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.tend, ws.head, ws.nxt, k,
-                                                                 hw[1], ws.lr.succ0);
-    CK_LAUNCH();
-    tr.mark("rotation");
-    list_rank_core(k, head, NoDown{}, ws.lr, st, sms);
-    tr.mark("list_rank");
-    const Lr0View lv = lr0_view(ws.lr);
-    k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
-    CK_LAUNCH();
-    scan_exclusive(DownIn{ws.flags},
-                   StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of, ws.size_by_pre,
-                            ws.pedge_by_pre},
-                   k, ws.scan_k, nullptr, st);
-    tr.mark("preorder");
-  }
-  k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre);
-  CK_LAUNCH();
-  CK(cudaEventRecord(ev[2], st));
+    if (w[0]) einval("edge endpoint out of range");
+    const u32 T = w[1];
+    if (T != n - 1) einval("disconnected graph; extract the largest component first");
 
-  // ---- low / high + classification ---------------------------------------
-  k_lowhigh_init<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.lh, n);
-  CK_LAUNCH();
-  if (m) {
-    k_lowhigh_edges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m,
-                                                                     ws.pre_of, ws.lh);
+    if (n > 1) {
+      const u32 k = 2 * T;
+      CK(cudaMemsetAsync(ws.head, 0xFF, static_cast<u64>(n) * 4, st));
+      tr.mark("compact");
+      k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, 0, ws.head,
+                                                                  ws.nxt, ws.tend, ws.words + 4);
+      CK_LAUNCH();
+      k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words);
+      CK_LAUNCH();
+      u32 hw[2];
+      CK(cudaMemcpyAsync(hw, ws.words + 2, sizeof hw, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const u32 head = hw[0];
+      k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.tend, ws.head, ws.nxt, k,
+                                                                   hw[1], ws.lr.succ0);
+      CK_LAUNCH();
+      tr.mark("rotation");
+      list_rank_core(k, head, NoDown{}, ws.lr, st, sms);
+      tr.mark("list_rank");
+      const Lr0View lv = lr0_view(ws.lr);
+      k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
+      CK_LAUNCH();
+      scan_exclusive(DownIn{ws.flags},
+                     StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of, ws.size_by_pre,
+                              ws.pedge_by_pre, ws.rec, ws.pedge_of},
+                     k, ws.scan_k, nullptr, st);
+      tr.mark("preorder");
+    }
+    k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre, ws.rec,
+                                  ws.pedge_of);
     CK_LAUNCH();
+    CK(cudaEventRecord(ev[2], st));
   }
-  tr.mark("lowhigh_edges");
-  k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,
-                                                                            ws.sp);
-  CK_LAUNCH();
-  for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
-    k_lh_level<<<std::min(g, blocks_for(ws.nb, 256)), 256, 0, st>>>(
-        ws.sp + static_cast<u64>(lvl - 1) * ws.nb, ws.sp + static_cast<u64>(lvl) * ws.nb, ws.nb,
-        1u << (lvl - 1));
+
+  if (engine == ETTG_BRIDGES_TV) {
+    // ---- low / high + classification -------------------------------------
+    k_lowhigh_init<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.lh, n);
     CK_LAUNCH();
+    if (m) {
+      k_lowhigh_edges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m,
+                                                                       ws.pre_of, ws.lh);
+      CK_LAUNCH();
+    }
+    tr.mark("lowhigh_edges");
+    k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,
+                                                                              ws.sp);
+    CK_LAUNCH();
+    for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
+      k_lh_level<<<std::min(g, blocks_for(ws.nb, 256)), 256, 0, st>>>(
+          ws.sp + static_cast<u64>(lvl - 1) * ws.nb, ws.sp + static_cast<u64>(lvl) * ws.nb,
+          ws.nb, 1u << (lvl - 1));
+      CK_LAUNCH();
+    }
+    k_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+        ws.lh, ws.sp, ws.nb, n, ws.size_by_pre, ws.pedge_by_pre, d_mask, m);
+    CK_LAUNCH();
+    tr.mark("rmq_classify");
+  } else {
+    // ---- CK marking (core/src/bridges.cpp:40-76) -------------------------
+    CK(cudaMemsetAsync(ws.marked, 0, n, st));
+    if (m) {
+      k_ck_mark<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m, ws.rec,
+                                                                 ws.marked);
+      CK_LAUNCH();
+    }
+    k_ck_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.pedge_of, ws.marked, n,
+                                                                   d_mask, m);
+    CK_LAUNCH();
+    tr.mark("marking");
   }
-  k_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
-      ws.lh, ws.sp, ws.nb, n, ws.size_by_pre, ws.pedge_by_pre, d_mask, m);
-  CK_LAUNCH();
-  tr.mark("rmq_classify");
   CK(cudaEventRecord(ev[3], st));
   if (h_mask && m) CK(cudaMemcpyAsync(h_mask, d_mask, m, cudaMemcpyDeviceToHost, st));
-  u32 lerr = 0;
-  if (n > 1) CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4,
-                                cudaMemcpyDeviceToHost, st));
+  if (n > 1 && engine != ETTG_BRIDGES_CK)
+    CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (lerr) throw Error(ETTG_EINTERNAL, "bridges: spanning-tree tour ranking failed");
   if (times) {
@@ -570,7 +646,8 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     CK(cudaEventElapsedTime(&tot, ev[0], ev[3]));
     times->spanning_ms = a;
     times->euler_ms = b;
-    times->lowhigh_ms = d;
+    times->lowhigh_ms = engine == ETTG_BRIDGES_TV ? d : 0.0;
+    times->marking_ms = engine == ETTG_BRIDGES_TV ? 0.0 : d;
     times->total_ms = tot;
   }
 }
@@ -583,20 +660,169 @@ extern "C" {
 
 int ettg_bridges(const int64_t* edges, int64_t n, int64_t m, int device, uint8_t* is_bridge,
                  ettg_phase_times* times) {
+  return ettg_bridges_engine(edges, n, m, device, ETTG_BRIDGES_TV, is_bridge, times);
+}
+
+int ettg_bridges_engine(const int64_t* edges, int64_t n, int64_t m, int device, int engine,
+                        uint8_t* is_bridge, ettg_phase_times* times) {
   return guard([&] {
     if ((!edges || !is_bridge) && m > 0) einval("null argument");
     DeviceScope ds(device);
-    run_bridges(edges, true, n, m, device, nullptr, is_bridge, nullptr, times);
+    run_bridges(edges, true, n, m, device, nullptr, is_bridge, nullptr, times, engine);
   });
 }
 
 int ettg_bridges_dev(const uint32_t* d_edges, int64_t n, int64_t m, int device,
                      uint8_t* d_is_bridge, void* stream, ettg_phase_times* times) {
+  return ettg_bridges_dev_engine(d_edges, n, m, device, ETTG_BRIDGES_TV, d_is_bridge, stream,
+                                 times);
+}
+
+int ettg_bridges_dev_engine(const uint32_t* d_edges, int64_t n, int64_t m, int device,
+                            int engine, uint8_t* d_is_bridge, void* stream,
+                            ettg_phase_times* times) {
   return guard([&] {
     if ((!d_edges || !d_is_bridge) && m > 0) einval("null argument");
     DeviceScope ds(device);
     run_bridges(d_edges, false, n, m, device, d_is_bridge, nullptr,
-                static_cast<cudaStream_t>(stream), times);
+                static_cast<cudaStream_t>(stream), times, engine);
+  });
+}
+
+namespace {
+// Host edges -> device u32 pairs with the reference's range check.
+struct HostGraph {
+  uint2* d = nullptr;
+  u32 n = 0, m = 0;
+};
+}  // namespace
+
+int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
+                         int64_t* offsets, int64_t* neighbors, int64_t* edge_ids) {
+  return guard([&] {
+    if (n <= 0 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 31))
+      einval("bad graph size");
+    if ((!edges && m) || !offsets || (m && (!neighbors || !edge_ids))) einval("null argument");
+    DeviceScope ds(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    const u32 nn = static_cast<u32>(n), mm = static_cast<u32>(m);
+    struct Ws {
+      longlong2* e64;
+      uint2* e;
+      u32 *offs, *nbr, *eid, *flags;
+      CsrWs csr;
+      void carve(Carver& c, u32 n, u32 m) {
+        e64 = c.take<longlong2>(m + 1);
+        e = c.take<uint2>(m + 1);
+        offs = c.take<u32>(static_cast<u64>(n) + 1);
+        nbr = c.take<u32>(2ull * m + 1);
+        eid = c.take<u32>(2ull * m + 1);
+        flags = c.take<u32>(8);
+        csr.carve(c, n, m);
+      }
+    } ws;
+    Carver c;
+    ws.carve(c, nn, mm);
+    Lease lease(device, st, c.off);
+    c = Carver{lease.base()};
+    ws.carve(c, nn, mm);
+    const int sms = sm_count(device);
+    CK(cudaMemsetAsync(ws.flags, 0, 32, st));
+    if (mm) {
+      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
+          ws.e64, mm, nn, ws.e, ws.flags);
+      CK_LAUNCH();
+    }
+    u32 bad = 0;
+    read_back(&bad, ws.flags, 4, st);
+    if (bad) einval("edge endpoint out of range");
+    build_csr(ws.e, nn, mm, ws.offs, ws.nbr, ws.eid, ws.csr, st, sms);
+    std::vector<u32> o(static_cast<u64>(nn) + 1), a(2ull * mm), b(2ull * mm);
+    CK(cudaMemcpyAsync(o.data(), ws.offs, o.size() * 4, cudaMemcpyDeviceToHost, st));
+    if (mm) {
+      CK(cudaMemcpyAsync(a.data(), ws.nbr, a.size() * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(b.data(), ws.eid, b.size() * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (u64 i = 0; i < o.size(); ++i) offsets[i] = o[i];
+    for (u64 i = 0; i < a.size(); ++i) {
+      neighbors[i] = a[i];
+      edge_ids[i] = b[i];
+    }
+  });
+}
+
+int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root, int device,
+                  uint8_t* tree_mask, int64_t* level, int64_t* parent, int64_t* parent_edge) {
+  return guard([&] {
+    if (n <= 0 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 31))
+      einval("graph too large for packed hooking keys");
+    if (root < 0 || root >= n) einval("root out of range");
+    if ((!edges && m) || (m && !tree_mask) || !level || !parent || !parent_edge)
+      einval("null argument");
+    DeviceScope ds(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    const u32 nn = static_cast<u32>(n), mm = static_cast<u32>(m);
+    struct Ws {
+      longlong2* e64;
+      uint2* e;
+      u32 *lev, *par, *pe, *flags;
+      uint8_t* tree;
+      BfsWs bfs;
+      void carve(Carver& c, u32 n, u32 m) {
+        e64 = c.take<longlong2>(m + 1);
+        e = c.take<uint2>(m + 1);
+        lev = c.take<u32>(n);
+        par = c.take<u32>(n);
+        pe = c.take<u32>(n);
+        flags = c.take<u32>(8);
+        tree = c.take<uint8_t>(m + 16);
+        bfs.carve(c, n, m);
+      }
+    } ws;
+    Carver c;
+    ws.carve(c, nn, mm);
+    Lease lease(device, st, c.off);
+    c = Carver{lease.base()};
+    ws.carve(c, nn, mm);
+    const int sms = sm_count(device);
+    CK(cudaMemsetAsync(ws.flags, 0, 32, st));
+    CK(cudaMemsetAsync(ws.tree, 0, mm + 16, st));
+    if (mm) {
+      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
+          ws.e64, mm, nn, ws.e, ws.flags);
+      CK_LAUNCH();
+    }
+    u32 bad = 0;
+    read_back(&bad, ws.flags, 4, st);
+    if (bad) einval("edge endpoint out of range");
+    const u32 reached =
+        run_bfs(ws.e, nn, mm, static_cast<u32>(root), ws.lev, ws.par, ws.pe, ws.tree, ws.bfs, st,
+                sms);
+    if (reached != nn) einval("disconnected graph; extract the largest component first");
+    std::vector<u32> l(nn), p(nn), q(nn);
+    CK(cudaMemcpyAsync(l.data(), ws.lev, nn * 4ull, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p.data(), ws.par, nn * 4ull, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(q.data(), ws.pe, nn * 4ull, cudaMemcpyDeviceToHost, st));
+    if (mm) CK(cudaMemcpyAsync(tree_mask, ws.tree, mm, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (u32 v = 0; v < nn; ++v) {
+      level[v] = l[v] == kNone ? int64_t(-1) : int64_t(l[v]);
+      parent[v] = p[v] == kNone ? int64_t(-1) : int64_t(p[v]);
+      parent_edge[v] = q[v] == kNone ? int64_t(-1) : int64_t(q[v]);
+    }
   });
 }
 

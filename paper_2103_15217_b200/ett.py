@@ -238,17 +238,77 @@ def node_stats(tree: RootedTree, device: int = 0) -> NodeStats:
 
 
 # ------------------------------------------------------------------ bridges
-def tv_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
-    """tv_bridges (core/src/bridges.cpp:311-316); times gets spanning/euler/lowhigh ms."""
+def _bridges(g: EdgeList, engine: int, device: int, times: dict | None) -> BridgeMask:
     e = g.edges
     mask = np.zeros(g.m(), np.uint8)
     pt = _lib.PhaseTimes()
-    check(lib().ettg_bridges(ptr(e), int(g.n), g.m(), device, ptr(mask), C.byref(pt)))
-    phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "lowhigh": pt.lowhigh_ms,
-              "total": pt.total_ms}
+    check(lib().ettg_bridges_engine(ptr(e), int(g.n), g.m(), device, engine, ptr(mask),
+                                    C.byref(pt)))
+    if engine == _lib.BRIDGES_TV:
+        phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "lowhigh": pt.lowhigh_ms}
+    elif engine == _lib.BRIDGES_CK:
+        phases = {"spanning": pt.spanning_ms, "marking": pt.marking_ms}
+    else:
+        phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "marking": pt.marking_ms}
+    phases["total"] = pt.total_ms
     if times is not None:
         times.update(phases)
     return BridgeMask(mask, phases)
+
+
+def tv_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """tv_bridges (core/src/bridges.cpp:311-316); times gets spanning/euler/lowhigh ms."""
+    return _bridges(g, _lib.BRIDGES_TV, device, times)
+
+
+def ck_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """ck_bridges (core/src/bridges.cpp:318-325): BFS tree + CK marking."""
+    return _bridges(g, _lib.BRIDGES_CK, device, times)
+
+
+def hybrid_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """hybrid_bridges (core/src/bridges.cpp:327-339): hooking + Euler rooting + CK marking."""
+    return _bridges(g, _lib.BRIDGES_HYBRID, device, times)
+
+
+@dataclass
+class AdjacencyIndex:
+    """core/include/ett/graph.hpp:44-63."""
+    n: int
+    m: int
+    offsets: np.ndarray
+    neighbors: np.ndarray
+    edge_ids: np.ndarray
+
+
+def build_adjacency(g: EdgeList, device: int = 0) -> AdjacencyIndex:
+    """build_adjacency (core/src/graph.cpp:135-173), on the device."""
+    m = g.m()
+    off = np.empty(g.n + 1, np.int64)
+    nbr = np.empty(max(2 * m, 1), np.int64)
+    eid = np.empty(max(2 * m, 1), np.int64)
+    check(lib().ettg_build_adjacency(ptr(g.edges), int(g.n), m, device, ptr(off), ptr(nbr),
+                                     ptr(eid)))
+    return AdjacencyIndex(g.n, m, off, nbr[:2 * m], eid[:2 * m])
+
+
+@dataclass
+class SpanningTree:
+    """core/include/ett/bridges.hpp:12-18 (BFS variant)."""
+    is_tree_edge: np.ndarray
+    level: np.ndarray
+    parent: np.ndarray
+    parent_edge: np.ndarray
+
+
+def bfs_tree(g: EdgeList, root: int = 0, device: int = 0) -> SpanningTree:
+    """bfs_tree (core/src/bridges.cpp:198-249), bit-identical to the reference."""
+    m = g.m()
+    mask = np.zeros(max(m, 1), np.uint8)
+    lev, par, pe = (np.empty(g.n, np.int64) for _ in range(3))
+    check(lib().ettg_bfs_tree(ptr(g.edges), int(g.n), m, int(root), device, ptr(mask), ptr(lev),
+                              ptr(par), ptr(pe)))
+    return SpanningTree(mask[:m], lev, par, pe)
 
 
 # --------------------------------------------------------------- primitives

@@ -81,3 +81,55 @@ def test_phase_times_named(ett):
     ett.tv_bridges(g, times=times)
     assert set(times) >= {"spanning", "euler", "lowhigh"}
     assert all(v >= 0 for v in times.values())
+
+
+# ------------------------------------------------ CK / hybrid / BFS / CSR
+@pytest.mark.parametrize("engine", ["ck", "hybrid"])
+def test_engines_on_corpus(ett, ref, engine):
+    """acceptance criterion 4 for the other engines (tests/acceptance.cpp:177-219)."""
+    fn = ett.ck_bridges if engine == "ck" else ett.hybrid_bridges
+    for i, (n, edges) in enumerate(bridge_corpus(ett)):
+        edges = np.asarray(edges, np.int64).reshape(-1, 2)
+        want, _ = ref.bridges("dfs", n, edges)
+        assert np.array_equal(fn(ett.EdgeList(n, edges)).is_bridge, want), i
+
+
+@pytest.mark.parametrize("engine", ["ck", "hybrid"])
+def test_engines_planted_and_road(ett, engine):
+    fn = ett.ck_bridges if engine == "ck" else ett.hybrid_bridges
+    g, truth = ett.planted_bridge_graph(100_000, 800_000, 1000, 5)
+    assert np.array_equal(fn(g).is_bridge, truth)
+    g2, truth2 = ett.road_like_graph(300, 200, 6, 3, 900, 5)
+    times = {}
+    assert np.array_equal(fn(g2, times=times).is_bridge, truth2)
+    assert "marking" in times and "spanning" in times
+
+
+def test_build_adjacency_bit_exact(ett, ref):
+    for n, m, seed in [(2, 1, 1), (50, 300, 2), (20_000, 150_000, 3)]:
+        g = ett.random_connected_graph(n, m, seed)
+        a = ett.build_adjacency(g)
+        off, nbr, eid = ref.build_adjacency(n, g.edges)
+        assert np.array_equal(a.offsets, off) and np.array_equal(a.neighbors, nbr)
+        assert np.array_equal(a.edge_ids, eid)
+    # multi-edges and self-loops keep the reference's (neighbour, edge id) order
+    e = np.array([[0, 1], [1, 0], [2, 2], [0, 1], [1, 2]], np.int64)
+    a = ett.build_adjacency(ett.EdgeList(3, e))
+    off, nbr, eid = ref.build_adjacency(3, e)
+    assert np.array_equal(a.neighbors, nbr) and np.array_equal(a.edge_ids, eid)
+
+
+def test_bfs_tree_bit_exact(ett, ref):
+    for n, m, seed in [(10, 20, 1), (3000, 9000, 2), (200_000, 600_000, 3)]:
+        g = ett.random_connected_graph(n, m, seed)
+        st = ett.bfs_tree(g, 0)
+        mask, lev, par, pe = ref.bfs_tree(n, g.edges, 0)
+        assert np.array_equal(st.is_tree_edge, mask)
+        assert np.array_equal(st.level, lev) and np.array_equal(st.parent, par)
+        assert np.array_equal(st.parent_edge, pe)
+    g2, _ = ett.road_like_graph(120, 90, 6, 3, 50, 7)
+    st = ett.bfs_tree(g2, 5)
+    mask, lev, par, pe = ref.bfs_tree(g2.n, g2.edges, 5)
+    assert np.array_equal(st.level, lev) and np.array_equal(st.parent_edge, pe)
+    with pytest.raises(ett.InvalidArgument, match="disconnected"):
+        ett.bfs_tree(ett.EdgeList(4, np.array([[0, 1], [2, 3]])))
