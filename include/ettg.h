@@ -173,6 +173,14 @@ int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root,
                   int device, uint8_t* tree_mask, int64_t* level,
                   int64_t* parent, int64_t* parent_edge);
 
+/* largest_component (core/src/graph.cpp:219-259): old_to_new[n] (-1 outside),
+ * the component's node count in *n_out, and its edges (renumbered, input
+ * order kept) in edges_out (capacity 2m) with the count in *m_out.  Ties go to
+ * the component with the smallest minimum original id, as in the reference. */
+int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int device,
+                           int64_t* old_to_new, int64_t* n_out, int64_t* m_out,
+                           int64_t* edges_out);
+
 /* ------------------------------------------------------------ tuning -- */
 /* cudaLimitMaxL2FetchGranularity for the device's context (bytes: 0..128).
  * Random 16-B record gathers over-fetch at the default; see DESIGN.md. */

@@ -207,7 +207,19 @@ def ref_bfs_tree(n, edges, root=0):
     return mask[:m], lev, par, pe
 
 
+def ref_largest_component(n, edges):
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    o2n = np.empty(max(n, 1), np.int64)
+    out = np.empty((max(m, 1), 2), np.int64)
+    nn, mm = C.c_int64(), C.c_int64()
+    _rc(ref(), ref().ref_largest_component(i64(n), i64(m), _p(edges), _p(o2n), C.byref(nn),
+                                           C.byref(mm), _p(out)), "ref_last_error")
+    return o2n[:n], nn.value, out[:mm.value]
+
+
 Ref.build_adjacency = staticmethod(ref_build_adjacency)
+Ref.largest_component = staticmethod(ref_largest_component)
 Ref.bfs_tree = staticmethod(ref_bfs_tree)
 
 

@@ -298,6 +298,21 @@ int ref_build_adjacency(int64_t n, int64_t m, const int64_t* edges, int64_t* off
   });
 }
 
+// largest_component (core/src/graph.cpp:219-259).
+int ref_largest_component(int64_t n, int64_t m, const int64_t* edges, int64_t* old_to_new,
+                          int64_t* n_out, int64_t* m_out, int64_t* edges_out) {
+  return guard([&] {
+    ComponentResult r = largest_component(make_edges(n, m, edges));
+    std::memcpy(old_to_new, r.old_to_new.data(), n * sizeof(int64_t));
+    *n_out = r.graph.n;
+    *m_out = r.graph.m();
+    for (int64_t i = 0; i < r.graph.m(); ++i) {
+      edges_out[2 * i] = r.graph.edges[i].first;
+      edges_out[2 * i + 1] = r.graph.edges[i].second;
+    }
+  });
+}
+
 // bfs_tree (core/src/bridges.cpp:198-249) from `root`.
 int ref_bfs_tree(int64_t n, int64_t m, const int64_t* edges, int64_t root, uint8_t* tree_mask,
                  int64_t* level, int64_t* parent, int64_t* parent_edge) {

@@ -758,6 +758,99 @@ int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
   });
 }
 
+int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int device,
+                           int64_t* old_to_new, int64_t* n_out, int64_t* m_out,
+                           int64_t* edges_out) {
+  return guard([&] {
+    if (n < 0 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 31))
+      einval("bad graph size");
+    if (!n_out || !m_out || (n && !old_to_new) || (m && (!edges || !edges_out)))
+      einval("null argument");
+    *n_out = 0;
+    *m_out = 0;
+    if (n == 0) return;
+    DeviceScope ds(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    const u32 nn = static_cast<u32>(n), mm = static_cast<u32>(m);
+    struct Ws {
+      longlong2* e64;
+      uint2 *e, *eo;
+      u32 *par, *size, *o2n, *flags, *counts;
+      unsigned long long* best;
+      u64 *sn, *se;
+      void carve(Carver& c, u32 n, u32 m) {
+        e64 = c.take<longlong2>(m + 1);
+        e = c.take<uint2>(m + 1);
+        eo = c.take<uint2>(m + 1);
+        par = c.take<u32>(n);
+        size = c.take<u32>(n);
+        o2n = c.take<u32>(n);
+        flags = c.take<u32>(8);
+        counts = c.take<u32>(8);
+        best = c.take<unsigned long long>(1);
+        sn = c.take<u64>(scan_ws_words(n));
+        se = c.take<u64>(scan_ws_words(m + 1));
+      }
+    } ws;
+    Carver c;
+    ws.carve(c, nn, mm);
+    Lease lease(device, st, c.off);
+    c = Carver{lease.base()};
+    ws.carve(c, nn, mm);
+    const int sms = sm_count(device);
+    const unsigned g = sms * 8;
+    CK(cudaMemsetAsync(ws.flags, 0, 32, st));
+    CK(cudaMemsetAsync(ws.counts, 0, 32, st));
+    CK(cudaMemsetAsync(ws.size, 0, nn * 4ull, st));
+    CK(cudaMemsetAsync(ws.best, 0, 8, st));
+    if (mm) {
+      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      k_edges_from_i64<<<std::min(g, blocks_for(mm, 256)), 256, 0, st>>>(ws.e64, mm, nn, ws.e,
+                                                                         ws.flags);
+      CK_LAUNCH();
+    }
+    u32 bad = 0;
+    read_back(&bad, ws.flags, 4, st);
+    if (bad) einval("edge endpoint out of range");
+    k_iota<<<std::min(g, blocks_for(nn, 256)), 256, 0, st>>>(ws.par, nn);
+    CK_LAUNCH();
+    if (mm) {
+      k_lcc_union<<<std::min(g, blocks_for(mm, 256)), 256, 0, st>>>(ws.e, mm, ws.par);
+      CK_LAUNCH();
+    }
+    k_lcc_sizes<<<std::min(g, blocks_for(nn, 256)), 256, 0, st>>>(ws.par, nn, ws.size);
+    CK_LAUNCH();
+    k_lcc_best<<<std::min(g, blocks_for(nn, 256)), 256, 0, st>>>(ws.par, ws.size, nn, ws.best);
+    CK_LAUNCH();
+    scan_exclusive(LccNodeIn{ws.par, ws.best}, LccNodeOut{ws.par, ws.best, ws.o2n}, nn, ws.sn,
+                   ws.counts, st);
+    scan_exclusive(LccEdgeIn{ws.e, ws.o2n}, LccEdgeOut{ws.e, ws.o2n, ws.eo}, mm, ws.se,
+                   ws.counts + 1, st);
+    u32 cnt[2];
+    CK(cudaMemcpyAsync(cnt, ws.counts, sizeof cnt, cudaMemcpyDeviceToHost, st));
+    std::vector<u32> o(nn);
+    CK(cudaMemcpyAsync(o.data(), ws.o2n, nn * 4ull, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint2> eo(cnt[1]);
+    if (cnt[1]) {
+      CK(cudaMemcpyAsync(eo.data(), ws.eo, cnt[1] * 8ull, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    for (u32 v = 0; v < nn; ++v) old_to_new[v] = o[v] == kNone ? int64_t(-1) : int64_t(o[v]);
+    for (u32 i = 0; i < cnt[1]; ++i) {
+      edges_out[2 * i] = eo[i].x;
+      edges_out[2 * i + 1] = eo[i].y;
+    }
+    *n_out = cnt[0];
+    *m_out = cnt[1];
+  });
+}
+
 int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root, int device,
                   uint8_t* tree_mask, int64_t* level, int64_t* parent, int64_t* parent_edge) {
   return guard([&] {

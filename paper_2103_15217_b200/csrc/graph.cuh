@@ -268,5 +268,108 @@ inline u32 run_bfs(const uint2* edges, u32 n, u32 m, u32 root, u32* level, u32* 
   return sizes[2];
 }
 
+// ---- largest_component (core/src/graph.cpp:219-259) ----------------------------
+// Union-find with min-id roots (so the reference's tie rule -- smallest
+// minimum original id -- is the smaller root), sizes by warp-aggregated
+// atomics, argmax by one packed atomicMax, then order-preserving relabel and
+// edge compaction with the look-back scan.
+__global__ void k_lcc_union(const uint2* __restrict__ edges, u32 m, u32* par) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const uint2 uv = edges[e];
+    u32 a = par[uv.x], b = par[uv.y];
+    // find with path halving (par[x] <= x always)
+    {
+      u32 x = uv.x;
+      while (a != x) {
+        const u32 g2 = par[a];
+        par[x] = g2;
+        x = a;
+        a = g2;
+      }
+      a = x;
+    }
+    {
+      u32 x = uv.y;
+      while (b != x) {
+        const u32 g2 = par[b];
+        par[x] = g2;
+        x = b;
+        b = g2;
+      }
+      b = x;
+    }
+    while (a != b) {
+      if (a < b) {
+        const u32 t = a;
+        a = b;
+        b = t;
+      }
+      const u32 old = atomicCAS(&par[a], a, b);
+      if (old == a) break;
+      a = old;
+      while (par[a] != a) a = par[a];
+      while (par[b] != b) b = par[b];
+    }
+  }
+}
+
+__global__ void k_lcc_sizes(u32* par, u32 n, u32* size) {
+  const u32 lt = lanemask_lt();
+  for (u32 base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const u32 v = base + threadIdx.x;
+    u32 r = kNone;
+    if (v < n) {
+      r = par[v];
+      while (par[r] != r) r = par[r];
+      par[v] = r;  // full compression
+    }
+    const u32 peers = __match_any_sync(0xffffffffu, r);
+    if (r != kNone && (peers & lt) == 0) atomicAdd(&size[r], __popc(peers));
+  }
+}
+
+// best = max over roots of (size << 32 | ~root): larger size, then smaller root.
+__global__ void k_lcc_best(const u32* __restrict__ par, const u32* __restrict__ size, u32 n,
+                           unsigned long long* best) {
+  unsigned long long b = 0;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (par[v] == v) b = max(b, (static_cast<unsigned long long>(size[v]) << 32) | (~v));
+  for (int d = 16; d > 0; d >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, d));
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(best, b);
+}
+
+struct LccNodeIn {
+  const u32* par;
+  const unsigned long long* best;
+  __device__ __forceinline__ u32 operator()(u64 v) const {
+    return par[v] == ~static_cast<u32>(*best) ? 1u : 0u;
+  }
+};
+struct LccNodeOut {
+  const u32* par;
+  const unsigned long long* best;
+  u32* old_to_new;
+  __device__ __forceinline__ void operator()(u64 v, u32 rank) const {
+    old_to_new[v] = par[v] == ~static_cast<u32>(*best) ? rank : kNone;
+  }
+};
+struct LccEdgeIn {
+  const uint2* edges;
+  const u32* old_to_new;
+  __device__ __forceinline__ u32 operator()(u64 e) const {
+    return old_to_new[edges[e].x] != kNone ? 1u : 0u;
+  }
+};
+struct LccEdgeOut {
+  const uint2* edges;
+  const u32* old_to_new;
+  uint2* out;
+  __device__ __forceinline__ void operator()(u64 e, u32 rank) const {
+    const uint2 uv = edges[e];
+    const u32 a = old_to_new[uv.x];
+    if (a != kNone) out[rank] = make_uint2(a, old_to_new[uv.y]);
+  }
+};
+
 }  // namespace
 }  // namespace ettg

@@ -293,6 +293,24 @@ def build_adjacency(g: EdgeList, device: int = 0) -> AdjacencyIndex:
 
 
 @dataclass
+class ComponentResult:
+    """core/include/ett/graph.hpp:76-79."""
+    graph: EdgeList
+    old_to_new: np.ndarray
+
+
+def largest_component(g: EdgeList, device: int = 0) -> ComponentResult:
+    """largest_component (core/src/graph.cpp:219-259), on the device."""
+    m = g.m()
+    o2n = np.empty(max(g.n, 1), np.int64)
+    out = np.empty((max(m, 1), 2), np.int64)
+    nn, mm = C.c_int64(), C.c_int64()
+    check(lib().ettg_largest_component(ptr(g.edges), int(g.n), m, device, ptr(o2n), C.byref(nn),
+                                       C.byref(mm), ptr(out)))
+    return ComponentResult(EdgeList(nn.value, out[:mm.value].copy()), o2n[:g.n])
+
+
+@dataclass
 class SpanningTree:
     """core/include/ett/bridges.hpp:12-18 (BFS variant)."""
     is_tree_edge: np.ndarray

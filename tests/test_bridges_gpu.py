@@ -133,3 +133,19 @@ def test_bfs_tree_bit_exact(ett, ref):
     assert np.array_equal(st.level, lev) and np.array_equal(st.parent_edge, pe)
     with pytest.raises(ett.InvalidArgument, match="disconnected"):
         ett.bfs_tree(ett.EdgeList(4, np.array([[0, 1], [2, 3]])))
+
+
+def test_largest_component_bit_exact(ett, ref):
+    rng = np.random.default_rng(5)
+    cases = []
+    # several components incl. ties and isolated vertices
+    cases.append((8, np.array([[0, 1], [2, 3], [4, 5], [5, 6], [6, 4]], np.int64)))
+    cases.append((6, np.array([[0, 1], [2, 3], [4, 5]], np.int64)))  # all tied: min-id wins
+    cases.append((5, np.zeros((0, 2), np.int64)))
+    big = rng.integers(0, 300_000, size=(200_000, 2))
+    cases.append((300_000, big))
+    for n, e in cases:
+        r = ett.largest_component(ett.EdgeList(n, e))
+        o2n, nn, eo = ref.largest_component(n, e)
+        assert np.array_equal(r.old_to_new, o2n) and r.graph.n == nn
+        assert np.array_equal(r.graph.edges, eo.reshape(-1, 2))
