@@ -30,6 +30,7 @@
 // The spanning forest may differ from the reference's; bridges are a graph
 // property, so the mask cannot (core/include/ett/bridges.hpp:56-58).
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -83,19 +84,48 @@ __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(pa
 // list is read once.
 constexpr int kHookE = 4;
 
+// Edge subset of a hooking pass: sample = 1 -> all edges; otherwise phase 0
+// takes every sample-th edge and phase 1 the others (Afforest-style: hook a
+// sparse sample, compress, then most remaining edges find equal roots).
+struct EdgeSubset {
+  u32 m, sample, phase;
+  __device__ __forceinline__ u64 count() const {
+    if (sample <= 1) return m;
+    const u64 first = (static_cast<u64>(m) + sample - 1) / sample;
+    return phase == 0 ? first : m - first;
+  }
+  __device__ __forceinline__ u64 edge(u64 i) const {
+    if (sample <= 1) return i;
+    if (phase == 0) return i * sample;
+    return (i / (sample - 1)) * sample + (i % (sample - 1)) + 1;
+  }
+};
+
+__global__ void k_cc_compress(u32* par, u32 n) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    u32 r = par[v];
+    while (par[r] != r) r = par[r];
+    par[v] = r;
+  }
+}
+
 __global__ void __launch_bounds__(256)
-    k_cc_hook(const uint2* __restrict__ edges, u32 m, u32 n, u32* par,
+    k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               uint8_t* __restrict__ tree, u32* flags) {
   u32 bad = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < m;
+  const u64 cnt = sub.count();
+  u64 eidx[kHookE];
+  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
        base += stride * kHookE) {
     uint2 uv[kHookE];
     bool ok[kHookE];
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      const u64 e = base + j * stride;
-      ok[j] = e < m;
+      const u64 i = base + j * stride;
+      ok[j] = i < cnt;
+      const u64 e = ok[j] ? sub.edge(i) : 0;
+      eidx[j] = e;
       uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
         bad = 1;
@@ -149,7 +179,7 @@ __global__ void __launch_bounds__(256)
           }
         }
       }
-      tree[base + j * stride] = t;
+      tree[eidx[j]] = t;
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
@@ -219,6 +249,9 @@ __global__ void k_tree_head(const u32* __restrict__ head, u32 root, const u32* l
 
 // flags[pos] = (t << 1) | is_down for the half-edge at tour position pos.
 // A half-edge is down iff it precedes its twin (core/src/euler.cpp:134-139).
+// (Round-1 A/B: also storing the twin position here -- as a second array or
+// packed into 8 B -- made this phase slower, 1.5-2.0 vs 1.2 ms on config D,
+// than re-gathering the two ranks in the scan epilogue.)
 __global__ void k_tour_flags(Lr0View lr, u32 T, u32* __restrict__ flags) {
   const u32 S1 = *lr.d_S1;
   for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
@@ -261,7 +294,7 @@ struct StatsOut {
     lr.get(2 * t + 1, S1, r1, d);
     const u32 e = tedge[t];
     const uint2 uv = tend[t];
-    const bool first_is_down = r0 < r1;           // half-edge 2t = (u -> v)
+    const bool first_is_down = r0 < r1;  // half-edge 2t = (u -> v)
     const u32 child = first_is_down ? uv.y : uv.x;
     const u32 pos_up = first_is_down ? r1 : r0;
     const u32 pre = dbefore + 2;
@@ -546,9 +579,24 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
     CK_LAUNCH();
     if (m) {
-      k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.par, ws.tree,
-                                                                 ws.words);
-      CK_LAUNCH();
+      // Hook every 4th edge first, compress, then the rest (round-1 A/B on
+      // config D: 3.28 vs 4.02 ms for one pass; ETTG_CC_SAMPLE overrides).
+      u32 sample = 4;
+      if (const char* ev = std::getenv("ETTG_CC_SAMPLE")) sample = std::max(1, std::atoi(ev));
+      if (sample <= 1) {
+        k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, EdgeSubset{m, 1, 0}, n,
+                                                                   ws.par, ws.tree, ws.words);
+        CK_LAUNCH();
+      } else {
+        k_cc_hook<<<std::min(g, blocks_for(m / sample + 1, 256)), 256, 0, st>>>(
+            edges, EdgeSubset{m, sample, 0}, n, ws.par, ws.tree, ws.words);
+        CK_LAUNCH();
+        k_cc_compress<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+        CK_LAUNCH();
+        k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(
+            edges, EdgeSubset{m, sample, 1}, n, ws.par, ws.tree, ws.words);
+        CK_LAUNCH();
+      }
       tr.mark("cc_hook");
     }
     CK(cudaEventRecord(ev[1], st));
@@ -585,8 +633,8 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
       CK_LAUNCH();
       scan_exclusive(DownIn{ws.flags},
-                     StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of, ws.size_by_pre,
-                              ws.pedge_by_pre, ws.rec, ws.pedge_of},
+                     StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of,
+                              ws.size_by_pre, ws.pedge_by_pre, ws.rec, ws.pedge_of},
                      k, ws.scan_k, nullptr, st);
       tr.mark("preorder");
     }
