@@ -304,6 +304,50 @@ def bridges_section(ett, args, device, peak):
     return out
 
 
+def bridges_config_c(ett, args, device, peak):
+    """Config C: planted_bridge_graph(1M, 8M, b=10,000, seed 4); the reference's
+    tv_bridges runs the full workload on the host for an exact comparison."""
+    g, truth = ett.planted_bridge_graph(1_000_000, 8_000_000, 10_000, 4)
+    n, m = g.n, g.m()
+    d_edges = torch.from_numpy(g.edges.astype(np.int32).ravel()).to(device)
+    d_mask = torch.empty(m, dtype=torch.uint8, device=device)
+    from paper_2103_15217_b200 import _lib
+    import ctypes
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+
+    def run():
+        pt = _lib.PhaseTimes()
+        _lib.check(L.ettg_bridges_dev(d_edges.data_ptr(), n, m, device.index, d_mask.data_ptr(),
+                                      stream.cuda_stream, ctypes.byref(pt)))
+        return pt
+    run()
+    ok = bool(np.array_equal(d_mask.cpu().numpy(), truth))
+    res = []
+    for _ in range(args.bridge_steps):
+        flush.fill_(1)
+        torch.cuda.synchronize(device)
+        res.append(run())
+    tot = float(np.mean([p.total_ms for p in res]))
+    out = {"workload": "bridges config C: planted_bridge_graph(1M, 8M, b=10000, seed 4)",
+           "value": m / (tot / 1e3), "unit": "edges/s", "ms_per_step": tot,
+           "parity": "bit-exact vs planted truth" if ok else "MISMATCH",
+           "roofline_frac_41m108n": (41 * m + 108 * n) / (tot / 1e3) / 1e9 / peak[0]}
+    if args.cpu_baseline:
+        from oracle import oracle as orc
+        if orc.have_ref():
+            cores = os.cpu_count() or 1
+            orc.Ref.set_workers(cores)
+            mask, ph = orc.Ref.bridges("tv", n, g.edges)
+            out["cpu_baseline"] = {
+                "value": m / (ph[3] / 1e9), "unit": "edges/s", "cores": cores,
+                "kind": "reference", "sample": "full config C, tv_bridges, build_adjacency "
+                                                "untimed (tools/ett_bench.cpp:310-317)",
+                "ms": ph[3] / 1e6, "parity_vs_truth": bool(np.array_equal(mask, truth))}
+    return out
+
+
 # --------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -414,6 +458,7 @@ def main():
     if not args.no_bridges and rank == 0 and world == 1:
         torch.cuda.empty_cache()
         line["bridges"] = bridges_section(ett, args, device, peak)
+        line["bridges_config_C"] = bridges_config_c(ett, args, device, peak)
 
     if rank == 0:
         print(json.dumps(line), flush=True)

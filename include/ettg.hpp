@@ -8,6 +8,10 @@
 //   ett::rmq_lca_build / rmq_lca                 -> ettg::rmq_lca_build / answer_batch
 //   ett::node_stats(linearize(...))              -> ettg::node_stats(tree)
 //   ett::tv_bridges(const AdjacencyIndex&, ...)  -> ettg::tv_bridges(const EdgeList&, ...)
+//   ett::ck_bridges / hybrid_bridges             -> ettg::ck_bridges / hybrid_bridges
+//   ett::naive_build / naive_lca                 -> ettg::naive_build / answer_batch
+//   ett::ancestor_doubling_levels                -> ettg::ancestor_doubling_levels
+//   ett::build_adjacency / bfs_tree / largest_component -> same names
 //
 // Errors: std::invalid_argument / std::out_of_range exactly where the
 // reference throws them (ETTG_EINVAL / ETTG_ERANGE); std::runtime_error for
@@ -97,6 +101,20 @@ inline LcaIndex inlabel_build(const RootedTree& t, int device = 0) {
   return LcaIndex(h, ETTG_ENGINE_INLABEL);
 }
 
+inline LcaIndex naive_build(const RootedTree& t, int device = 0) {
+  if (static_cast<i64>(t.parent.size()) != t.n)
+    throw std::invalid_argument("parent array size mismatch");
+  ettg_lca* h = nullptr;
+  check(ettg_lca_build(t.parent.data(), t.n, t.root, device, ETTG_ENGINE_NAIVE, &h));
+  return LcaIndex(h, ETTG_ENGINE_NAIVE);
+}
+
+inline std::vector<i64> ancestor_doubling_levels(const RootedTree& t, int device = 0) {
+  std::vector<i64> level(t.n);
+  check(ettg_ancestor_levels(t.parent.data(), t.n, t.root, device, level.data()));
+  return level;
+}
+
 inline LcaIndex rmq_lca_build(const RootedTree& t, int device = 0) {
   if (static_cast<i64>(t.parent.size()) != t.n)
     throw std::invalid_argument("parent array size mismatch");
@@ -135,19 +153,84 @@ inline NodeStats node_stats(const RootedTree& t, int device = 0) {
 
 // tv_bridges (bridges.hpp:55).  Takes the EdgeList the reference builds its
 // AdjacencyIndex from (build_adjacency is not needed on the device).
-inline BridgeMask tv_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+inline BridgeMask bridges_engine(const EdgeList& g, int engine, PhaseTimes* times, int device) {
   std::vector<uint8_t> mask(g.edges.size());
   ettg_phase_times pt{};
-  check(ettg_bridges(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), device,
-                     mask.data(), &pt));
-  if (times) {
+  check(ettg_bridges_engine(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), device,
+                            engine, mask.data(), &pt));
+  if (times) {  // phase names as the reference records them (bridges.cpp:292-337)
     times->ms.emplace_back("spanning", pt.spanning_ms);
-    times->ms.emplace_back("euler", pt.euler_ms);
-    times->ms.emplace_back("lowhigh", pt.lowhigh_ms);
+    if (engine != ETTG_BRIDGES_CK) times->ms.emplace_back("euler", pt.euler_ms);
+    if (engine == ETTG_BRIDGES_TV) times->ms.emplace_back("lowhigh", pt.lowhigh_ms);
+    else times->ms.emplace_back("marking", pt.marking_ms);
   }
   BridgeMask out;
   out.is_bridge.assign(mask.begin(), mask.end());
   return out;
+}
+
+inline BridgeMask tv_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return bridges_engine(g, ETTG_BRIDGES_TV, times, device);
+}
+inline BridgeMask ck_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return bridges_engine(g, ETTG_BRIDGES_CK, times, device);
+}
+inline BridgeMask hybrid_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return bridges_engine(g, ETTG_BRIDGES_HYBRID, times, device);
+}
+
+// AdjacencyIndex (graph.hpp:44-61), built on the device.
+struct AdjacencyIndex {
+  i64 n = 0, m = 0;
+  std::vector<i64> offsets, neighbors, edge_ids;
+};
+
+inline AdjacencyIndex build_adjacency(const EdgeList& g, int device = 0) {
+  AdjacencyIndex a;
+  a.n = g.n;
+  a.m = g.m();
+  a.offsets.resize(g.n + 1);
+  a.neighbors.resize(2 * a.m);
+  a.edge_ids.resize(2 * a.m);
+  check(ettg_build_adjacency(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, a.m, device,
+                             a.offsets.data(), a.neighbors.data(), a.edge_ids.data()));
+  return a;
+}
+
+// SpanningTree fields of bfs_tree (bridges.hpp:12-18, :50).
+struct SpanningTree {
+  std::vector<char> is_tree_edge;
+  std::vector<i64> level, parent, parent_edge;
+};
+
+inline SpanningTree bfs_tree(const EdgeList& g, i64 root, int device = 0) {
+  SpanningTree st;
+  std::vector<uint8_t> mask(g.edges.size());
+  st.level.resize(g.n);
+  st.parent.resize(g.n);
+  st.parent_edge.resize(g.n);
+  check(ettg_bfs_tree(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), root, device,
+                      mask.data(), st.level.data(), st.parent.data(), st.parent_edge.data()));
+  st.is_tree_edge.assign(mask.begin(), mask.end());
+  return st;
+}
+
+struct ComponentResult {  // graph.hpp:76-79
+  EdgeList graph;
+  std::vector<i64> old_to_new;
+};
+
+inline ComponentResult largest_component(const EdgeList& g, int device = 0) {
+  ComponentResult r;
+  r.old_to_new.resize(g.n);
+  std::vector<int64_t> out(2 * g.edges.size() + 2);
+  int64_t nn = 0, mm = 0;
+  check(ettg_largest_component(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(),
+                               device, r.old_to_new.data(), &nn, &mm, out.data()));
+  r.graph.n = nn;
+  r.graph.edges.resize(mm);
+  for (int64_t i = 0; i < mm; ++i) r.graph.edges[i] = {out[2 * i], out[2 * i + 1]};
+  return r;
 }
 
 }  // namespace ettg

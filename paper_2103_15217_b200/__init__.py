@@ -12,7 +12,8 @@ from .ett import (AdjacencyIndex, BridgeMask, EdgeList, InlabelIndex, NaiveIndex
 from ._lib import InvalidArgument, OutOfRange, lib
 
 __all__ = [
-    "BridgeMask", "EdgeList", "InlabelIndex", "NodeStats", "RmqLcaIndex", "RootedTree",
-    "answer_batch", "inlabel_build", "inlabel_lca", "node_stats", "rmq_lca", "rmq_lca_build",
-    "tv_bridges", "InvalidArgument", "OutOfRange", "lib",
+    "AdjacencyIndex", "BridgeMask", "EdgeList", "InlabelIndex", "NaiveIndex", "NodeStats",
+    "RmqLcaIndex", "RootedTree", "SpanningTree", "answer_batch", "bfs_tree", "build_adjacency",
+    "ck_bridges", "hybrid_bridges", "inlabel_build", "inlabel_lca", "naive_build", "naive_lca",
+    "node_stats", "rmq_lca", "rmq_lca_build", "tv_bridges", "InvalidArgument", "OutOfRange", "lib",
 ]

@@ -43,6 +43,20 @@ int main() {
   auto mask = ettg::tv_bridges(g, &pt);
   CHECK(mask.is_bridge == std::vector<char>({0, 0, 0, 1}));
   CHECK(mask.count() == 1 && pt.ms.size() == 3 && pt.ms[0].first == "spanning");
+  auto nv = ettg::naive_build(t);
+  CHECK(ettg::answer_batch(nv, {{1, 5}, {3, 4}}, 2) == std::vector<ettg::i64>({2, 0}));
+  CHECK(ettg::ancestor_doubling_levels(t) == std::vector<ettg::i64>({0, 2, 1, 1, 1, 2}));
+  CHECK(ettg::ck_bridges(g).is_bridge == std::vector<char>({0, 0, 0, 1}));
+  ettg::PhaseTimes ph;
+  CHECK(ettg::hybrid_bridges(g, &ph).is_bridge == std::vector<char>({0, 0, 0, 1}));
+  CHECK(ph.ms.size() == 3 && ph.ms[2].first == "marking");
+  auto adj = ettg::build_adjacency(g);
+  CHECK(adj.offsets == std::vector<ettg::i64>({0, 2, 4, 7, 8}));
+  CHECK(adj.neighbors == std::vector<ettg::i64>({1, 2, 0, 2, 0, 1, 3, 2}));
+  auto bt = ettg::bfs_tree(g, 0);
+  CHECK(bt.parent == std::vector<ettg::i64>({-1, 0, 0, 2}));
+  auto lc = ettg::largest_component(ettg::EdgeList{6, {{0, 1}, {2, 3}, {3, 4}}});
+  CHECK(lc.graph.n == 3 && lc.old_to_new == std::vector<ettg::i64>({-1, -1, 0, 1, 2, -1}));
   std::printf("shim ok\n");
   return 0;
 }
