@@ -409,7 +409,9 @@ def main():
         Bq = 12 + 32 * (2 + Lbar)
         per_launch_bytes = Bq * sec["q_rank"]
         achieved = per_launch_bytes / (sec["step_ms"] / 1e3) / 1e9
-        traffic = ncu_traffic("k_lca_inlabel_B")
+        layout, labels = idx.layout()
+        kname = "k_lca_inlabel" if layout == "wide" else "k_lca_inlabel_narrow"
+        traffic = ncu_traffic(f"{kname}_B")
         line = {
             "metric": METRIC, "value": sec["value"], "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec["step_ms"],
@@ -419,15 +421,17 @@ def main():
             "config": {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) "
                                    "path tree, 16M sample_queries sharded across GPUs",
                        "n": tree.n, "queries": args.q, "engine": "inlabel",
+                       "index_layout": layout, "inlabel_paths": labels,
                        "parallelism": f"index replicated, queries sharded x{world}",
-                       "l2": "flushed (256 MiB write) before every step; index 384 MB > L2"},
+                       "l2": f"flushed (256 MiB write) before every step; index "
+                             f"{idx.index_bytes() / 1e6:.0f} MB > L2"},
             "e2e": e2e,
             "gpu_launches": sec["gpu_launches"],
             "build_ms": sec["build_ms"],
             "clocks": sec["clocks"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak[0], "unit": "GB/s",
                          "frac": achieved / peak[0], "traffic": traffic,
-                         "peak_kind": peak[1], "kernel": "k_lca_inlabel",
+                         "peak_kind": peak[1], "kernel": kname,
                          "bytes_per_query": Bq, "lifts_per_query": Lbar,
                          "floor_76B_frac": 76 * sec["q_rank"] / (sec["step_ms"] / 1e3) / 1e9
                          / peak[0]},
@@ -450,6 +454,7 @@ def main():
                 "workload": "permute_labels(grasp_tree(16M, inf)), 1G queries sharded",
                 "value": secE["value"], "unit": "queries/s", "ms_per_step": secE["step_ms"],
                 "steps": args.scaling_steps, "build_ms": secE["build_ms"],
+                "index_layout": secE["idx"].layout()[0],
                 "roofline_frac_140B": 140 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
                 / peak[0]}
         del secE

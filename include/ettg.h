@@ -55,6 +55,16 @@ extern "C" {
 #define ETTG_ENGINE_NAIVE 4u   /* walk-up over pointer-jumping levels (core/src/lca.cpp:111-126,
                                   core/src/primitives.cpp:208-241) */
 
+/* Inlabel index layout (build flags, OR-ed into `engines`).  Both layouts
+ * give identical answers; by default the build picks one from the tree:
+ *   WIDE   16-B node record {inlabel, ascendant, level}: one gather per
+ *          endpoint; best when many labels are in use (random trees).
+ *   NARROW 8-B node record {inlabel, level} + ascendant per label: half the
+ *          random-gather footprint; best for deep trees with few labels.
+ * ettg_lca_layout() reports the choice (0 = wide, 1 = narrow). */
+#define ETTG_LAYOUT_WIDE 0x100u
+#define ETTG_LAYOUT_NARROW 0x200u
+
 typedef struct ettg_lca ettg_lca;
 
 /* Per-phase device times of one bridges call, named as the reference's
@@ -93,6 +103,9 @@ int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root,
 void ettg_lca_free(ettg_lca* h);
 
 int ettg_lca_size(const ettg_lca* h, int64_t* n);
+/* Layout the inlabel engine queries with (0 wide, 1 narrow) and the number
+ * of inlabel paths (distinct labels) in the tree (0 for attached replicas). */
+int ettg_lca_layout(const ettg_lca* h, int* layout, int64_t* labels);
 /* Device time of the last build (ms), measured with CUDA events. */
 int ettg_lca_build_ms(const ettg_lca* h, double* ms);
 

@@ -16,6 +16,8 @@ ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL = ran
 ENGINE_INLABEL = 1
 ENGINE_RMQ = 2
 ENGINE_NAIVE = 4
+LAYOUT_WIDE = 0x100    # build flags (OR into engines); default: chosen per tree
+LAYOUT_NARROW = 0x200
 
 _lock = threading.Lock()
 _lib = None
@@ -44,6 +46,7 @@ _SIGS = {
     "ettg_lca_build_dev": ([p, i64, i64, C.c_int, C.c_uint, p, C.POINTER(p)], C.c_int),
     "ettg_lca_free": ([p], None),
     "ettg_lca_size": ([p, i64p], C.c_int),
+    "ettg_lca_layout": ([p, C.POINTER(C.c_int), i64p], C.c_int),
     "ettg_lca_build_ms": ([p, C.POINTER(C.c_double)], C.c_int),
     "ettg_lca_query": ([p, p, i64, i64, p], C.c_int),
     "ettg_lca_query_engine": ([p, C.c_uint, p, i64, i64, p], C.c_int),

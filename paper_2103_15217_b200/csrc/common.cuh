@@ -63,6 +63,11 @@ __device__ __forceinline__ uint4 ldg_rec(const uint4* p) {
                : "l"(p));
   return r;
 }
+__device__ __forceinline__ u32 ldg_u32(const u32* p) {
+  u32 r;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint2 ldg_rec(const uint2* p) {
   uint2 r;
   asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));

@@ -31,6 +31,7 @@
 // exactly 2n elements and rank r(down(v)) equals the reference's tour step of
 // v's first occurrence (rmq tour_nodes, core/src/lca.cpp:135-146).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -175,7 +176,8 @@ __global__ void k_tree_stats(Lr0View lr, u32 n, const u32* __restrict__ par,
 // input of :59-78).  lab[L] = {parent(head(L)), level(parent(head(L)))}.
 __global__ void k_head(const u32* __restrict__ inlabel, const u32* __restrict__ par,
                        const u32* __restrict__ level, u32 n, u32* __restrict__ head,
-                       uint2* __restrict__ lab, u32* __restrict__ up) {
+                       uint2* __restrict__ lab, u32* __restrict__ up, u32* __restrict__ nheads) {
+  u32 heads = 0;
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const u32 L = inlabel[v];
     if (L == 0 || L > n) continue;  // malformed input, already rejected
@@ -185,8 +187,11 @@ __global__ void k_head(const u32* __restrict__ inlabel, const u32* __restrict__ 
       head[L] = v;
       lab[L] = make_uint2(p, p == kNone ? kNone : level[v] - 1);
       up[L] = p == kNone ? 0u : pl;
+      ++heads;
     }
   }
+  for (int o = 16; o; o >>= 1) heads += __shfl_xor_sync(0xffffffffu, heads, o);
+  if ((threadIdx.x & 31) == 0 && heads) atomicAdd(nheads, heads);
 }
 
 // ascendant(L) = ascendant(up(L)) | 2^tz(L), with up(L) the label of
@@ -206,10 +211,13 @@ __global__ void k_asc_level(const u32* __restrict__ up, u32 n, int t, u32* __res
 }
 
 __global__ void k_pack(const u32* __restrict__ inlabel, const u32* __restrict__ level,
-                       const u32* __restrict__ asc, u32 n, uint4* __restrict__ node) {
+                       const u32* __restrict__ asc, u32 n, uint4* __restrict__ node,
+                       uint2* __restrict__ node8) {
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const u32 L = inlabel[v];
-    node[v] = make_uint4(L, (L >= 1 && L <= n) ? asc[L] : 0u, level[v], 0u);
+    const u32 lev = level[v];
+    if (node) node[v] = make_uint4(L, (L >= 1 && L <= n) ? asc[L] : 0u, lev, 0u);
+    if (node8) node8[v] = make_uint2(L, lev);
   }
 }
 
@@ -385,6 +393,88 @@ __global__ void __launch_bounds__(kQThreads)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// inlabel_lca, narrow layout: 8-B node record {inlabel, level} plus the
+// ascendant looked up per label (asc[L], 4 B).  Halves the node table that
+// every query gathers from at random (16M nodes: 128 MB instead of 256 MB,
+// about the size of L2), at the price of a dependent ascendant gather when
+// the inlabels differ.  Pays when few labels are in use (deep, path-like
+// trees: the ascendant and label records stay in L2); see choose_layout().
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads)
+    k_lca_inlabel_narrow(const uint2* __restrict__ node8, const u32* __restrict__ lasc,
+                         const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
+  u32 bad_any = 0;
+  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
+       base += stride) {
+    u32 x[kQPer], y[kQPer];
+    bool ok[kQPer], bad[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      const u64 i = base + static_cast<u64>(j) * kQThreads;
+      ok[j] = i < q;
+      x[j] = y[j] = 0;
+      if (ok[j]) in.get(i, x[j], y[j]);
+      bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
+      if (bad[j]) x[j] = y[j] = 0;
+    }
+    uint2 A[kQPer], B[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      A[j] = ldg_rec(node8 + x[j]);
+      B[j] = ldg_rec(node8 + y[j]);
+    }
+    u32 ax[kQPer], by[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      ax[j] = by[j] = 0;
+      if (A[j].x != B[j].x) {
+        ax[j] = ldg_u32(lasc + min(A[j].x, n));
+        by[j] = ldg_u32(lasc + min(B[j].x, n));
+      }
+    }
+    u32 ans[kQPer], wx[kQPer], wy[kQPer];
+    bool lx[kQPer], ly[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      lx[j] = ly[j] = false;
+      wx[j] = wy[j] = 0;
+      if (A[j].x == B[j].x) {
+        ans[j] = A[j].y <= B[j].y ? x[j] : y[j];
+      } else {
+        const int i = hb32(A[j].x ^ B[j].x);
+        const u32 common = ax[j] & by[j] & ~((1u << i) - 1u);
+        const int jb = tz32(common);
+        const u32 target = (A[j].x & ~((2u << jb) - 1u)) | (1u << jb);
+        const u32 lowmask = (1u << jb) - 1u;
+        if (A[j].x != target) {
+          const int kx = hb32(ax[j] & lowmask);
+          wx[j] = min((A[j].x & ~((2u << kx) - 1u)) | (1u << kx), n);
+          lx[j] = true;
+        }
+        if (B[j].x != target) {
+          const int ky = hb32(by[j] & lowmask);
+          wy[j] = min((B[j].x & ~((2u << ky) - 1u)) | (1u << ky), n);
+          ly[j] = true;
+        }
+      }
+    }
+    uint2 LX[kQPer], LY[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      LX[j] = lx[j] ? ldg_rec(lab + wx[j]) : make_uint2(x[j], A[j].y);
+      LY[j] = ly[j] ? ldg_rec(lab + wy[j]) : make_uint2(y[j], B[j].y);
+    }
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      if (A[j].x != B[j].x) ans[j] = LX[j].y <= LY[j].y ? LX[j].x : LY[j].x;
+      if (ok[j]) out.put(base + static_cast<u64>(j) * kQThreads, bad[j] ? kNone : ans[j]);
+      bad_any |= bad[j];
+    }
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 // naive_lca (core/src/lca.cpp:118-126): walk the deeper node up, then both.
 // One query per thread; cost is the x-y tree distance (the paper's baseline).
 template <class In, class Out>
@@ -474,6 +564,8 @@ __global__ void __launch_bounds__(kQThreads)
 // ============================================================================
 using namespace ettg;
 
+constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1;
+
 struct ettg_lca {
   int device = 0;
   u32 n = 0;
@@ -483,8 +575,12 @@ struct ettg_lca {
   cudaStream_t stream = nullptr;
   cudaStream_t qs[2] = {nullptr, nullptr};
   char* mem = nullptr;
-  uint4* node = nullptr;
-  uint2* lab = nullptr;
+  uint4* node = nullptr;   // wide layout: {inlabel, ascendant, level, 0}
+  uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
+  u32* lasc = nullptr;     // ... + ascendant per label
+  uint2* lab = nullptr;    // label record {parent(head(L)), level of it}
+  u32 layout = kLayoutWide;
+  u64 labels = 0;          // inlabel paths in the tree (full builds)
   u32 *par = nullptr, *pre = nullptr, *size = nullptr, *level = nullptr, *inlabel = nullptr,
       *first = nullptr, *head = nullptr;
   // rmq
@@ -500,7 +596,12 @@ struct ettg_lca {
 
   void carve(Carver& c) {
     if (engines & ETTG_ENGINE_INLABEL) {
-      node = c.take<uint4>(n);
+      // a full build packs both layouts (12 B/node extra); replicas carry one
+      if (full || layout == kLayoutWide) node = c.take<uint4>(n);
+      if (full || layout == kLayoutNarrow) {
+        node8 = c.take<uint2>(n);
+        lasc = c.take<u32>(static_cast<u64>(n) + 1);
+      }
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
     }
     if (engines & ETTG_ENGINE_NAIVE) nrec = c.take<uint2>(n);
@@ -541,7 +642,6 @@ struct BuildWs {
   u32* jj = nullptr;
   ListRankWs lr;
   u32* up = nullptr;
-  u32* asc = nullptr;
   u32* flags = nullptr;
   void carve(Carver& c, u32 n, bool host_i64) {
     if (host_i64) par64 = c.take<int64_t>(n);
@@ -555,7 +655,6 @@ struct BuildWs {
     jj = c.take<u32>(n);
     lr.carve(c, 2 * n);
     up = c.take<u32>(static_cast<u64>(n) + 1);
-    asc = c.take<u32>(static_cast<u64>(n) + 1);
     flags = c.take<u32>(8);
   }
 };
@@ -656,11 +755,32 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
   return h.release();
 }
 
+// Layout choice (measured, profiles/r1_lca_layout.md): random gathers get
+// faster as the gathered table shrinks toward L2 (B200 footprint sweep: 256 MB
+// -> 72, 128 MB -> 113 G gathers/s).  The narrow layout halves the node table
+// but adds an ascendant gather per label, which is only cheap when the labels
+// in use are few enough to stay L2-resident (~64 B of sectors per label).
+// 16M path tree (7 labels): narrow 52 vs wide 32 G q/s; 16M random tree
+// (10M labels): wide 31.5 vs narrow 21.7; gamma=2 (4.6M labels): equal.
+u32 choose_layout(u32 n, u64 labels, int device, unsigned flags) {
+  if (flags & ETTG_LAYOUT_WIDE) return kLayoutWide;
+  if (flags & ETTG_LAYOUT_NARROW) return kLayoutNarrow;
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) != cudaSuccess || l2 <= 0)
+    l2 = 126 << 20;
+  const u64 L2 = static_cast<u64>(l2);
+  if (u64(16) * n <= L2 / 2) return kLayoutWide;  // wide table mostly L2-resident anyway
+  return labels * 64 <= L2 / 8 ? kLayoutNarrow : kLayoutWide;
+}
+
 ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
                       int64_t root64, int device, unsigned engines, cudaStream_t user_st) {
   if (n64 <= 0) einval("parent array size mismatch");
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
+  const unsigned layout_flags = engines & (ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW);
+  engines &= ~(ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW);
+  if (layout_flags == (ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW)) einval("conflicting layout flags");
   if (engines == 0) engines = ETTG_ENGINE_INLABEL;
   if (engines & ~(ETTG_ENGINE_INLABEL | ETTG_ENGINE_RMQ | ETTG_ENGINE_NAIVE))
     einval("unknown engine flag");
@@ -752,15 +872,15 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   CK(cudaMemsetAsync(h->lab, 0xFF, (static_cast<u64>(n) + 1) * 8, st));
   CK(cudaMemsetAsync(ws.up, 0xFF, (static_cast<u64>(n) + 1) * 4, st));
   k_head<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->par, h->level, n,
-                                                         h->head, h->lab, ws.up);
+                                                         h->head, h->lab, ws.up, ws.flags + 1);
   CK_LAUNCH();
   for (int t = 31 - __builtin_clz(n); t >= 0; --t) {
     const u32 count = ((n >> t) + 1) >> 1;
-    k_asc_level<<<std::min(g, blocks_for(count, 256)), 256, 0, st>>>(ws.up, n, t, ws.asc);
+    k_asc_level<<<std::min(g, blocks_for(count, 256)), 256, 0, st>>>(ws.up, n, t, h->lasc);
     CK_LAUNCH();
   }
-  k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, ws.asc, n,
-                                                         h->node);
+  k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, h->lasc, n,
+                                                         h->node, h->node8);
   CK_LAUNCH();
   tr.mark("head_asc_pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
@@ -769,6 +889,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_pack_naive<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->par, h->level, n, h->nrec);
     CK_LAUNCH();
   }
+  u32 nheads = 0;
+  CK(cudaMemcpyAsync(&nheads, ws.flags + 1, sizeof nheads, cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -776,6 +898,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   h->build_ms = ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  h->labels = nheads;
+  h->layout = choose_layout(n, nheads, device, layout_flags);
   return h.release();
 }
 
@@ -808,10 +932,15 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     unsigned blocks = std::min<u64>((q + kQThreads - 1) / kQThreads, u64(sms) * 16);
     k_lca_rmq<In, Out><<<blocks, kQThreads, 0, st>>>(rv, h->n, in, out, q, err);
   } else {
-    if (!h->node) einval("index was built without the inlabel engine");
+    if (!h->lab) einval("index was built without the inlabel engine");
     const u64 per = u64(kQThreads) * kQPer;
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * 16);
-    k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->lab, h->n, in, out, q, err);
+    if (h->layout == kLayoutNarrow)
+      k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
+                                                                  in, out, q, err);
+    else
+      k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->lab, h->n, in, out, q,
+                                                           err);
   }
   CK_LAUNCH();
 }
@@ -981,24 +1110,68 @@ int ettg_ancestor_levels(const int64_t* parent, int64_t n, int64_t root, int dev
   });
 }
 
+int ettg_lca_layout(const ettg_lca* h, int* layout, int64_t* labels) {
+  return guard([&] {
+    if (!h) einval("null handle");
+    if (!(h->engines & ETTG_ENGINE_INLABEL)) einval("index has no inlabel engine");
+    if (layout) *layout = static_cast<int>(h->layout);
+    if (labels) *labels = static_cast<int64_t>(h->labels);
+  });
+}
+
+// Packed replica blob: a 256-B header {magic, layout, n} followed by the
+// arrays of the handle's layout, each 256-B aligned (Carver offsets).
+namespace {
+constexpr u32 kBlobMagic = 0x47545445u;  // "ETTG"
+struct BlobView {
+  u32* header = nullptr;
+  uint4* node = nullptr;
+  uint2* node8 = nullptr;
+  u32* lasc = nullptr;
+  uint2* lab = nullptr;
+  size_t bytes = 0;
+};
+BlobView blob_view(char* base, u32 n, u32 layout) {
+  Carver c{base};
+  BlobView b;
+  b.header = c.take<u32>(64);
+  if (layout == kLayoutWide) {
+    b.node = c.take<uint4>(n);
+  } else {
+    b.node8 = c.take<uint2>(n);
+    b.lasc = c.take<u32>(static_cast<u64>(n) + 1);
+  }
+  b.lab = c.take<uint2>(static_cast<u64>(n) + 1);
+  b.bytes = (c.off + 255) & ~size_t(255);
+  return b;
+}
+}  // namespace
+
 int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes) {
   return guard([&] {
     if (!h || !bytes) einval("null argument");
-    if (!h->node) einval("index has no inlabel engine");
-    *bytes = static_cast<int64_t>(h->n) * 16 + (static_cast<int64_t>(h->n) + 1) * 8;
+    if (!h->lab) einval("index has no inlabel engine");
+    *bytes = static_cast<int64_t>(blob_view(nullptr, h->n, h->layout).bytes);
   });
 }
 
 int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
   return guard([&] {
     if (!h || !d_dst) einval("null argument");
-    if (!h->node) einval("index has no inlabel engine");
+    if (!h->lab) einval("index has no inlabel engine");
     DeviceScope ds(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    char* dst = static_cast<char*>(d_dst);
-    CK(cudaMemcpyAsync(dst, h->node, static_cast<u64>(h->n) * 16, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(dst + static_cast<u64>(h->n) * 16, h->lab,
-                       (static_cast<u64>(h->n) + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    const u64 n = h->n;
+    BlobView b = blob_view(static_cast<char*>(d_dst), h->n, h->layout);
+    u32 head[4] = {kBlobMagic, h->layout, h->n, 0};
+    CK(cudaMemcpyAsync(b.header, head, sizeof head, cudaMemcpyHostToDevice, st));
+    if (b.node) CK(cudaMemcpyAsync(b.node, h->node, n * 16, cudaMemcpyDeviceToDevice, st));
+    if (b.node8) {
+      CK(cudaMemcpyAsync(b.node8, h->node8, n * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(b.lasc, h->lasc, (n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));  // `head` is a host stack buffer
   });
 }
 
@@ -1009,22 +1182,32 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     if (n <= 0 || n >= (int64_t(1) << 31)) einval("bad node count");
     *out = nullptr;
     DeviceScope ds(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    u32 head[4];
+    CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (head[0] != kBlobMagic || head[1] > kLayoutNarrow || head[2] != static_cast<u32>(n))
+      einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
     h->device = device;
     h->n = static_cast<u32>(n);
     h->engines = ETTG_ENGINE_INLABEL;
     h->full = false;
+    h->layout = head[1];
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     Carver c;
     h->carve(c);
     CK(cudaMalloc(&h->mem, c.off));
     c = Carver{h->mem};
     h->carve(c);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const char* src = static_cast<const char*>(d_src);
-    CK(cudaMemcpyAsync(h->node, src, static_cast<u64>(n) * 16, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(h->lab, src + static_cast<u64>(n) * 16, (static_cast<u64>(n) + 1) * 8,
-                       cudaMemcpyDeviceToDevice, st));
+    BlobView b = blob_view(const_cast<char*>(static_cast<const char*>(d_src)), h->n, h->layout);
+    const u64 un = h->n;
+    if (b.node) CK(cudaMemcpyAsync(h->node, b.node, un * 16, cudaMemcpyDeviceToDevice, st));
+    if (b.node8) {
+      CK(cudaMemcpyAsync(h->node8, b.node8, un * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->lasc, b.lasc, (un + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     *out = h.release();
   });

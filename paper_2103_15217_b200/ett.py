@@ -18,8 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import (ENGINE_INLABEL, ENGINE_NAIVE, ENGINE_RMQ, InvalidArgument, OutOfRange, check,
-                   lib, ptr)
+from ._lib import (ENGINE_INLABEL, ENGINE_NAIVE, ENGINE_RMQ, LAYOUT_NARROW, LAYOUT_WIDE,
+                   InvalidArgument, OutOfRange, check, lib, ptr)
 
 K_NONE = -1
 K_GRASP_INFINITY = (1 << 64) - 1
@@ -116,6 +116,12 @@ class _LcaHandle:
         q = d_answers.numel()
         check(lib().ettg_lca_query_dev(self._h, engine, ptr(d_pairs), q, ptr(d_answers),
                                        stream))
+
+    def layout(self) -> tuple[str, int]:
+        """("wide" | "narrow", number of inlabel paths) of the inlabel engine."""
+        lay, labels = C.c_int(), C.c_int64()
+        check(lib().ettg_lca_layout(self._h, C.byref(lay), C.byref(labels)))
+        return ("wide", "narrow")[lay.value], labels.value
 
     def index_bytes(self) -> int:
         v = C.c_int64()

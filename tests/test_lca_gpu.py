@@ -235,3 +235,67 @@ def test_naive_errors(ett):
         idx.query(np.array([[0, 1]]), 1, ett.ENGINE_INLABEL)  # engine not built
     with pytest.raises(ett.InvalidArgument):
         idx.stats()
+
+
+# ------------------------------------------------------- index layouts
+LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW")]
+
+
+@pytest.mark.parametrize("name,flag", LAYOUTS)
+def test_forced_layout_corpus_vs_reference(ett, ref, name, flag):
+    """Both inlabel layouts answer the 200-tree corpus like the reference."""
+    for ti, t in enumerate(lca_corpus(ett)):
+        idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag))
+        assert idx.layout()[0] == name
+        q = ett.sample_queries(t.n, 4_000, t.n + 7)
+        want = ref.lca("inlabel", t.parent, t.root, q)
+        assert np.array_equal(ett.answer_batch(idx, q, len(q)), want), ti
+
+
+@pytest.mark.parametrize("name,flag", LAYOUTS)
+@pytest.mark.parametrize("gamma", [1, 2, GRASP_INF])
+def test_forced_layout_medium_trees(ett, ref, name, flag, gamma):
+    t = ett.permute_labels(ett.grasp_tree(300_007, gamma, 21), 22)
+    q = ett.sample_queries(t.n, 200_000, 23)
+    idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag))
+    want = ref.lca("inlabel", t.parent, t.root, q)
+    assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
+    assert idx.layout()[1] == len(np.unique(ref.inlabel_index(t.parent, t.root)[0]))
+
+
+def test_auto_layout_choice_and_replicas(ett):
+    """Auto picks narrow for a long path (few labels), wide for a random tree;
+    forced layouts and replicas of each answer identically on the device."""
+    import torch
+    for gamma, expect in [(1, "narrow"), (GRASP_INF, "wide")]:
+        t = ett.permute_labels(ett.grasp_tree(6_000_000, gamma, 1), 2)
+        idx = ett.inlabel_build(t)
+        lay, labels = idx.layout()
+        assert lay == expect, (gamma, lay, labels)
+        q = 2_000_000
+        d = torch.empty(2 * q, dtype=torch.int32, device="cuda:0")
+        assert ett.gen_queries_dev(t.n, q, 3, 0, d)
+        outs = []
+        for h in (idx, ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE),
+                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_NARROW)):
+            buf = torch.empty(h.index_bytes(), dtype=torch.uint8, device="cuda:0")
+            h.export_index(buf)
+            rep = ett.attach_index(buf, t.n)
+            assert rep.layout()[0] == h.layout()[0]
+            for x in (h, rep):
+                a = torch.empty(q, dtype=torch.int32, device="cuda:0")
+                x.query_dev(d, a, ett.ENGINE_INLABEL)
+                outs.append(a)
+        for a in outs[1:]:
+            assert torch.equal(a, outs[0])
+
+
+def test_layout_flag_errors(ett):
+    t = ett.RootedTree(len(EXAMPLE), 0, EXAMPLE.copy())
+    with pytest.raises(ett.InvalidArgument, match="conflicting layout"):
+        ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE | ett.LAYOUT_NARROW)
+    import torch
+    idx = ett.inlabel_build(t)
+    buf = torch.zeros(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ett.InvalidArgument, match="not an exported"):
+        ett.attach_index(buf, t.n)
