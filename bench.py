@@ -49,6 +49,12 @@ def peaks():
         return 6650.0, "fallback"
 
 
+# Random-gather ceiling of B200 at the node-table footprint of each layout at
+# n = 16M (tools/footprint_micro.cu, profiles/r1_lca_layout.md): 64 MB table
+# (compact) 263.8, 128 MB (narrow) 113.1, 256 MB (wide) 71.6 G gathers/s.
+L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "wide": 71.6}
+
+
 def ncu_traffic(kernel_key: str):
     """DRAM bytes per launch from the committed ncu --set full summary."""
     try:
@@ -406,12 +412,23 @@ def main():
     if rank == 0:
         pairs_host = ett.sample_queries(tree.n, args.q, 3)
         Lbar = lift_mean(idx, pairs_host[: min(len(pairs_host), 2_000_000)])
-        Bq = 12 + 32 * (2 + Lbar)
-        per_launch_bytes = Bq * sec["q_rank"]
-        achieved = per_launch_bytes / (sec["step_ms"] / 1e3) / 1e9
+        Bq_survey = 12 + 32 * (2 + Lbar)  # one 32-B sector per gather
         layout, labels = idx.layout()
-        kname = "k_lca_inlabel" if layout == "wide" else "k_lca_inlabel_narrow"
+        kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
+                 "compact": "k_lca_inlabel_compact"}[layout]
+        q_r = sec["q_rank"]
+        if layout == "compact":
+            # 12 B streamed + the index read once per launch (node words + label
+            # table); the 4-B node table is L2-resident after its first touch
+            Bq = 12 + (4 * tree.n + 16 * labels) / q_r
+            model = "12 B streamed + (4 n + 16 labels) B index read once, per query"
+        else:
+            Bq = Bq_survey
+            model = "12 + 32 * (2 + lifts) B per query (SURVEY.md 8(d))"
+        secs = sec["step_ms"] / 1e3
+        achieved = Bq * q_r / secs / 1e9
         traffic = ncu_traffic(f"{kname}_B")
+        node_gathers = 2 * q_r / secs / 1e9
         line = {
             "metric": METRIC, "value": sec["value"], "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec["step_ms"],
@@ -424,17 +441,23 @@ def main():
                        "index_layout": layout, "inlabel_paths": labels,
                        "parallelism": f"index replicated, queries sharded x{world}",
                        "l2": f"flushed (256 MiB write) before every step; index "
-                             f"{idx.index_bytes() / 1e6:.0f} MB > L2"},
+                             f"{idx.index_bytes() / 1e6:.0f} MB"},
             "e2e": e2e,
             "gpu_launches": sec["gpu_launches"],
             "build_ms": sec["build_ms"],
             "clocks": sec["clocks"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak[0], "unit": "GB/s",
                          "frac": achieved / peak[0], "traffic": traffic,
-                         "peak_kind": peak[1], "kernel": kname,
-                         "bytes_per_query": Bq, "lifts_per_query": Lbar,
-                         "floor_76B_frac": 76 * sec["q_rank"] / (sec["step_ms"] / 1e3) / 1e9
-                         / peak[0]},
+                         "peak_kind": peak[1], "kernel": kname, "bytes_per_query": Bq,
+                         "model": model,
+                         "survey_model": {"bytes_per_query": Bq_survey, "lifts_per_query": Lbar,
+                                          "achieved": Bq_survey * q_r / secs / 1e9,
+                                          "frac": Bq_survey * q_r / secs / 1e9 / peak[0]},
+                         "l2_gather": {"node_gathers_G_per_s": node_gathers,
+                                       "ceiling_G_per_s": L2_GATHER_CEILING.get(layout),
+                                       "frac": (node_gathers / L2_GATHER_CEILING[layout]
+                                                if layout in L2_GATHER_CEILING else None),
+                                       "source": "profiles/r1_lca_layout.md footprint sweep"}},
             "answers_consistent_dev_vs_e2e": consistent,
         }
         if args.cpu_baseline and world == 1:

@@ -210,14 +210,48 @@ __global__ void k_asc_level(const u32* __restrict__ up, u32 n, int t, u32* __res
   }
 }
 
+// Level of head(L): the label record holds level(parent(head(L))).
+__device__ __forceinline__ u32 head_level(uint2 labrec) {
+  return labrec.x == kNone ? 0u : labrec.y + 1u;
+}
+
 __global__ void k_pack(const u32* __restrict__ inlabel, const u32* __restrict__ level,
-                       const u32* __restrict__ asc, u32 n, uint4* __restrict__ node,
-                       uint2* __restrict__ node8) {
+                       const u32* __restrict__ asc, const uint2* __restrict__ lab, u32 n,
+                       uint4* __restrict__ node, uint2* __restrict__ node8,
+                       u32* __restrict__ maxoff) {
+  u32 mo = 0;
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const u32 L = inlabel[v];
     const u32 lev = level[v];
-    if (node) node[v] = make_uint4(L, (L >= 1 && L <= n) ? asc[L] : 0u, lev, 0u);
+    const bool okL = L >= 1 && L <= n;
+    if (node) node[v] = make_uint4(L, okL ? asc[L] : 0u, lev, 0u);
     if (node8) node8[v] = make_uint2(L, lev);
+    if (okL) mo = max(mo, lev - head_level(lab[L]));
+  }
+  for (int o = 16; o; o >>= 1) mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxoff, mo);
+}
+
+// Compact layout (deep trees with few inlabel paths): a 4-B node word
+// (label index << off_bits | level - level(head)) and a dense per-label table
+// {inlabel, ascendant, level(head), 0}.  Label indices come from an
+// exclusive scan over "label L is in use" (head[L] != none).
+struct LabelUsedIn {
+  const u32* head;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return head[i] != kNone ? 1u : 0u; }
+};
+
+__global__ void k_pack_compact(const u32* __restrict__ inlabel, const u32* __restrict__ level,
+                               const u32* __restrict__ head, const u32* __restrict__ asc,
+                               const uint2* __restrict__ lab, const u32* __restrict__ lidx,
+                               u32 n, int off_bits, u32* __restrict__ node4,
+                               uint4* __restrict__ ltab) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const u32 L = inlabel[v];
+    const u32 li = lidx[L];
+    const u32 hl = head_level(lab[L]);
+    node4[v] = (off_bits < 32 ? (li << off_bits) : 0u) | (level[v] - hl);
+    if (head[L] == v) ltab[li] = make_uint4(L, asc[L], hl, 0u);
   }
 }
 
@@ -321,13 +355,19 @@ struct AnsI64 {
   }
 };
 
+// Query launch shape (A/B on B200, profiles/r1_lca_layout.md): the kernels
+// are gather-latency bound, and full occupancy (8 x 256 threads per SM, <= 32
+// registers) beats per-thread ILP (4 queries in flight at 64-72 registers):
+// compact 75.6 -> 97.3, wide 32.9 -> 33.4 G q/s.
 constexpr int kQThreads = 256;
-constexpr int kQPer = 4;  // independent queries per thread (memory-level parallelism)
+constexpr int kQPer = 1;          // queries per thread per loop trip
+constexpr int kQMinBlocks = 8;    // resident CTAs per SM (caps registers at 32)
+constexpr int kQGridPerSM = 64;   // grid = min(ceil(q / 256), 64 x SMs), grid-stride
 
 // inlabel_lca (core/src/lca.cpp:84-109), four queries in flight per thread:
 // two 16-B node-record gathers, then at most two 8-B label-record gathers.
 template <class In, class Out>
-__global__ void __launch_bounds__(kQThreads)
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel(const uint4* __restrict__ node, const uint2* __restrict__ lab, u32 n, In in,
                   Out out, u64 q, u32* err) {
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
@@ -400,7 +440,7 @@ __global__ void __launch_bounds__(kQThreads)
 // the inlabels differ.  Pays when few labels are in use (deep, path-like
 // trees: the ascendant and label records stay in L2); see choose_layout().
 template <class In, class Out>
-__global__ void __launch_bounds__(kQThreads)
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_narrow(const uint2* __restrict__ node8, const u32* __restrict__ lasc,
                          const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
@@ -468,6 +508,96 @@ __global__ void __launch_bounds__(kQThreads)
 #pragma unroll
     for (int j = 0; j < kQPer; ++j) {
       if (A[j].x != B[j].x) ans[j] = LX[j].y <= LY[j].y ? LX[j].x : LY[j].x;
+      if (ok[j]) out.put(base + static_cast<u64>(j) * kQThreads, bad[j] ? kNone : ans[j]);
+      bad_any |= bad[j];
+    }
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+// inlabel_lca, compact layout: one 4-B node word per endpoint.  Endpoints on
+// the same inlabel path (same label index) are answered from the words alone
+// (the smaller in-path offset is the ancestor); otherwise the two label-table
+// entries restore {inlabel, ascendant, level} and the query proceeds exactly
+// as in k_lca_inlabel.  On the 16M path tree the node table is 64 MB and the
+// label table holds 7 entries, so every gather is served by L2 after its
+// first touch.
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
+    k_lca_inlabel_compact(const u32* __restrict__ node4, const uint4* __restrict__ ltab,
+                          const uint2* __restrict__ lab, u32 n, int off_bits, In in, Out out,
+                          u64 q, u32* err) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
+  const u32 omask = off_bits >= 32 ? ~0u : ((1u << off_bits) - 1u);
+  u32 bad_any = 0;
+  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
+       base += stride) {
+    u32 x[kQPer], y[kQPer];
+    bool ok[kQPer], bad[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      const u64 i = base + static_cast<u64>(j) * kQThreads;
+      ok[j] = i < q;
+      x[j] = y[j] = 0;
+      if (ok[j]) in.get(i, x[j], y[j]);
+      bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
+      if (bad[j]) x[j] = y[j] = 0;
+    }
+    u32 wa[kQPer], wb[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      wa[j] = ldg_u32(node4 + x[j]);
+      wb[j] = ldg_u32(node4 + y[j]);
+    }
+    uint4 A[kQPer], B[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      const u32 la = off_bits >= 32 ? 0u : wa[j] >> off_bits;
+      const u32 lb = off_bits >= 32 ? 0u : wb[j] >> off_bits;
+      A[j] = B[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (la != lb) {
+        A[j] = ldg_rec(ltab + la);
+        B[j] = ldg_rec(ltab + lb);
+      }
+    }
+    u32 ans[kQPer], wx[kQPer], wy[kQPer];
+    bool same[kQPer], lx[kQPer], ly[kQPer];
+    uint2 LX[kQPer], LY[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      const u32 ox = wa[j] & omask, oy = wb[j] & omask;
+      same[j] = (wa[j] ^ wb[j]) <= omask;  // same label index
+      lx[j] = ly[j] = false;
+      wx[j] = wy[j] = 0;
+      ans[j] = ox <= oy ? x[j] : y[j];
+      LX[j] = make_uint2(x[j], A[j].z + ox);
+      LY[j] = make_uint2(y[j], B[j].z + oy);
+      if (!same[j]) {
+        const int i = hb32(A[j].x ^ B[j].x);
+        const u32 common = A[j].y & B[j].y & ~((1u << i) - 1u);
+        const int jb = tz32(common);
+        const u32 target = (A[j].x & ~((2u << jb) - 1u)) | (1u << jb);
+        const u32 lowmask = (1u << jb) - 1u;
+        if (A[j].x != target) {
+          const int kx = hb32(A[j].y & lowmask);
+          wx[j] = min((A[j].x & ~((2u << kx) - 1u)) | (1u << kx), n);
+          lx[j] = true;
+        }
+        if (B[j].x != target) {
+          const int ky = hb32(B[j].y & lowmask);
+          wy[j] = min((B[j].x & ~((2u << ky) - 1u)) | (1u << ky), n);
+          ly[j] = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      if (lx[j]) LX[j] = ldg_rec(lab + wx[j]);
+      if (ly[j]) LY[j] = ldg_rec(lab + wy[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+      if (!same[j]) ans[j] = LX[j].y <= LY[j].y ? LX[j].x : LY[j].x;
       if (ok[j]) out.put(base + static_cast<u64>(j) * kQThreads, bad[j] ? kNone : ans[j]);
       bad_any |= bad[j];
     }
@@ -564,7 +694,7 @@ __global__ void __launch_bounds__(kQThreads)
 // ============================================================================
 using namespace ettg;
 
-constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1;
+constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2;
 
 struct ettg_lca {
   int device = 0;
@@ -579,8 +709,13 @@ struct ettg_lca {
   uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
   u32* lasc = nullptr;     // ... + ascendant per label
   uint2* lab = nullptr;    // label record {parent(head(L)), level of it}
+  u32* node4 = nullptr;    // compact layout: label index << off_bits | in-path offset
+  uint4* ltab = nullptr;   // ... + {inlabel, ascendant, level(head), 0} per label index
+  char* cmem = nullptr;    // compact arrays not carved from `mem`
+  u64 ltab_cap = 0;
+  int off_bits = 0;
   u32 layout = kLayoutWide;
-  u64 labels = 0;          // inlabel paths in the tree (full builds)
+  u64 labels = 0;          // inlabel paths in the tree
   u32 *par = nullptr, *pre = nullptr, *size = nullptr, *level = nullptr, *inlabel = nullptr,
       *first = nullptr, *head = nullptr;
   // rmq
@@ -603,6 +738,11 @@ struct ettg_lca {
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
       }
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
+      if (full) {
+        node4 = c.take<u32>(n);
+        ltab_cap = std::min<u64>(n, kLtabCap);
+        ltab = c.take<uint4>(ltab_cap);
+      }
     }
     if (engines & ETTG_ENGINE_NAIVE) nrec = c.take<uint2>(n);
     if (!full) return;
@@ -623,7 +763,23 @@ struct ettg_lca {
       sp = c.take<u64>(static_cast<u64>(levels) * nb);
     }
   }
+  // Compact arrays: full builds carve the node words and a label table of
+  // kLtabCap entries up front (the auto rule only picks compact for fewer
+  // labels); a larger forced table, or a replica, gets its own allocation.
+  static constexpr u64 kLtabCap = u64(1) << 18;
+  void alloc_compact() {
+    if (node4 && labels <= ltab_cap) return;
+    Carver c;
+    if (!node4) c.take<u32>(n);
+    c.take<uint4>(labels);
+    CK(cudaMalloc(&cmem, c.off));
+    c = Carver{cmem};
+    if (!node4) node4 = c.take<u32>(n);
+    ltab = c.take<uint4>(labels);
+    ltab_cap = labels;
+  }
   ~ettg_lca() {
+    if (cmem) cudaFree(cmem);
     if (mem) cudaFree(mem);
     if (qmem) cudaFree(qmem);
     for (auto s : qs)
@@ -642,6 +798,7 @@ struct BuildWs {
   u32* jj = nullptr;
   ListRankWs lr;
   u32* up = nullptr;
+  u64* scan = nullptr;
   u32* flags = nullptr;
   void carve(Carver& c, u32 n, bool host_i64) {
     if (host_i64) par64 = c.take<int64_t>(n);
@@ -655,6 +812,7 @@ struct BuildWs {
     jj = c.take<u32>(n);
     lr.carve(c, 2 * n);
     up = c.take<u32>(static_cast<u64>(n) + 1);
+    scan = c.take<u64>(scan_ws_words(static_cast<u64>(n) + 1));
     flags = c.take<u32>(8);
   }
 };
@@ -762,15 +920,20 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
 // in use are few enough to stay L2-resident (~64 B of sectors per label).
 // 16M path tree (7 labels): narrow 52 vs wide 32 G q/s; 16M random tree
 // (10M labels): wide 31.5 vs narrow 21.7; gamma=2 (4.6M labels): equal.
-u32 choose_layout(u32 n, u64 labels, int device, unsigned flags) {
-  if (flags & ETTG_LAYOUT_WIDE) return kLayoutWide;
-  if (flags & ETTG_LAYOUT_NARROW) return kLayoutNarrow;
+u32 choose_layout(u32 n, u64 labels, bool compact_fits, int device, unsigned flags) {
+  if (flags == ETTG_LAYOUT_WIDE) return kLayoutWide;
+  if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
+  if (flags == ETTG_LAYOUT_COMPACT) {
+    if (!compact_fits) einval("compact layout: label index + in-path offset exceed 32 bits");
+    return kLayoutCompact;
+  }
   int l2 = 0;
   if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) != cudaSuccess || l2 <= 0)
     l2 = 126 << 20;
   const u64 L2 = static_cast<u64>(l2);
   if (u64(16) * n <= L2 / 2) return kLayoutWide;  // wide table mostly L2-resident anyway
-  return labels * 64 <= L2 / 8 ? kLayoutNarrow : kLayoutWide;
+  if (labels * 64 > L2 / 8) return kLayoutWide;    // many labels: per-label gathers miss
+  return compact_fits ? kLayoutCompact : kLayoutNarrow;
 }
 
 ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
@@ -778,9 +941,10 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   if (n64 <= 0) einval("parent array size mismatch");
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
-  const unsigned layout_flags = engines & (ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW);
-  engines &= ~(ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW);
-  if (layout_flags == (ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW)) einval("conflicting layout flags");
+  constexpr unsigned kLayoutMask = ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT;
+  const unsigned layout_flags = engines & kLayoutMask;
+  engines &= ~kLayoutMask;
+  if (layout_flags & (layout_flags - 1)) einval("conflicting layout flags");
   if (engines == 0) engines = ETTG_ENGINE_INLABEL;
   if (engines & ~(ETTG_ENGINE_INLABEL | ETTG_ENGINE_RMQ | ETTG_ENGINE_NAIVE))
     einval("unknown engine flag");
@@ -879,8 +1043,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_asc_level<<<std::min(g, blocks_for(count, 256)), 256, 0, st>>>(ws.up, n, t, h->lasc);
     CK_LAUNCH();
   }
-  k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->level, h->lasc, n,
-                                                         h->node, h->node8);
+  k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+      h->inlabel, h->level, h->lasc, h->lab, n, h->node, h->node8, ws.flags + 2);
   CK_LAUNCH();
   tr.mark("head_asc_pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
@@ -889,8 +1053,22 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_pack_naive<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->par, h->level, n, h->nrec);
     CK_LAUNCH();
   }
-  u32 nheads = 0;
-  CK(cudaMemcpyAsync(&nheads, ws.flags + 1, sizeof nheads, cudaMemcpyDeviceToHost, st));
+  u32 cnt[2] = {0, 0};  // {inlabel paths, max in-path offset}
+  CK(cudaMemcpyAsync(cnt, ws.flags + 1, sizeof cnt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->labels = cnt[0];
+  const int label_bits = cnt[0] > 1 ? 32 - __builtin_clz(cnt[0] - 1) : 0;
+  h->off_bits = cnt[1] ? 32 - __builtin_clz(cnt[1]) : 0;
+  h->layout = choose_layout(n, cnt[0], label_bits + h->off_bits <= 32, device, layout_flags);
+  if (h->layout == kLayoutCompact) {
+    h->alloc_compact();
+    scan_exclusive(LabelUsedIn{h->head}, ArrayOut{ws.up}, static_cast<u64>(n) + 1, ws.scan,
+                   nullptr, st);
+    k_pack_compact<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+        h->inlabel, h->level, h->head, h->lasc, h->lab, ws.up, n, h->off_bits, h->node4,
+        h->ltab);
+    CK_LAUNCH();
+  }
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -898,8 +1076,6 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   h->build_ms = ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  h->labels = nheads;
-  h->layout = choose_layout(n, nheads, device, layout_flags);
   return h.release();
 }
 
@@ -934,8 +1110,11 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
   } else {
     if (!h->lab) einval("index was built without the inlabel engine");
     const u64 per = u64(kQThreads) * kQPer;
-    unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * 16);
-    if (h->layout == kLayoutNarrow)
+    unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * kQGridPerSM);
+    if (h->layout == kLayoutCompact)
+      k_lca_inlabel_compact<In, Out><<<blocks, kQThreads, 0, st>>>(
+          h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q, err);
+    else if (h->layout == kLayoutNarrow)
       k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
                                                                   in, out, q, err);
     else
@@ -1128,18 +1307,23 @@ struct BlobView {
   uint4* node = nullptr;
   uint2* node8 = nullptr;
   u32* lasc = nullptr;
+  u32* node4 = nullptr;
+  uint4* ltab = nullptr;
   uint2* lab = nullptr;
   size_t bytes = 0;
 };
-BlobView blob_view(char* base, u32 n, u32 layout) {
+BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
   Carver c{base};
   BlobView b;
   b.header = c.take<u32>(64);
   if (layout == kLayoutWide) {
     b.node = c.take<uint4>(n);
-  } else {
+  } else if (layout == kLayoutNarrow) {
     b.node8 = c.take<uint2>(n);
     b.lasc = c.take<u32>(static_cast<u64>(n) + 1);
+  } else {
+    b.node4 = c.take<u32>(n);
+    b.ltab = c.take<uint4>(labels);
   }
   b.lab = c.take<uint2>(static_cast<u64>(n) + 1);
   b.bytes = (c.off + 255) & ~size_t(255);
@@ -1151,7 +1335,7 @@ int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes) {
   return guard([&] {
     if (!h || !bytes) einval("null argument");
     if (!h->lab) einval("index has no inlabel engine");
-    *bytes = static_cast<int64_t>(blob_view(nullptr, h->n, h->layout).bytes);
+    *bytes = static_cast<int64_t>(blob_view(nullptr, h->n, h->layout, h->labels).bytes);
   });
 }
 
@@ -1162,13 +1346,18 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
     DeviceScope ds(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const u64 n = h->n;
-    BlobView b = blob_view(static_cast<char*>(d_dst), h->n, h->layout);
-    u32 head[4] = {kBlobMagic, h->layout, h->n, 0};
+    BlobView b = blob_view(static_cast<char*>(d_dst), h->n, h->layout, h->labels);
+    u32 head[8] = {kBlobMagic, h->layout, h->n, static_cast<u32>(h->off_bits),
+                   static_cast<u32>(h->labels), 0, 0, 0};
     CK(cudaMemcpyAsync(b.header, head, sizeof head, cudaMemcpyHostToDevice, st));
     if (b.node) CK(cudaMemcpyAsync(b.node, h->node, n * 16, cudaMemcpyDeviceToDevice, st));
     if (b.node8) {
       CK(cudaMemcpyAsync(b.node8, h->node8, n * 8, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(b.lasc, h->lasc, (n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    if (b.node4) {
+      CK(cudaMemcpyAsync(b.node4, h->node4, n * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(b.ltab, h->ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));  // `head` is a host stack buffer
@@ -1183,10 +1372,11 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     *out = nullptr;
     DeviceScope ds(device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    u32 head[4];
+    u32 head[8];
     CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (head[0] != kBlobMagic || head[1] > kLayoutNarrow || head[2] != static_cast<u32>(n))
+    if (head[0] != kBlobMagic || head[1] > kLayoutCompact || head[2] != static_cast<u32>(n) ||
+        head[3] > 32 || head[4] > static_cast<u32>(n))
       einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
     h->device = device;
@@ -1194,18 +1384,26 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     h->engines = ETTG_ENGINE_INLABEL;
     h->full = false;
     h->layout = head[1];
+    h->off_bits = static_cast<int>(head[3]);
+    h->labels = head[4];
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     Carver c;
     h->carve(c);
     CK(cudaMalloc(&h->mem, c.off));
     c = Carver{h->mem};
     h->carve(c);
-    BlobView b = blob_view(const_cast<char*>(static_cast<const char*>(d_src)), h->n, h->layout);
+    if (h->layout == kLayoutCompact) h->alloc_compact();
+    BlobView b = blob_view(const_cast<char*>(static_cast<const char*>(d_src)), h->n, h->layout,
+                           h->labels);
     const u64 un = h->n;
     if (b.node) CK(cudaMemcpyAsync(h->node, b.node, un * 16, cudaMemcpyDeviceToDevice, st));
     if (b.node8) {
       CK(cudaMemcpyAsync(h->node8, b.node8, un * 8, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(h->lasc, b.lasc, (un + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    if (b.node4) {
+      CK(cudaMemcpyAsync(h->node4, b.node4, un * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->ltab, b.ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));

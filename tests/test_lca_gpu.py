@@ -238,14 +238,32 @@ def test_naive_errors(ett):
 
 
 # ------------------------------------------------------- index layouts
-LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW")]
+LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT")]
+
+
+def _compact_bits(ref, t):
+    """Label-index bits + in-path offset bits of the compact layout (oracle side)."""
+    inl, asc, head, lev, par = ref.inlabel_index(t.parent, t.root)
+    labels = len(np.unique(inl))
+    hl = lev[head[inl]]  # level of the head of each node's path
+    maxoff = int((lev - hl).max())
+    return (int(labels - 1).bit_length() if labels > 1 else 0) + maxoff.bit_length()
+
+
+def _build_layout(ett, ref, t, name, flag):
+    try:
+        return ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag))
+    except ett.InvalidArgument as e:
+        assert name == "compact" and "exceed 32 bits" in str(e)
+        assert _compact_bits(ref, t) > 32
+        return None
 
 
 @pytest.mark.parametrize("name,flag", LAYOUTS)
 def test_forced_layout_corpus_vs_reference(ett, ref, name, flag):
     """Both inlabel layouts answer the 200-tree corpus like the reference."""
     for ti, t in enumerate(lca_corpus(ett)):
-        idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag))
+        idx = _build_layout(ett, ref, t, name, flag)
         assert idx.layout()[0] == name
         q = ett.sample_queries(t.n, 4_000, t.n + 7)
         want = ref.lca("inlabel", t.parent, t.root, q)
@@ -257,17 +275,20 @@ def test_forced_layout_corpus_vs_reference(ett, ref, name, flag):
 def test_forced_layout_medium_trees(ett, ref, name, flag, gamma):
     t = ett.permute_labels(ett.grasp_tree(300_007, gamma, 21), 22)
     q = ett.sample_queries(t.n, 200_000, 23)
-    idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag))
+    idx = _build_layout(ett, ref, t, name, flag)
+    if idx is None:
+        return
+    assert idx.layout()[0] == name
     want = ref.lca("inlabel", t.parent, t.root, q)
     assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
     assert idx.layout()[1] == len(np.unique(ref.inlabel_index(t.parent, t.root)[0]))
 
 
 def test_auto_layout_choice_and_replicas(ett):
-    """Auto picks narrow for a long path (few labels), wide for a random tree;
+    """Auto picks compact for a long path (few labels), wide for a random tree;
     forced layouts and replicas of each answer identically on the device."""
     import torch
-    for gamma, expect in [(1, "narrow"), (GRASP_INF, "wide")]:
+    for gamma, expect in [(1, "compact"), (GRASP_INF, "wide")]:
         t = ett.permute_labels(ett.grasp_tree(6_000_000, gamma, 1), 2)
         idx = ett.inlabel_build(t)
         lay, labels = idx.layout()
@@ -277,7 +298,8 @@ def test_auto_layout_choice_and_replicas(ett):
         assert ett.gen_queries_dev(t.n, q, 3, 0, d)
         outs = []
         for h in (idx, ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE),
-                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_NARROW)):
+                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_NARROW),
+                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_COMPACT)):
             buf = torch.empty(h.index_bytes(), dtype=torch.uint8, device="cuda:0")
             h.export_index(buf)
             rep = ett.attach_index(buf, t.n)
@@ -294,6 +316,8 @@ def test_layout_flag_errors(ett):
     t = ett.RootedTree(len(EXAMPLE), 0, EXAMPLE.copy())
     with pytest.raises(ett.InvalidArgument, match="conflicting layout"):
         ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE | ett.LAYOUT_NARROW)
+    with pytest.raises(ett.InvalidArgument, match="conflicting layout"):
+        ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_COMPACT | ett.LAYOUT_NARROW)
     import torch
     idx = ett.inlabel_build(t)
     buf = torch.zeros(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")

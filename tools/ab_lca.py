@@ -19,8 +19,12 @@ def child():
                            ("g2", 2, 16_000_000), ("g8", 8, 16_000_000), ("A_1M", ett.K_GRASP_INFINITY, 1_000_000)]:
         n = 1_000_000 if name == "A_1M" else 16_000_000
         t = ett.permute_labels(ett.grasp_tree(n, gamma, 1), 2)
-        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW}.get(os.environ.get("AB_MODE"), 0)
-        idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | flags)
+        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW, "compact": ett.LAYOUT_COMPACT}.get(os.environ.get("AB_MODE"), 0)
+        try:
+            idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | flags)
+        except ett.InvalidArgument as e:
+            out[name] = str(e)
+            continue
         d = torch.empty(2 * q, dtype=torch.int32, device="cuda")
         ett.gen_queries_dev(t.n, q, 3, 0, d)
         ans = torch.empty(q, dtype=torch.int32, device="cuda")
@@ -41,8 +45,10 @@ def child():
 if __name__ == "__main__":
     if os.environ.get("AB_CHILD"):
         child(); sys.exit(0)
-    for mode in (sys.argv[1:] or ["wide", "narrow", "auto"]):
-        env = dict(os.environ, AB_CHILD="1", AB_MODE=mode)
+    for mode in (sys.argv[1:] or ["wide", "narrow", "compact", "auto"]):
+        env = dict(os.environ, AB_CHILD="1", AB_MODE=mode.split(":")[0])
+        if ":" in mode:
+            env["ETTG_CQ"] = env["ETTG_WQ"] = mode.split(":")[1]
         if mode == "old":
             env["AB_LIB"] = os.path.join(ROOT, "tools", "_old", "libettg_head.so")
         r = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True)
