@@ -51,8 +51,8 @@ def peaks():
 
 # Random-gather ceiling of B200 at the node-table footprint of each layout at
 # n = 16M (tools/footprint_micro.cu, profiles/r1_lca_layout.md): 64 MB table
-# (compact) 263.8, 128 MB (narrow) 113.1, 256 MB (wide) 71.6 G gathers/s.
-L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "wide": 71.6}
+# (compact) 263.8, 128 MB (narrow, split) 113.1, 256 MB (wide) 71.6 G gathers/s.
+L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "split": 113.1, "wide": 71.6}
 
 
 def ncu_traffic(kernel_key: str):
@@ -415,7 +415,7 @@ def main():
         Bq_survey = 12 + 32 * (2 + Lbar)  # one 32-B sector per gather
         layout, labels = idx.layout()
         kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
-                 "compact": "k_lca_inlabel_compact"}[layout]
+                 "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split"}[layout]
         q_r = sec["q_rank"]
         if layout == "compact":
             # 12 B streamed + the index read once per launch (node words + label
@@ -478,8 +478,13 @@ def main():
                 "value": secE["value"], "unit": "queries/s", "ms_per_step": secE["step_ms"],
                 "steps": args.scaling_steps, "build_ms": secE["build_ms"],
                 "index_layout": secE["idx"].layout()[0],
-                "roofline_frac_140B": 140 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
-                / peak[0]}
+                "survey_model_frac_140B": 140 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
+                / peak[0],
+                "l2_gather_frac": (2 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
+                                   / L2_GATHER_CEILING[secE["idx"].layout()[0]]),
+                "note": "140 B/query assumes every gather is an HBM sector; the split "
+                        "layout's 128 MB node table is half L2-resident and lifts hit "
+                        "L2, so the survey-model fraction can exceed 1"}
         del secE
 
     # ---- bridges config D (replicas only: rank 0 of an N=1 run) -------------

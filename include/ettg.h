@@ -58,16 +58,19 @@ extern "C" {
 /* Inlabel index layout (build flags, OR-ed into `engines`).  All layouts
  * give identical answers; by default the build picks one from the tree:
  *   WIDE    16-B node record {inlabel, ascendant, level}: one gather per
- *           endpoint; best when many labels are in use (random trees).
+ *           endpoint; for trees between the two cases below.
  *   NARROW  8-B node record {inlabel, level} + ascendant per label: half the
  *           random-gather footprint, for few labels when COMPACT does not fit.
  *   COMPACT 4-B node word {label index, level - level(head)} + a dense
  *           per-label table: a quarter of the footprint, for deep trees with
  *           few inlabel paths (label-index bits + offset bits <= 32).
- * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact). */
+ *   SPLIT   8-B node record {inlabel, ascendant} + level in its own array,
+ *           read only for endpoints that are not lifted (shallow trees).
+ * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split). */
 #define ETTG_LAYOUT_WIDE 0x100u
 #define ETTG_LAYOUT_NARROW 0x200u
 #define ETTG_LAYOUT_COMPACT 0x400u
+#define ETTG_LAYOUT_SPLIT 0x800u
 
 typedef struct ettg_lca ettg_lca;
 
@@ -107,7 +110,7 @@ int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root,
 void ettg_lca_free(ettg_lca* h);
 
 int ettg_lca_size(const ettg_lca* h, int64_t* n);
-/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact) and the number
+/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact, 3 split) and the number
  * of inlabel paths (distinct labels) in the tree (0 for attached replicas). */
 int ettg_lca_layout(const ettg_lca* h, int* layout, int64_t* labels);
 /* Device time of the last build (ms), measured with CUDA events. */

@@ -19,6 +19,7 @@ ENGINE_NAIVE = 4
 LAYOUT_WIDE = 0x100    # build flags (OR into engines); default: chosen per tree
 LAYOUT_NARROW = 0x200
 LAYOUT_COMPACT = 0x400
+LAYOUT_SPLIT = 0x800
 
 _lock = threading.Lock()
 _lib = None

@@ -218,7 +218,7 @@ __device__ __forceinline__ u32 head_level(uint2 labrec) {
 __global__ void k_pack(const u32* __restrict__ inlabel, const u32* __restrict__ level,
                        const u32* __restrict__ asc, const uint2* __restrict__ lab, u32 n,
                        uint4* __restrict__ node, uint2* __restrict__ node8,
-                       u32* __restrict__ maxoff) {
+                       uint2* __restrict__ nodes, u32* __restrict__ maxoff) {
   u32 mo = 0;
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const u32 L = inlabel[v];
@@ -226,6 +226,7 @@ __global__ void k_pack(const u32* __restrict__ inlabel, const u32* __restrict__ 
     const bool okL = L >= 1 && L <= n;
     if (node) node[v] = make_uint4(L, okL ? asc[L] : 0u, lev, 0u);
     if (node8) node8[v] = make_uint2(L, lev);
+    if (nodes) nodes[v] = make_uint2(L, okL ? asc[L] : 0u);
     if (okL) mo = max(mo, lev - head_level(lab[L]));
   }
   for (int o = 16; o; o >>= 1) mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
@@ -515,6 +516,50 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// inlabel_lca, split layout: 8-B node record {inlabel, ascendant} and the
+// level in a separate 4-B array, read only where the answer needs it (equal
+// inlabels, or an endpoint that is not lifted).  On random trees nearly
+// every query lifts both endpoints, so the hot table is 128 MB instead of
+// the wide layout's 256 MB.
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
+    k_lca_inlabel_split(const uint2* __restrict__ nodes, const u32* __restrict__ level,
+                        const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
+  u32 bad_any = 0;
+  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
+       i += static_cast<u64>(gridDim.x) * kQThreads) {
+    u32 x, y;
+    in.get(i, x, y);
+    const bool bad = x >= n || y >= n;
+    if (bad) x = y = 0;
+    const uint2 A = ldg_rec(nodes + x), B = ldg_rec(nodes + y);
+    bool lx = false, ly = false;
+    u32 wx = 0, wy = 0;
+    if (A.x != B.x) {
+      const int hbit = hb32(A.x ^ B.x);
+      const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
+      const int jb = tz32(common);
+      const u32 target = (A.x & ~((2u << jb) - 1u)) | (1u << jb);
+      const u32 lowmask = (1u << jb) - 1u;
+      if (A.x != target) {
+        const int kx = hb32(A.y & lowmask);
+        wx = min((A.x & ~((2u << kx) - 1u)) | (1u << kx), n);
+        lx = true;
+      }
+      if (B.x != target) {
+        const int ky = hb32(B.y & lowmask);
+        wy = min((B.x & ~((2u << ky) - 1u)) | (1u << ky), n);
+        ly = true;
+      }
+    }
+    const uint2 LX = lx ? ldg_rec(lab + wx) : make_uint2(x, ldg_u32(level + x));
+    const uint2 LY = ly ? ldg_rec(lab + wy) : make_uint2(y, ldg_u32(level + y));
+    out.put(i, bad ? kNone : (LX.y <= LY.y ? LX.x : LY.x));
+    bad_any |= bad;
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 // inlabel_lca, compact layout: one 4-B node word per endpoint.  Endpoints on
 // the same inlabel path (same label index) are answered from the words alone
 // (the smaller in-path offset is the ancestor); otherwise the two label-table
@@ -694,7 +739,7 @@ __global__ void __launch_bounds__(kQThreads)
 // ============================================================================
 using namespace ettg;
 
-constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2;
+constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSplit = 3;
 
 struct ettg_lca {
   int device = 0;
@@ -706,6 +751,8 @@ struct ettg_lca {
   cudaStream_t qs[2] = {nullptr, nullptr};
   char* mem = nullptr;
   uint4* node = nullptr;   // wide layout: {inlabel, ascendant, level, 0}
+  uint2* nodes = nullptr;  // split layout: {inlabel, ascendant} ...
+  u32* slevel = nullptr;   // ... + level per node
   uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
   u32* lasc = nullptr;     // ... + ascendant per label
   uint2* lab = nullptr;    // label record {parent(head(L)), level of it}
@@ -731,11 +778,15 @@ struct ettg_lca {
 
   void carve(Carver& c) {
     if (engines & ETTG_ENGINE_INLABEL) {
-      // a full build packs both layouts (12 B/node extra); replicas carry one
+      // a full build packs every layout (~28 B/node extra); replicas carry one
       if (full || layout == kLayoutWide) node = c.take<uint4>(n);
       if (full || layout == kLayoutNarrow) {
         node8 = c.take<uint2>(n);
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
+      }
+      if (full || layout == kLayoutSplit) {
+        nodes = c.take<uint2>(n);
+        slevel = full ? nullptr : c.take<u32>(n);  // full builds query h->level
       }
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
       if (full) {
@@ -750,6 +801,7 @@ struct ettg_lca {
     pre = c.take<u32>(n);
     size = c.take<u32>(n);
     level = c.take<u32>(n);
+    if (nodes) slevel = level;
     inlabel = c.take<u32>(n);
     first = c.take<u32>(n);
     head = c.take<u32>(static_cast<u64>(n) + 1);
@@ -913,16 +965,19 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
   return h.release();
 }
 
-// Layout choice (measured, profiles/r1_lca_layout.md): random gathers get
+// Layout choice (measured, profiles/r1_lca_layout.md).  Random gathers get
 // faster as the gathered table shrinks toward L2 (B200 footprint sweep: 256 MB
-// -> 72, 128 MB -> 113 G gathers/s).  The narrow layout halves the node table
-// but adds an ascendant gather per label, which is only cheap when the labels
-// in use are few enough to stay L2-resident (~64 B of sectors per label).
-// 16M path tree (7 labels): narrow 52 vs wide 32 G q/s; 16M random tree
-// (10M labels): wide 31.5 vs narrow 21.7; gamma=2 (4.6M labels): equal.
+// -> 72, 128 MB -> 113, 64 MB -> 264 G gathers/s), so each layout trades
+// node-record bytes against extra per-label or per-node reads:
+//   few labels (deep trees; per-label tables stay in L2): compact if its
+//     bit budget fits, else narrow          16M path: compact 97.5 G q/s
+//   labels >= n/2 (shallow trees: almost every query lifts both endpoints,
+//     so the level array is rarely read): split    16M grasp(inf): 55.7
+//   otherwise wide                              16M gamma=2: wide 24.3
 u32 choose_layout(u32 n, u64 labels, bool compact_fits, int device, unsigned flags) {
   if (flags == ETTG_LAYOUT_WIDE) return kLayoutWide;
   if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
+  if (flags == ETTG_LAYOUT_SPLIT) return kLayoutSplit;
   if (flags == ETTG_LAYOUT_COMPACT) {
     if (!compact_fits) einval("compact layout: label index + in-path offset exceed 32 bits");
     return kLayoutCompact;
@@ -931,9 +986,9 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, int device, unsigned fla
   if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) != cudaSuccess || l2 <= 0)
     l2 = 126 << 20;
   const u64 L2 = static_cast<u64>(l2);
-  if (u64(16) * n <= L2 / 2) return kLayoutWide;  // wide table mostly L2-resident anyway
-  if (labels * 64 > L2 / 8) return kLayoutWide;    // many labels: per-label gathers miss
-  return compact_fits ? kLayoutCompact : kLayoutNarrow;
+  if (labels * 64 <= L2 / 8) return compact_fits ? kLayoutCompact : kLayoutNarrow;
+  if (2 * labels >= n) return kLayoutSplit;
+  return kLayoutWide;
 }
 
 ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
@@ -941,7 +996,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   if (n64 <= 0) einval("parent array size mismatch");
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
-  constexpr unsigned kLayoutMask = ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT;
+  constexpr unsigned kLayoutMask =
+      ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT | ETTG_LAYOUT_SPLIT;
   const unsigned layout_flags = engines & kLayoutMask;
   engines &= ~kLayoutMask;
   if (layout_flags & (layout_flags - 1)) einval("conflicting layout flags");
@@ -1044,7 +1100,7 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     CK_LAUNCH();
   }
   k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
-      h->inlabel, h->level, h->lasc, h->lab, n, h->node, h->node8, ws.flags + 2);
+      h->inlabel, h->level, h->lasc, h->lab, n, h->node, h->node8, h->nodes, ws.flags + 2);
   CK_LAUNCH();
   tr.mark("head_asc_pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
@@ -1114,6 +1170,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     if (h->layout == kLayoutCompact)
       k_lca_inlabel_compact<In, Out><<<blocks, kQThreads, 0, st>>>(
           h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q, err);
+    else if (h->layout == kLayoutSplit)
+      k_lca_inlabel_split<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab,
+                                                                 h->n, in, out, q, err);
     else if (h->layout == kLayoutNarrow)
       k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
                                                                   in, out, q, err);
@@ -1309,6 +1368,8 @@ struct BlobView {
   u32* lasc = nullptr;
   u32* node4 = nullptr;
   uint4* ltab = nullptr;
+  uint2* nodes = nullptr;
+  u32* slevel = nullptr;
   uint2* lab = nullptr;
   size_t bytes = 0;
 };
@@ -1321,9 +1382,12 @@ BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
   } else if (layout == kLayoutNarrow) {
     b.node8 = c.take<uint2>(n);
     b.lasc = c.take<u32>(static_cast<u64>(n) + 1);
-  } else {
+  } else if (layout == kLayoutCompact) {
     b.node4 = c.take<u32>(n);
     b.ltab = c.take<uint4>(labels);
+  } else {
+    b.nodes = c.take<uint2>(n);
+    b.slevel = c.take<u32>(n);
   }
   b.lab = c.take<uint2>(static_cast<u64>(n) + 1);
   b.bytes = (c.off + 255) & ~size_t(255);
@@ -1359,6 +1423,10 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
       CK(cudaMemcpyAsync(b.node4, h->node4, n * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(b.ltab, h->ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
+    if (b.nodes) {
+      CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(b.slevel, h->slevel, n * 4, cudaMemcpyDeviceToDevice, st));
+    }
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));  // `head` is a host stack buffer
   });
@@ -1375,7 +1443,7 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     u32 head[8];
     CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (head[0] != kBlobMagic || head[1] > kLayoutCompact || head[2] != static_cast<u32>(n) ||
+    if (head[0] != kBlobMagic || head[1] > kLayoutSplit || head[2] != static_cast<u32>(n) ||
         head[3] > 32 || head[4] > static_cast<u32>(n))
       einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
@@ -1404,6 +1472,10 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     if (b.node4) {
       CK(cudaMemcpyAsync(h->node4, b.node4, un * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(h->ltab, b.ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
+    }
+    if (b.nodes) {
+      CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->slevel, b.slevel, un * 4, cudaMemcpyDeviceToDevice, st));
     }
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));

@@ -238,7 +238,8 @@ def test_naive_errors(ett):
 
 
 # ------------------------------------------------------- index layouts
-LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT")]
+LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT"),
+           ("split", "LAYOUT_SPLIT")]
 
 
 def _compact_bits(ref, t):
@@ -285,10 +286,11 @@ def test_forced_layout_medium_trees(ett, ref, name, flag, gamma):
 
 
 def test_auto_layout_choice_and_replicas(ett):
-    """Auto picks compact for a long path (few labels), wide for a random tree;
+    """Auto picks compact for a long path (few labels), split for a random tree,
+    wide in between;
     forced layouts and replicas of each answer identically on the device."""
     import torch
-    for gamma, expect in [(1, "compact"), (GRASP_INF, "wide")]:
+    for gamma, expect in [(1, "compact"), (GRASP_INF, "split"), (2, "wide")]:
         t = ett.permute_labels(ett.grasp_tree(6_000_000, gamma, 1), 2)
         idx = ett.inlabel_build(t)
         lay, labels = idx.layout()
@@ -297,9 +299,13 @@ def test_auto_layout_choice_and_replicas(ett):
         d = torch.empty(2 * q, dtype=torch.int32, device="cuda:0")
         assert ett.gen_queries_dev(t.n, q, 3, 0, d)
         outs = []
-        for h in (idx, ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE),
-                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_NARROW),
-                  ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_COMPACT)):
+        handles = [idx]
+        for _, flag in LAYOUTS:
+            try:
+                handles.append(ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | getattr(ett, flag)))
+            except ett.InvalidArgument as e:  # compact bit budget exceeded (gamma=2)
+                assert flag == "LAYOUT_COMPACT" and gamma == 2, e
+        for h in handles:
             buf = torch.empty(h.index_bytes(), dtype=torch.uint8, device="cuda:0")
             h.export_index(buf)
             rep = ett.attach_index(buf, t.n)

@@ -16,10 +16,15 @@ def child():
     out = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for name, gamma, q in [("B_path", 1, 16_000_000), ("E_rand", ett.K_GRASP_INFINITY, 64_000_000),
-                           ("g2", 2, 16_000_000), ("g8", 8, 16_000_000), ("A_1M", ett.K_GRASP_INFINITY, 1_000_000)]:
-        n = 1_000_000 if name == "A_1M" else 16_000_000
+                           ("g2", 2, 16_000_000), ("g8", 8, 16_000_000), ("A_1M", ett.K_GRASP_INFINITY, 1_000_000),
+                           ("path_1M", 1, 1_000_000), ("g2_1M", 2, 1_000_000), ("rand_4M", ett.K_GRASP_INFINITY, 4_000_000),
+                           ("path_4M", 1, 4_000_000)]:
+        if os.environ.get("AB_ONLY") and name not in os.environ["AB_ONLY"].split(","):
+            continue
+        n = {"A_1M": 1_000_000, "path_1M": 1_000_000, "g2_1M": 1_000_000, "rand_4M": 4_000_000,
+             "path_4M": 4_000_000}.get(name, 16_000_000)
         t = ett.permute_labels(ett.grasp_tree(n, gamma, 1), 2)
-        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW, "compact": ett.LAYOUT_COMPACT}.get(os.environ.get("AB_MODE"), 0)
+        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW, "compact": ett.LAYOUT_COMPACT, "split": ett.LAYOUT_SPLIT}.get(os.environ.get("AB_MODE"), 0)
         try:
             idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | flags)
         except ett.InvalidArgument as e:
@@ -45,7 +50,7 @@ def child():
 if __name__ == "__main__":
     if os.environ.get("AB_CHILD"):
         child(); sys.exit(0)
-    for mode in (sys.argv[1:] or ["wide", "narrow", "compact", "auto"]):
+    for mode in (sys.argv[1:] or ["wide", "split", "narrow", "compact", "auto"]):
         env = dict(os.environ, AB_CHILD="1", AB_MODE=mode.split(":")[0])
         if ":" in mode:
             env["ETTG_CQ"] = env["ETTG_WQ"] = mode.split(":")[1]
