@@ -59,17 +59,25 @@ __global__ void k_iota(u32* __restrict__ a, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
 }
 
-// Representative with path halving, starting from an already loaded par[x];
-// parents always point to smaller ids, so a tree's root is its minimum vertex.
+// Representative of x, starting from an already loaded cur = par[x].  Parents
+// always point to smaller ids, so a tree's root is its minimum vertex.  The
+// walk is read-only; only a start vertex that needed >= kShortcutHops hops is
+// pointed straight at the root found (a benign race: the old root stays an
+// ancestor).  Path halving -- a store at every hop -- made random graphs 10x
+// slower (config C hooking 1.96 ms vs 0.21 ms): every find in a giant
+// component wrote the same few upper-level entries from all SMs.  A pure
+// read-only walk was fastest on C (0.18 ms) but let lattice chains grow on
+// road graphs (config D 3.80 vs 2.31 ms); profiles/r1_bridges_tuning.md.
+constexpr int kShortcutHops = 8;
 __device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
-  if (cur != x) {
-    u32 prev = x, next;
-    while (cur > (next = par[cur])) {
-      par[prev] = next;  // benign race: only ever shortens paths
-      prev = cur;
-      cur = next;
-    }
+  if (cur == x) return x;
+  u32 next;
+  int hops = 1;
+  while (cur > (next = par[cur])) {
+    cur = next;
+    ++hops;
   }
+  if (hops >= kShortcutHops) par[x] = cur;
   return cur;
 }
 __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(par, x, par[x]); }
@@ -82,7 +90,6 @@ __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(pa
 // n - #components edges are marked.  Endpoints are range-checked here (the
 // reference's build_adjacency check, core/src/graph.cpp:141-143) so the edge
 // list is read once.
-constexpr int kHookE = 4;
 
 // Edge subset of a hooking pass: sample = 1 -> all edges; otherwise phase 0
 // takes every sample-th edge and phase 1 the others (Afforest-style: hook a
@@ -109,7 +116,8 @@ __global__ void k_cc_compress(u32* par, u32 n) {
   }
 }
 
-__global__ void __launch_bounds__(256)
+template <int kHookE, int kMinB>
+__global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               uint8_t* __restrict__ tree, u32* flags) {
   u32 bad = 0;
@@ -332,7 +340,8 @@ __global__ void k_lowhigh_init(uint2* __restrict__ lh, u32 n) {
 // high(u) <- max(., pre(v))  (core/src/bridges.cpp:256-273).  kHookE edges per
 // thread so their preorder gathers and extreme reads are in flight together;
 // an atomic is issued only when it can change the slot.
-__global__ void __launch_bounds__(256)
+template <int kHookE, int kMinB>
+__global__ void __launch_bounds__(256, kMinB)
     k_lowhigh_edges(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
                     const u32* __restrict__ pre_of, uint2* lh) {
   u32* w = reinterpret_cast<u32*>(lh);  // slot = preorder - 1; .x = low, .y = high
@@ -431,6 +440,39 @@ __global__ void __launch_bounds__(256)
     const u32 e = pedge_by_pre[i];
     if (e < m) mask[e] = inside ? 1 : 0;
   }
+}
+
+// Edge-kernel launch shape: 2 edges per thread at 8 CTAs/SM (<= 32 regs),
+// grid = whole waves of resident CTAs from the occupancy API.  A/B on config
+// D (tools/trace_bridges.py, profiles/r1_bridges_tuning.md): hooking 2.88 ->
+// 2.60 ms, low/high 2.12 -> 1.73 ms vs 4 edges/thread at 48-69 regs on a
+// fixed 8-CTA/SM grid (6 resident: a one-third-full second wave).
+constexpr int kEdgesPerThread = 2;
+
+template <class K>
+unsigned occ_grid(K kern, u64 work, int sms) {
+  int per = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0));
+  return static_cast<unsigned>(
+      std::min<u64>(blocks_for(work, 256, ~0u), u64(sms) * std::max(per, 1)));
+}
+
+void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* tree, u32* flags,
+                 int sms, cudaStream_t st) {
+  const u64 first = (u64(sub.m) + sub.sample - 1) / sub.sample;
+  const u64 cnt = sub.sample <= 1 ? sub.m : sub.phase == 0 ? first : sub.m - first;
+  auto kern = k_cc_hook<kEdgesPerThread, 8>;
+  kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
+      edges, sub, n, par, tree, flags);
+  CK_LAUNCH();
+}
+
+void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* pre_of, uint2* lh,
+                    int sms, cudaStream_t st) {
+  auto kern = k_lowhigh_edges<kEdgesPerThread, 8>;
+  kern<<<occ_grid(kern, (u64(m) + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
+      edges, tree, m, pre_of, lh);
+  CK_LAUNCH();
 }
 
 struct BridgeWs {
@@ -584,18 +626,12 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       u32 sample = 4;
       if (const char* ev = std::getenv("ETTG_CC_SAMPLE")) sample = std::max(1, std::atoi(ev));
       if (sample <= 1) {
-        k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, EdgeSubset{m, 1, 0}, n,
-                                                                   ws.par, ws.tree, ws.words);
-        CK_LAUNCH();
+        launch_hook(edges, EdgeSubset{m, 1, 0}, n, ws.par, ws.tree, ws.words, sms, st);
       } else {
-        k_cc_hook<<<std::min(g, blocks_for(m / sample + 1, 256)), 256, 0, st>>>(
-            edges, EdgeSubset{m, sample, 0}, n, ws.par, ws.tree, ws.words);
-        CK_LAUNCH();
+        launch_hook(edges, EdgeSubset{m, sample, 0}, n, ws.par, ws.tree, ws.words, sms, st);
         k_cc_compress<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
         CK_LAUNCH();
-        k_cc_hook<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(
-            edges, EdgeSubset{m, sample, 1}, n, ws.par, ws.tree, ws.words);
-        CK_LAUNCH();
+        launch_hook(edges, EdgeSubset{m, sample, 1}, n, ws.par, ws.tree, ws.words, sms, st);
       }
       tr.mark("cc_hook");
     }
@@ -649,9 +685,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     k_lowhigh_init<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.lh, n);
     CK_LAUNCH();
     if (m) {
-      k_lowhigh_edges<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m,
-                                                                       ws.pre_of, ws.lh);
-      CK_LAUNCH();
+      launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, sms, st);
     }
     tr.mark("lowhigh_edges");
     k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,

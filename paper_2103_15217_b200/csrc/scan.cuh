@@ -144,10 +144,17 @@ __global__ void __launch_bounds__(kScanThreads)
 inline size_t scan_ws_words(u64 n) { return (n + kScanTile - 1) / kScanTile + 1; }
 
 // Stream compaction of a 0/1 byte-flag array: out(i, rank) for every set
-// flag, rank = number of set flags before i.  Each thread loads its 16 flags
-// as one 16-B vector (a warp reads 512 contiguous bytes), sums them with
-// byte arithmetic, and the tile prefix comes from the same look-back.
+// flag, rank = number of set flags before i.  Each thread loads its
+// kCompactVec x 16 flags as 16-B vectors (a warp reads 512 contiguous bytes
+// per vector), sums them with byte arithmetic, and the tile prefix comes from
+// the same look-back.  Tiles are 16 KB of flags: with 4-KB tiles the
+// look-back chain, not HBM, bounded the kernel (config D: 61K tiles).
 // `flags` must be 16-B aligned.
+constexpr int kCompactVec = 4;
+constexpr u32 kCompactTile = kScanThreads * 16 * kCompactVec;  // 16384 flags
+
+__device__ __forceinline__ u32 byte_sum4(u32 w) { return (w * 0x01010101u) >> 24; }
+
 template <class Out>
 __global__ void __launch_bounds__(kScanThreads)
     k_compact_u8(const uint8_t* __restrict__ flags, u64 n, Out out, u64* status, u32* ticket,
@@ -158,37 +165,61 @@ __global__ void __launch_bounds__(kScanThreads)
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const u32 tile = s_tile;
-  const u64 base = static_cast<u64>(tile) * kScanTile + static_cast<u64>(tid) * kScanItems;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (base + kScanItems <= n) {
-    v = *reinterpret_cast<const uint4*>(flags + base);
-  } else if (base < n) {
-    u32 w[4] = {0, 0, 0, 0};
-    for (u64 i = base; i < n; ++i) w[(i - base) >> 2] |= static_cast<u32>(flags[i]) << (8 * ((i - base) & 3));
-    v = make_uint4(w[0], w[1], w[2], w[3]);
+  const u64 tbase = static_cast<u64>(tile) * kCompactTile;
+  uint4 v[kCompactVec];
+#pragma unroll
+  for (int k = 0; k < kCompactVec; ++k) {
+    // vector k of thread tid: a warp's 32 vectors are contiguous (coalesced)
+    const u64 base = tbase + (static_cast<u64>(k) * kScanThreads + tid) * 16;
+    v[k] = make_uint4(0, 0, 0, 0);
+    if (base + 16 <= n) {
+      v[k] = *reinterpret_cast<const uint4*>(flags + base);
+    } else if (base < n) {
+      u32 w[4] = {0, 0, 0, 0};
+      for (u64 i = base; i < n; ++i)
+        w[(i - base) >> 2] |= static_cast<u32>(flags[i]) << (8 * ((i - base) & 3));
+      v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
-  const u32 cnt = ((v.x * 0x01010101u) >> 24) + ((v.y * 0x01010101u) >> 24) +
-                  ((v.z * 0x01010101u) >> 24) + ((v.w * 0x01010101u) >> 24);
-  const u32 incl = warp_incl_scan(cnt);
-  if (lane == 31) s_warp[warp] = incl;
+  // ranks must follow flag order: vector k of every thread precedes vector
+  // k+1 of every thread, so scan per vector round
+  u32 cntk[kCompactVec];
+#pragma unroll
+  for (int k = 0; k < kCompactVec; ++k)
+    cntk[k] = byte_sum4(v[k].x) + byte_sum4(v[k].y) + byte_sum4(v[k].z) + byte_sum4(v[k].w);
+  __shared__ u32 s_round[kCompactVec][kScanThreads / 32];
+  u32 inclk[kCompactVec];
+#pragma unroll
+  for (int k = 0; k < kCompactVec; ++k) {
+    inclk[k] = warp_incl_scan(cntk[k]);
+    if (lane == 31) s_round[k][warp] = inclk[k];
+  }
   __syncthreads();
   if (warp == 0) {
-    const u32 w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
-    const u32 wi = warp_incl_scan(w);
-    const u32 agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
-    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
-    const u32 pre = tile_lookback(status, tile, agg);
+    // exclusive offsets of (round k, warp w) in round-major order
+    u32 carry = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactVec; ++k) {
+      const u32 w = lane < kScanThreads / 32 ? s_round[k][lane] : 0u;
+      const u32 wi = warp_incl_scan(w);
+      if (lane < kScanThreads / 32) s_round[k][lane] = carry + wi - w;
+      carry += __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    }
+    const u32 pre = tile_lookback(status, tile, carry);
     if (lane == 0) {
       s_prefix = pre;
-      if (total && static_cast<u64>(tile + 1) * kScanTile >= n) *total = pre + agg;
+      if (total && static_cast<u64>(tile + 1) * kCompactTile >= n) *total = pre + carry;
     }
   }
   __syncthreads();
-  u32 r = s_prefix + s_warp[warp] + (incl - cnt);
-  if (cnt) {
-    const u32 words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
+  for (int k = 0; k < kCompactVec; ++k) {
+    if (!cntk[k]) continue;
+    u32 r = s_prefix + s_round[k][warp] + (inclk[k] - cntk[k]);
+    const u64 base = tbase + (static_cast<u64>(k) * kScanThreads + tid) * 16;
+    const u32 words[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
       if ((words[j >> 2] >> (8 * (j & 3))) & 0xFFu) out(base + j, r++);
     }
   }
@@ -200,7 +231,7 @@ void compact_u8(const uint8_t* flags, u64 n, Out out, u64* status, u32* total, c
     if (total) CK(cudaMemsetAsync(total, 0, sizeof(u32), st));
     return;
   }
-  const u64 tiles = (n + kScanTile - 1) / kScanTile;
+  const u64 tiles = (n + kCompactTile - 1) / kCompactTile;
   CK(cudaMemsetAsync(status, 0, (tiles + 1) * sizeof(u64), st));
   u32* ticket = reinterpret_cast<u32*>(status + tiles);
   k_compact_u8<Out><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(flags, n, out, status,
