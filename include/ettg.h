@@ -49,6 +49,7 @@ extern "C" {
 #define ETTG_ECUDA 3
 #define ETTG_ENOMEM 4
 #define ETTG_EINTERNAL 5
+#define ETTG_EPARSE 6 /* malformed text input: the reference's std::runtime_error */
 
 #define ETTG_ENGINE_INLABEL 1u /* Schieber-Vishkin inlabel (core/src/lca.cpp:20-109) */
 #define ETTG_ENGINE_RMQ 2u     /* RMQ over the Euler tour (core/src/lca.cpp:128-157) */
@@ -257,6 +258,26 @@ int64_t ettg_road_like_edge_count(int64_t W, int64_t H, int64_t extra,
 int ettg_gen_road_like_graph(int64_t W, int64_t H, int64_t extra, int64_t r,
                              int64_t pendant, uint64_t seed, int64_t* edges,
                              uint8_t* truth);
+
+/* ------------------------------------------------------------ ingestion -- */
+
+/* ParseStats (core/include/ett/graph.hpp:27-32). */
+typedef struct ettg_parse_stats {
+  int64_t self_loops_removed;
+  int64_t duplicates_removed;
+} ettg_parse_stats;
+
+/* parse_edge_list / parse_dimacs_gr (core/src/graph.cpp:57-133) on the
+ * device.  `text` is the whole file (host memory, `len` bytes).  Output: n,
+ * m and the normalised simple edge list (min, max) in first-occurrence
+ * order into `edges` (2*cap int64).  If cap < m the call fails with
+ * ETTG_ERANGE and *m holds the size needed (the number of lines always
+ * suffices).  Malformed input gives ETTG_EPARSE with the reference's message
+ * ("line N: ...").  Node ids must be < 2^32 (ETTG_ERANGE otherwise). */
+int ettg_parse_edge_list(const char* text, int64_t len, int device, int64_t* edges,
+                         int64_t cap, int64_t* n, int64_t* m, ettg_parse_stats* stats);
+int ettg_parse_dimacs_gr(const char* text, int64_t len, int device, int64_t* edges,
+                         int64_t cap, int64_t* n, int64_t* m, ettg_parse_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -12,14 +12,17 @@
 //   ett::naive_build / naive_lca                 -> ettg::naive_build / answer_batch
 //   ett::ancestor_doubling_levels                -> ettg::ancestor_doubling_levels
 //   ett::build_adjacency / bfs_tree / largest_component -> same names
+//   ett::parse_edge_list / parse_dimacs_gr (std::istream&) -> same names
 //
 // Errors: std::invalid_argument / std::out_of_range exactly where the
 // reference throws them (ETTG_EINVAL / ETTG_ERANGE); std::runtime_error for
-// CUDA failures.  Link: -I<repo>/include -L<repo>/paper_2103_15217_b200/_lib -lettg
+// parse errors (ETTG_EPARSE, the reference's messages) and CUDA failures.  Link: -I<repo>/include -L<repo>/paper_2103_15217_b200/_lib -lettg
 #ifndef ETTG_HPP_
 #define ETTG_HPP_
 
 #include <cstdint>
+#include <istream>
+#include <iterator>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -231,6 +234,39 @@ inline ComponentResult largest_component(const EdgeList& g, int device = 0) {
   r.graph.edges.resize(mm);
   for (int64_t i = 0; i < mm; ++i) r.graph.edges[i] = {out[2 * i], out[2 * i + 1]};
   return r;
+}
+
+// ParseStats (graph.hpp:27-32) and the text parsers (graph.cpp:57-133).
+struct ParseStats {
+  i64 self_loops_removed = 0;
+  i64 duplicates_removed = 0;
+  i64 removed() const { return self_loops_removed + duplicates_removed; }
+};
+
+namespace detail {
+template <class Fn>
+EdgeList parse_stream(Fn fn, std::istream& in, ParseStats* stats, int device) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  i64 cap = 1;
+  for (char c : text) cap += c == '\n';
+  std::vector<i64> buf(2 * static_cast<size_t>(cap));
+  i64 n = 0, m = 0;
+  ettg_parse_stats st{0, 0};
+  check(fn(text.data(), static_cast<i64>(text.size()), device, buf.data(), cap, &n, &m, &st));
+  EdgeList g;
+  g.n = n;
+  g.edges.resize(static_cast<size_t>(m));
+  for (i64 i = 0; i < m; ++i) g.edges[i] = {buf[2 * i], buf[2 * i + 1]};
+  if (stats) *stats = ParseStats{st.self_loops_removed, st.duplicates_removed};
+  return g;
+}
+}  // namespace detail
+
+inline EdgeList parse_edge_list(std::istream& in, ParseStats* stats = nullptr, int device = 0) {
+  return detail::parse_stream(ettg_parse_edge_list, in, stats, device);
+}
+inline EdgeList parse_dimacs_gr(std::istream& in, ParseStats* stats = nullptr, int device = 0) {
+  return detail::parse_stream(ettg_parse_dimacs_gr, in, stats, device);
 }
 
 }  // namespace ettg

@@ -186,6 +186,18 @@ class Ref:
         return mask, ph
 
 
+def ref_parse(kind, text: bytes):
+    """Reference parse_edge_list / parse_dimacs_gr -> (n, edges[m,2], stats) or OracleError."""
+    L = ref()
+    cap = text.count(b"\n") + 1
+    edges = np.empty(2 * cap, np.int64)
+    n, m, sl, du = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    rc = L.ref_parse(kind.encode(), C.c_char_p(text), i64(len(text)), C.byref(n), C.byref(m),
+                     C.byref(sl), C.byref(du), _p(edges), i64(cap))
+    _rc(L, rc, "ref_last_error")
+    return n.value, edges[: 2 * m.value].reshape(-1, 2), (sl.value, du.value)
+
+
 def ref_build_adjacency(n, edges):
     edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
     m = edges.shape[0]

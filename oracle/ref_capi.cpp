@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -323,6 +324,27 @@ int ref_bfs_tree(int64_t n, int64_t m, const int64_t* edges, int64_t root, uint8
     std::memcpy(level, st.level.data(), n * sizeof(int64_t));
     std::memcpy(parent, st.rooted.parent.data(), n * sizeof(int64_t));
     std::memcpy(parent_edge, st.parent_edge.data(), n * sizeof(int64_t));
+  });
+}
+
+// parse_edge_list / parse_dimacs_gr (core/src/graph.cpp:57-133) over an
+// in-memory text; parse errors (std::runtime_error) return 3 with the message.
+int ref_parse(const char* kind, const char* text, int64_t len, int64_t* n, int64_t* m,
+              int64_t* self_loops, int64_t* duplicates, int64_t* edges, int64_t cap) {
+  return guard([&] {
+    std::istringstream in(std::string(text, static_cast<size_t>(len)));
+    ParseStats st;
+    EdgeList g = std::strcmp(kind, "dimacs") == 0 ? parse_dimacs_gr(in, &st)
+                                                   : parse_edge_list(in, &st);
+    *n = g.n;
+    *m = g.m();
+    *self_loops = st.self_loops_removed;
+    *duplicates = st.duplicates_removed;
+    if (g.m() > cap) throw std::out_of_range("edge buffer too small");
+    for (int64_t i = 0; i < g.m(); ++i) {
+      edges[2 * i] = g.edges[i].first;
+      edges[2 * i + 1] = g.edges[i].second;
+    }
   });
 }
 

@@ -9,11 +9,11 @@ from .ett import (AdjacencyIndex, BridgeMask, EdgeList, InlabelIndex, NaiveIndex
                   RmqLcaIndex, RootedTree, SpanningTree, answer_batch, bfs_tree, build_adjacency,
                   ck_bridges, hybrid_bridges, inlabel_build, inlabel_lca, naive_build, naive_lca,
                   node_stats, rmq_lca, rmq_lca_build, tv_bridges)
-from ._lib import InvalidArgument, OutOfRange, lib
+from ._lib import InvalidArgument, OutOfRange, ParseError, lib
 
 __all__ = [
     "AdjacencyIndex", "BridgeMask", "EdgeList", "InlabelIndex", "NaiveIndex", "NodeStats",
     "RmqLcaIndex", "RootedTree", "SpanningTree", "answer_batch", "bfs_tree", "build_adjacency",
     "ck_bridges", "hybrid_bridges", "inlabel_build", "inlabel_lca", "naive_build", "naive_lca",
-    "node_stats", "rmq_lca", "rmq_lca_build", "tv_bridges", "InvalidArgument", "OutOfRange", "lib",
+    "node_stats", "rmq_lca", "rmq_lca_build", "tv_bridges", "InvalidArgument", "OutOfRange", "ParseError", "lib",
 ]

@@ -12,7 +12,7 @@ import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libettg.so")
 
-ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL = range(6)
+ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL, ETTG_EPARSE = range(7)
 ENGINE_INLABEL = 1
 ENGINE_RMQ = 2
 ENGINE_NAIVE = 4
@@ -28,6 +28,10 @@ i64 = C.c_int64
 u64 = C.c_uint64
 p = C.c_void_p
 i64p = C.POINTER(C.c_int64)
+
+
+class ParseStatsC(C.Structure):
+    _fields_ = [("self_loops_removed", C.c_int64), ("duplicates_removed", C.c_int64)]
 
 
 class PhaseTimes(C.Structure):
@@ -80,6 +84,10 @@ _SIGS = {
     "ettg_gen_queries_dev": ([i64, i64, u64, i64, p, C.POINTER(C.c_int), C.c_int, p], C.c_int),
     "ettg_gen_planted_bridge_graph": ([i64, i64, i64, u64, p, p], C.c_int),
     "ettg_road_like_edge_count": ([i64, i64, i64, i64, i64], i64),
+    "ettg_parse_edge_list": ([C.c_char_p, i64, C.c_int, p, i64, i64p, i64p,
+                              C.POINTER(ParseStatsC)], C.c_int),
+    "ettg_parse_dimacs_gr": ([C.c_char_p, i64, C.c_int, p, i64, i64p, i64p,
+                              C.POINTER(ParseStatsC)], C.c_int),
     "ettg_gen_road_like_graph": ([i64, i64, i64, i64, i64, u64, p, p], C.c_int),
 }
 
@@ -123,7 +131,13 @@ class CudaError(EttgError):
     code = ETTG_ECUDA
 
 
-_EXC = {ETTG_EINVAL: InvalidArgument, ETTG_ERANGE: OutOfRange, ETTG_ECUDA: CudaError}
+class ParseError(EttgError):
+    """std::runtime_error thrown by the reference's text parsers."""
+    code = ETTG_EPARSE
+
+
+_EXC = {ETTG_EINVAL: InvalidArgument, ETTG_ERANGE: OutOfRange, ETTG_ECUDA: CudaError,
+        ETTG_EPARSE: ParseError}
 
 
 def check(rc: int, gen: bool = False) -> None:

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from ._lib import (ENGINE_INLABEL, ENGINE_NAIVE, ENGINE_RMQ, LAYOUT_COMPACT, LAYOUT_NARROW, LAYOUT_SPLIT,
                    LAYOUT_WIDE,
-                   InvalidArgument, OutOfRange, check, lib, ptr)
+                   InvalidArgument, OutOfRange, ParseError, check, lib, ptr)
 
 K_NONE = -1
 K_GRASP_INFINITY = (1 << 64) - 1
@@ -286,6 +286,45 @@ class AdjacencyIndex:
     offsets: np.ndarray
     neighbors: np.ndarray
     edge_ids: np.ndarray
+
+
+@dataclass
+class ParseStats:
+    """core/include/ett/graph.hpp:27-32."""
+    self_loops_removed: int = 0
+    duplicates_removed: int = 0
+
+    def removed(self) -> int:
+        return self.self_loops_removed + self.duplicates_removed
+
+
+def _parse(fn: str, data, stats: ParseStats | None, device: int) -> EdgeList:
+    if hasattr(data, "read"):
+        data = data.read()
+    if isinstance(data, str):
+        data = data.encode()
+    data = bytes(data)
+    cap = data.count(b"\n") + 1  # lines: always enough room
+    edges = np.empty((cap, 2), np.int64)
+    n, m, st = C.c_int64(), C.c_int64(), _lib.ParseStatsC()
+    check(getattr(lib(), fn)(data, len(data), device, ptr(edges), cap, C.byref(n), C.byref(m),
+                             C.byref(st)))
+    if stats is not None:
+        stats.self_loops_removed = st.self_loops_removed
+        stats.duplicates_removed = st.duplicates_removed
+    return EdgeList(n.value, edges[: m.value])
+
+
+def parse_edge_list(data, stats: ParseStats | None = None, device: int = 0) -> EdgeList:
+    """parse_edge_list (core/src/graph.cpp:57-82) on the device; `data` is the
+    file's bytes / str or a binary file object.  Raises ParseError (the
+    reference's std::runtime_error) with the same "line N: ..." message."""
+    return _parse("ettg_parse_edge_list", data, stats, device)
+
+
+def parse_dimacs_gr(data, stats: ParseStats | None = None, device: int = 0) -> EdgeList:
+    """parse_dimacs_gr (core/src/graph.cpp:84-128) on the device."""
+    return _parse("ettg_parse_dimacs_gr", data, stats, device)
 
 
 def build_adjacency(g: EdgeList, device: int = 0) -> AdjacencyIndex:

@@ -1,6 +1,7 @@
 // C++ caller through include/ettg.hpp, written like the reference's own tests
 // (tests/lca_test.cpp:47-74, tests/bridges_test.cpp): exits non-zero on failure.
 #include <cstdio>
+#include <sstream>
 #include <stdexcept>
 
 #include "ettg.hpp"
@@ -57,6 +58,24 @@ int main() {
   CHECK(bt.parent == std::vector<ettg::i64>({-1, 0, 0, 2}));
   auto lc = ettg::largest_component(ettg::EdgeList{6, {{0, 1}, {2, 3}, {3, 4}}});
   CHECK(lc.graph.n == 3 && lc.old_to_new == std::vector<ettg::i64>({-1, -1, 0, 1, 2, -1}));
+  {  // tests/graph_test.cpp:21-31, :41-45
+    std::istringstream in("0 1\n1 0\n0 0\n");
+    ettg::ParseStats ps;
+    auto g = ettg::parse_edge_list(in, &ps);
+    CHECK((g.n == 2 && g.m() == 1 && g.edges[0].first == 0 && g.edges[0].second == 1));
+    CHECK(ps.self_loops_removed == 1 && ps.duplicates_removed == 1);
+    std::istringstream bad("0 1\nfoo 2\n");
+    bool threw = false;
+    try {
+      ettg::parse_edge_list(bad);
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()).find("line 2") != std::string::npos;
+    }
+    CHECK(threw);
+    std::istringstream gr("p sp 2 2\na 1 2 1\na 2 1 1\n");
+    auto d = ettg::parse_dimacs_gr(gr);
+    CHECK(d.n == 2 && d.m() == 1);
+  }
   std::printf("shim ok\n");
   return 0;
 }
