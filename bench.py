@@ -310,6 +310,49 @@ def bridges_section(ett, args, device, peak):
     return out
 
 
+def ingestion_config_c(ett, args):
+    """parse_edge_list of config C written as text
+    (write_edge_list, 8M lines, ~110 MB), end to end from host bytes to host
+    edges through ettg_parse_edge_list, vs the reference parser on a bounded
+    prefix (it is sequential: ~1.3 us per line)."""
+    import time
+    g, _ = ett.planted_bridge_graph(1_000_000, 8_000_000, 10_000, 4)
+    text = ett.write_edge_list(g)
+    lines = text.count(b"\n")
+    got = ett.parse_edge_list(text)  # warm-up (arena, module load)
+    ok = bool(got.n == g.n and np.array_equal(got.edges, np.sort(g.edges, axis=1)))
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ett.parse_edge_list(text)
+        ts.append(time.perf_counter() - t0)
+    out = {"workload": "parse_edge_list(write_edge_list(config C)): 8M lines, "
+                       f"{len(text) / 1e6:.0f} MB, host bytes -> host int64 edges",
+           "value": lines / min(ts), "unit": "lines/s", "ms": 1e3 * min(ts),
+           "bytes_per_s": len(text) / min(ts),
+           "parity": "identical to write_edge_list input (normalised)" if ok else "MISMATCH"}
+    if args.cpu_baseline:
+        try:
+            from oracle import oracle as orc
+            if orc.have_ref():
+                cut = 0
+                for _ in range(2_000_000):
+                    cut = text.index(b"\n", cut) + 1
+                sample = text[:cut]
+                t0 = time.perf_counter()
+                want = orc.ref_parse("edges", sample)
+                dt = time.perf_counter() - t0
+                mine = ett.parse_edge_list(sample)
+                out["cpu_baseline"] = {
+                    "value": 2_000_000 / dt, "unit": "lines/s", "cores": 1, "kind": "reference",
+                    "sample": "reference parse_edge_list (sequential) on the first 2M lines",
+                    "parity_vs_ours": bool(want[0] == mine.n and np.array_equal(want[1],
+                                                                                mine.edges))}
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"error": str(e)[:200]}
+    return out
+
+
 def bridges_config_c(ett, args, device, peak):
     """Config C: planted_bridge_graph(1M, 8M, b=10,000, seed 4); the reference's
     tv_bridges runs the full workload on the host for an exact comparison."""
@@ -492,6 +535,7 @@ def main():
         torch.cuda.empty_cache()
         line["bridges"] = bridges_section(ett, args, device, peak)
         line["bridges_config_C"] = bridges_config_c(ett, args, device, peak)
+        line["ingestion_config_C"] = ingestion_config_c(ett, args)
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -271,13 +271,18 @@ typedef struct ettg_parse_stats {
  * device.  `text` is the whole file (host memory, `len` bytes).  Output: n,
  * m and the normalised simple edge list (min, max) in first-occurrence
  * order into `edges` (2*cap int64).  If cap < m the call fails with
- * ETTG_ERANGE and *m holds the size needed (the number of lines always
- * suffices).  Malformed input gives ETTG_EPARSE with the reference's message
+ * ETTG_ERANGE and *m holds the size needed (len/4 + 2 always suffices:
+ * an edge line takes at least 4 bytes).  Malformed input gives ETTG_EPARSE with the reference's message
  * ("line N: ...").  Node ids must be < 2^32 (ETTG_ERANGE otherwise). */
 int ettg_parse_edge_list(const char* text, int64_t len, int device, int64_t* edges,
                          int64_t cap, int64_t* n, int64_t* m, ettg_parse_stats* stats);
 int ettg_parse_dimacs_gr(const char* text, int64_t len, int device, int64_t* edges,
                          int64_t cap, int64_t* n, int64_t* m, ettg_parse_stats* stats);
+/* write_edge_list (core/src/graph.cpp:131-133): "u v\n" per edge into `out`
+ * (host formatting).  *len = bytes needed; ETTG_ERANGE if cap < *len.
+ * Errors are reported by ettg_gen_last_error(). */
+int ettg_write_edge_list(const int64_t* edges, int64_t m, char* out, int64_t cap,
+                         int64_t* len);
 
 #ifdef __cplusplus
 }

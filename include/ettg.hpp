@@ -247,8 +247,7 @@ namespace detail {
 template <class Fn>
 EdgeList parse_stream(Fn fn, std::istream& in, ParseStats* stats, int device) {
   const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
-  i64 cap = 1;
-  for (char c : text) cap += c == '\n';
+  const i64 cap = static_cast<i64>(text.size()) / 4 + 2;  // an edge line takes >= 4 bytes
   std::vector<i64> buf(2 * static_cast<size_t>(cap));
   i64 n = 0, m = 0;
   ettg_parse_stats st{0, 0};

@@ -88,6 +88,7 @@ _SIGS = {
                               C.POINTER(ParseStatsC)], C.c_int),
     "ettg_parse_dimacs_gr": ([C.c_char_p, i64, C.c_int, p, i64, i64p, i64p,
                               C.POINTER(ParseStatsC)], C.c_int),
+    "ettg_write_edge_list": ([p, i64, p, i64, i64p], C.c_int),
     "ettg_gen_road_like_graph": ([i64, i64, i64, i64, i64, u64, p, p], C.c_int),
 }
 

@@ -10,6 +10,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <charconv>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -63,6 +64,12 @@ int gen_guard(F&& f) {
   } catch (const GenError& e) {
     g_gen_err = e.what();
     return ETTG_EINVAL;
+  } catch (const std::invalid_argument& e) {
+    g_gen_err = e.what();
+    return ETTG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_gen_err = e.what();
+    return ETTG_ERANGE;
   } catch (const std::exception& e) {
     g_gen_err = e.what();
     return ETTG_EINTERNAL;
@@ -387,6 +394,29 @@ int ettg_gen_road_like_graph(int64_t W, int64_t H, int64_t extra, int64_t r, int
       edges[2 * k + 1] = v;
       truth[k++] = 1;
     }
+  });
+}
+
+// write_edge_list (core/src/graph.cpp:131-133): "u v\n" per edge into a
+// caller buffer (host text formatting; the parsers' inverse).  *len receives
+// the bytes needed; returns ETTG_ERANGE without writing past cap if short.
+int ettg_write_edge_list(const int64_t* edges, int64_t m, char* out, int64_t cap, int64_t* len) {
+  return gen_guard([&] {
+    if (m < 0 || (m > 0 && !edges) || !len || cap < 0 || (cap > 0 && !out))
+      throw std::invalid_argument("null or negative argument");
+    int64_t pos = 0;
+    char tmp[48];
+    for (int64_t i = 0; i < m; ++i) {
+      char* p = std::to_chars(tmp, tmp + 24, edges[2 * i]).ptr;
+      *p++ = ' ';
+      p = std::to_chars(p, tmp + 48, edges[2 * i + 1]).ptr;
+      *p++ = '\n';
+      const int64_t k = p - tmp;
+      if (pos + k <= cap) std::memcpy(out + pos, tmp, static_cast<size_t>(k));
+      pos += k;
+    }
+    *len = pos;
+    if (pos > cap) throw std::out_of_range("text buffer too small (len returned)");
   });
 }
 

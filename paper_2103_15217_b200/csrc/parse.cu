@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
+#include "trace.cuh"
 
 namespace ettg {
 namespace {
@@ -254,13 +255,13 @@ __global__ void k_first_occurrence(const u32* __restrict__ kmin, const u32* __re
   }
 }
 
-struct EdgeOut {
+struct EdgeOut {  // the reference's i64 pairs, so the host copy is one memcpy
   const u32* kmin;
   const u32* kmax;
   u32 cap;
-  uint2* out;
+  longlong2* out;
   __device__ __forceinline__ void operator()(u64 c, u32 r) const {
-    if (r < cap) out[r] = make_uint2(kmin[c], kmax[c]);
+    if (r < cap) out[r] = make_longlong2(kmin[c], kmax[c]);
   }
 };
 
@@ -277,7 +278,7 @@ struct ParseWs {
   u32 *kmin = nullptr, *kmax = nullptr, *iota = nullptr, *k1 = nullptr, *v1 = nullptr,
       *k2 = nullptr, *v2 = nullptr;
   uint8_t* keep = nullptr;
-  uint2* edges = nullptr;
+  longlong2* edges = nullptr;
   unsigned long long* counters = nullptr;
   u32* words = nullptr;
   SortWs sort;
@@ -300,7 +301,7 @@ struct ParseWs {
     k2 = c.take<u32>(L + 1);
     v2 = c.take<u32>(L + 1);
     keep = c.take<uint8_t>(L + 16);
-    edges = c.take<uint2>(L + 1);
+    edges = c.take<longlong2>(L + 1);
     counters = c.take<unsigned long long>(4);
     words = c.take<u32>(8);
     sort.carve(c, L + 1);
@@ -375,14 +376,17 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   c = Carver{lease.base()};
   ws.carve(c, len, nlines);
 
+  Trace tr(dimacs ? "parse_dimacs_gr" : "parse_edge_list", st);
   CK(cudaMemsetAsync(ws.counters, 0, 4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(ws.words, 0xFF, 8 * sizeof(u32), st));
   if (len) CK(cudaMemcpyAsync(ws.text, text, len, cudaMemcpyHostToDevice, st));
+  tr.mark("h2d");
   if (len) {
     k_newlines<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.text, len, ws.flags);
     CK_LAUNCH();
     compact_u8(ws.flags, len, PosOut{ws.nlpos}, ws.scan, ws.words + 1, st);
   }
+  tr.mark("lines");
   const Lines L{ws.text, len, ws.nlpos, static_cast<u32>(nnl_host)};
   if (nlines) {
     if (dimacs)
@@ -393,6 +397,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
           L, nlines, ws.kind, ws.err, ws.va, ws.vb);
     CK_LAUNCH();
   }
+  tr.mark("tokens");
   u32 np = 0;
   if (dimacs && nlines) {
     k_kind_flags<<<std::min(g, blocks_for(nlines, 256)), 256, 0, st>>>(ws.kind, nlines,
@@ -423,6 +428,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
     parse_error(text, s, sb[1], first[0], code, dimacs);
   }
   if (dimacs && np == 0) throw Error(ETTG_EPARSE, "missing DIMACS problem line");
+  tr.mark("errors");
 
   // ---- normalise: n, self-loops, first occurrence of each unordered pair ----
   unsigned long long cnt[4] = {0, 0, 0, 0};
@@ -440,6 +446,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
     CK(cudaMemcpyAsync(&C, ws.words + 3, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
+  tr.mark("candidates");
   u32 m = 0;
   if (C) {
     const u64 nmax = cnt[0];
@@ -455,6 +462,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
     CK(cudaMemcpyAsync(&m, ws.words + 4, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
+  tr.mark("dedup");
   *n_out = static_cast<int64_t>(cnt[0]);
   *m_out = m;
   if (stats) {
@@ -463,14 +471,10 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   }
   if (static_cast<u64>(cap) < m) throw Error(ETTG_ERANGE, "edge buffer too small (m returned)");
   if (m) {
-    std::vector<uint2> tmp(m);
-    CK(cudaMemcpyAsync(tmp.data(), ws.edges, u64(m) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(edges_out, ws.edges, u64(m) * 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (u32 i = 0; i < m; ++i) {
-      edges_out[2 * i] = tmp[i].x;
-      edges_out[2 * i + 1] = tmp[i].y;
-    }
   }
+  tr.mark("d2h");
 }
 
 }  // namespace

@@ -304,7 +304,7 @@ def _parse(fn: str, data, stats: ParseStats | None, device: int) -> EdgeList:
     if isinstance(data, str):
         data = data.encode()
     data = bytes(data)
-    cap = data.count(b"\n") + 1  # lines: always enough room
+    cap = len(data) // 4 + 2  # an edge line takes >= 4 bytes ("u v\\n"): always enough
     edges = np.empty((cap, 2), np.int64)
     n, m, st = C.c_int64(), C.c_int64(), _lib.ParseStatsC()
     check(getattr(lib(), fn)(data, len(data), device, ptr(edges), cap, C.byref(n), C.byref(m),
@@ -325,6 +325,18 @@ def parse_edge_list(data, stats: ParseStats | None = None, device: int = 0) -> E
 def parse_dimacs_gr(data, stats: ParseStats | None = None, device: int = 0) -> EdgeList:
     """parse_dimacs_gr (core/src/graph.cpp:84-128) on the device."""
     return _parse("ettg_parse_dimacs_gr", data, stats, device)
+
+
+def write_edge_list(g: EdgeList) -> bytes:
+    """write_edge_list (core/src/graph.cpp:131-133): "u v\\n" per edge."""
+    need = C.c_int64()
+    rc = lib().ettg_write_edge_list(ptr(g.edges), g.m(), None, 0, C.byref(need))
+    if rc not in (_lib.ETTG_OK, _lib.ETTG_ERANGE):
+        check(rc, gen=True)
+    buf = C.create_string_buffer(max(need.value, 1))
+    check(lib().ettg_write_edge_list(ptr(g.edges), g.m(), buf, need.value, C.byref(need)),
+          gen=True)
+    return buf.raw[: need.value]
 
 
 def build_adjacency(g: EdgeList, device: int = 0) -> AdjacencyIndex:
