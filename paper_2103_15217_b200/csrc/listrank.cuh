@@ -63,22 +63,11 @@ __device__ __forceinline__ bool lr_is_splitter(u32 e, u32 head, u32 seed, u32 ma
   return e == head || (mix32(e ^ seed) & mask) == 0u;
 }
 
-// ---- splitter compaction via the look-back scan ---------------------------
+// ---- splitter predicates ---------------------------------------------------
 struct SplIn {
   u32 head, seed, mask;
   __device__ __forceinline__ u32 operator()(u64 i) const {
     return lr_is_splitter(static_cast<u32>(i), head, seed, mask) ? 1u : 0u;
-  }
-};
-struct SplOut {
-  u32 head, seed, mask, cap;
-  u32* spl;
-  u32* err;
-  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
-    if (lr_is_splitter(static_cast<u32>(i), head, seed, mask)) {
-      if (excl < cap) spl[excl] = static_cast<u32>(i);
-      else atomicOr(err, kErrCapacity);
-    }
   }
 };
 // Level >= 1: head and size live in device memory; the scan runs over the
@@ -91,19 +80,60 @@ struct SplInDev {
     return (i < *S && lr_is_splitter(static_cast<u32>(i), *head, seed, mask)) ? 1u : 0u;
   }
 };
-struct SplOutDev {
-  const u32* head;
-  const u32* S;
-  u32 seed, mask, cap;
-  u32* spl;
-  u32* err;
-  __device__ __forceinline__ void operator()(u64 i, u32 excl) const {
-    if (i < *S && lr_is_splitter(static_cast<u32>(i), *head, seed, mask)) {
-      if (excl < cap) spl[excl] = static_cast<u32>(i);
-      else atomicOr(err, kErrCapacity);
-    }
+
+// Splitter compaction without a look-back chain.  The walk consumes
+// splitters through a work ticket, so their order in `spl` only names the
+// sublists and never affects a rank; each CTA therefore counts the
+// splitters of its contiguous 8192-index chunk (pure hashing, no loads),
+// reserves a range with one atomicAdd and writes them in index order
+// within the chunk.  Replaces a 4096-item-tile decoupled look-back scan
+// whose 16K-tile chain took 0.30 ms on 64M elements with no DRAM traffic
+// (ncu, config D).
+constexpr int kSplThreads = 256;
+constexpr int kSplPer = 32;  // consecutive indices per thread
+template <class In>
+__global__ void __launch_bounds__(kSplThreads)
+    k_spl_compact(In in, u64 n, u32* __restrict__ spl, u32 cap, u32* count, u32* err) {
+  __shared__ u32 s_warp[kSplThreads / 32];
+  __shared__ u32 s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 i0 = (static_cast<u64>(blockIdx.x) * kSplThreads + tid) * kSplPer;
+  u32 bits = 0;
+#pragma unroll
+  for (int j = 0; j < kSplPer; ++j) {
+    const u64 i = i0 + j;
+    if (i < n && in(i)) bits |= 1u << j;
   }
-};
+  const u32 c = __popc(bits);
+  const u32 incl = warp_incl_scan(c);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 w = lane < kSplThreads / 32 ? s_warp[lane] : 0u;
+    const u32 wi = warp_incl_scan(w);
+    if (lane < kSplThreads / 32) s_warp[lane] = wi - w;
+    const u32 tot = __shfl_sync(0xffffffffu, wi, kSplThreads / 32 - 1);
+    if (lane == 0) s_base = tot ? atomicAdd(count, tot) : 0u;
+  }
+  __syncthreads();
+  u32 pos = s_base + s_warp[warp] + incl - c;
+  while (bits) {
+    const int j = __ffs(bits) - 1;
+    bits &= bits - 1;
+    if (pos < cap) spl[pos] = static_cast<u32>(i0 + j);
+    else atomicOr(err, kErrCapacity);
+    ++pos;
+  }
+}
+
+template <class In>
+void spl_compact(In in, u64 n, u32* spl, u32 cap, u32* count, u32* err, cudaStream_t st) {
+  if (n == 0) return;
+  const u64 per = u64(kSplThreads) * kSplPer;
+  k_spl_compact<In><<<static_cast<unsigned>((n + per - 1) / per), kSplThreads, 0, st>>>(
+      in, n, spl, cap, count, err);
+  CK_LAUNCH();
+}
 
 // Counters block (u32 words) shared by one ranking.
 struct LrCounters {
@@ -480,9 +510,8 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
   const u32 seed0 = lr_seed(0);
   const u32 cap1 = ws.lv[1].cap;
   // level 0 splitters -> counters[kNspl]; sublists beyond come from cap splits
-  scan_exclusive(SplIn{head, seed0, mask0},
-                 SplOut{head, seed0, mask0, cap1, ws.lv[0].spl, cnt + LrCounters::kErr}, k,
-                 ws.lv[0].scan_status, cnt + LrCounters::kNspl, st);
+  spl_compact(SplIn{head, seed0, mask0}, k, ws.lv[0].spl, cap1, cnt + LrCounters::kNspl,
+              cnt + LrCounters::kErr, st);
   CK(cudaMemcpyAsync(cnt + LrCounters::kSubTotal0, cnt + LrCounters::kNspl, sizeof(u32),
                      cudaMemcpyDeviceToDevice, st));
   tr.mark("splitters0");
@@ -509,9 +538,8 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
     u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
     u32* hd_next = cnt + LrCounters::kLevelBase + 4 * (l + 1) + 2;
     const u32 seed = lr_seed(l), mask = kLrL - 1;
-    scan_exclusive(SplInDev{hd, S_l, seed, mask},
-                   SplOutDev{hd, S_l, seed, mask, N.cap, L.spl, cnt + LrCounters::kErr}, L.cap,
-                   L.scan_status, nspl, st);
+    spl_compact(SplInDev{hd, S_l, seed, mask}, L.cap, L.spl, N.cap, nspl,
+                cnt + LrCounters::kErr, st);
     k_lr_clamp<<<1, 1, 0, st>>>(nspl, N.cap, cnt + LrCounters::kErr);
     k_lr_walk<<<walk_blocks, 256, 0, st>>>(L.succ, L.w, S_l, hd, seed, mask, L.spl, nspl, tick,
                                           L.rec_sid, L.rec_loc, L.sub_next, L.sub_w,
