@@ -65,6 +65,17 @@ def ncu_traffic(kernel_key: str):
         return None
 
 
+def bridges_traffic(n, m):
+    """DRAM bytes per tv_bridges call on config D from the committed ncu sweep
+    (all kernels of one call), or None for another graph size."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f).get("bridges_D", {})
+        return s["dram_bytes_per_call"] if (s.get("n"), s.get("m")) == (n, m) else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """pynvml sampling of SM clock + clock-event reasons during a region."""
 
@@ -290,8 +301,10 @@ def bridges_section(ett, args, device, peak):
            "roofline": {"bound": "hbm", "achieved": bytes_model / (tot / 1e3) / 1e9,
                         "peak": peak[0], "unit": "GB/s",
                         "frac": bytes_model / (tot / 1e3) / 1e9 / peak[0],
-                        "traffic": None, "peak_kind": peak[1],
+                        "traffic": bridges_traffic(n, m), "peak_kind": peak[1],
                         "model": "41*m + 108*n bytes per call (SURVEY.md 8(d))",
+                        "traffic_note": "DRAM bytes of every kernel of one call (ncu, cold, "
+                                        "profiles/ncu_summary.json bridges_D)",
                         "io_floor_frac": 9 * m / (tot / 1e3) / 1e9 / peak[0]}}
     if args.cpu_baseline:
         from oracle import oracle as orc
