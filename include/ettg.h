@@ -236,6 +236,16 @@ int ettg_gen_sample_queries(int64_t n, int64_t q, uint64_t seed,
                             int64_t* pairs);
 int ettg_gen_random_connected_graph(int64_t n, int64_t m, uint64_t seed,
                                     int64_t* edges);
+/* grasp_tree on the device in counter mode (parent[i] = draw i); u32 parent
+ * array, 0xFFFFFFFF at the root 0.  *rejected as for ettg_gen_queries_dev. */
+int ettg_gen_grasp_tree_dev(int64_t n, uint64_t gamma, uint64_t seed, uint32_t* d_parent,
+                            int* rejected, int device, void* stream);
+/* permute_labels on the device: the reference's Fisher-Yates swap sequence
+ * executed as parallel rounds of deterministic reservations (bit-identical
+ * to the sequential loop).  d_parent_out must not alias d_parent. */
+int ettg_gen_permute_labels_dev(const uint32_t* d_parent, int64_t n, int64_t root,
+                                uint64_t seed, uint32_t* d_parent_out, int64_t* root_out,
+                                int* rejected, int device, void* stream);
 /* sample_queries on the device in counter mode: query i of the stream
  * (offset + i) is SplitMix64 draws 2(offset+i)+1 and 2(offset+i)+2.
  * *rejected is set non-zero if any Lemire rejection occurred (the counter

@@ -82,6 +82,9 @@ _SIGS = {
     "ettg_gen_sample_queries": ([i64, i64, u64, p], C.c_int),
     "ettg_gen_random_connected_graph": ([i64, i64, u64, p], C.c_int),
     "ettg_gen_queries_dev": ([i64, i64, u64, i64, p, C.POINTER(C.c_int), C.c_int, p], C.c_int),
+    "ettg_gen_grasp_tree_dev": ([i64, u64, u64, p, C.POINTER(C.c_int), C.c_int, p], C.c_int),
+    "ettg_gen_permute_labels_dev": ([p, i64, i64, u64, p, i64p, C.POINTER(C.c_int), C.c_int, p],
+                                    C.c_int),
     "ettg_gen_planted_bridge_graph": ([i64, i64, i64, u64, p, p], C.c_int),
     "ettg_road_like_edge_count": ([i64, i64, i64, i64, i64], i64),
     "ettg_parse_edge_list": ([C.c_char_p, i64, C.c_int, p, i64, i64p, i64p,

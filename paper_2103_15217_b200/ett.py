@@ -484,6 +484,26 @@ def road_like_graph(W: int, H: int, extra: int, r: int, pendant: int, seed: int)
     return EdgeList(W * H + pendant, out), truth
 
 
+def grasp_tree_dev(n: int, gamma: int, seed: int, d_parent, device: int = 0,
+                   stream: int | None = None) -> bool:
+    """Counter-mode grasp_tree into a uint32/int32 device tensor (root 0 ->
+    0xFFFFFFFF); False if a Lemire rejection invalidated the counter replay."""
+    rej = C.c_int()
+    check(lib().ettg_gen_grasp_tree_dev(n, gamma, seed, ptr(d_parent), C.byref(rej), device,
+                                        stream))
+    return rej.value == 0
+
+
+def permute_labels_dev(d_parent, n: int, root: int, seed: int, d_out, device: int = 0,
+                       stream: int | None = None) -> tuple[int, bool]:
+    """permute_labels on the device (parallel Fisher-Yates, bit-identical);
+    returns (new root, counter replay valid)."""
+    r, rej = C.c_int64(), C.c_int()
+    check(lib().ettg_gen_permute_labels_dev(ptr(d_parent), n, root, seed, ptr(d_out), C.byref(r),
+                                            C.byref(rej), device, stream))
+    return r.value, rej.value == 0
+
+
 def gen_queries_dev(n: int, q: int, seed: int, offset: int, d_pairs, device: int = 0,
                     stream: int | None = None) -> bool:
     """Counter-mode sample_queries into a uint32 device tensor; False on rejection."""

@@ -329,3 +329,37 @@ def test_layout_flag_errors(ett):
     buf = torch.zeros(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")
     with pytest.raises(ett.InvalidArgument, match="not an exported"):
         ett.attach_index(buf, t.n)
+
+
+# --------------------------------------------- device generators (8(f) row 4)
+@pytest.mark.parametrize("n", [1, 2, 3, 1000, 1_000_003])
+@pytest.mark.parametrize("gamma", [1, 2, 7, GRASP_INF])
+def test_device_grasp_and_permute_match_host(ett, n, gamma):
+    import torch
+    d = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    assert ett.grasp_tree_dev(n, gamma, 11, d)
+    t = ett.grasp_tree(n, gamma, 11)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32).astype(np.int64),
+                          np.where(t.parent < 0, 0xFFFFFFFF, t.parent))
+    out = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    root, ok = ett.permute_labels_dev(d, n, 0, 12, out)
+    assert ok
+    pt = ett.permute_labels(t, 12)
+    assert root == pt.root
+    assert np.array_equal(out.cpu().numpy().view(np.uint32).astype(np.int64),
+                          np.where(pt.parent < 0, 0xFFFFFFFF, pt.parent))
+
+
+def test_device_permute_large_matches_reference(ett, ref):
+    """Config B's tree built entirely on the device equals the reference's."""
+    import torch
+    n = 4_000_000
+    d = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    assert ett.grasp_tree_dev(n, 1, 1, d)
+    out = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    root, ok = ett.permute_labels_dev(d, n, 0, 2, out)
+    assert ok
+    want, want_root = ref.permute_labels(ref.grasp_tree(n, 1, 1), 0, 2)
+    got = out.cpu().numpy().view(np.uint32).astype(np.int64)
+    assert root == want_root
+    assert np.array_equal(np.where(got == 0xFFFFFFFF, -1, got), want)
