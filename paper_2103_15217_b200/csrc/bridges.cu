@@ -162,8 +162,12 @@ __global__ void __launch_bounds__(256, kMinB)
     }
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      a[j] = uf_find_from(par, uv[j].x, a[j]);
-      b[j] = uf_find_from(par, uv[j].y, b[j]);
+      // equal parents => same tree: no find needed (after the compress pass
+      // between the phases this settles most phase-1 edges with two loads)
+      if (a[j] != b[j]) {
+        a[j] = uf_find_from(par, uv[j].x, a[j]);
+        b[j] = uf_find_from(par, uv[j].y, b[j]);
+      }
       if (a[j] < b[j]) {
         const u32 tmp = a[j];
         a[j] = b[j];
