@@ -65,6 +65,26 @@ def ncu_traffic(kernel_key: str):
         return None
 
 
+def l1_tag_stage(key, queries, secs, clocks):
+    """Scattered gathers are issued through the L1/TEX tag stage, which looks
+    up about one 32-B sector per clock per SM (tools/tma_gather_micro.cu: 276.5
+    G random 4-B loads/s = 0.95 x 148 SMs x 1.965 GHz).  Sectors per query come
+    from the committed ncu capture of the same kernel and config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)[key]
+        per_q = s["l1_tag_sectors_per_launch"] / s["units_per_launch"]
+    except Exception:
+        return None
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    achieved = per_q * queries / secs / 1e9
+    peak = sms * mhz / 1e3
+    return {"sectors_per_query": per_q, "achieved_G_sectors_per_s": achieved,
+            "peak_G_sectors_per_s": peak, "frac": achieved / peak,
+            "source": "profiles/ncu_summary.json (l1tex__t_sectors ld+st per launch)"}
+
+
 def bridges_traffic(n, m):
     """DRAM bytes per tv_bridges call on config D from the committed ncu sweep
     (all kernels of one call), or None for another graph size."""
@@ -509,6 +529,8 @@ def main():
                          "survey_model": {"bytes_per_query": Bq_survey, "lifts_per_query": Lbar,
                                           "achieved": Bq_survey * q_r / secs / 1e9,
                                           "frac": Bq_survey * q_r / secs / 1e9 / peak[0]},
+                         "l1_tag_stage": l1_tag_stage(f"{kname}_B", q_r, secs,
+                                                      sec["clocks"]),
                          "l2_gather": {"node_gathers_G_per_s": node_gathers,
                                        "ceiling_G_per_s": L2_GATHER_CEILING.get(layout),
                                        "frac": (node_gathers / L2_GATHER_CEILING[layout]
@@ -538,6 +560,9 @@ def main():
                 / peak[0],
                 "l2_gather_frac": (2 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
                                    / L2_GATHER_CEILING[secE["idx"].layout()[0]]),
+                "l1_tag_stage": l1_tag_stage(
+                    {"split": "k_lca_inlabel_split_E"}.get(secE["idx"].layout()[0], ""),
+                    secE["q_rank"], secE["step_ms"] / 1e3, secE["clocks"]),
                 "note": "140 B/query assumes every gather is an HBM sector; the split "
                         "layout's 128 MB node table is half L2-resident and lifts hit "
                         "L2, so the survey-model fraction can exceed 1"}

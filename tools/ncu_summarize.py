@@ -39,6 +39,8 @@ def main():
         "l2_hit_pct": avg("lts__t_sector_hit_rate.pct"),
         "l1_hit_pct": avg("l1tex__t_sector_hit_rate.pct"),
         "achieved_occupancy_pct": avg("sm__warps_active.avg.pct_of_peak_sustained_active"),
+        "l1_tag_sectors_per_launch": (avg("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
+                                      + avg("l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum")),
         "launches_averaged": len(sel),
         "source": source,
     }
