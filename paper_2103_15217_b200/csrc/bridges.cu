@@ -18,14 +18,16 @@
 //                              any rotation gives a valid tour)
 //             k_tree_succ      succ(e) = next(twin(e)); cut before first(0)
 //             list_rank_core   ranks of the tour rooted at vertex 0
-//             k_tour_flags     position -> (tree edge, is-down)
-//             scan + functor   #downs before each position => preorder, size and
-//                              parent edge, written preorder-indexed
-//   lowhigh   k_lowhigh_init / k_lowhigh_edges (one atomicMin + one atomicMax
-//             per non-tree edge: the reference's other two updates are provably
-//             no-ops because each slot is seeded with its own preorder),
-//             block-sparse min/max table over preorder, k_classify writes the
-//             bridge mask by input edge id.
+//             k_tv_keys        node key = tour rank of its down half-edge + 2
+//                              (order-isomorphic to the preorder; a subtree is
+//                              the key range up to its up half-edge), so TV
+//                              needs no "#downs before" scan (CK / hybrid still
+//                              use k_tour_flags + the StatsOut scan for levels)
+//   lowhigh   k_lh_neutral / k_lowhigh_edges (one atomicMin + one atomicMax
+//             per non-tree edge into the slots of the endpoints' keys; the
+//             reference's other two updates, and its own-preorder seeds, never
+//             change the test), block-sparse min/max table over the 2n key
+//             slots, k_classify_tour writes the bridge mask by input edge id.
 //
 // The spanning forest may differ from the reference's; bridges are a graph
 // property, so the mask cannot (core/include/ett/bridges.hpp:56-58).
@@ -458,6 +460,63 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- TV on Euler-tour positions (no preorder scan) -------------------------
+// Any DFS numbering in which every subtree is contiguous serves the TV test
+// (core/src/bridges.cpp:280-306); the tour itself is one.  Node key K(c) =
+// rank(down(c)) + 2 (K(root) = 1) is order-isomorphic to the preorder, and
+// c's subtree is exactly the nodes with keys in [K(c), U(c)), U(c) =
+// rank(up(c)) + 2.  Low/high slots are indexed by key - 1 over 2n entries
+// (up positions stay neutral), so the per-position "#downs before" scan of
+// node_stats is not needed: bridge(c) iff low >= K(c) and high < U(c).
+__global__ void k_tv_keys(Lr0View lr, u32 T, const uint2* __restrict__ tend, u32 root,
+                          u32* __restrict__ key_of, uint2* __restrict__ kt) {
+  const u32 S1 = *lr.d_S1;
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    u32 r0, r1, d;
+    lr.get(2 * t, S1, r0, d);
+    lr.get(2 * t + 1, S1, r1, d);
+    const uint2 uv = tend[t];
+    const bool first_is_down = r0 < r1;  // half-edge 2t = (u -> v)
+    const u32 child = first_is_down ? uv.y : uv.x;
+    const u32 kd = min(r0, r1) + 2, ku = max(r0, r1) + 2;
+    key_of[child] = kd;
+    kt[t] = make_uint2(kd, ku);
+    if (t == 0) key_of[root] = 1;
+  }
+}
+
+__global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    lh[i] = make_uint2(0xFFFFFFFFu, 0u);
+}
+
+__global__ void __launch_bounds__(256)
+    k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ sp, u32 nb, u32 len,
+                    const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
+                    uint8_t* __restrict__ mask, u32 m) {
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    const uint2 k = kt[t];
+    const u32 a = k.x - 1, b = min(k.y - 1, len - 1);
+    uint2 acc = lh[a];
+    if (b - a < 64) {
+      for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+    } else {
+      const u32 la = a >> 5, lb = b >> 5;
+      for (u32 j = a + 1; j < (la + 1) * 32; ++j) acc = lh_merge(acc, __ldg(lh + j));
+      for (u32 j = lb * 32; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+      if (lb > la + 1) {
+        const u32 cnt = lb - la - 1;
+        const int kk = hb32(cnt);
+        const uint2* row = sp + static_cast<u64>(kk) * nb;
+        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kk)]));
+      }
+    }
+    const bool inside = acc.x >= k.x && acc.y < k.y;
+    const u32 e = tedge[t];
+    if (e < m) mask[e] = inside ? 1 : 0;
+  }
+}
+
 // Edge-kernel launch shape: 2 edges per thread at 8 CTAs/SM (<= 32 regs),
 // grid = whole waves of resident CTAs from the occupancy API.  A/B on config
 // D (tools/trace_bridges.py, profiles/r1_bridges_tuning.md): hooking 2.88 ->
@@ -508,6 +567,7 @@ struct BridgeWs {
   u32* size_by_pre = nullptr;
   u32* pedge_by_pre = nullptr;
   uint2* lh = nullptr;
+  uint2* kt = nullptr;  // TV: (key, up key) per tree edge
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
   u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
@@ -546,8 +606,10 @@ struct BridgeWs {
     pre_of = c.take<u32>(n);
     size_by_pre = c.take<u32>(n);
     pedge_by_pre = c.take<u32>(n);
-    lh = c.take<uint2>(n);
-    nb = (n + 31) / 32;
+    const u32 lh_len = engine == ETTG_BRIDGES_TV ? 2 * n : n;
+    lh = c.take<uint2>(lh_len);
+    if (engine == ETTG_BRIDGES_TV) kt = c.take<uint2>(n);
+    nb = (lh_len + 31) / 32;
     levels = 32 - __builtin_clz(nb);
     sp = c.take<uint2>(static_cast<u64>(levels) * nb);
     words = c.take<u32>(16);
@@ -682,29 +744,37 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       list_rank_core(k, head, NoDown{}, ws.lr, st, sms);
       tr.mark("list_rank");
       const Lr0View lv = lr0_view(ws.lr);
-      k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
-      CK_LAUNCH();
-      scan_exclusive(DownIn{ws.flags},
-                     StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of,
-                              ws.size_by_pre, ws.pedge_by_pre, ws.rec, ws.pedge_of},
-                     k, ws.scan_k, nullptr, st);
-      tr.mark("preorder");
+      if (engine == ETTG_BRIDGES_TV) {
+        k_tv_keys<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.tend, 0,
+                                                                   ws.pre_of, ws.kt);
+        CK_LAUNCH();
+        tr.mark("keys");
+      } else {
+        k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
+        CK_LAUNCH();
+        scan_exclusive(DownIn{ws.flags},
+                       StatsOut{ws.flags, ws.tedge, ws.tend, lv, n, ws.pre_of,
+                                ws.size_by_pre, ws.pedge_by_pre, ws.rec, ws.pedge_of},
+                       k, ws.scan_k, nullptr, st);
+        tr.mark("preorder");
+      }
     }
-    k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre, ws.rec,
-                                  ws.pedge_of);
-    CK_LAUNCH();
+    if (engine != ETTG_BRIDGES_TV || n == 1) {
+      k_root_stats<<<1, 1, 0, st>>>(0, n, ws.pre_of, ws.size_by_pre, ws.pedge_by_pre, ws.rec,
+                                    ws.pedge_of);
+      CK_LAUNCH();
+    }
     CK(cudaEventRecord(ev[2], st));
   }
 
   if (engine == ETTG_BRIDGES_TV) {
-    // ---- low / high + classification -------------------------------------
-    k_lowhigh_init<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.lh, n);
+    // ---- low / high over tour keys + classification ------------------------
+    const u32 len = 2 * n;  // slots key - 1, keys in [1, 2n - 1]
+    k_lh_neutral<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.lh, len);
     CK_LAUNCH();
-    if (m) {
-      launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, sms, st);
-    }
+    if (m && n > 1) launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, sms, st);
     tr.mark("lowhigh_edges");
-    k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, n, ws.nb,
+    k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, len, ws.nb,
                                                                               ws.sp);
     CK_LAUNCH();
     for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
@@ -713,9 +783,11 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
           ws.nb, 1u << (lvl - 1));
       CK_LAUNCH();
     }
-    k_classify<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
-        ws.lh, ws.sp, ws.nb, n, ws.size_by_pre, ws.pedge_by_pre, d_mask, m);
-    CK_LAUNCH();
+    if (n > 1) {
+      k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
+          ws.lh, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m);
+      CK_LAUNCH();
+    }
     tr.mark("rmq_classify");
   } else {
     // ---- CK marking (core/src/bridges.cpp:40-76) -------------------------
