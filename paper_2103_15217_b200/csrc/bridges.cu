@@ -422,6 +422,36 @@ __global__ void k_lh_block(const uint2* __restrict__ lh, u32 n, u32 nb, uint2* _
   }
 }
 
+// Level 0 plus in-block prefix and suffix extrema (32-entry blocks), so a
+// range that crosses a block boundary costs two gathers plus the sparse
+// table instead of a scan of its partial blocks.
+__global__ void k_lh_block_ps(const uint2* __restrict__ lh, u32 n, u32 nb,
+                              uint2* __restrict__ sp0, uint2* __restrict__ pre,
+                              uint2* __restrict__ suf) {
+  const u32 lane = threadIdx.x & 31;
+  const u32 warps = (gridDim.x * blockDim.x) >> 5;
+  for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const u32 i = b * 32 + lane;
+    const uint2 v = i < n ? lh[i] : make_uint2(0xFFFFFFFFu, 0u);
+    uint2 f = v, g = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint2 o;
+      o.x = __shfl_up_sync(0xffffffffu, f.x, d);
+      o.y = __shfl_up_sync(0xffffffffu, f.y, d);
+      if (lane >= static_cast<u32>(d)) f = lh_merge(f, o);
+      o.x = __shfl_down_sync(0xffffffffu, g.x, d);
+      o.y = __shfl_down_sync(0xffffffffu, g.y, d);
+      if (lane + d < 32) g = lh_merge(g, o);
+    }
+    if (i < n) {
+      pre[i] = f;
+      suf[i] = g;
+    }
+    if (lane == 31) sp0[b] = f;
+  }
+}
+
 __global__ void k_lh_level(const uint2* __restrict__ prev, uint2* __restrict__ cur, u32 nb,
                            u32 half) {
   for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
@@ -491,19 +521,20 @@ __global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
 }
 
 __global__ void __launch_bounds__(256)
-    k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ sp, u32 nb, u32 len,
+    k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ pre,
+                    const uint2* __restrict__ suf, const uint2* __restrict__ sp, u32 nb, u32 len,
                     const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
                     uint8_t* __restrict__ mask, u32 m) {
   for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     const uint2 k = kt[t];
     const u32 a = k.x - 1, b = min(k.y - 1, len - 1);
-    uint2 acc = lh[a];
-    if (b - a < 64) {
+    const u32 la = a >> 5, lb = b >> 5;
+    uint2 acc;
+    if (la == lb) {
+      acc = lh[a];
       for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
     } else {
-      const u32 la = a >> 5, lb = b >> 5;
-      for (u32 j = a + 1; j < (la + 1) * 32; ++j) acc = lh_merge(acc, __ldg(lh + j));
-      for (u32 j = lb * 32; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+      acc = lh_merge(__ldg(suf + a), __ldg(pre + b));
       if (lb > la + 1) {
         const u32 cnt = lb - la - 1;
         const int kk = hb32(cnt);
@@ -568,6 +599,7 @@ struct BridgeWs {
   u32* pedge_by_pre = nullptr;
   uint2* lh = nullptr;
   uint2* kt = nullptr;  // TV: (key, up key) per tree edge
+  uint2 *lh_pre = nullptr, *lh_suf = nullptr;  // TV: in-block prefix / suffix extrema
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
   u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
@@ -608,7 +640,11 @@ struct BridgeWs {
     pedge_by_pre = c.take<u32>(n);
     const u32 lh_len = engine == ETTG_BRIDGES_TV ? 2 * n : n;
     lh = c.take<uint2>(lh_len);
-    if (engine == ETTG_BRIDGES_TV) kt = c.take<uint2>(n);
+    if (engine == ETTG_BRIDGES_TV) {
+      kt = c.take<uint2>(n);
+      lh_pre = c.take<uint2>(lh_len);
+      lh_suf = c.take<uint2>(lh_len);
+    }
     nb = (lh_len + 31) / 32;
     levels = 32 - __builtin_clz(nb);
     sp = c.take<uint2>(static_cast<u64>(levels) * nb);
@@ -774,8 +810,8 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     CK_LAUNCH();
     if (m && n > 1) launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, sms, st);
     tr.mark("lowhigh_edges");
-    k_lh_block<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(ws.lh, len, ws.nb,
-                                                                              ws.sp);
+    k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
+        ws.lh, len, ws.nb, ws.sp, ws.lh_pre, ws.lh_suf);
     CK_LAUNCH();
     for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
       k_lh_level<<<std::min(g, blocks_for(ws.nb, 256)), 256, 0, st>>>(
@@ -785,7 +821,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     }
     if (n > 1) {
       k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
-          ws.lh, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m);
+          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m);
       CK_LAUNCH();
     }
     tr.mark("rmq_classify");
