@@ -29,13 +29,23 @@ __global__ void __launch_bounds__(256) walk(const u32* __restrict__ succ, u64* _
       if (MODE == 0) { rec[cur] = ((u64)acc << 32) | sid; nxt = succ[cur]; }
       else if (MODE == 1) { const u64 v = slot[cur]; slot[cur] = ((u64)acc << 32) | sid; nxt = (u32)v; }
       else if (MODE == 2) { nxt = succ[cur]; rec[cur] = ((u64)acc << 32) | sid; }
-      else { u64 v; asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(slot + cur)); asm volatile("st.global.cg.u64 [%0], %1;" :: "l"(slot + cur), "l"(((u64)acc << 32) | sid)); nxt = (u32)v; }
+      else if (MODE == 3) { u64 v; asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(slot + cur)); asm volatile("st.global.cg.u64 [%0], %1;" :: "l"(slot + cur), "l"(((u64)acc << 32) | sid)); nxt = (u32)v; }
+      else if (MODE == 4) {  // AoS 16 B: {succ, pad, rec}: store rec (bytes 8..15), load succ (0..3)
+        u64* e = slot + 2 * (u64)cur;
+        e[1] = ((u64)acc << 32) | sid;
+        nxt = *reinterpret_cast<const volatile u32*>(e);
+      } else {  // AoS 16 B, load succ first then store rec
+        u64* e = slot + 2 * (u64)cur;
+        nxt = *reinterpret_cast<const volatile u32*>(e);
+        e[1] = ((u64)acc << 32) | sid;
+      }
       acc += 1;
       if (nxt == 0xFFFFFFFFu || spl(nxt, head)) { sub_next[sid] = nxt; active = false; } else cur = nxt;
     }
   }
 }
 __global__ void fill_slots(const u32* succ, u64* slot, u32 k) { for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) slot[i] = (0xFFFFFFFFull << 32) | succ[i]; }
+__global__ void fill_aos(const u32* succ, u64* slot, u32 k) { for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) { slot[2 * (u64)i] = succ[i]; slot[2 * (u64)i + 1] = 0; } }
 int main() {
   const u32 k = 32u << 20;
   std::vector<u32> order(k); for (u32 i = 0; i < k; ++i) order[i] = i;
@@ -46,20 +56,22 @@ int main() {
   auto mix = [](u32 x) { x ^= x >> 16; x *= 0x85ebca6bu; x ^= x >> 13; x *= 0xc2b2ae35u; x ^= x >> 16; return x; };
   std::vector<u32> sp; for (u32 e = 0; e < k; ++e) if (e == head || (mix(e ^ 0x1234u) & 7u) == 0) sp.push_back(e);
   u32 *dsucc, *dspl, *dt, *dnext; u64 *drec, *dslot;
-  cudaMalloc(&dsucc, k * 4ull); cudaMalloc(&drec, k * 8ull); cudaMalloc(&dslot, k * 8ull); cudaMalloc(&dspl, sp.size() * 4); cudaMalloc(&dt, 4); cudaMalloc(&dnext, sp.size() * 4);
+  cudaMalloc(&dsucc, k * 4ull); cudaMalloc(&drec, k * 8ull); cudaMalloc(&dslot, k * 16ull); cudaMalloc(&dspl, sp.size() * 4); cudaMalloc(&dt, 4); cudaMalloc(&dnext, sp.size() * 4);
   cudaMemcpy(dsucc, succ.data(), k * 4ull, cudaMemcpyHostToDevice); cudaMemcpy(dspl, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice);
-  const char* names[] = {"separate: store rec then load succ", "in-place u64 slot (ld, st)", "separate: load succ then store rec", "in-place .cg"};
+  const char* names[] = {"separate: store rec then load succ", "in-place u64 slot (ld, st)", "separate: load succ then store rec", "in-place .cg", "AoS 16B: store rec, load succ", "AoS 16B: load succ, store rec"};
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int rep = 0; rep < 3; ++rep)
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 6; ++mode) {
     float tot = 0;
     for (int it = 0; it < 4; ++it) {
-      fill_slots<<<1184, 256>>>(dsucc, dslot, k); cudaMemset(dt, 0, 4);
+      if (mode >= 4) fill_aos<<<1184, 256>>>(dsucc, dslot, k); else fill_slots<<<1184, 256>>>(dsucc, dslot, k); cudaMemset(dt, 0, 4);
       cudaEventRecord(a);
       if (mode == 0) walk<0><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       if (mode == 1) walk<1><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       if (mode == 2) walk<2><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       if (mode == 3) walk<3><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
+      if (mode == 4) walk<4><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
+      if (mode == 5) walk<5><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (it) tot += ms;
     }
     if (rep) printf("%-40s %.3f ms  (%.2f G elem/s)\n", names[mode], tot / 3, k / (tot / 3) / 1e6);
