@@ -348,12 +348,6 @@ __global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32
   }
 }
 
-// lh[i] = (low seed, high seed) = (i + 1, i + 1): each node's own preorder.
-__global__ void k_lowhigh_init(uint2* __restrict__ lh, u32 n) {
-  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    lh[i] = make_uint2(i + 1, i + 1);
-}
-
 // Non-tree edge {u, v} with pre(u) < pre(v): low(v) <- min(., pre(u)) and
 // high(u) <- max(., pre(v))  (core/src/bridges.cpp:256-273).  kHookE edges per
 // thread so their preorder gathers and extreme reads are in flight together;
@@ -404,24 +398,6 @@ __device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
   return make_uint2(min(a.x, b.x), max(a.y, b.y));
 }
 
-// Block-sparse (min low, max high) table: level 0 = 32-entry block extrema.
-__global__ void k_lh_block(const uint2* __restrict__ lh, u32 n, u32 nb, uint2* __restrict__ sp0) {
-  const u32 lane = threadIdx.x & 31;
-  const u32 warps = (gridDim.x * blockDim.x) >> 5;
-  for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
-    const u32 i = b * 32 + lane;
-    uint2 v = i < n ? lh[i] : make_uint2(0xFFFFFFFFu, 0u);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      uint2 o;
-      o.x = __shfl_xor_sync(0xffffffffu, v.x, d);
-      o.y = __shfl_xor_sync(0xffffffffu, v.y, d);
-      v = lh_merge(v, o);
-    }
-    if (lane == 0) sp0[b] = v;
-  }
-}
-
 // Level 0 plus in-block prefix and suffix extrema (32-entry blocks), so a
 // range that crosses a block boundary costs two gathers plus the sparse
 // table instead of a scan of its partial blocks.
@@ -457,37 +433,6 @@ __global__ void k_lh_level(const uint2* __restrict__ prev, uint2* __restrict__ c
   for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
        b += gridDim.x * blockDim.x)
     cur[b] = lh_merge(prev[b], prev[b + half]);
-}
-
-// Subtree range [i, i + size - 1] in preorder -> (low, high) -> bridge test
-// (core/src/bridges.cpp:280-285, :301-306).
-__global__ void __launch_bounds__(256)
-    k_classify(const uint2* __restrict__ lh, const uint2* __restrict__ sp, u32 nb, u32 n,
-               const u32* __restrict__ size_by_pre, const u32* __restrict__ pedge_by_pre,
-               uint8_t* __restrict__ mask, u32 m) {
-  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (i == 0) continue;  // the root has no parent edge
-    const u32 sz = size_by_pre[i];
-    const u32 a = i, b = min(i + sz - 1, n - 1);
-    uint2 acc = lh[a];
-    if (b - a < 64) {
-      for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
-    } else {
-      const u32 la = a >> 5, lb = b >> 5;
-      for (u32 j = a + 1; j < (la + 1) * 32; ++j) acc = lh_merge(acc, __ldg(lh + j));
-      for (u32 j = lb * 32; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
-      if (lb > la + 1) {
-        const u32 cnt = lb - la - 1;
-        const int k = hb32(cnt);
-        const uint2* row = sp + static_cast<u64>(k) * nb;
-        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << k)]));
-      }
-    }
-    const u32 pre = i + 1;
-    const bool inside = acc.x >= pre && acc.y < pre + sz;
-    const u32 e = pedge_by_pre[i];
-    if (e < m) mask[e] = inside ? 1 : 0;
-  }
 }
 
 // ---- TV on Euler-tour positions (no preorder scan) -------------------------
