@@ -363,3 +363,43 @@ def test_device_permute_large_matches_reference(ett, ref):
     got = out.cpu().numpy().view(np.uint32).astype(np.int64)
     assert root == want_root
     assert np.array_equal(np.where(got == 0xFFFFFFFF, -1, got), want)
+
+
+def _shapes(ett, rng, n):
+    """Parent arrays of varied shapes (all rooted at 0 before permutation)."""
+    kind = int(rng.integers(0, 6))
+    if kind == 0:
+        return ett.grasp_tree(n, int(rng.integers(1, 9)), int(rng.integers(1 << 30)))
+    if kind == 1:
+        return ett.grasp_tree(n, GRASP_INF, int(rng.integers(1 << 30)))
+    if kind == 2:
+        return ett.barabasi_tree(n, int(rng.integers(1 << 30)))
+    par = np.full(n, -1, np.int64)
+    if kind == 3:  # star
+        par[1:] = 0
+    elif kind == 4:  # caterpillar: a spine with one leaf per spine node
+        for v in range(1, n):
+            par[v] = v - 2 if (v % 2 == 0 and v >= 2) else max(v - 1, 0) if v % 2 else 0
+    else:  # complete binary tree
+        par[1:] = (np.arange(1, n) - 1) // 2
+    return ett.RootedTree(n, 0, par)
+
+
+@pytest.mark.parametrize("name,flag", LAYOUTS + [("auto", None)])
+def test_layouts_random_shapes_vs_reference(ett, ref, name, flag):
+    """Every layout on 120 small trees of mixed shapes (n from 1 to 5000),
+    including tiny n and single-label / single-path trees."""
+    rng = np.random.default_rng(0x6c61796f + len(name))
+    for it in range(120):
+        n = int(rng.choice([1, 2, 3, 4, 5, 31, 32, 33, 64])) if it < 30 else int(rng.integers(6, 5000))
+        t = _shapes(ett, rng, n)
+        t = ett.permute_labels(t, it + 1)
+        if flag is None:
+            idx = ett.inlabel_build(t)
+        else:
+            idx = _build_layout(ett, ref, t, name, flag)
+            if idx is None:
+                continue
+        q = ett.sample_queries(t.n, 3000, it + 2)
+        want = ref.lca("inlabel", t.parent, t.root, q)
+        assert np.array_equal(ett.answer_batch(idx, q, len(q)), want), (it, n, idx.layout())
