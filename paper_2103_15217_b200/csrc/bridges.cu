@@ -237,18 +237,51 @@ struct TreeOut {
 // the reference's two counting-sort passes (core/src/euler.cpp:58-69) by one
 // scattered atomic per half-edge.  The half-edge that found an empty list at
 // the root is the last of the root's rotation: the tour is cut before its twin.
+// Push half-edge h onto vertex x's rotation list.  When every active lane of
+// the warp pushes onto the same vertex (a hub whose edges are contiguous in
+// the input, e.g. a source-sorted edge list), the lanes are chained among
+// themselves and the warp does one atomicExch instead of 32 serialised ones
+// on the hub's head (10M-leaf star: 8.8 -> 2.3 ms).  The check is two warp
+// reductions, so bounded-degree graphs keep the plain per-lane atomic (a
+// general match_any grouping cost 0.28 ms on config D).  The lane linking to
+// an empty list is the list's tail; at the root it is remembered as the last
+// half-edge of the root's rotation.
+__device__ __forceinline__ void rot_push(u32 active, u32 x, u32 h, u32 root,
+                                         u32* __restrict__ head, u32* __restrict__ nxt,
+                                         u32* last_root) {
+  const int lane = threadIdx.x & 31;
+  u32 p;
+  bool tail = true;
+  if (__reduce_min_sync(active, x) == __reduce_max_sync(active, x)) {
+    const int leader = __ffs(active) - 1;
+    const u32 above = active & ~((2u << lane) - 1u);  // lanes after mine
+    p = 0;
+    if (lane == leader) p = atomicExch(&head[x], h);  // the leader's h becomes the head
+    p = __shfl_sync(active, p, leader);
+    const u32 nh = __shfl_sync(active, h, above ? __ffs(above) - 1 : lane);
+    if (above) {
+      p = nh;
+      tail = false;
+    }
+  } else {
+    p = atomicExch(&head[x], h);
+  }
+  nxt[h] = p;
+  if (tail && p == kNone && x == root) *last_root = h;
+}
+
 __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
                            u32 root, u32* __restrict__ head, u32* __restrict__ nxt,
                            uint2* __restrict__ tend, u32* last_root) {
-  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+  const u32 stride = gridDim.x * blockDim.x;
+  for (u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < T; base += stride) {
+    const u32 t = base + (threadIdx.x & 31);
+    const u32 active = __ballot_sync(0xffffffffu, t < T);
+    if (t >= T) continue;
     const uint2 uv = edges[tedge[t]];
     tend[t] = uv;
-    const u32 p0 = atomicExch(&head[uv.x], 2 * t);
-    const u32 p1 = atomicExch(&head[uv.y], 2 * t + 1);
-    nxt[2 * t] = p0;
-    nxt[2 * t + 1] = p1;
-    if (p0 == kNone && uv.x == root) *last_root = 2 * t;
-    if (p1 == kNone && uv.y == root) *last_root = 2 * t + 1;
+    rot_push(active, uv.x, 2 * t, root, head, nxt, last_root);
+    rot_push(active, uv.y, 2 * t + 1, root, head, nxt, last_root);
   }
 }
 

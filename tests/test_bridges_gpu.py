@@ -149,3 +149,33 @@ def test_largest_component_bit_exact(ett, ref):
         o2n, nn, eo = ref.largest_component(n, e)
         assert np.array_equal(r.old_to_new, o2n) and r.graph.n == nn
         assert np.array_equal(r.graph.edges, eo.reshape(-1, 2))
+
+
+@pytest.mark.parametrize("shape", ["star_sorted", "star_shuffled", "path_sorted", "path_reversed",
+                                   "ladder"])
+def test_adversarial_shapes_known_answer(ett, shape):
+    """Hubs (a star: one vertex in every edge, contiguous or shuffled), long
+    chains in sorted / reversed edge order, and a 2-edge-connected ladder."""
+    rng = np.random.default_rng(3)
+    n = 1_000_003
+    if shape.startswith("star"):
+        e = np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1)
+        truth = np.ones(n - 1, np.uint8)
+    elif shape.startswith("path"):
+        e = np.stack([np.arange(n - 1), np.arange(1, n)], 1)
+        truth = np.ones(n - 1, np.uint8)
+    else:
+        k = n // 2
+        rails = np.concatenate([np.stack([np.arange(k - 1), np.arange(1, k)], 1),
+                                np.stack([np.arange(k, 2 * k - 1), np.arange(k + 1, 2 * k)], 1)])
+        e = np.concatenate([rails, np.stack([np.arange(k), np.arange(k, 2 * k)], 1)])
+        n = 2 * k
+        truth = np.zeros(len(e), np.uint8)
+    if shape.endswith("shuffled") or shape == "ladder":
+        e = e[rng.permutation(len(e))]
+    if shape.endswith("reversed"):
+        e = e[::-1].copy()
+    for eng in ("tv", "hybrid"):
+        fn = ett.tv_bridges if eng == "tv" else ett.hybrid_bridges
+        mask = fn(ett.EdgeList(n, e)).is_bridge
+        assert np.array_equal(mask, truth), (shape, eng)
