@@ -52,7 +52,8 @@ def peaks():
 # Random-gather ceiling of B200 at the node-table footprint of each layout at
 # n = 16M (tools/footprint_micro.cu, profiles/r1_lca_layout.md): 64 MB table
 # (compact) 263.8, 128 MB (narrow, split) 113.1, 256 MB (wide) 71.6 G gathers/s.
-L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "split": 113.1, "wide": 71.6}
+L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "split": 113.1, "wide": 71.6,
+                     "split_own": 71.6}
 
 
 def ncu_traffic(kernel_key: str):
@@ -491,7 +492,8 @@ def main():
         Bq_survey = 12 + 32 * (2 + Lbar)  # one 32-B sector per gather
         layout, labels = idx.layout()
         kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
-                 "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split"}[layout]
+                 "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split",
+                 "split_own": "k_lca_inlabel_split_own"}[layout]
         q_r = sec["q_rank"]
         if layout == "compact":
             # 12 B streamed + the index read once per launch (node words + label

@@ -67,11 +67,15 @@ extern "C" {
  *           few inlabel paths (label-index bits + offset bits <= 32).
  *   SPLIT   8-B node record {inlabel, ascendant} + level in its own array,
  *           read only for endpoints that are not lifted (shallow trees).
- * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split). */
+ *   SPLIT_OWN 16-B {inlabel, ascendant, own-label lift record} + level:
+ *           shallow-wide trees whose lifts go to the endpoint's own label
+ *           (stars, caterpillars; chosen by a build-time query sample).
+ * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split, 4 split_own). */
 #define ETTG_LAYOUT_WIDE 0x100u
 #define ETTG_LAYOUT_NARROW 0x200u
 #define ETTG_LAYOUT_COMPACT 0x400u
 #define ETTG_LAYOUT_SPLIT 0x800u
+#define ETTG_LAYOUT_SPLIT_OWN 0x1000u
 
 typedef struct ettg_lca ettg_lca;
 
@@ -111,7 +115,7 @@ int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root,
 void ettg_lca_free(ettg_lca* h);
 
 int ettg_lca_size(const ettg_lca* h, int64_t* n);
-/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact, 3 split) and the number
+/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact, 3 split, 4 split_own) and the number
  * of inlabel paths (distinct labels) in the tree (0 for attached replicas). */
 int ettg_lca_layout(const ettg_lca* h, int* layout, int64_t* labels);
 /* Device time of the last build (ms), measured with CUDA events. */

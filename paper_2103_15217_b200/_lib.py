@@ -20,6 +20,7 @@ LAYOUT_WIDE = 0x100    # build flags (OR into engines); default: chosen per tree
 LAYOUT_NARROW = 0x200
 LAYOUT_COMPACT = 0x400
 LAYOUT_SPLIT = 0x800
+LAYOUT_SPLIT_OWN = 0x1000
 
 _lock = threading.Lock()
 _lib = None

@@ -256,6 +256,54 @@ __global__ void k_pack_compact(const u32* __restrict__ inlabel, const u32* __res
   }
 }
 
+// Build-time sample of uniform query pairs (the reference's sample_queries
+// distribution) over the split records: counts endpoint lifts and the lifts
+// whose target is the endpoint's own label (popc(asc & lowmask) == 1).  On
+// shallow-wide trees (stars, caterpillars) nearly every lift is an own-label
+// lift -- a random label-record gather that an own-lift field in the node
+// record removes; on random trees almost none are.
+__global__ void k_lift_sample(const uint2* __restrict__ nodes, u32 n, u32 samples,
+                              u32* __restrict__ counts) {
+  u32 lifts = 0, own = 0;
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
+    const u32 x = __umulhi(mix32(2 * s + 0x9e37u), n), y = __umulhi(mix32(2 * s + 0x79b9u), n);
+    const uint2 A = nodes[x], B = nodes[y];
+    if (A.x == B.x) continue;
+    const int hbit = hb32(A.x ^ B.x);
+    const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
+    const int jb = tz32(common);
+    const u32 target = (A.x & ~((2u << jb) - 1u)) | (1u << jb);
+    const u32 lowmask = (1u << jb) - 1u;
+    if (A.x != target) {
+      ++lifts;
+      own += __popc(A.y & lowmask) == 1;
+    }
+    if (B.x != target) {
+      ++lifts;
+      own += __popc(B.y & lowmask) == 1;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lifts += __shfl_xor_sync(0xffffffffu, lifts, o);
+    own += __shfl_xor_sync(0xffffffffu, own, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&counts[0], lifts);
+    atomicAdd(&counts[1], own);
+  }
+}
+
+// split_own node record {inlabel, ascendant, lab[inlabel]} (16 B): the own-
+// label lift target (core/src/lca.cpp:99-103 with k = tz(inlabel)) inline.
+__global__ void k_pack_own(const uint2* __restrict__ nodes, const uint2* __restrict__ lab, u32 n,
+                           uint4* __restrict__ node) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint2 a = nodes[v];
+    const uint2 o = (a.x >= 1 && a.x <= n) ? lab[a.x] : make_uint2(kNone, kNone);
+    node[v] = make_uint4(a.x, a.y, o.x, o.y);
+  }
+}
+
 // ---- RMQ over the tour (block-sparse table, 32-step blocks) ---------------
 // Keys (level << 32 | node) make the minimum's low word the LCA itself.
 __global__ void k_rmq_block(const u64* __restrict__ key, u32 steps, u32 nb,
@@ -560,6 +608,56 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// inlabel_lca, split_own layout: 16-B node record {inlabel, ascendant,
+// own-label lift record}; the level in its own array as in split.  A lift to
+// the endpoint's own label (the only ascendant bit below j is tz(inlabel))
+// is answered from the record.
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
+    k_lca_inlabel_split_own(const uint4* __restrict__ node, const u32* __restrict__ level,
+                            const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q,
+                            u32* err) {
+  u32 bad_any = 0;
+  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
+       i += static_cast<u64>(gridDim.x) * kQThreads) {
+    u32 x, y;
+    in.get(i, x, y);
+    const bool bad = x >= n || y >= n;
+    if (bad) x = y = 0;
+    const uint4 A = ldg_rec(node + x), B = ldg_rec(node + y);
+    bool lx = false, ly = false, ox = false, oy = false;
+    u32 wx = 0, wy = 0;
+    if (A.x != B.x) {
+      const int hbit = hb32(A.x ^ B.x);
+      const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
+      const int jb = tz32(common);
+      const u32 target = (A.x & ~((2u << jb) - 1u)) | (1u << jb);
+      const u32 lowmask = (1u << jb) - 1u;
+      if (A.x != target) {
+        const u32 below = A.y & lowmask;
+        ox = __popc(below) == 1;
+        const int kx = hb32(below);
+        wx = min((A.x & ~((2u << kx) - 1u)) | (1u << kx), n);
+        lx = !ox;
+      }
+      if (B.x != target) {
+        const u32 below = B.y & lowmask;
+        oy = __popc(below) == 1;
+        const int ky = hb32(below);
+        wy = min((B.x & ~((2u << ky) - 1u)) | (1u << ky), n);
+        ly = !oy;
+      }
+    }
+    const uint2 LX = ox ? make_uint2(A.z, A.w)
+                        : lx ? ldg_rec(lab + wx) : make_uint2(x, ldg_u32(level + x));
+    const uint2 LY = oy ? make_uint2(B.z, B.w)
+                        : ly ? ldg_rec(lab + wy) : make_uint2(y, ldg_u32(level + y));
+    out.put(i, bad ? kNone : (LX.y <= LY.y ? LX.x : LY.x));
+    bad_any |= bad;
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 // inlabel_lca, compact layout: one 4-B node word per endpoint.  Endpoints on
 // the same inlabel path (same label index) are answered from the words alone
 // (the smaller in-path offset is the ancestor); otherwise the two label-table
@@ -739,7 +837,8 @@ __global__ void __launch_bounds__(kQThreads)
 // ============================================================================
 using namespace ettg;
 
-constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSplit = 3;
+constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSplit = 3,
+              kLayoutSplitOwn = 4;
 
 struct ettg_lca {
   int device = 0;
@@ -779,15 +878,14 @@ struct ettg_lca {
   void carve(Carver& c) {
     if (engines & ETTG_ENGINE_INLABEL) {
       // a full build packs every layout (~28 B/node extra); replicas carry one
-      if (full || layout == kLayoutWide) node = c.take<uint4>(n);
+      if (full || layout == kLayoutWide || layout == kLayoutSplitOwn) node = c.take<uint4>(n);
       if (full || layout == kLayoutNarrow) {
         node8 = c.take<uint2>(n);
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
       }
-      if (full || layout == kLayoutSplit) {
-        nodes = c.take<uint2>(n);
-        slevel = full ? nullptr : c.take<u32>(n);  // full builds query h->level
-      }
+      if (full || layout == kLayoutSplit) nodes = c.take<uint2>(n);
+      if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn))
+        slevel = c.take<u32>(n);  // full builds query h->level
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
       if (full) {
         node4 = c.take<u32>(n);
@@ -972,12 +1070,16 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
 //   few labels (deep trees; per-label tables stay in L2): compact if its
 //     bit budget fits, else narrow          16M path: compact 97.5 G q/s
 //   labels >= n/2 (shallow trees: almost every query lifts both endpoints,
-//     so the level array is rarely read): split    16M grasp(inf): 55.7
+//     so the level array is rarely read): split    16M grasp(inf): 55.7;
+//     split_own when a build-time query sample sees > 50% own-label lifts
+//     (16M star: see profiles/r1_lca_layout.md)
 //   otherwise wide                              16M gamma=2: wide 24.3
-u32 choose_layout(u32 n, u64 labels, bool compact_fits, int device, unsigned flags) {
+u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, int device,
+                  unsigned flags) {
   if (flags == ETTG_LAYOUT_WIDE) return kLayoutWide;
   if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
   if (flags == ETTG_LAYOUT_SPLIT) return kLayoutSplit;
+  if (flags == ETTG_LAYOUT_SPLIT_OWN) return kLayoutSplitOwn;
   if (flags == ETTG_LAYOUT_COMPACT) {
     if (!compact_fits) einval("compact layout: label index + in-path offset exceed 32 bits");
     return kLayoutCompact;
@@ -987,7 +1089,9 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, int device, unsigned fla
     l2 = 126 << 20;
   const u64 L2 = static_cast<u64>(l2);
   if (labels * 64 <= L2 / 8) return compact_fits ? kLayoutCompact : kLayoutNarrow;
-  if (2 * labels >= n) return kLayoutSplit;
+  // shallow trees; if most sampled lifts go to the endpoint's own label
+  // (stars, caterpillars) carry that lift target in the node record
+  if (2 * labels >= n) return own_frac > 0.5 ? kLayoutSplitOwn : kLayoutSplit;
   return kLayoutWide;
 }
 
@@ -996,8 +1100,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   if (n64 <= 0) einval("parent array size mismatch");
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
-  constexpr unsigned kLayoutMask =
-      ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT | ETTG_LAYOUT_SPLIT;
+  constexpr unsigned kLayoutMask = ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT |
+                                   ETTG_LAYOUT_SPLIT | ETTG_LAYOUT_SPLIT_OWN;
   const unsigned layout_flags = engines & kLayoutMask;
   engines &= ~kLayoutMask;
   if (layout_flags & (layout_flags - 1)) einval("conflicting layout flags");
@@ -1109,13 +1213,22 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_pack_naive<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->par, h->level, n, h->nrec);
     CK_LAUNCH();
   }
-  u32 cnt[2] = {0, 0};  // {inlabel paths, max in-path offset}
+  constexpr u32 kLiftSamples = 1u << 16;
+  k_lift_sample<<<64, 256, 0, st>>>(h->nodes, n, kLiftSamples, ws.flags + 3);
+  CK_LAUNCH();
+  u32 cnt[4] = {0, 0, 0, 0};  // {inlabel paths, max in-path offset, lifts, own lifts}
   CK(cudaMemcpyAsync(cnt, ws.flags + 1, sizeof cnt, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->labels = cnt[0];
   const int label_bits = cnt[0] > 1 ? 32 - __builtin_clz(cnt[0] - 1) : 0;
   h->off_bits = cnt[1] ? 32 - __builtin_clz(cnt[1]) : 0;
-  h->layout = choose_layout(n, cnt[0], label_bits + h->off_bits <= 32, device, layout_flags);
+  const double own_frac = cnt[2] ? static_cast<double>(cnt[3]) / cnt[2] : 0.0;
+  h->layout = choose_layout(n, cnt[0], label_bits + h->off_bits <= 32, own_frac, device,
+                            layout_flags);
+  if (h->layout == kLayoutSplitOwn) {  // the wide node array holds the own-lift records
+    k_pack_own<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, h->lab, n, h->node);
+    CK_LAUNCH();
+  }
   if (h->layout == kLayoutCompact) {
     h->alloc_compact();
     scan_exclusive(LabelUsedIn{h->head}, ArrayOut{ws.up}, static_cast<u64>(n) + 1, ws.scan,
@@ -1170,6 +1283,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     if (h->layout == kLayoutCompact)
       k_lca_inlabel_compact<In, Out><<<blocks, kQThreads, 0, st>>>(
           h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q, err);
+    else if (h->layout == kLayoutSplitOwn)
+      k_lca_inlabel_split_own<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->slevel, h->lab,
+                                                                     h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit)
       k_lca_inlabel_split<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab,
                                                                  h->n, in, out, q, err);
@@ -1382,6 +1498,9 @@ BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
   b.header = c.take<u32>(64);
   if (layout == kLayoutWide) {
     b.node = c.take<uint4>(n);
+  } else if (layout == kLayoutSplitOwn) {
+    b.node = c.take<uint4>(n);
+    b.slevel = c.take<u32>(n);
   } else if (layout == kLayoutNarrow) {
     b.node8 = c.take<uint2>(n);
     b.lasc = c.take<u32>(static_cast<u64>(n) + 1);
@@ -1426,10 +1545,9 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
       CK(cudaMemcpyAsync(b.node4, h->node4, n * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(b.ltab, h->ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
-    if (b.nodes) {
-      CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes) CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.slevel)
       CK(cudaMemcpyAsync(b.slevel, h->slevel, n * 4, cudaMemcpyDeviceToDevice, st));
-    }
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));  // `head` is a host stack buffer
   });
@@ -1446,7 +1564,7 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     u32 head[8];
     CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (head[0] != kBlobMagic || head[1] > kLayoutSplit || head[2] != static_cast<u32>(n) ||
+    if (head[0] != kBlobMagic || head[1] > kLayoutSplitOwn || head[2] != static_cast<u32>(n) ||
         head[3] > 32 || head[4] > static_cast<u32>(n))
       einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
@@ -1476,10 +1594,9 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
       CK(cudaMemcpyAsync(h->node4, b.node4, un * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(h->ltab, b.ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
-    if (b.nodes) {
-      CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes) CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.slevel)
       CK(cudaMemcpyAsync(h->slevel, b.slevel, un * 4, cudaMemcpyDeviceToDevice, st));
-    }
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     *out = h.release();

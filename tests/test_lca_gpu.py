@@ -239,7 +239,7 @@ def test_naive_errors(ett):
 
 # ------------------------------------------------------- index layouts
 LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT"),
-           ("split", "LAYOUT_SPLIT")]
+           ("split", "LAYOUT_SPLIT"), ("split_own", "LAYOUT_SPLIT_OWN")]
 
 
 def _compact_bits(ref, t):
@@ -403,3 +403,23 @@ def test_layouts_random_shapes_vs_reference(ett, ref, name, flag):
         q = ett.sample_queries(t.n, 3000, it + 2)
         want = ref.lca("inlabel", t.parent, t.root, q)
         assert np.array_equal(ett.answer_batch(idx, q, len(q)), want), (it, n, idx.layout())
+
+
+def test_star_picks_split_own_and_matches(ett, ref):
+    """A star's queries lift to the endpoints' own labels: the build-time sample
+    picks split_own; answers equal the reference and every forced layout."""
+    import torch
+    n = 1_500_000
+    par = np.zeros(n, np.int64)
+    par[0] = -1
+    t = ett.permute_labels(ett.RootedTree(n, 0, par), 9)
+    idx = ett.inlabel_build(t)
+    assert idx.layout()[0] == "split_own"
+    q = ett.sample_queries(n, 100_000, 10)
+    want = ref.lca("inlabel", t.parent, t.root, q)
+    assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
+    buf = torch.empty(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")
+    idx.export_index(buf)
+    rep = ett.attach_index(buf, n)
+    assert rep.layout()[0] == "split_own"
+    assert np.array_equal(ett.answer_batch(rep, q, len(q)), want)
