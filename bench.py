@@ -327,6 +327,29 @@ def bridges_section(ett, args, device, peak):
                         "traffic_note": "DRAM bytes of every kernel of one call (ncu, cold, "
                                         "profiles/ncu_summary.json bridges_D)",
                         "io_floor_frac": 9 * m / (tot / 1e3) / 1e9 / peak[0]}}
+    # e2e: the reference-facing call (tv_bridges on an int64 host edge list,
+    # core/src/bridges.cpp:311) through ettg_bridges with pinned host buffers;
+    # the H2D of the 16-B pairs is inside the timed region
+    import ctypes
+    import time
+    pin_e = torch.from_numpy(np.ascontiguousarray(g.edges, dtype=np.int64)).pin_memory()
+    pin_m = torch.empty(m, dtype=torch.uint8).pin_memory()
+
+    def call_host():
+        _lib.check(L.ettg_bridges(pin_e.data_ptr(), n, m, device.index, pin_m.data_ptr(), None))
+    call_host()
+    ok_h = bool(np.array_equal(pin_m.numpy(), truth))
+    ts = []
+    for _ in range(2):
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        call_host()
+        ts.append(time.perf_counter() - t0)
+    out["e2e"] = {"value": m / min(ts), "unit": "edges/s", "ms_per_step": 1e3 * min(ts),
+                  "h2d_bytes_per_step": m * 16, "d2h_bytes_per_step": m,
+                  "path": "ettg_bridges (pinned int64 host edge list -> host mask)",
+                  "parity": "bit-exact vs planted truth" if ok_h else "MISMATCH"}
+    del pin_e, pin_m
     if args.cpu_baseline:
         from oracle import oracle as orc
         if orc.have_ref():
