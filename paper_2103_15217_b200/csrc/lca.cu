@@ -264,11 +264,14 @@ __global__ void k_pack_compact(const u32* __restrict__ inlabel, const u32* __res
 // record removes; on random trees almost none are.
 __global__ void k_lift_sample(const uint2* __restrict__ nodes, u32 n, u32 samples,
                               u32* __restrict__ counts) {
-  u32 lifts = 0, own = 0;
+  u32 lifts = 0, own = 0, lev = 0;
   for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
     const u32 x = __umulhi(mix32(2 * s + 0x9e37u), n), y = __umulhi(mix32(2 * s + 0x79b9u), n);
     const uint2 A = nodes[x], B = nodes[y];
-    if (A.x == B.x) continue;
+    if (A.x == B.x) {
+      lev += 2;  // equal inlabels: both levels decide
+      continue;
+    }
     const int hbit = hb32(A.x ^ B.x);
     const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
     const int jb = tz32(common);
@@ -277,19 +280,25 @@ __global__ void k_lift_sample(const uint2* __restrict__ nodes, u32 n, u32 sample
     if (A.x != target) {
       ++lifts;
       own += __popc(A.y & lowmask) == 1;
+    } else {
+      ++lev;  // an endpoint on the target path compares by its own level
     }
     if (B.x != target) {
       ++lifts;
       own += __popc(B.y & lowmask) == 1;
+    } else {
+      ++lev;
     }
   }
   for (int o = 16; o; o >>= 1) {
     lifts += __shfl_xor_sync(0xffffffffu, lifts, o);
     own += __shfl_xor_sync(0xffffffffu, own, o);
+    lev += __shfl_xor_sync(0xffffffffu, lev, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&counts[0], lifts);
     atomicAdd(&counts[1], own);
+    atomicAdd(&counts[2], lev);
   }
 }
 
@@ -1074,8 +1083,8 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
 //     split_own when a build-time query sample sees > 50% own-label lifts
 //     (16M star: see profiles/r1_lca_layout.md)
 //   otherwise wide                              16M gamma=2: wide 24.3
-u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, int device,
-                  unsigned flags) {
+u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, double level_per_q,
+                  int device, unsigned flags) {
   if (flags == ETTG_LAYOUT_WIDE) return kLayoutWide;
   if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
   if (flags == ETTG_LAYOUT_SPLIT) return kLayoutSplit;
@@ -1089,9 +1098,16 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, int dev
     l2 = 126 << 20;
   const u64 L2 = static_cast<u64>(l2);
   if (labels * 64 <= L2 / 8) return compact_fits ? kLayoutCompact : kLayoutNarrow;
-  // shallow trees; if most sampled lifts go to the endpoint's own label
-  // (stars, caterpillars) carry that lift target in the node record
-  if (2 * labels >= n) return own_frac > 0.5 ? kLayoutSplitOwn : kLayoutSplit;
+  (void)n;
+  // split keeps the level out of the gathered record, so it wins when the
+  // sampled queries rarely need a level (most endpoints are lifted); when most
+  // lifts go to the endpoint's own label (stars, caterpillars) that lift
+  // target rides in the record (split_own).  16M trees, G q/s wide/split:
+  // grasp(inf) 33.4/55.7, gamma=64 26.9/35.6, 16 20.0/21.4, 8 18.9/18.7,
+  // 4 20.4/18.7, 2 24.3/20.2 (level reads per query 0, 0.06, ~0.2, 0.38, ..,
+  // 0.99).
+  if (own_frac > 0.5 && level_per_q < 0.25) return kLayoutSplitOwn;
+  if (level_per_q < 0.25) return kLayoutSplit;
   return kLayoutWide;
 }
 
@@ -1216,15 +1232,17 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   constexpr u32 kLiftSamples = 1u << 16;
   k_lift_sample<<<64, 256, 0, st>>>(h->nodes, n, kLiftSamples, ws.flags + 3);
   CK_LAUNCH();
-  u32 cnt[4] = {0, 0, 0, 0};  // {inlabel paths, max in-path offset, lifts, own lifts}
+  // {inlabel paths, max in-path offset, lifts, own lifts, level reads}
+  u32 cnt[5] = {0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(cnt, ws.flags + 1, sizeof cnt, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->labels = cnt[0];
   const int label_bits = cnt[0] > 1 ? 32 - __builtin_clz(cnt[0] - 1) : 0;
   h->off_bits = cnt[1] ? 32 - __builtin_clz(cnt[1]) : 0;
   const double own_frac = cnt[2] ? static_cast<double>(cnt[3]) / cnt[2] : 0.0;
-  h->layout = choose_layout(n, cnt[0], label_bits + h->off_bits <= 32, own_frac, device,
-                            layout_flags);
+  const double level_per_q = static_cast<double>(cnt[4]) / kLiftSamples;
+  h->layout = choose_layout(n, cnt[0], label_bits + h->off_bits <= 32, own_frac, level_per_q,
+                            device, layout_flags);
   if (h->layout == kLayoutSplitOwn) {  // the wide node array holds the own-lift records
     k_pack_own<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, h->lab, n, h->node);
     CK_LAUNCH();

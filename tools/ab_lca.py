@@ -18,7 +18,8 @@ def child():
     for name, gamma, q in [("B_path", 1, 16_000_000), ("E_rand", ett.K_GRASP_INFINITY, 64_000_000),
                            ("g2", 2, 16_000_000), ("g8", 8, 16_000_000), ("A_1M", ett.K_GRASP_INFINITY, 1_000_000),
                            ("path_1M", 1, 1_000_000), ("g2_1M", 2, 1_000_000), ("rand_4M", ett.K_GRASP_INFINITY, 4_000_000),
-                           ("path_4M", 1, 4_000_000)]:
+                           ("path_4M", 1, 4_000_000), ("g16", 16, 16_000_000), ("g64", 64, 16_000_000),
+                           ("g4", 4, 16_000_000)]:
         if os.environ.get("AB_ONLY") and name not in os.environ["AB_ONLY"].split(","):
             continue
         n = {"A_1M": 1_000_000, "path_1M": 1_000_000, "g2_1M": 1_000_000, "rand_4M": 4_000_000,
