@@ -367,6 +367,42 @@ def bridges_section(ett, args, device, peak):
     return out
 
 
+def lca_engines_config_a(ett, device):
+    """The paper's engine comparison (Figs. 3-6) on config A: inlabel
+    vs RMQ-on-tour vs naive walk-up, one Euler-tour build, device-resident
+    queries, L2 flushed before each timed launch; answers must agree."""
+    t = make_tree(ett, 1_000_000, GRASP_INF)
+    q = 1_000_000
+    idx = ett.inlabel_build(t, device=device.index,
+                            engines=ett.ENGINE_INLABEL | ett.ENGINE_RMQ | ett.ENGINE_NAIVE)
+    pairs = torch.empty(2 * q, dtype=torch.int32, device=device)
+    ett.gen_queries_dev(t.n, q, 3, 0, pairs, device.index)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
+    st = torch.cuda.current_stream(device)
+    out, ref_ans = {"workload": "config A: permute_labels(grasp_tree(1M, inf)), 1M queries",
+                    "unit": "queries/s"}, None
+    for eng, name in [(ett.ENGINE_INLABEL, "inlabel"), (ett.ENGINE_RMQ, "rmq"),
+                      (ett.ENGINE_NAIVE, "naive")]:
+        ans = torch.empty(q, dtype=torch.int32, device=device)
+        idx.query_dev(pairs, ans, eng, st.cuda_stream)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(20)]
+        torch.cuda.synchronize(device)
+        for e0, e1 in evs:
+            flush.fill_(1)
+            e0.record(st)
+            idx.query_dev(pairs, ans, eng, st.cuda_stream)
+            e1.record(st)
+        torch.cuda.synchronize(device)
+        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        if ref_ans is None:
+            ref_ans = ans.clone()
+        out[name] = {"value": q / (ms / 1e3), "ms": ms,
+                     "agrees_with_inlabel": bool(torch.equal(ans, ref_ans))}
+    out["inlabel_layout"] = idx.layout()[0]
+    return out
+
+
 def ingestion_config_c(ett, args):
     """parse_edge_list of config C written as text
     (write_edge_list, 8M lines, ~110 MB), end to end from host bytes to host
@@ -599,6 +635,7 @@ def main():
         line["bridges"] = bridges_section(ett, args, device, peak)
         line["bridges_config_C"] = bridges_config_c(ett, args, device, peak)
         line["ingestion_config_C"] = ingestion_config_c(ett, args)
+        line["lca_engines_config_A"] = lca_engines_config_a(ett, device)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
