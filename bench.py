@@ -476,6 +476,25 @@ def bridges_config_c(ett, args, device, peak):
            "value": m / (tot / 1e3), "unit": "edges/s", "ms_per_step": tot,
            "parity": "bit-exact vs planted truth" if ok else "MISMATCH",
            "roofline_frac_41m108n": (41 * m + 108 * n) / (tot / 1e3) / 1e9 / peak[0]}
+    # the paper's engine comparison on the same graph
+    engines = {}
+    for eng, name in [(0, "tv"), (2, "hybrid"), (1, "ck")]:
+        def run_e():
+            pt = _lib.PhaseTimes()
+            _lib.check(L.ettg_bridges_dev_engine(d_edges.data_ptr(), n, m, device.index, eng,
+                                                 d_mask.data_ptr(), stream.cuda_stream,
+                                                 ctypes.byref(pt)))
+            return pt
+        run_e()
+        ok_e = bool(np.array_equal(d_mask.cpu().numpy(), truth))
+        ts = []
+        for _ in range(2):
+            flush.fill_(1)
+            torch.cuda.synchronize(device)
+            ts.append(run_e().total_ms)
+        engines[name] = {"ms": float(np.mean(ts)), "value": m / (np.mean(ts) / 1e3),
+                         "parity": "bit-exact vs planted truth" if ok_e else "MISMATCH"}
+    out["engines"] = engines
     if args.cpu_baseline:
         from oracle import oracle as orc
         if orc.have_ref():
