@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
+#include "trace.cuh"
 
 namespace ettg {
 namespace {  // header-defined kernels: internal linkage per TU
@@ -238,7 +239,9 @@ constexpr int kBfsChunk = 16;  // levels per CUDA-graph replay
 // Returns the number of vertices reached.  tree[m] must be zeroed by the caller.
 inline u32 run_bfs(const uint2* edges, u32 n, u32 m, u32 root, u32* level, u32* parent,
                    u32* pedge, uint8_t* tree, const BfsWs& ws, cudaStream_t st, int sms) {
+  Trace tr("bfs", st);
   build_csr(edges, n, m, ws.offs, ws.nbr, ws.eid, ws.csr, st, sms);
+  tr.mark("csr");
   BfsState s{{ws.front0, ws.front1}, ws.size, ws.cand, level, parent, pedge, tree};
   const unsigned g = std::min<unsigned>(sms * 8, blocks_for(n, 256));
   k_bfs_init<<<g, 256, 0, st>>>(s, n, root);
@@ -255,13 +258,17 @@ inline u32 run_bfs(const uint2* edges, u32 n, u32 m, u32 root, u32* level, u32* 
   CK(cudaStreamEndCapture(cap, &graph));
   cudaGraphExec_t exec;
   CK(cudaGraphInstantiate(&exec, graph, 0));
+  tr.mark("capture");
   u32 sizes[3] = {1, 0, 1};
+  u32 chunks = 0;
   for (u32 levels = 0; levels <= n; levels += kBfsChunk) {
     CK(cudaGraphLaunch(exec, st));
     CK(cudaMemcpyAsync(sizes, ws.size, sizeof sizes, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ++chunks;
     if (sizes[0] == 0 && sizes[1] == 0) break;
   }
+  tr.mark(chunks > 4 ? "levels(>64)" : "levels");
   cudaGraphExecDestroy(exec);
   cudaGraphDestroy(graph);
   cudaStreamDestroy(cap);
