@@ -34,6 +34,9 @@ __global__ void __launch_bounds__(256) walk(const u32* __restrict__ succ, u64* _
         u64* e = slot + 2 * (u64)cur;
         e[1] = ((u64)acc << 32) | sid;
         nxt = *reinterpret_cast<const volatile u32*>(e);
+      } else if (MODE == 6) {  // separate arrays, 4-B rec (local:12 | sid:20 packing)
+        reinterpret_cast<u32*>(rec)[cur] = (acc << 20) | (sid & 0xFFFFFu);
+        nxt = succ[cur];
       } else {  // AoS 16 B, load succ first then store rec
         u64* e = slot + 2 * (u64)cur;
         nxt = *reinterpret_cast<const volatile u32*>(e);
@@ -58,10 +61,10 @@ int main() {
   u32 *dsucc, *dspl, *dt, *dnext; u64 *drec, *dslot;
   cudaMalloc(&dsucc, k * 4ull); cudaMalloc(&drec, k * 8ull); cudaMalloc(&dslot, k * 16ull); cudaMalloc(&dspl, sp.size() * 4); cudaMalloc(&dt, 4); cudaMalloc(&dnext, sp.size() * 4);
   cudaMemcpy(dsucc, succ.data(), k * 4ull, cudaMemcpyHostToDevice); cudaMemcpy(dspl, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice);
-  const char* names[] = {"separate: store rec then load succ", "in-place u64 slot (ld, st)", "separate: load succ then store rec", "in-place .cg", "AoS 16B: store rec, load succ", "AoS 16B: load succ, store rec"};
+  const char* names[] = {"separate: store rec then load succ", "in-place u64 slot (ld, st)", "separate: load succ then store rec", "in-place .cg", "AoS 16B: store rec, load succ", "AoS 16B: load succ, store rec", "separate, 4-B rec"};
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int rep = 0; rep < 3; ++rep)
-  for (int mode = 0; mode < 6; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     float tot = 0;
     for (int it = 0; it < 4; ++it) {
       if (mode >= 4) fill_aos<<<1184, 256>>>(dsucc, dslot, k); else fill_slots<<<1184, 256>>>(dsucc, dslot, k); cudaMemset(dt, 0, 4);
@@ -72,6 +75,7 @@ int main() {
       if (mode == 3) walk<3><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       if (mode == 4) walk<4><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       if (mode == 5) walk<5><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
+      if (mode == 6) walk<6><<<148 * 8, 256>>>(dsucc, drec, dslot, k, head, dspl, sp.size(), dt, dnext);
       cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (it) tot += ms;
     }
     if (rep) printf("%-40s %.3f ms  (%.2f G elem/s)\n", names[mode], tot / 3, k / (tot / 3) / 1e6);
