@@ -13,6 +13,10 @@
  *   ett::tv_bridges(const AdjacencyIndex&, PhaseTimes*) bridges.hpp:55 -> ettg_bridges
  *   ett::list_rank(const LinkedListArray&)           primitives.hpp:68 -> ettg_list_rank_dev
  *   ett::exclusive_scan(values, +, 0)                primitives.hpp:29 -> ettg_exclusive_scan_dev
+ *                                                                       / ettg_exclusive_scan_i64_dev
+ *   ett::list_scan(list, values)                     primitives.hpp:73 -> ettg_list_scan
+ *   ett::segmented_reduce(values, offsets, f, id)    primitives.hpp:81 -> ettg_segmented_reduce
+ *   ett::RangeIndex / rmq_build / rmq_min / rmq_max  primitives.hpp:100 -> ettg_range_index_*
  *   generators.hpp (grasp_tree, permute_labels, sample_queries, ...) -> ettg_gen_*
  *
  * Conventions
@@ -227,6 +231,57 @@ int ettg_exclusive_scan_dev(const uint32_t* d_in, int64_t n, uint32_t* d_out,
 int ettg_sort_pairs_dev(const uint32_t* d_keys, const uint32_t* d_vals,
                         int64_t n, uint32_t* d_keys_out, uint32_t* d_vals_out,
                         int device, void* stream);
+
+/* exclusive_scan(values, +, 0) over int64 (sums wrap modulo 2^64).  d_out
+ * may equal d_in. */
+int ettg_exclusive_scan_i64_dev(const int64_t* d_in, int64_t n, int64_t* d_out,
+                                int device, void* stream);
+
+/* list_scan (core/src/primitives.cpp:156-162): out[i] = sum of values over
+ * the elements strictly before i in list order.  succ[k] int64, -1 = tail.
+ * Successors outside [-1, k), cycles and uncovered elements -> ETTG_EINVAL.
+ * Synchronous. */
+int ettg_list_scan(const int64_t* succ, const int64_t* values, int64_t k,
+                   int64_t head, int device, int64_t* out);
+
+/* segmented_reduce (core/include/ett/primitives.hpp:81-98):
+ * out[s] = identity (op) values[offsets[s]] (op) ... (op) values[offsets[s+1]-1]
+ * for s < n_offsets-1; an empty (or decreasing) segment yields identity.
+ * n_offsets == 0 or offsets[n_offsets-1] != n_values -> ETTG_EINVAL
+ * "segmented_reduce: bad offsets" (also for a non-empty segment reaching
+ * outside [0, n_values), which the reference does not check).  The reference
+ * takes any combiner; the device supports the three it uses. */
+#define ETTG_REDUCE_MIN 0
+#define ETTG_REDUCE_MAX 1
+#define ETTG_REDUCE_SUM 2 /* wraps modulo 2^64 */
+int ettg_segmented_reduce(const int64_t* values, int64_t n_values,
+                          const int64_t* offsets, int64_t n_offsets, int op,
+                          int64_t identity, int device, int64_t* out);
+int ettg_segmented_reduce_dev(const int64_t* d_values, int64_t n_values,
+                              const int64_t* d_offsets, int64_t n_offsets,
+                              int op, int64_t identity, int64_t* d_out,
+                              int device, void* stream); /* synchronous */
+
+/* RangeIndex (core/include/ett/primitives.hpp:100-121,
+ * core/src/primitives.cpp:169-206): inclusive range min/max over int64 keys.
+ * ranges[2q] holds (l, r) pairs; mins or maxs may be NULL (not both).  Any
+ * pair with l < 0, r >= n or l > r fails the whole batch with ETTG_ERANGE
+ * "RangeIndex::min: bad range" ("::max" when mins is NULL).  Device layout:
+ * 32-key blocks with in-block prefix/suffix {min,max} and a sparse table
+ * over block extrema, so a query is at most four 16-B loads. */
+typedef struct ettg_range_index ettg_range_index;
+int ettg_range_index_build(const int64_t* keys, int64_t n, int device,
+                           ettg_range_index** out);
+int ettg_range_index_build_dev(const int64_t* d_keys, int64_t n, int device,
+                               void* stream, ettg_range_index** out); /* synchronous */
+int64_t ettg_range_index_size(const ettg_range_index* idx);
+int ettg_range_index_query(const ettg_range_index* idx, const int64_t* ranges,
+                           int64_t q, int64_t* mins, int64_t* maxs);
+int ettg_range_index_query_dev(const ettg_range_index* idx,
+                               const int64_t* d_ranges, int64_t q,
+                               int64_t* d_mins, int64_t* d_maxs,
+                               void* stream); /* synchronous (reads the error flag) */
+void ettg_range_index_free(ettg_range_index* idx);
 
 /* --------------------------------------------------------- generators -- */
 /* Bit-identical to core/src/generators.cpp (SplitMix64, core/include/ett/rng.hpp). */

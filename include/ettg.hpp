@@ -13,6 +13,9 @@
 //   ett::ancestor_doubling_levels                -> ettg::ancestor_doubling_levels
 //   ett::build_adjacency / bfs_tree / largest_component -> same names
 //   ett::parse_edge_list / parse_dimacs_gr (std::istream&) -> same names
+//   ett::list_scan / segmented_reduce / RangeIndex, rmq_build/min/max -> same names
+//     (segmented_reduce takes ettg::Min / Max / Plus instead of an arbitrary
+//     lambda: the combiner runs on the device)
 //
 // Errors: std::invalid_argument / std::out_of_range exactly where the
 // reference throws them (ETTG_EINVAL / ETTG_ERANGE); std::runtime_error for
@@ -267,6 +270,93 @@ inline EdgeList parse_edge_list(std::istream& in, ParseStats* stats = nullptr, i
 inline EdgeList parse_dimacs_gr(std::istream& in, ParseStats* stats = nullptr, int device = 0) {
   return detail::parse_stream(ettg_parse_dimacs_gr, in, stats, device);
 }
+
+// ---- primitives (core/include/ett/primitives.hpp) ----------------------
+inline constexpr i64 kPlusInf = INT64_MAX;
+inline constexpr i64 kMinusInf = INT64_MIN;
+
+struct LinkedListArray {  // primitives.hpp:17-24
+  std::vector<i64> succ;
+  i64 head = 0;
+  i64 size() const { return static_cast<i64>(succ.size()); }
+};
+
+inline std::vector<i64> list_scan(const LinkedListArray& list, const std::vector<i64>& values,
+                                  int device = 0) {
+  if (static_cast<i64>(values.size()) != list.size())
+    throw std::invalid_argument("list_scan: values size mismatch");
+  std::vector<i64> out(values.size());
+  if (!out.empty())
+    check(ettg_list_scan(list.succ.data(), values.data(), list.size(), list.head, device,
+                         out.data()));
+  return out;
+}
+
+struct Min { static constexpr int op = ETTG_REDUCE_MIN; };
+struct Max { static constexpr int op = ETTG_REDUCE_MAX; };
+struct Plus { static constexpr int op = ETTG_REDUCE_SUM; };
+
+template <class Combine>
+std::vector<i64> segmented_reduce(const std::vector<i64>& values, const std::vector<i64>& offsets,
+                                  Combine, i64 identity, int device = 0) {
+  std::vector<i64> out(offsets.empty() ? 0 : offsets.size() - 1);
+  check(ettg_segmented_reduce(values.data(), static_cast<i64>(values.size()), offsets.data(),
+                              static_cast<i64>(offsets.size()), Combine::op, identity, device,
+                              out.data()));
+  return out;
+}
+
+// primitives.hpp:100-121.  min/max answer one inclusive range like the
+// reference; mins/maxs answer a batch of (l, r) pairs in one launch.
+class RangeIndex {
+ public:
+  explicit RangeIndex(const std::vector<i64>& keys, int device = 0) {
+    ettg_range_index* h = nullptr;
+    check(ettg_range_index_build(keys.data(), static_cast<i64>(keys.size()), device, &h));
+    h_.reset(h);
+  }
+  i64 size() const { return ettg_range_index_size(h_.get()); }
+  i64 min(i64 l, i64 r) const { return one(l, r, true); }
+  i64 max(i64 l, i64 r) const { return one(l, r, false); }
+  std::vector<i64> mins(const std::vector<std::pair<i64, i64>>& ranges) const {
+    return batch(ranges, true);
+  }
+  std::vector<i64> maxs(const std::vector<std::pair<i64, i64>>& ranges) const {
+    return batch(ranges, false);
+  }
+  const ettg_range_index* handle() const { return h_.get(); }
+
+ private:
+  struct Free {
+    void operator()(ettg_range_index* h) const { ettg_range_index_free(h); }
+  };
+  std::unique_ptr<ettg_range_index, Free> h_;
+  i64 one(i64 l, i64 r, bool want_min) const {
+    const i64 q[2] = {l, r};
+    i64 v = 0;
+    check(ettg_range_index_query(h_.get(), q, 1, want_min ? &v : nullptr,
+                                 want_min ? nullptr : &v));
+    return v;
+  }
+  std::vector<i64> batch(const std::vector<std::pair<i64, i64>>& ranges, bool want_min) const {
+    std::vector<i64> flat(2 * ranges.size()), out(ranges.size());
+    for (size_t i = 0; i < ranges.size(); ++i) {
+      flat[2 * i] = ranges[i].first;
+      flat[2 * i + 1] = ranges[i].second;
+    }
+    if (!ranges.empty())
+      check(ettg_range_index_query(h_.get(), flat.data(), static_cast<i64>(ranges.size()),
+                                   want_min ? out.data() : nullptr,
+                                   want_min ? nullptr : out.data()));
+    return out;
+  }
+};
+
+inline RangeIndex rmq_build(const std::vector<i64>& keys, int device = 0) {
+  return RangeIndex(keys, device);
+}
+inline i64 rmq_min(const RangeIndex& idx, i64 l, i64 r) { return idx.min(l, r); }
+inline i64 rmq_max(const RangeIndex& idx, i64 l, i64 r) { return idx.max(l, r); }
 
 }  // namespace ettg
 

@@ -58,8 +58,10 @@ int orc_validate_tree(int64_t n, const int64_t* parent, int64_t root) {
   return 0;
 }
 
-/* ---- list_rank_sequential: core/src/primitives.cpp:117-141 --------------- */
-static int list_prefix_seq(int64_t k, const int64_t* succ, int64_t head, int64_t* out) {
+/* ---- list_rank_sequential / list_scan_sequential:
+ *      core/src/primitives.cpp:117-141, :164-167 (values == NULL: ranks) ---- */
+static int list_prefix_seq(int64_t k, const int64_t* succ, int64_t head, const int64_t* values,
+                           int64_t* out) {
   if (k == 0) return 0;
   if (head < 0 || head >= k) return fail(1, "list head out of range");
   char* visited = ALLOC(char, k);
@@ -70,7 +72,8 @@ static int list_prefix_seq(int64_t k, const int64_t* succ, int64_t head, int64_t
       return fail(1, "linked list contains a cycle");
     }
     visited[cur] = 1;
-    out[cur] = acc++;
+    out[cur] = acc;
+    acc = (int64_t)((uint64_t)acc + (values ? (uint64_t)values[cur] : 1u));
     ++count;
     cur = succ[cur];
   }
@@ -80,7 +83,30 @@ static int list_prefix_seq(int64_t k, const int64_t* succ, int64_t head, int64_t
 }
 
 int orc_list_rank(int64_t k, const int64_t* succ, int64_t head, int64_t* out) {
-  return list_prefix_seq(k, succ, head, out);
+  return list_prefix_seq(k, succ, head, NULL, out);
+}
+
+int orc_list_scan(int64_t k, const int64_t* succ, int64_t head, const int64_t* values,
+                  int64_t* out) {
+  return list_prefix_seq(k, succ, head, values, out);
+}
+
+/* ---- segmented_reduce: core/include/ett/primitives.hpp:81-98 ---------------
+ * op 0 min, 1 max, 2 sum (wrapping). */
+int orc_segmented_reduce(int64_t nv, const int64_t* values, int64_t no, const int64_t* offsets,
+                         int op, int64_t identity, int64_t* out) {
+  if (no <= 0 || offsets[no - 1] != nv) return fail(1, "segmented_reduce: bad offsets");
+  for (int64_t s = 0; s + 1 < no; ++s) {
+    int64_t acc = identity;
+    for (int64_t i = offsets[s]; i < offsets[s + 1]; ++i) {
+      const int64_t v = values[i];
+      if (op == 0) acc = v < acc ? v : acc;
+      else if (op == 1) acc = v > acc ? v : acc;
+      else acc = (int64_t)((uint64_t)acc + (uint64_t)v);
+    }
+    out[s] = acc;
+  }
+  return 0;
 }
 
 /* ---- exclusive_scan(+): core/include/ett/primitives.hpp:29-66 -------------- */
@@ -200,7 +226,7 @@ static int linearize(const HE* h, int64_t root, int64_t* order, int64_t* pos) {
   int64_t last = h->first[root];
   while (h->next[last] != h->first[root]) last = h->next[last];
   succ[h->twin[last]] = NONE;
-  int rc = list_prefix_seq(k, succ, h->first[root], pos);
+  int rc = list_prefix_seq(k, succ, h->first[root], NULL, pos);
   free(succ);
   if (rc) return rc;
   for (int64_t e = 0; e < k; ++e) order[pos[e]] = e;
@@ -439,6 +465,25 @@ static int64_t ri_max(const RI* r, int64_t l, int64_t h) {
 static void ri_free(RI* r) {
   free(r->mn);
   free(r->mx);
+}
+
+/* RangeIndex::min / ::max (core/src/primitives.cpp:184-206): the first bad
+ * range fails the batch with out_of_range. */
+int orc_range_index(int64_t n, const int64_t* keys, int64_t q, const int64_t* ranges,
+                    int64_t* mins, int64_t* maxs) {
+  RI r;
+  ri_build(&r, keys, n);
+  for (int64_t i = 0; i < q; ++i) {
+    const int64_t l = ranges[2 * i], h = ranges[2 * i + 1];
+    if (l < 0 || h >= n || l > h) {
+      ri_free(&r);
+      return fail(2, mins ? "RangeIndex::min: bad range" : "RangeIndex::max: bad range");
+    }
+    if (mins) mins[i] = ri_min(&r, l, h);
+    if (maxs) maxs[i] = ri_max(&r, l, h);
+  }
+  ri_free(&r);
+  return 0;
 }
 
 /* ---- rmq_lca_build / rmq_lca: core/src/lca.cpp:128-157 ---------------------- */

@@ -19,6 +19,12 @@ const char* orc_last_error(void);
 int orc_validate_tree(int64_t n, const int64_t* parent, int64_t root);
 int orc_list_rank(int64_t k, const int64_t* succ, int64_t head, int64_t* out);
 int orc_exclusive_scan(int64_t n, const int64_t* in, int64_t* out);
+int orc_list_scan(int64_t k, const int64_t* succ, int64_t head, const int64_t* values,
+                  int64_t* out);
+int orc_segmented_reduce(int64_t nv, const int64_t* values, int64_t no, const int64_t* offsets,
+                         int op, int64_t identity, int64_t* out);
+int orc_range_index(int64_t n, const int64_t* keys, int64_t q, const int64_t* ranges,
+                    int64_t* mins, int64_t* maxs);
 int orc_euler_tour(int64_t n, const int64_t* parent, int64_t root, int64_t* tour_src,
                    int64_t* tour_dst);
 int orc_node_stats(int64_t n, const int64_t* parent, int64_t root, int64_t* preorder,

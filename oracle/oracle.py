@@ -129,6 +129,37 @@ class Ref:
         return out
 
     @staticmethod
+    def list_scan(succ, head, values):
+        succ = np.ascontiguousarray(succ, np.int64)
+        values = np.ascontiguousarray(values, np.int64)
+        out = np.empty(len(succ), np.int64)
+        _rc(ref(), ref().ref_list_scan(i64(len(succ)), _p(succ), i64(head), _p(values), _p(out)),
+            "ref_last_error")
+        return out
+
+    @staticmethod
+    def segmented_reduce(values, offsets, op, identity):
+        """op in {"min", "max", "sum"}."""
+        v = np.ascontiguousarray(values, np.int64)
+        o = np.ascontiguousarray(offsets, np.int64)
+        out = np.empty(max(len(o) - 1, 0), np.int64)
+        _rc(ref(), ref().ref_segmented_reduce(i64(len(v)), _p(v), i64(len(o)), _p(o),
+                                              C.c_int({"min": 0, "max": 1, "sum": 2}[op]),
+                                              i64(identity), _p(out)), "ref_last_error")
+        return out
+
+    @staticmethod
+    def range_index(keys, ranges, want_min=True, want_max=True):
+        k = np.ascontiguousarray(keys, np.int64)
+        r = np.ascontiguousarray(ranges, np.int64).reshape(-1, 2)
+        mins = np.empty(len(r), np.int64) if want_min else None
+        maxs = np.empty(len(r), np.int64) if want_max else None
+        _rc(ref(), ref().ref_range_index(i64(len(k)), _p(k), i64(len(r)), _p(r),
+                                         _p(mins) if want_min else None,
+                                         _p(maxs) if want_max else None), "ref_last_error")
+        return mins, maxs
+
+    @staticmethod
     def exclusive_scan_sum(values):
         v = np.ascontiguousarray(values, np.int64)
         out = np.empty(len(v), np.int64)
@@ -283,6 +314,32 @@ class Port:
         out = np.empty(len(succ), np.int64)
         Port._call("orc_list_rank", i64(len(succ)), _p(succ), i64(head), _p(out))
         return out
+
+    @staticmethod
+    def list_scan(succ, head, values):
+        succ = np.ascontiguousarray(succ, np.int64)
+        values = np.ascontiguousarray(values, np.int64)
+        out = np.empty(len(succ), np.int64)
+        Port._call("orc_list_scan", i64(len(succ)), _p(succ), i64(head), _p(values), _p(out))
+        return out
+
+    @staticmethod
+    def segmented_reduce(values, offsets, op, identity):
+        v = np.ascontiguousarray(values, np.int64)
+        o = np.ascontiguousarray(offsets, np.int64)
+        out = np.empty(max(len(o) - 1, 0), np.int64)
+        Port._call("orc_segmented_reduce", i64(len(v)), _p(v), i64(len(o)), _p(o),
+                   C.c_int({"min": 0, "max": 1, "sum": 2}[op]), i64(identity), _p(out))
+        return out
+
+    @staticmethod
+    def range_index(keys, ranges, want_min=True, want_max=True):
+        k = np.ascontiguousarray(keys, np.int64)
+        r = np.ascontiguousarray(ranges, np.int64).reshape(-1, 2)
+        mins = np.empty(len(r), np.int64) if want_min else None
+        maxs = np.empty(len(r), np.int64) if want_max else None
+        Port._call("orc_range_index", i64(len(k)), _p(k), i64(len(r)), _p(r), _p(mins), _p(maxs))
+        return mins, maxs
 
     @staticmethod
     def exclusive_scan(v):

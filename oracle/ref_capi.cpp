@@ -9,6 +9,7 @@
 // Every function returns 0 on success, 1 for std::invalid_argument,
 // 2 for std::out_of_range, 3 for anything else; ref_last_error() holds the
 // exception text.  Ids cross the boundary as int64 (the reference's i64).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -142,6 +143,45 @@ int ref_exclusive_scan_sum(int64_t n, const int64_t* in, int64_t* out) {
     auto r = exclusive_scan(std::span<const i64>(in, n),
                             [](i64 a, i64 b) { return a + b; }, 0);
     std::memcpy(out, r.data(), n * sizeof(int64_t));
+  });
+}
+
+int ref_list_scan(int64_t k, const int64_t* succ, int64_t head, const int64_t* values,
+                  int64_t* out) {
+  return guard([&] {
+    LinkedListArray l;
+    l.succ.assign(succ, succ + k);
+    l.head = head;
+    auto r = list_scan(l, std::span<const i64>(values, k));
+    std::memcpy(out, r.data(), k * sizeof(int64_t));
+  });
+}
+
+// op: 0 min, 1 max, 2 sum (the combiners the reference's callers pass).
+int ref_segmented_reduce(int64_t nv, const int64_t* values, int64_t no, const int64_t* offsets,
+                         int op, int64_t identity, int64_t* out) {
+  return guard([&] {
+    std::span<const i64> v(values, nv), o(offsets, no);
+    std::vector<i64> r;
+    if (op == 0)
+      r = segmented_reduce(v, o, [](i64 a, i64 b) { return std::min(a, b); }, identity);
+    else if (op == 1)
+      r = segmented_reduce(v, o, [](i64 a, i64 b) { return std::max(a, b); }, identity);
+    else
+      r = segmented_reduce(v, o, [](i64 a, i64 b) { return a + b; }, identity);
+    std::memcpy(out, r.data(), r.size() * sizeof(int64_t));
+  });
+}
+
+// ranges[2q] = (l, r); mins/maxs may be null.  Throws on the first bad range.
+int ref_range_index(int64_t n, const int64_t* keys, int64_t q, const int64_t* ranges,
+                    int64_t* mins, int64_t* maxs) {
+  return guard([&] {
+    RangeIndex idx(std::span<const i64>(keys, n));
+    for (int64_t i = 0; i < q; ++i) {
+      if (mins) mins[i] = idx.min(ranges[2 * i], ranges[2 * i + 1]);
+      if (maxs) maxs[i] = idx.max(ranges[2 * i], ranges[2 * i + 1]);
+    }
   });
 }
 

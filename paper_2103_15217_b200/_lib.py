@@ -21,6 +21,7 @@ LAYOUT_NARROW = 0x200
 LAYOUT_COMPACT = 0x400
 LAYOUT_SPLIT = 0x800
 LAYOUT_SPLIT_OWN = 0x1000
+REDUCE_MIN, REDUCE_MAX, REDUCE_SUM = range(3)  # ettg_segmented_reduce ops
 
 _lock = threading.Lock()
 _lib = None
@@ -77,6 +78,16 @@ _SIGS = {
     "ettg_list_rank_dev": ([p, i64, i64, p, C.c_int, p], C.c_int),
     "ettg_exclusive_scan_dev": ([p, i64, p, C.c_int, p], C.c_int),
     "ettg_sort_pairs_dev": ([p, p, i64, p, p, C.c_int, p], C.c_int),
+    "ettg_exclusive_scan_i64_dev": ([p, i64, p, C.c_int, p], C.c_int),
+    "ettg_list_scan": ([p, p, i64, i64, C.c_int, p], C.c_int),
+    "ettg_segmented_reduce": ([p, i64, p, i64, C.c_int, i64, C.c_int, p], C.c_int),
+    "ettg_segmented_reduce_dev": ([p, i64, p, i64, C.c_int, i64, p, C.c_int, p], C.c_int),
+    "ettg_range_index_build": ([p, i64, C.c_int, C.POINTER(p)], C.c_int),
+    "ettg_range_index_build_dev": ([p, i64, C.c_int, p, C.POINTER(p)], C.c_int),
+    "ettg_range_index_size": ([p], i64),
+    "ettg_range_index_query": ([p, p, i64, p, p], C.c_int),
+    "ettg_range_index_query_dev": ([p, p, i64, p, p, p], C.c_int),
+    "ettg_range_index_free": ([p], None),
     "ettg_gen_grasp_tree": ([i64, u64, u64, p], C.c_int),
     "ettg_gen_barabasi_tree": ([i64, u64, p], C.c_int),
     "ettg_gen_permute_labels": ([i64, p, i64, u64, p, i64p], C.c_int),

@@ -432,6 +432,137 @@ def sort_pairs(keys, vals, device: int = 0):
     return ko.cpu().numpy(), vo.cpu().numpy()
 
 
+K_PLUS_INF = (1 << 63) - 1   # ett::kPlusInf
+K_MINUS_INF = -(1 << 63)     # ett::kMinusInf
+
+
+def list_scan(succ, values, head: int, device: int = 0) -> np.ndarray:
+    """list_scan (core/src/primitives.cpp:156-162): out[i] = sum of values
+    strictly before i in list order; succ uses -1 as the tail."""
+    s = np.ascontiguousarray(succ, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    if len(v) != len(s):
+        raise InvalidArgument("list_scan: values size mismatch")
+    out = np.empty(len(s), np.int64)
+    if len(s) == 0:
+        return out
+    check(lib().ettg_list_scan(ptr(s), ptr(v), len(s), int(head), device, ptr(out)))
+    return out
+
+
+_REDUCE_OPS = {"min": _lib.REDUCE_MIN, "max": _lib.REDUCE_MAX, "sum": _lib.REDUCE_SUM}
+
+
+def segmented_reduce(values, offsets, op: str, identity: int, device: int = 0):
+    """segmented_reduce (core/include/ett/primitives.hpp:81-98) with op in
+    {"min", "max", "sum"}.  Host arrays in, numpy out; torch CUDA tensors in,
+    a CUDA tensor out (ettg_segmented_reduce_dev)."""
+    if op not in _REDUCE_OPS:
+        raise InvalidArgument(f"segmented_reduce: unknown op {op!r}")
+    if hasattr(values, "is_cuda") and values.is_cuda:
+        torch = _torch()
+        segs = max(offsets.numel() - 1, 0)
+        out = torch.empty(segs, dtype=torch.int64, device=values.device)
+        check(lib().ettg_segmented_reduce_dev(
+            ptr(values), values.numel(), ptr(offsets), offsets.numel(), _REDUCE_OPS[op],
+            int(identity), ptr(out), values.device.index or 0,
+            torch.cuda.current_stream(values.device).cuda_stream))
+        return out
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    o = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = np.empty(max(len(o) - 1, 0), np.int64)
+    check(lib().ettg_segmented_reduce(ptr(v), len(v), ptr(o), len(o), _REDUCE_OPS[op],
+                                      int(identity), device, ptr(out)))
+    return out
+
+
+class RangeIndex:
+    """RangeIndex (core/include/ett/primitives.hpp:100-121): inclusive range
+    min/max over int64 keys, built and queried on the device.  ``min(l, r)``
+    and ``max(l, r)`` answer one range like the reference; ``mins`` /
+    ``maxs`` / ``minmax`` answer a batch of (l, r) pairs in one launch."""
+
+    def __init__(self, keys, device: int = 0):
+        self._h = None
+        self.device = device
+        h = C.c_void_p()
+        if hasattr(keys, "is_cuda") and keys.is_cuda:
+            torch = _torch()
+            k = keys.contiguous().to(torch.int64)
+            self.device = k.device.index or 0
+            check(lib().ettg_range_index_build_dev(
+                ptr(k), k.numel(), self.device, torch.cuda.current_stream(k.device).cuda_stream,
+                C.byref(h)))
+        else:
+            k = np.ascontiguousarray(keys, dtype=np.int64)
+            check(lib().ettg_range_index_build(ptr(k), len(k), device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ettg_range_index_free(self._h)
+            self._h = None
+
+    def size(self) -> int:
+        return int(lib().ettg_range_index_size(self._h))
+
+    def _query(self, ranges, want_min: bool, want_max: bool):
+        r = np.ascontiguousarray(ranges, dtype=np.int64).reshape(-1, 2)
+        q = len(r)
+        mins = np.empty(q, np.int64) if want_min else None
+        maxs = np.empty(q, np.int64) if want_max else None
+        if q:
+            check(lib().ettg_range_index_query(self._h, ptr(r), q, ptr(mins), ptr(maxs)))
+        return mins, maxs
+
+    def min(self, l: int, r: int) -> int:
+        return int(self._query([(l, r)], True, False)[0][0])
+
+    def max(self, l: int, r: int) -> int:
+        return int(self._query([(l, r)], False, True)[1][0])
+
+    def mins(self, ranges) -> np.ndarray:
+        return self._query(ranges, True, False)[0]
+
+    def maxs(self, ranges) -> np.ndarray:
+        return self._query(ranges, False, True)[1]
+
+    def minmax(self, ranges):
+        return self._query(ranges, True, True)
+
+    def query_dev(self, d_ranges, d_mins=None, d_maxs=None, stream=None):
+        """Device-resident batch: d_ranges int64[q, 2] CUDA tensor."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        check(lib().ettg_range_index_query_dev(self._h, ptr(d_ranges), d_ranges.numel() // 2,
+                                               ptr(d_mins), ptr(d_maxs), st))
+
+
+def rmq_build(keys, device: int = 0) -> RangeIndex:
+    """rmq_build (core/include/ett/primitives.hpp:116-118)."""
+    return RangeIndex(keys, device)
+
+
+def rmq_min(idx: RangeIndex, l: int, r: int) -> int:
+    return idx.min(l, r)
+
+
+def rmq_max(idx: RangeIndex, l: int, r: int) -> int:
+    return idx.max(l, r)
+
+
+def exclusive_scan_i64(values, device: int = 0) -> np.ndarray:
+    """exclusive_scan(values, +, 0) over int64, wrapping modulo 2^64."""
+    torch = _torch()
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    if len(v) == 0:
+        return np.zeros(0, np.int64)
+    d = torch.from_numpy(v).to(f"cuda:{device}")
+    check(lib().ettg_exclusive_scan_i64_dev(ptr(d), len(v), ptr(d), device,
+                                            torch.cuda.current_stream(device).cuda_stream))
+    return d.cpu().numpy()
+
+
 # --------------------------------------------------------------- generators
 def grasp_tree(n: int, gamma: int = K_GRASP_INFINITY, seed: int = 0) -> RootedTree:
     par = np.empty(n, np.int64)

@@ -76,6 +76,31 @@ int main() {
     auto d = ettg::parse_dimacs_gr(gr);
     CHECK(d.n == 2 && d.m() == 1);
   }
+  {  // tests/primitives_test.cpp:88-170
+    CHECK(ettg::list_scan({{1, 2, -1}, 0}, {5, 7, 9}) == std::vector<ettg::i64>({0, 5, 12}));
+    CHECK(ettg::segmented_reduce({3, 1, 2}, {0, 2, 3}, ettg::Min{}, ettg::kPlusInf) ==
+          std::vector<ettg::i64>({1, 2}));
+    CHECK(ettg::segmented_reduce({3, 1, 2}, {0, 0, 3}, ettg::Min{}, ettg::kPlusInf) ==
+          std::vector<ettg::i64>({ettg::kPlusInf, 1}));
+    bool threw = false;
+    try {
+      ettg::segmented_reduce({3, 1, 2}, {0, 2}, ettg::Max{}, ettg::kMinusInf);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    auto idx = ettg::rmq_build({2, 9, 4, 1});
+    CHECK(idx.size() == 4 && ettg::rmq_min(idx, 0, 3) == 1 && ettg::rmq_max(idx, 0, 3) == 9);
+    CHECK(idx.min(1, 1) == 9);
+    CHECK(idx.maxs({{0, 1}, {2, 3}}) == std::vector<ettg::i64>({9, 4}));
+    threw = false;
+    try {
+      idx.min(0, 4);
+    } catch (const std::out_of_range&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   std::printf("shim ok\n");
   return 0;
 }

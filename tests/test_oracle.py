@@ -60,6 +60,50 @@ def test_golden_primitives(port):
         port.list_rank([1, 2, 0], 0)
 
 
+PLUS_INF, MINUS_INF = (1 << 63) - 1, -(1 << 63)
+
+
+def test_golden_list_scan_segreduce_rangeindex(port):
+    # tests/primitives_test.cpp:88-97 (list_scan), :110-129 (segmented_reduce),
+    # :131-170 (RangeIndex)
+    assert port.list_scan([1, 2, -1], 0, [5, 7, 9]).tolist() == [0, 5, 12]
+    assert port.segmented_reduce([3, 1, 2], [0, 2, 3], "min", PLUS_INF).tolist() == [1, 2]
+    assert port.segmented_reduce([3, 1, 2], [0, 0, 3], "min", PLUS_INF).tolist() == [PLUS_INF, 1]
+    with pytest.raises(Exception, match="bad offsets"):
+        port.segmented_reduce([3, 1, 2], [0, 2], "min", PLUS_INF)
+    mins, maxs = port.range_index([2, 9, 4, 1], [(0, 3), (1, 1), (1, 2)])
+    assert mins.tolist() == [1, 9, 4] and maxs.tolist() == [9, 9, 9]
+    for bad in [(0, 4), (-1, 2), (2, 1)]:
+        with pytest.raises(Exception, match="bad range"):
+            port.range_index([2, 9, 4, 1], [bad])
+
+
+def test_list_scan_segreduce_rangeindex_vs_reference(port, ref):
+    rng = np.random.default_rng(11)
+    for k in (1, 2, 7, 1000, 20_000):
+        order = rng.permutation(k)
+        succ = np.full(k, -1, np.int64)
+        succ[order[:-1]] = order[1:]
+        vals = rng.integers(-(1 << 40), 1 << 40, k)
+        assert np.array_equal(port.list_scan(succ, int(order[0]), vals),
+                              ref.list_scan(succ, int(order[0]), vals))
+    for segs in (1, 5, 300):
+        lens = rng.integers(0, 40, segs)
+        offs = np.concatenate([[0], np.cumsum(lens)])
+        vals = rng.integers(-1000, 1000, int(offs[-1]))
+        for op, ident in (("min", PLUS_INF), ("max", MINUS_INF), ("sum", 0), ("min", 3)):
+            assert np.array_equal(port.segmented_reduce(vals, offs, op, ident),
+                                  ref.segmented_reduce(vals, offs, op, ident))
+    for n in (1, 2, 33, 1000):
+        keys = rng.integers(-(1 << 62), 1 << 62, n)
+        l = rng.integers(0, n, 500)
+        r = rng.integers(0, n, 500)
+        rr = np.stack([np.minimum(l, r), np.maximum(l, r)], 1)
+        pm, px = port.range_index(keys, rr)
+        qm, qx = ref.range_index(keys, rr)
+        assert np.array_equal(pm, qm) and np.array_equal(px, qx)
+
+
 def test_golden_bridges(port):
     # tests/bridges_test.cpp:45-147
     cases = [
