@@ -31,6 +31,7 @@
 // no second scan, unlike node_stats in core/src/euler.cpp:134-142).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -47,6 +48,7 @@ constexpr u32 kLrL0 = 16;   // level-0 mean sublist length (power of two); round
                             // 16 beat 8 (2.84 vs 3.17 ms on 64M elements)
 constexpr u32 kLrL = 16;    // deeper levels
 constexpr u32 kLrCapStep = 0xFFFFu;
+constexpr u32 kLrWyllieMax = 1u << 19;  // final level in global memory up to this size
 
 // error bits
 constexpr u32 kErrStructure = 1u;  // cycle / uncovered / bad successor
@@ -349,18 +351,13 @@ __global__ void k_lr_expand(const u32* __restrict__ rec_sid, const u64* __restri
 
 // Final level: Wyllie pointer jumping in shared memory, one CTA.
 // total_rank_expect: the head chain must have this many level-0 elements.
-__global__ void __launch_bounds__(kLrFinalThreads)
-    k_lr_final(const u32* __restrict__ succ, const u64* __restrict__ w, const u32* d_S,
-               const u32* d_head, u64* __restrict__ prefix, u32 total_rank_expect,
-               u32* err) {
+__device__ __forceinline__ void lr_final_smem(const u32* __restrict__ succ,
+                                              const u64* __restrict__ w, u32 S, const u32* d_head,
+                                              u64* __restrict__ prefix, u32 total_rank_expect,
+                                              u32* err) {
   extern __shared__ u64 s_dyn[];  // kLrFinalMax u64 values, then u32 links
   u64* s_val = s_dyn;
   u32* s_nxt = reinterpret_cast<u32*>(s_dyn + kLrFinalMax);
-  const u32 S = *d_S;
-  if (S > kLrFinalMax) {
-    if (threadIdx.x == 0) atomicOr(err, kErrCapacity);
-    return;
-  }
   constexpr int kPer = kLrFinalMax / kLrFinalThreads;
   for (u32 i = threadIdx.x; i < S; i += kLrFinalThreads) {
     u32 nx = succ[i];
@@ -413,6 +410,73 @@ __global__ void __launch_bounds__(kLrFinalThreads)
     atomicOr(err, kErrStructure);  // head chain does not cover every element
 }
 
+__global__ void __launch_bounds__(kLrFinalThreads)
+    k_lr_final(const u32* __restrict__ succ, const u64* __restrict__ w, const u32* d_S,
+               const u32* d_head, u64* __restrict__ prefix, u32 total_rank_expect,
+               u32* err) {
+  const u32 S = *d_S;
+  if (S > kLrFinalMax) {
+    if (threadIdx.x == 0) atomicOr(err, kErrCapacity);
+    return;
+  }
+  lr_final_smem(succ, w, S, d_head, prefix, total_rank_expect, err);
+}
+
+// Final level for up to kLrWyllieMax elements: Wyllie pointer jumping over
+// global memory in one cooperative launch, ping-ponging (succ, value)
+// between two buffers with a grid barrier per round.  A small level (<=
+// kLrFinalMax, known only on the device) takes the one-CTA smem path
+// instead.  Replaces further walk levels whose cost on small lists is the
+// longest sublist's dependent-load chain (about L ln(S/L) steps), not
+// bandwidth: ceil(log2 S) fully parallel rounds are shorter.
+__global__ void __launch_bounds__(kLrFinalThreads)
+    k_lr_wyllie(const u32* __restrict__ succ_in, const u64* __restrict__ w_in, u32* succ_a,
+                u64* val_a, u32* succ_b, u64* val_b, const u32* d_S, const u32* d_head,
+                u64* __restrict__ prefix, u32 total_rank_expect, u32* err) {
+  const u32 S = *d_S;
+  if (S <= kLrFinalMax) {
+    if (blockIdx.x == 0) lr_final_smem(succ_in, w_in, S, d_head, prefix, total_rank_expect, err);
+    return;  // uniform across the grid: no barrier is reached
+  }
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const u32 stride = gridDim.x * blockDim.x;
+  const u32 t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rounds = 32 - __clz(S - 1);  // 2^rounds >= S
+  const u32* src_s = succ_in;
+  const u64* src_v = w_in;
+  u32* dst_s = succ_a;
+  u64* dst_v = val_a;
+  for (int r = 0; r < rounds; ++r) {
+    for (u32 i = t0; i < S; i += stride) {
+      u32 nx = src_s[i];
+      u64 v = src_v[i];
+      if (r == 0 && nx != kNone && nx >= S) {
+        atomicOr(err, kErrStructure);
+        nx = kNone;
+      }
+      u32 nn = kNone;
+      if (nx != kNone) {
+        v += src_v[nx];
+        nn = src_s[nx];
+        if (r == 0 && nn != kNone && nn >= S) nn = kNone;  // flagged by element nx
+      }
+      dst_s[i] = nn;
+      dst_v[i] = v;
+    }
+    grid.sync();
+    src_s = dst_s;
+    src_v = dst_v;
+    dst_s = (dst_s == succ_a) ? succ_b : succ_a;
+    dst_v = (dst_v == val_a) ? val_b : val_a;
+  }
+  const u64 total = src_v[*d_head];
+  for (u32 i = t0; i < S; i += stride) {
+    if (src_s[i] != kNone) atomicOr(err, kErrStructure);  // cycle
+    prefix[i] = total - src_v[i];
+  }
+  if (t0 == 0 && static_cast<u32>(total) != total_rank_expect) atomicOr(err, kErrStructure);
+}
+
 // ---- orchestration ---------------------------------------------------------
 struct LrLevel {
   u32 cap = 0;            // capacity of this level's element arrays
@@ -425,6 +489,10 @@ struct LrLevel {
   u32* sub_next = nullptr;
   u64* sub_w = nullptr;
   u64* scan_status = nullptr;
+  u32* succ2 = nullptr;   // final level > kLrFinalMax: Wyllie ping-pong buffers
+  u64* w2 = nullptr;
+  u32* succ3 = nullptr;
+  u64* w3 = nullptr;
 };
 
 struct ListRankWs {
@@ -444,12 +512,14 @@ struct ListRankWs {
   }
 
   u32 L0 = kLrL0;  // level-0 mean sublist length (power of two); ETTG_LR_L0 overrides
+  double wyllie_max = kLrWyllieMax;  // ETTG_LR_WYLLIE overrides (0: smem final only)
   void carve(Carver& c, u32 k_) {
     k = k_;
     if (const char* e = std::getenv("ETTG_LR_L0")) {
       const u32 v = static_cast<u32>(std::atoi(e));
       if (v >= 2 && v <= 1024 && (v & (v - 1)) == 0) L0 = v;
     }
+    if (const char* e = std::getenv("ETTG_LR_WYLLIE")) wyllie_max = std::atof(e);
     succ0 = c.take<u32>(k);
     rec0 = c.take<u64>(k);
     counters = c.take<u32>(64);
@@ -469,7 +539,14 @@ struct ListRankWs {
       L.succ = c.take<u32>(cap);
       L.w = c.take<u64>(cap);
       L.prefix = c.take<u64>(cap);
-      if (expect <= 2048.0 || l == kMaxLevels) break;  // final Wyllie level
+      if (expect <= 2048.0 || l == kMaxLevels) break;  // final Wyllie level (smem)
+      if (expect * 1.25 <= wyllie_max) {                // final Wyllie level (global)
+        L.succ2 = c.take<u32>(cap);
+        L.w2 = c.take<u64>(cap);
+        L.succ3 = c.take<u32>(cap);
+        L.w3 = c.take<u64>(cap);
+        break;
+      }
       L.rec_sid = c.take<u32>(cap);
       L.rec_loc = c.take<u64>(cap);
       u32 capn = next_cap(cap, kLrL);
@@ -556,11 +633,29 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
     const int l = ws.levels;
     LrLevel& F = ws.lv[l];
     const u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
-    CK(cudaFuncSetAttribute(k_lr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kLrFinalSmem));
-    k_lr_final<<<1, kLrFinalThreads, kLrFinalSmem, st>>>(F.succ, F.w, S_l, hd, F.prefix, k,
-                                              cnt + LrCounters::kErr);
-    CK_LAUNCH();
+    if (!F.succ2) {
+      CK(cudaFuncSetAttribute(k_lr_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kLrFinalSmem));
+      k_lr_final<<<1, kLrFinalThreads, kLrFinalSmem, st>>>(F.succ, F.w, S_l, hd, F.prefix, k,
+                                                           cnt + LrCounters::kErr);
+      CK_LAUNCH();
+    } else {
+      // S_l is clamped to F.cap; one grid barrier per round
+      CK(cudaFuncSetAttribute(k_lr_wyllie, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kLrFinalSmem));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lr_wyllie, kLrFinalThreads,
+                                                       kLrFinalSmem));
+      const unsigned grid = static_cast<unsigned>(std::max(1, per_sm) * sms);
+      const u32* fs = F.succ;
+      const u64* fw = F.w;
+      u32* ek = cnt + LrCounters::kErr;
+      u32 expect = k;
+      void* args[] = {&fs, &fw, &F.succ2, &F.w2, &F.succ3, &F.w3, &S_l, &hd, &F.prefix,
+                      &expect, &ek};
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lr_wyllie), grid,
+                                     kLrFinalThreads, args, kLrFinalSmem, st));
+    }
     tr.mark("final");
   }
   // expand back down to level 1
