@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "listrank.cuh"
 #include "scan.cuh"
+#include "sparse.cuh"
 #include "graph.cuh"
 #include "trace.cuh"
 
@@ -461,12 +462,9 @@ __global__ void k_lh_block_ps(const uint2* __restrict__ lh, u32 n, u32 nb,
   }
 }
 
-__global__ void k_lh_level(const uint2* __restrict__ prev, uint2* __restrict__ cur, u32 nb,
-                           u32 half) {
-  for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
-       b += gridDim.x * blockDim.x)
-    cur[b] = lh_merge(prev[b], prev[b + half]);
-}
+struct LhMerge {
+  __device__ __forceinline__ uint2 operator()(uint2 a, uint2 b) const { return lh_merge(a, b); }
+};
 
 // ---- TV on Euler-tour positions (no preorder scan) -------------------------
 // Any DFS numbering in which every subtree is contiguous serves the TV test
@@ -791,12 +789,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
         ws.lh, len, ws.nb, ws.sp, ws.lh_pre, ws.lh_suf);
     CK_LAUNCH();
-    for (u32 lvl = 1; lvl < ws.levels; ++lvl) {
-      k_lh_level<<<std::min(g, blocks_for(ws.nb, 256)), 256, 0, st>>>(
-          ws.sp + static_cast<u64>(lvl - 1) * ws.nb, ws.sp + static_cast<u64>(lvl) * ws.nb,
-          ws.nb, 1u << (lvl - 1));
-      CK_LAUNCH();
-    }
+    build_sparse_rows(ws.sp, ws.nb, ws.levels, LhMerge{}, g, st);
     if (n > 1) {
       k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
           ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m);

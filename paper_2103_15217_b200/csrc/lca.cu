@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "listrank.cuh"
 #include "scan.cuh"
+#include "sparse.cuh"
 #include "sort.cuh"
 #include "trace.cuh"
 
@@ -339,12 +340,9 @@ __global__ void k_rmq_block(const u64* __restrict__ key, u32 steps, u32 nb,
   }
 }
 
-__global__ void k_rmq_level(const u64* __restrict__ prev, u64* __restrict__ cur, u32 nb,
-                            u32 half) {
-  for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b + 2 * half <= nb;
-       b += gridDim.x * blockDim.x)
-    cur[b] = min(prev[b], prev[b + half]);
-}
+struct MinU64 {
+  __device__ __forceinline__ u64 operator()(u64 a, u64 b) const { return min(a, b); }
+};
 
 // ---- naive engine: pointer-jumping levels + walk-up queries ----------------
 // ancestor_doubling_levels (core/src/primitives.cpp:208-241) and naive_lca
@@ -983,12 +981,7 @@ void launch_stats_rmq(ettg_lca* h, cudaStream_t st, int sms) {
   k_rmq_block<<<blocks_for(static_cast<u64>(h->nb) * 32, 256), 256, 0, st>>>(
       h->tkey, steps, h->nb, h->pre_in, h->suf_in, h->sp);
   CK_LAUNCH();
-  for (u32 k = 1; k < h->levels; ++k) {
-    k_rmq_level<<<std::min<unsigned>(g, blocks_for(h->nb, 256)), 256, 0, st>>>(
-        h->sp + static_cast<u64>(k - 1) * h->nb, h->sp + static_cast<u64>(k) * h->nb, h->nb,
-        1u << (k - 1));
-    CK_LAUNCH();
-  }
+  build_sparse_rows(h->sp, h->nb, h->levels, MinU64{}, g, st);
 }
 
 // naive_build (core/src/lca.cpp:111-116): validate + pointer-jumping levels.

@@ -19,6 +19,7 @@
 #include "api_internal.cuh"
 #include "common.cuh"
 #include "listrank.cuh"
+#include "sparse.cuh"
 
 namespace ettg {
 namespace {
@@ -184,11 +185,16 @@ template <int kOp>
 __global__ void __launch_bounds__(256)
     k_segreduce(const i64* __restrict__ values, i64 nvals, const i64* __restrict__ offsets,
                 i64 segs, i64 identity, i64* __restrict__ out, u32* __restrict__ err) {
+  // Whole warps iterate together (the shuffles below name all 32 lanes).
+  constexpr int kGroups = 32 / kSegLanes;
   const int sub = threadIdx.x & (kSegLanes - 1);
-  const i64 groups = static_cast<i64>(gridDim.x) * (blockDim.x / kSegLanes);
-  for (i64 s = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) / kSegLanes; s < segs;
-       s += groups) {
-    const i64 lo = offsets[s], hi = offsets[s + 1];
+  const int grp = (threadIdx.x & 31) / kSegLanes;
+  const i64 warps = static_cast<i64>(gridDim.x) * (blockDim.x / 32);
+  for (i64 base = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) / 32 * kGroups;
+       base < segs; base += warps * kGroups) {
+    const i64 s = base + grp;
+    const bool live = s < segs;
+    const i64 lo = live ? offsets[s] : 0, hi = live ? offsets[s + 1] : 0;
     i64 acc = sub == 0 ? identity : seg_neutral<kOp>();
     if (lo < hi) {
       if (lo < 0 || hi > nvals) {
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int d = kSegLanes / 2; d > 0; d >>= 1)
       acc = seg_combine<kOp>(acc, __shfl_xor_sync(0xffffffffu, acc, d, kSegLanes));
-    if (sub == 0) out[s] = acc;
+    if (live && sub == 0) out[s] = acc;
   }
 }
 
@@ -241,12 +247,9 @@ __global__ void k_ri_blocks(const i64* __restrict__ keys, i64 n, i64 nb, longlon
   }
 }
 
-__global__ void k_ri_level(const longlong2* __restrict__ prev, longlong2* __restrict__ cur, i64 cnt,
-                           i64 half) {
-  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
-       i += static_cast<i64>(gridDim.x) * blockDim.x)
-    cur[i] = mm(prev[i], prev[i + half]);
-}
+struct MinMax64 {
+  __device__ __forceinline__ longlong2 operator()(longlong2 a, longlong2 b) const { return mm(a, b); }
+};
 
 struct RiView {
   const i64* keys;
@@ -366,13 +369,8 @@ ettg_range_index* ri_build(const i64* keys, bool host, i64 n, int device, cudaSt
     k_ri_blocks<<<grid_for(h->nb * 32, device), 256, 0, st>>>(
         dk, n, h->nb, const_cast<longlong2*>(h->view.pre), const_cast<longlong2*>(h->view.suf), tab);
     CK_LAUNCH();
-    for (int j = 1; j < levels; ++j) {
-      const i64 half = i64(1) << (j - 1);
-      const i64 cnt = h->nb - (i64(1) << j) + 1;
-      k_ri_level<<<grid_for(cnt, device), 256, 0, st>>>(tab + (j - 1) * h->nb, tab + j * h->nb, cnt,
-                                                         half);
-      CK_LAUNCH();
-    }
+    build_sparse_rows(tab, static_cast<u32>(h->nb), static_cast<u32>(levels), MinMax64{},
+                      static_cast<unsigned>(sm_count(device) * 8), st);
     CK(cudaStreamSynchronize(st));
   } catch (...) {
     if (h->mem) cudaFree(h->mem);
