@@ -221,6 +221,15 @@ __global__ void k_cc_range(const uint2* __restrict__ edges, u32 m, u32 n, u32* f
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
+// TV runs from the forest to the mask without a host round trip: the
+// endpoint-range flag (words[0]) and the tree-edge count (words[1], which
+// must be n - 1) stay on the device.  On a bad input the kernels that index
+// by tree edge or key do nothing, and the host raises after its one final
+// synchronisation.  Other engines pass abort = nullptr and check on the host.
+__device__ __forceinline__ bool tv_abort(const u32* w, u32 n) {
+  return w && (w[0] != 0u || w[1] != n - 1);
+}
+
 // Tree-edge compaction: tedge[t] = e for the t-th tree edge.
 struct TreeOut {
   u32* tedge;
@@ -273,7 +282,8 @@ __device__ __forceinline__ void rot_push(u32 active, u32 x, u32 h, u32 root,
 
 __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
                            u32 root, u32* __restrict__ head, u32* __restrict__ nxt,
-                           uint2* __restrict__ tend, u32* last_root) {
+                           uint2* __restrict__ tend, u32* last_root, const u32* abort, u32 n) {
+  if (tv_abort(abort, n)) return;
   const u32 stride = gridDim.x * blockDim.x;
   for (u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < T; base += stride) {
     const u32 t = base + (threadIdx.x & 31);
@@ -290,9 +300,15 @@ __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restric
 // is e's destination (core/src/euler.cpp:85-88, :105).  Written as list-rank
 // slots; the cut before head[root] makes the tour a list.
 __global__ void k_tree_succ(const uint2* __restrict__ tend, const u32* __restrict__ head,
-                            const u32* __restrict__ nxt, u32 k, u32 cut,
-                            u32* __restrict__ slot) {
+                            const u32* __restrict__ nxt, u32 k, const u32* d_cut,
+                            u32* __restrict__ slot, const u32* abort, u32 n) {
+  const bool off = tv_abort(abort, n);
+  const u32 cut = *d_cut;
   for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    if (off) {
+      slot[e] = kNone;  // a list of isolated tails: ranked without faults, flagged
+      continue;
+    }
     const u32 tw = e ^ 1u;
     const uint2 uv = tend[e >> 1];
     const u32 dst = (e & 1u) ? uv.x : uv.y;
@@ -302,7 +318,12 @@ __global__ void k_tree_succ(const uint2* __restrict__ tend, const u32* __restric
 }
 
 __global__ void k_tree_head(const u32* __restrict__ head, u32 root, const u32* last_root,
-                            u32* words) {
+                            u32* words, const u32* abort, u32 n) {
+  if (tv_abort(abort, n)) {
+    words[2] = 0;
+    words[3] = kNone;
+    return;
+  }
   words[2] = head[root];        // tour head: first half-edge of root's rotation
   words[3] = *last_root ^ 1u;   // its tour predecessor: twin of the last one
 }
@@ -389,7 +410,8 @@ __global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32
 template <int kHookE, int kMinB>
 __global__ void __launch_bounds__(256, kMinB)
     k_lowhigh_edges(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
-                    const u32* __restrict__ pre_of, uint2* lh) {
+                    const u32* __restrict__ pre_of, uint2* lh, const u32* abort, u32 n) {
+  if (tv_abort(abort, n)) return;
   u32* w = reinterpret_cast<u32*>(lh);  // slot = preorder - 1; .x = low, .y = high
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < m;
@@ -475,7 +497,9 @@ struct LhMerge {
 // (up positions stay neutral), so the per-position "#downs before" scan of
 // node_stats is not needed: bridge(c) iff low >= K(c) and high < U(c).
 __global__ void k_tv_keys(Lr0View lr, u32 T, const uint2* __restrict__ tend, u32 root,
-                          u32* __restrict__ key_of, uint2* __restrict__ kt) {
+                          u32* __restrict__ key_of, uint2* __restrict__ kt, const u32* abort,
+                          u32 n) {
+  if (tv_abort(abort, n)) return;
   const u32 S1 = *lr.d_S1;
   for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     u32 r0, r1, d;
@@ -500,7 +524,8 @@ __global__ void __launch_bounds__(256)
     k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ pre,
                     const uint2* __restrict__ suf, const uint2* __restrict__ sp, u32 nb, u32 len,
                     const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
-                    uint8_t* __restrict__ mask, u32 m) {
+                    uint8_t* __restrict__ mask, u32 m, const u32* abort, u32 n) {
+  if (tv_abort(abort, n)) return;
   for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     const uint2 k = kt[t];
     const u32 a = k.x - 1, b = min(k.y - 1, len - 1);
@@ -550,10 +575,10 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* t
 }
 
 void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* pre_of, uint2* lh,
-                    int sms, cudaStream_t st) {
+                    const u32* abort, u32 n, int sms, cudaStream_t st) {
   auto kern = k_lowhigh_edges<kEdgesPerThread, 8>;
   kern<<<occ_grid(kern, (u64(m) + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
-      edges, tree, m, pre_of, lh);
+      edges, tree, m, pre_of, lh, abort, n);
   CK_LAUNCH();
 }
 
@@ -686,6 +711,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   if (m) CK(cudaMemsetAsync(d_mask, 0, m, st));
   tr.mark("input");
   u32 lerr = 0;
+  const u32* abort = nullptr;  // TV: device-side input checks (tv_abort)
 
   if (engine == ETTG_BRIDGES_CK) {
     // ---- ck_bridges (core/src/bridges.cpp:477-485): BFS tree + marking ----
@@ -729,36 +755,37 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
 
     // ---- Euler tour of the forest, rooted at 0 ---------------------------
     compact_u8(ws.tree, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
-    u32 w[2];
-    CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (w[0]) einval("edge endpoint out of range");
-    const u32 T = w[1];
-    if (T != n - 1) einval("disconnected graph; extract the largest component first");
+    const bool tv = engine == ETTG_BRIDGES_TV;
+    if (!tv) {
+      u32 w[2];
+      CK(cudaMemcpyAsync(w, ws.words, sizeof w, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (w[0]) einval("edge endpoint out of range");
+      if (w[1] != n - 1) einval("disconnected graph; extract the largest component first");
+    }
+    abort = tv ? ws.words : nullptr;  // TV: checked once at the end
+    const u32 T = n - 1;
 
     if (n > 1) {
       const u32 k = 2 * T;
       CK(cudaMemsetAsync(ws.head, 0xFF, static_cast<u64>(n) * 4, st));
       tr.mark("compact");
-      k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(edges, ws.tedge, T, 0, ws.head,
-                                                                  ws.nxt, ws.tend, ws.words + 4);
+      k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(
+          edges, ws.tedge, T, 0, ws.head, ws.nxt, ws.tend, ws.words + 4, abort, n);
       CK_LAUNCH();
-      k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words);
+      k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words, abort, n);
       CK_LAUNCH();
-      u32 hw[2];
-      CK(cudaMemcpyAsync(hw, ws.words + 2, sizeof hw, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const u32 head = hw[0];
-      k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(ws.tend, ws.head, ws.nxt, k,
-                                                                   hw[1], ws.lr.succ0);
+      // head and cut stay on the device (words[2], words[3])
+      k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(
+          ws.tend, ws.head, ws.nxt, k, ws.words + 3, ws.lr.succ0, abort, n);
       CK_LAUNCH();
       tr.mark("rotation");
-      list_rank_core(k, head, NoDown{}, ws.lr, st, sms);
+      list_rank_core_h(k, DevHead{ws.words + 2}, NoDown{}, ws.lr, st, sms);
       tr.mark("list_rank");
       const Lr0View lv = lr0_view(ws.lr);
       if (engine == ETTG_BRIDGES_TV) {
         k_tv_keys<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.tend, 0,
-                                                                   ws.pre_of, ws.kt);
+                                                                   ws.pre_of, ws.kt, abort, n);
         CK_LAUNCH();
         tr.mark("keys");
       } else {
@@ -784,7 +811,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     const u32 len = 2 * n;  // slots key - 1, keys in [1, 2n - 1]
     k_lh_neutral<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.lh, len);
     CK_LAUNCH();
-    if (m && n > 1) launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, sms, st);
+    if (m && n > 1) launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, abort, n, sms, st);
     tr.mark("lowhigh_edges");
     k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
         ws.lh, len, ws.nb, ws.sp, ws.lh_pre, ws.lh_suf);
@@ -792,7 +819,8 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     build_sparse_rows(ws.sp, ws.nb, ws.levels, LhMerge{}, g, st);
     if (n > 1) {
       k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
-          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m);
+          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m,
+          abort, n);
       CK_LAUNCH();
     }
     tr.mark("rmq_classify");
@@ -813,7 +841,11 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   if (h_mask && m) CK(cudaMemcpyAsync(h_mask, d_mask, m, cudaMemcpyDeviceToHost, st));
   if (n > 1 && engine != ETTG_BRIDGES_CK)
     CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4, cudaMemcpyDeviceToHost, st));
+  u32 w[2] = {0, n - 1};
+  if (abort) CK(cudaMemcpyAsync(w, abort, sizeof w, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (w[0]) einval("edge endpoint out of range");
+  if (w[1] != n - 1) einval("disconnected graph; extract the largest component first");
   if (lerr) throw Error(ETTG_EINTERNAL, "bridges: spanning-tree tour ranking failed");
   if (times) {
     float a = 0, b = 0, d = 0, tot = 0;

@@ -65,11 +65,24 @@ __device__ __forceinline__ bool lr_is_splitter(u32 e, u32 head, u32 seed, u32 ma
   return e == head || (mix32(e ^ seed) & mask) == 0u;
 }
 
+// ---- list head: a host value, or a device word written by an earlier kernel
+// (lets a caller enqueue the ranking without reading the head back).
+struct HostHead {
+  u32 v;
+  __device__ __forceinline__ u32 get() const { return v; }
+};
+struct DevHead {
+  const u32* p;
+  __device__ __forceinline__ u32 get() const { return *p; }
+};
+
 // ---- splitter predicates ---------------------------------------------------
+template <class H>
 struct SplIn {
-  u32 head, seed, mask;
+  H head;
+  u32 seed, mask;
   __device__ __forceinline__ u32 operator()(u64 i) const {
-    return lr_is_splitter(static_cast<u32>(i), head, seed, mask) ? 1u : 0u;
+    return lr_is_splitter(static_cast<u32>(i), head.get(), seed, mask) ? 1u : 0u;
   }
 };
 // Level >= 1: head and size live in device memory; the scan runs over the
@@ -156,12 +169,13 @@ struct LrCounters {
 // the memory system is already saturated by the resident warps -- so 1.
 constexpr int kLrWalkers = 1;
 
-template <class Down>
+template <class Down, class H>
 __global__ void __launch_bounds__(256)
-    k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, u32 head, u32 seed,
+    k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, H head_src, u32 seed,
                u32 mask, const u32* __restrict__ spl, u32* counters, u32 sub_cap,
                u32* __restrict__ sub_next, u64* __restrict__ sub_w, Down down) {
   const int lane = threadIdx.x & 31;
+  const u32 head = head_src.get();
   const u32 lt = lanemask_lt();
   // A malformed list (shared successors, found by k_pred_check) is not walked.
   const u32 nspl = counters[LrCounters::kErr] ? 0u : min(counters[LrCounters::kNspl], sub_cap);
@@ -242,7 +256,10 @@ __global__ void __launch_bounds__(256)
 
 // Every element has at most one predecessor and the head has none (checked
 // before walking when the successor array comes from a caller).
-__global__ void k_pred_check(const u32* __restrict__ succ, u32 k, u32 head, u32* pred, u32* err) {
+template <class H>
+__global__ void k_pred_check(const u32* __restrict__ succ, u32 k, H head_src, u32* pred,
+                             u32* err) {
+  const u32 head = head_src.get();
   for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
     const u32 s = succ[e];
     if (s == kNone) continue;
@@ -313,10 +330,12 @@ __global__ void k_lr_clamp(u32* count, u32 cap, u32* err) {
 
 // Next-level list: succ'[sid] = sublist of the element after sublist sid.
 // Level-0 records are packed (local<<32 | sid).
+template <class H>
 __global__ void k_lr_next_level0(const u64* __restrict__ rec, const u32* __restrict__ sub_next,
-                                 const u64* __restrict__ sub_w, const u32* d_S, u32 head,
+                                 const u64* __restrict__ sub_w, const u32* d_S, H head_src,
                                  u32* __restrict__ succ2, u64* __restrict__ w2, u32* d_head2) {
   const u32 S = *d_S;
+  const u32 head = head_src.get();
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const u32 ne = sub_next[i];
     succ2[i] = ne == kNone ? kNone : static_cast<u32>(rec[ne]);
@@ -571,15 +590,15 @@ inline u32 lr_seed(int level) { return 0x65746b5fu ^ (0x9e3779b9u * (level + 1))
 // per-element kernel (Lr0View).  `pred` (k words of scratch) enables the
 // injectivity check for caller-supplied lists.  No host synchronisation;
 // errors accumulate in counters[kErr].
-template <class Down>
-void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st, int sms,
-                    u32* pred = nullptr) {
+template <class Down, class H>
+void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st, int sms,
+                      u32* pred = nullptr) {
   Trace tr("list_rank", st);
   CK(cudaMemsetAsync(ws.counters, 0, 64 * sizeof(u32), st));
   u32* cnt = ws.counters;
   if (pred) {
     CK(cudaMemsetAsync(pred, 0, static_cast<u64>(k) * 4, st));
-    k_pred_check<<<blocks_for(k, 256), 256, 0, st>>>(ws.succ0, k, head, pred,
+    k_pred_check<H><<<blocks_for(k, 256), 256, 0, st>>>(ws.succ0, k, head, pred,
                                                      cnt + LrCounters::kErr);
     CK_LAUNCH();
   }
@@ -587,13 +606,13 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
   const u32 seed0 = lr_seed(0);
   const u32 cap1 = ws.lv[1].cap;
   // level 0 splitters -> counters[kNspl]; sublists beyond come from cap splits
-  spl_compact(SplIn{head, seed0, mask0}, k, ws.lv[0].spl, cap1, cnt + LrCounters::kNspl,
+  spl_compact(SplIn<H>{head, seed0, mask0}, k, ws.lv[0].spl, cap1, cnt + LrCounters::kNspl,
               cnt + LrCounters::kErr, st);
   CK(cudaMemcpyAsync(cnt + LrCounters::kSubTotal0, cnt + LrCounters::kNspl, sizeof(u32),
                      cudaMemcpyDeviceToDevice, st));
   tr.mark("splitters0");
   const unsigned walk_blocks = sms * 8;  // 2048 threads / SM resident
-  k_lr_walk0<Down><<<walk_blocks, 256, 0, st>>>(ws.succ0, ws.rec0, k, head, seed0, mask0,
+  k_lr_walk0<Down, H><<<walk_blocks, 256, 0, st>>>(ws.succ0, ws.rec0, k, head, seed0, mask0,
                                                 ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
                                                 ws.lv[0].sub_w, down);
   CK_LAUNCH();
@@ -602,7 +621,7 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
   u32* S1 = cnt + LrCounters::kSubTotal0;
   k_lr_clamp<<<1, 1, 0, st>>>(S1, cap1, cnt + LrCounters::kErr);
   u32* head1 = cnt + LrCounters::kLevelBase + 4 * 1 + 2;
-  k_lr_next_level0<<<blocks_for(cap1, 256), 256, 0, st>>>(
+  k_lr_next_level0<H><<<blocks_for(cap1, 256), 256, 0, st>>>(
       ws.rec0, ws.lv[0].sub_next, ws.lv[0].sub_w, S1, head, ws.lv[1].succ, ws.lv[1].w, head1);
   CK_LAUNCH();
   // deeper levels
@@ -669,6 +688,12 @@ void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st,
     CK_LAUNCH();
   }
   tr.mark("expand");
+}
+
+template <class Down>
+void list_rank_core(u32 k, u32 head, Down down, ListRankWs& ws, cudaStream_t st, int sms,
+                    u32* pred = nullptr) {
+  list_rank_core_h(k, HostHead{head}, down, ws, st, sms, pred);
 }
 
 // Level-0 element prefix: (rank, down-weight sum) of everything before e.

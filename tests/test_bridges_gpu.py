@@ -75,6 +75,49 @@ def test_errors(ett):
         ett.tv_bridges(ett.EdgeList(0, np.zeros((0, 2), np.int64)))
 
 
+@pytest.mark.parametrize("engine", ["tv", "hybrid", "ck"])
+def test_errors_large_then_recovers(ett, engine):
+    # TV checks the forest on the device and raises after its one final sync:
+    # bad inputs must fail cleanly and leave the library usable.
+    fn = {"tv": ett.tv_bridges, "ck": ett.ck_bridges, "hybrid": ett.hybrid_bridges}[engine]
+    g, truth = ett.planted_bridge_graph(200_000, 1_000_000, 500, 4)
+    two = np.concatenate([g.edges, g.edges + g.n])  # two copies: disconnected
+    with pytest.raises(ett.InvalidArgument, match="disconnected"):
+        fn(ett.EdgeList(2 * g.n, two))
+    iso0 = g.edges + 1  # vertex 0 isolated (the forest root)
+    with pytest.raises(ett.InvalidArgument, match="disconnected"):
+        fn(ett.EdgeList(g.n + 1, iso0))
+    bad = g.edges.copy()
+    bad[12345, 1] = g.n + 7
+    with pytest.raises(ett.InvalidArgument, match="out of range"):
+        fn(ett.EdgeList(g.n, bad))
+    assert np.array_equal(fn(g).is_bridge, truth)
+
+
+def test_dev_path_errors_then_recovers(ett):
+    import ctypes
+    import torch
+    from paper_2103_15217_b200 import _lib
+    L = _lib.lib()
+    g, truth = ett.planted_bridge_graph(100_000, 600_000, 300, 4)
+
+    def run(edges, n):
+        de = torch.from_numpy(edges.astype(np.int32).ravel()).cuda()
+        dm = torch.empty(len(edges), dtype=torch.uint8, device="cuda")
+        rc = L.ettg_bridges_dev(de.data_ptr(), n, len(edges), 0, dm.data_ptr(), None, None)
+        torch.cuda.synchronize()
+        return rc, dm.cpu().numpy()
+
+    bad = g.edges.copy()
+    bad[777, 0] = g.n
+    rc, _ = run(bad, g.n)
+    assert rc == _lib.ETTG_EINVAL and b"out of range" in L.ettg_last_error()
+    rc, _ = run(np.concatenate([g.edges, g.edges + g.n]), 2 * g.n)
+    assert rc == _lib.ETTG_EINVAL and b"disconnected" in L.ettg_last_error()
+    rc, mask = run(g.edges, g.n)
+    assert rc == 0 and np.array_equal(mask, truth)
+
+
 def test_phase_times_named(ett):
     g, truth = ett.planted_bridge_graph(3000, 20_000, 40, 4)
     times = {}
