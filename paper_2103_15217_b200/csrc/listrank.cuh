@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kLrFinalThreads)
 __global__ void __launch_bounds__(kLrFinalThreads)
     k_lr_wyllie(const u32* __restrict__ succ_in, const u64* __restrict__ w_in, u32* succ_a,
                 u64* val_a, u32* succ_b, u64* val_b, const u32* d_S, const u32* d_head,
-                u64* __restrict__ prefix, u32 total_rank_expect, u32* err) {
+                u64* __restrict__ prefix, u32 total_rank_expect, u32* err, int hops) {
   const u32 S = *d_S;
   if (S <= kLrFinalMax) {
     if (blockIdx.x == 0) lr_final_smem(succ_in, w_in, S, d_head, prefix, total_rank_expect, err);
@@ -460,7 +460,10 @@ __global__ void __launch_bounds__(kLrFinalThreads)
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const u32 stride = gridDim.x * blockDim.x;
   const u32 t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int rounds = 32 - __clz(S - 1);  // 2^rounds >= S
+  // `hops` links per round: a pointer's span multiplies by `hops` per
+  // barrier (plain Wyllie: 2), trading dependent loads for grid barriers.
+  int rounds = 0;
+  for (u64 span = 1; span < S; span *= static_cast<u64>(hops)) ++rounds;
   const u32* src_s = succ_in;
   const u64* src_v = w_in;
   u32* dst_s = succ_a;
@@ -473,13 +476,13 @@ __global__ void __launch_bounds__(kLrFinalThreads)
         atomicOr(err, kErrStructure);
         nx = kNone;
       }
-      u32 nn = kNone;
-      if (nx != kNone) {
+      for (int h = 1; h < hops && nx != kNone; ++h) {
         v += src_v[nx];
-        nn = src_s[nx];
+        u32 nn = src_s[nx];
         if (r == 0 && nn != kNone && nn >= S) nn = kNone;  // flagged by element nx
+        nx = nn;
       }
-      dst_s[i] = nn;
+      dst_s[i] = nx;
       dst_v[i] = v;
     }
     grid.sync();
@@ -665,13 +668,17 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lr_wyllie, kLrFinalThreads,
                                                        kLrFinalSmem));
-      const unsigned grid = static_cast<unsigned>(std::max(1, per_sm) * sms);
+      int blocks = sms, hops = 3;
+      if (const char* e = std::getenv("ETTG_LR_WBLOCKS")) blocks = std::atoi(e);
+      if (const char* e = std::getenv("ETTG_LR_WHOPS")) hops = std::max(2, std::atoi(e));
+      blocks = std::max(1, std::min(blocks, std::max(1, per_sm) * sms));
+      const unsigned grid = static_cast<unsigned>(blocks);
       const u32* fs = F.succ;
       const u64* fw = F.w;
       u32* ek = cnt + LrCounters::kErr;
       u32 expect = k;
       void* args[] = {&fs, &fw, &F.succ2, &F.w2, &F.succ3, &F.w3, &S_l, &hd, &F.prefix,
-                      &expect, &ek};
+                      &expect, &ek, &hops};
       CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lr_wyllie), grid,
                                      kLrFinalThreads, args, kLrFinalSmem, st));
     }
