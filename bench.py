@@ -51,9 +51,10 @@ def peaks():
 
 # Random-gather ceiling of B200 at the node-table footprint of each layout at
 # n = 16M (tools/footprint_micro.cu, profiles/r1_lca_layout.md): 64 MB table
-# (compact) 263.8, 128 MB (narrow, split) 113.1, 256 MB (wide) 71.6 G gathers/s.
+# (compact) 263.8, 96 MB (split6) 150.7, 128 MB (narrow, split) 113.1, 256 MB
+# (wide) 71.6 G gathers/s.
 L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "split": 113.1, "wide": 71.6,
-                     "split_own": 71.6}
+                     "split_own": 71.6, "split6": 150.7}
 
 
 def ncu_traffic(kernel_key: str):
@@ -571,7 +572,8 @@ def main():
         layout, labels = idx.layout()
         kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
                  "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split",
-                 "split_own": "k_lca_inlabel_split_own"}[layout]
+                 "split_own": "k_lca_inlabel_split_own",
+                 "split6": "k_lca_inlabel_split6"}[layout]
         q_r = sec["q_rank"]
         if layout == "compact":
             # 12 B streamed + the index read once per launch (node words + label
@@ -641,10 +643,11 @@ def main():
                 "l2_gather_frac": (2 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
                                    / L2_GATHER_CEILING[secE["idx"].layout()[0]]),
                 "l1_tag_stage": l1_tag_stage(
-                    {"split": "k_lca_inlabel_split_E"}.get(secE["idx"].layout()[0], ""),
+                    {"split": "k_lca_inlabel_split_E",
+                     "split6": "k_lca_inlabel_split6_E"}.get(secE["idx"].layout()[0], ""),
                     secE["q_rank"], secE["step_ms"] / 1e3, secE["clocks"]),
-                "note": "140 B/query assumes every gather is an HBM sector; the split "
-                        "layout's 128 MB node table is half L2-resident and lifts hit "
+                "note": "140 B/query assumes every gather is an HBM sector; the split6 "
+                        "layout's 96 MB node table is mostly L2-resident and lifts hit "
                         "L2, so the survey-model fraction can exceed 1"}
         del secE
 

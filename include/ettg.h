@@ -74,12 +74,16 @@ extern "C" {
  *   SPLIT_OWN 16-B {inlabel, ascendant, own-label lift record} + level:
  *           shallow-wide trees whose lifts go to the endpoint's own label
  *           (stars, caterpillars; chosen by a build-time query sample).
- * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split, 4 split_own). */
+ *   SPLIT6  the split record packed into 6 B (n < 2^24): a 16M-node table of
+ *           96 MB instead of 128 MB, which B200 gathers from ~1.3x faster.
+ * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split,
+ * 4 split_own, 5 split6). */
 #define ETTG_LAYOUT_WIDE 0x100u
 #define ETTG_LAYOUT_NARROW 0x200u
 #define ETTG_LAYOUT_COMPACT 0x400u
 #define ETTG_LAYOUT_SPLIT 0x800u
 #define ETTG_LAYOUT_SPLIT_OWN 0x1000u
+#define ETTG_LAYOUT_SPLIT6 0x2000u
 
 typedef struct ettg_lca ettg_lca;
 

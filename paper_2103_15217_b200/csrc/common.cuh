@@ -73,6 +73,25 @@ __device__ __forceinline__ uint2 ldg_rec(const uint2* p) {
   asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
+// 6-B record {inlabel:24, ascendant:24} at byte 6v of a 16-B aligned array:
+// one 16-B load, plus a 4-B load of the next 16 B when the record straddles
+// them (u16 index 6 or 7 within its 16 B: one record in four).
+__device__ __forceinline__ uint2 ldg_rec6(const uint16_t* base, u32 v) {
+  const u64 o = static_cast<u64>(v) * 6;
+  const char* a = reinterpret_cast<const char*>(base) + (o & ~u64(15));
+  const uint4 r = ldg_rec(reinterpret_cast<const uint4*>(a));
+  const u32 k = static_cast<u32>(o & 15) >> 1;  // u16 index of the record's first half-word
+  const u64 lo = r.x | (static_cast<u64>(r.y) << 32), hi = r.z | (static_cast<u64>(r.w) << 32);
+  u64 rec;
+  if (k < 4) {
+    rec = k ? (lo >> (16 * k)) | (hi << (64 - 16 * k)) : lo;
+  } else {
+    rec = hi >> (16 * (k - 4));
+    if (k >= 6) rec |= static_cast<u64>(ldg_u32(reinterpret_cast<const u32*>(a + 16)))
+                       << (16 * (8 - k));
+  }
+  return make_uint2(static_cast<u32>(rec) & 0xFFFFFFu, static_cast<u32>(rec >> 24) & 0xFFFFFFu);
+}
 // Streaming loads/stores (read once / write once).
 __device__ __forceinline__ uint2 ld_stream(const uint2* p) {
   uint2 r;

@@ -314,6 +314,17 @@ __global__ void k_pack_own(const uint2* __restrict__ nodes, const uint2* __restr
   }
 }
 
+// split6 record: {inlabel, ascendant} as 48 bits at byte 6v (n < 2^24).
+__global__ void k_pack6(const uint2* __restrict__ nodes, u32 n, uint16_t* __restrict__ nodes6) {
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint2 a = nodes[v];
+    const u64 rec = (a.x & 0xFFFFFFu) | (static_cast<u64>(a.y & 0xFFFFFFu) << 24);
+    nodes6[3 * static_cast<u64>(v)] = static_cast<uint16_t>(rec);
+    nodes6[3 * static_cast<u64>(v) + 1] = static_cast<uint16_t>(rec >> 16);
+    nodes6[3 * static_cast<u64>(v) + 2] = static_cast<uint16_t>(rec >> 32);
+  }
+}
+
 // ---- RMQ over the tour (block-sparse table, 32-step blocks) ---------------
 // Keys (level << 32 | node) make the minimum's low word the LCA itself.
 __global__ void k_rmq_block(const u64* __restrict__ key, u32 steps, u32 nb,
@@ -615,6 +626,49 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// inlabel_lca, split6 layout: the split record packed into 6 B (inlabel and
+// ascendant are < 2^24 when n < 2^24), so the gathered node table of a 16M
+// tree is 96 MB instead of 128 MB -- under the size at which B200's random
+// gather rate falls off (footprint sweep: 96 MB 151, 128 MB 113 G gathers/s).
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
+    k_lca_inlabel_split6(const uint16_t* __restrict__ nodes6, const u32* __restrict__ level,
+                        const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
+  u32 bad_any = 0;
+  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
+       i += static_cast<u64>(gridDim.x) * kQThreads) {
+    u32 x, y;
+    in.get(i, x, y);
+    const bool bad = x >= n || y >= n;
+    if (bad) x = y = 0;
+    const uint2 A = ldg_rec6(nodes6, x), B = ldg_rec6(nodes6, y);
+    bool lx = false, ly = false;
+    u32 wx = 0, wy = 0;
+    if (A.x != B.x) {
+      const int hbit = hb32(A.x ^ B.x);
+      const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
+      const int jb = tz32(common);
+      const u32 target = (A.x & ~((2u << jb) - 1u)) | (1u << jb);
+      const u32 lowmask = (1u << jb) - 1u;
+      if (A.x != target) {
+        const int kx = hb32(A.y & lowmask);
+        wx = min((A.x & ~((2u << kx) - 1u)) | (1u << kx), n);
+        lx = true;
+      }
+      if (B.x != target) {
+        const int ky = hb32(B.y & lowmask);
+        wy = min((B.x & ~((2u << ky) - 1u)) | (1u << ky), n);
+        ly = true;
+      }
+    }
+    const uint2 LX = lx ? ldg_rec(lab + wx) : make_uint2(x, ldg_u32(level + x));
+    const uint2 LY = ly ? ldg_rec(lab + wy) : make_uint2(y, ldg_u32(level + y));
+    out.put(i, bad ? kNone : (LX.y <= LY.y ? LX.x : LY.x));
+    bad_any |= bad;
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 // inlabel_lca, split_own layout: 16-B node record {inlabel, ascendant,
 // own-label lift record}; the level in its own array as in split.  A lift to
 // the endpoint's own label (the only ascendant bit below j is tz(inlabel))
@@ -845,7 +899,7 @@ __global__ void __launch_bounds__(kQThreads)
 using namespace ettg;
 
 constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSplit = 3,
-              kLayoutSplitOwn = 4;
+              kLayoutSplitOwn = 4, kLayoutSplit6 = 5;
 
 struct ettg_lca {
   int device = 0;
@@ -858,6 +912,7 @@ struct ettg_lca {
   char* mem = nullptr;
   uint4* node = nullptr;   // wide layout: {inlabel, ascendant, level, 0}
   uint2* nodes = nullptr;  // split layout: {inlabel, ascendant} ...
+  uint16_t* nodes6 = nullptr;  // split6 layout: the same record in 6 B ...
   u32* slevel = nullptr;   // ... + level per node
   uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
   u32* lasc = nullptr;     // ... + ascendant per label
@@ -891,7 +946,8 @@ struct ettg_lca {
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
       }
       if (full || layout == kLayoutSplit) nodes = c.take<uint2>(n);
-      if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn))
+      if (full || layout == kLayoutSplit6) nodes6 = c.take<uint16_t>(3 * static_cast<u64>(n) + 32);
+      if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn || layout == kLayoutSplit6))
         slevel = c.take<u32>(n);  // full builds query h->level
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
       if (full) {
@@ -1073,15 +1129,25 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
 //     bit budget fits, else narrow          16M path: compact 97.5 G q/s
 //   labels >= n/2 (shallow trees: almost every query lifts both endpoints,
 //     so the level array is rarely read): split    16M grasp(inf): 55.7;
+//     split6 (the same record in 6 B) when n >= L2/16  16M grasp(inf): 67.3;
 //     split_own when a build-time query sample sees > 50% own-label lifts
 //     (16M star: see profiles/r1_lca_layout.md)
 //   otherwise wide                              16M gamma=2: wide 24.3
+bool split6_enabled() {
+  const char* e = std::getenv("ETTG_SPLIT6");
+  return !e || std::atoi(e) != 0;
+}
+
 u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, double level_per_q,
                   int device, unsigned flags) {
   if (flags == ETTG_LAYOUT_WIDE) return kLayoutWide;
   if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
   if (flags == ETTG_LAYOUT_SPLIT) return kLayoutSplit;
   if (flags == ETTG_LAYOUT_SPLIT_OWN) return kLayoutSplitOwn;
+  if (flags == ETTG_LAYOUT_SPLIT6) {
+    if (n >= (1u << 24)) einval("split6 layout: needs n < 2^24 (24-bit inlabels)");
+    return kLayoutSplit6;
+  }
   if (flags == ETTG_LAYOUT_COMPACT) {
     if (!compact_fits) einval("compact layout: label index + in-path offset exceed 32 bits");
     return kLayoutCompact;
@@ -1099,7 +1165,13 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, double 
   // grasp(inf) 33.4/55.7, gamma=64 26.9/35.6, 16 20.0/21.4, 8 18.9/18.7,
   // 4 20.4/18.7, 2 24.3/20.2 (level reads per query 0, 0.06, ~0.2, 0.38, ..,
   // 0.99).
+  // split6 (6-B records) once the 8-B table would outgrow the fast-gather
+  // footprint: 16M trees, G q/s split/split6/wide: grasp(inf) 55.6/67.3/-,
+  // gamma=64 35.5/40.1/-, 16 21.4/23.2/-, 8 18.7/20.0/18.9, 4 -/20.0/20.4,
+  // 2 -/21.9/24.3; on 1M-4M trees (tables in L2) split is faster.
   if (own_frac > 0.5 && level_per_q < 0.25) return kLayoutSplitOwn;
+  const bool six = n < (1u << 24) && static_cast<u64>(n) * 8 > L2 / 2 && split6_enabled();
+  if (six && level_per_q < 0.45) return kLayoutSplit6;
   if (level_per_q < 0.25) return kLayoutSplit;
   return kLayoutWide;
 }
@@ -1110,7 +1182,7 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
   constexpr unsigned kLayoutMask = ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT |
-                                   ETTG_LAYOUT_SPLIT | ETTG_LAYOUT_SPLIT_OWN;
+                                   ETTG_LAYOUT_SPLIT | ETTG_LAYOUT_SPLIT_OWN | ETTG_LAYOUT_SPLIT6;
   const unsigned layout_flags = engines & kLayoutMask;
   engines &= ~kLayoutMask;
   if (layout_flags & (layout_flags - 1)) einval("conflicting layout flags");
@@ -1240,6 +1312,10 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_pack_own<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, h->lab, n, h->node);
     CK_LAUNCH();
   }
+  if (h->layout == kLayoutSplit6) {
+    k_pack6<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, n, h->nodes6);
+    CK_LAUNCH();
+  }
   if (h->layout == kLayoutCompact) {
     h->alloc_compact();
     scan_exclusive(LabelUsedIn{h->head}, ArrayOut{ws.up}, static_cast<u64>(n) + 1, ws.scan,
@@ -1300,6 +1376,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     else if (h->layout == kLayoutSplit)
       k_lca_inlabel_split<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab,
                                                                  h->n, in, out, q, err);
+    else if (h->layout == kLayoutSplit6)
+      k_lca_inlabel_split6<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab,
+                                                                  h->n, in, out, q, err);
     else if (h->layout == kLayoutNarrow)
       k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
                                                                   in, out, q, err);
@@ -1499,6 +1578,7 @@ struct BlobView {
   u32* node4 = nullptr;
   uint4* ltab = nullptr;
   uint2* nodes = nullptr;
+  uint16_t* nodes6 = nullptr;
   u32* slevel = nullptr;
   uint2* lab = nullptr;
   size_t bytes = 0;
@@ -1518,6 +1598,9 @@ BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
   } else if (layout == kLayoutCompact) {
     b.node4 = c.take<u32>(n);
     b.ltab = c.take<uint4>(labels);
+  } else if (layout == kLayoutSplit6) {
+    b.nodes6 = c.take<uint16_t>(3 * static_cast<u64>(n) + 32);
+    b.slevel = c.take<u32>(n);
   } else {
     b.nodes = c.take<uint2>(n);
     b.slevel = c.take<u32>(n);
@@ -1557,6 +1640,7 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
       CK(cudaMemcpyAsync(b.ltab, h->ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     if (b.nodes) CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes6) CK(cudaMemcpyAsync(b.nodes6, h->nodes6, n * 6, cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(b.slevel, h->slevel, n * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
@@ -1575,7 +1659,7 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     u32 head[8];
     CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (head[0] != kBlobMagic || head[1] > kLayoutSplitOwn || head[2] != static_cast<u32>(n) ||
+    if (head[0] != kBlobMagic || head[1] > kLayoutSplit6 || head[2] != static_cast<u32>(n) ||
         head[3] > 32 || head[4] > static_cast<u32>(n))
       einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
@@ -1606,6 +1690,7 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
       CK(cudaMemcpyAsync(h->ltab, b.ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     if (b.nodes) CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes6) CK(cudaMemcpyAsync(h->nodes6, b.nodes6, un * 6, cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(h->slevel, b.slevel, un * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));

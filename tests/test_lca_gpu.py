@@ -239,7 +239,7 @@ def test_naive_errors(ett):
 
 # ------------------------------------------------------- index layouts
 LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT"),
-           ("split", "LAYOUT_SPLIT"), ("split_own", "LAYOUT_SPLIT_OWN")]
+           ("split", "LAYOUT_SPLIT"), ("split_own", "LAYOUT_SPLIT_OWN"), ("split6", "LAYOUT_SPLIT6")]
 
 
 def _compact_bits(ref, t):
@@ -403,6 +403,30 @@ def test_layouts_random_shapes_vs_reference(ett, ref, name, flag):
         q = ett.sample_queries(t.n, 3000, it + 2)
         want = ref.lca("inlabel", t.parent, t.root, q)
         assert np.array_equal(ett.answer_batch(idx, q, len(q)), want), (it, n, idx.layout())
+
+
+def test_large_random_tree_picks_split6_and_replicates(ett):
+    """16M random tree: the 8-B split table would exceed half of L2, so auto
+    picks the 6-B records; a replica (export/attach) answers identically, and
+    the forced layout refuses n >= 2^24 (24-bit inlabels)."""
+    import torch
+    n = 16_000_000
+    t = ett.permute_labels(ett.grasp_tree(n, GRASP_INF, 1), 2)
+    idx = ett.inlabel_build(t)
+    assert idx.layout()[0] == "split6"
+    q = ett.sample_queries(n, 200_000, 3)
+    want = ett.answer_batch(ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.LAYOUT_WIDE),
+                            q, len(q))
+    assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)  # wide: pinned on the corpus
+    buf = torch.empty(idx.index_bytes(), dtype=torch.uint8, device="cuda:0")
+    idx.export_index(buf)
+    rep = ett.attach_index(buf, n)
+    assert rep.layout()[0] == "split6"
+    assert np.array_equal(ett.answer_batch(rep, q, len(q)), want)
+    big = 1 << 24
+    path = np.arange(-1, big - 1, dtype=np.int64)
+    with pytest.raises(ett.InvalidArgument, match="split6"):
+        ett.inlabel_build(ett.RootedTree(big, 0, path), engines=ett.ENGINE_INLABEL | ett.LAYOUT_SPLIT6)
 
 
 def test_star_picks_split_own_and_matches(ett, ref):
