@@ -54,7 +54,7 @@ if __name__ == "__main__":
     for mode in (sys.argv[1:] or ["wide", "split", "narrow", "compact", "auto"]):
         env = dict(os.environ, AB_CHILD="1", AB_MODE=mode.split(":")[0])
         if ":" in mode:
-            env["ETTG_CQ"] = env["ETTG_WQ"] = mode.split(":")[1]
+            env["ETTG_QGRID"] = mode.split(":")[1]
         if mode == "old":
             env["AB_LIB"] = os.path.join(ROOT, "tools", "_old", "libettg_head.so")
         r = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True)
