@@ -260,10 +260,42 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
         times.append(time.perf_counter() - t0)
     barrier()
     t = all_max(float(np.mean(times)), device)
+    link = host_link_bound(pin_pairs, torch.empty_like(pin_ans).pin_memory(), device)
     return {"value": q_total / t, "unit": "queries/s",
             "h2d_bytes_per_step": (hi - lo) * 16, "d2h_bytes_per_step": (hi - lo) * 8,
-            "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)"}, \
+            "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)",
+            "link_bound": {"ms": link, "frac": (link / (t * 1e3)) if link else None,
+                           "what": "the same H2D + D2H bytes as plain concurrent copies on two "
+                                   "streams (no kernel), CUDA events, best of 5; "
+                                   "profiles/r1_pcie_micro.md"}}, \
         pin_ans.numpy()
+
+
+def host_link_bound(pin_in, pin_out, device):
+    """Duplex copy time of one step's bytes: the floor of any e2e step."""
+    if pin_in.numel() == 0:
+        return None
+    d_in = torch.empty(pin_in.shape, dtype=pin_in.dtype, device=device)
+    d_out = torch.empty(pin_out.shape, dtype=pin_out.dtype, device=device)
+    s0, s1 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    best = None
+    for _ in range(6):
+        torch.cuda.synchronize(device)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(s0)
+        s1.wait_event(e0)
+        with torch.cuda.stream(s0):
+            d_in.copy_(pin_in, non_blocking=True)
+        with torch.cuda.stream(s1):
+            pin_out.copy_(d_out, non_blocking=True)
+        e1.record(s1)
+        s0.wait_event(e1)
+        e2.record(s0)
+        e2.synchronize()
+        ms = e0.elapsed_time(e2)
+        best = ms if best is None else min(best, ms)
+    del d_in, d_out
+    return best
 
 
 def cpu_lca_baseline(tree, pairs_host, reps=3):
