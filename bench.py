@@ -378,10 +378,27 @@ def bridges_section(ett, args, device, peak):
         t0 = time.perf_counter()
         call_host()
         ts.append(time.perf_counter() - t0)
+    # floor: the edge list's H2D then the mask's D2H (the mask needs every edge)
+    d_e = torch.empty(pin_e.shape, dtype=pin_e.dtype, device=device)
+    d_m = torch.empty(m, dtype=torch.uint8, device=device)
+    spare = torch.empty_like(pin_m).pin_memory()
+    copies = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d_e.copy_(pin_e, non_blocking=True)
+        spare.copy_(d_m, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        copies.append(e0.elapsed_time(e1))
+    del d_e, d_m, spare
     out["e2e"] = {"value": m / min(ts), "unit": "edges/s", "ms_per_step": 1e3 * min(ts),
                   "h2d_bytes_per_step": m * 16, "d2h_bytes_per_step": m,
                   "path": "ettg_bridges (pinned int64 host edge list -> host mask)",
-                  "parity": "bit-exact vs planted truth" if ok_h else "MISMATCH"}
+                  "parity": "bit-exact vs planted truth" if ok_h else "MISMATCH",
+                  "link_bound": {"ms": min(copies), "frac": min(copies) / (1e3 * min(ts)),
+                                 "what": "H2D of the edge list then D2H of the mask as plain "
+                                         "copies (no kernel), CUDA events, best of 3"}}
     del pin_e, pin_m
     if args.cpu_baseline:
         from oracle import oracle as orc
