@@ -697,8 +697,50 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   Trace tr("bridges", st);
   CK(cudaMemsetAsync(ws.words, 0, 16 * sizeof(u32), st));
   const uint2* edges;
+  bool hooked = false;  // spanning forest hooked while the edge list streamed in
   if (host_i64) {
-    if (m) {
+    // Host edge lists: the H2D copy dominates an end-to-end call (16 B per
+    // edge over PCIe vs ~35 ps of device work), and union-find hooking is
+    // incremental, so large inputs arrive in 16M-edge chunks on a copy stream
+    // while the previous chunk is converted and hooked (all its edges, no
+    // sampling: the sampled two-pass order only matters when hooking is on
+    // the critical path).  Any spanning forest gives the same bridge mask.
+    u32 kChunk = 16u << 20;
+    if (const char* e = std::getenv("ETTG_BR_CHUNK")) kChunk = std::max(1, std::atoi(e));
+    bool stream_hook = engine != ETTG_BRIDGES_CK && m > 2 * static_cast<u64>(kChunk);
+    if (const char* e = std::getenv("ETTG_BR_STREAM")) stream_hook &= std::atoi(e) != 0;
+    if (stream_hook) {
+      cudaStream_t cs;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaEvent_t arrived;
+      CK(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming));
+      struct CopyGuard {
+        cudaStream_t s;
+        cudaEvent_t e;
+        ~CopyGuard() {
+          cudaEventDestroy(e);
+          cudaStreamDestroy(s);
+        }
+      } cg{cs, arrived};
+      CK(cudaEventRecord(ev[1], st));  // words cleared before the first chunk lands
+      CK(cudaStreamWaitEvent(cs, ev[1], 0));
+      k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+      CK_LAUNCH();
+      const auto* src = static_cast<const longlong2*>(edges_in);
+      for (u32 lo = 0; lo < m; lo += kChunk) {
+        const u32 cnt = std::min(kChunk, m - lo);
+        CK(cudaMemcpyAsync(ws.e64 + lo, src + lo, static_cast<u64>(cnt) * 16,
+                           cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(arrived, cs));
+        CK(cudaStreamWaitEvent(st, arrived, 0));
+        k_edges_from_i64<<<std::min(g, blocks_for(cnt, 256)), 256, 0, st>>>(
+            ws.e64 + lo, cnt, n, ws.edges + lo, ws.words);
+        CK_LAUNCH();
+        launch_hook(ws.edges + lo, EdgeSubset{cnt, 1, 0}, n, ws.par, ws.tree + lo, ws.words, sms,
+                    st);
+      }
+      hooked = true;
+    } else if (m) {
       CK(cudaMemcpyAsync(ws.e64, edges_in, static_cast<u64>(m) * 16, cudaMemcpyHostToDevice, st));
       k_edges_from_i64<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.e64, m, n, ws.edges,
                                                                         ws.words);
@@ -734,9 +776,11 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     CK_LAUNCH();
   } else {
     // ---- spanning forest --------------------------------------------------
-    k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
-    CK_LAUNCH();
-    if (m) {
+    if (!hooked) {
+      k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+      CK_LAUNCH();
+    }
+    if (m && !hooked) {
       // Hook every 4th edge first, compress, then the rest (round-1 A/B on
       // config D: 3.28 vs 4.02 ms for one pass; ETTG_CC_SAMPLE overrides).
       u32 sample = 4;

@@ -118,6 +118,29 @@ def test_dev_path_errors_then_recovers(ett):
     assert rc == 0 and np.array_equal(mask, truth)
 
 
+@pytest.mark.parametrize("engine", ["tv", "hybrid"])
+def test_streamed_host_input_chunks(ett, ref, engine, monkeypatch):
+    """Large host edge lists are copied in chunks and hooked as they land;
+    small chunks (ETTG_BR_CHUNK) exercise every chunk boundary on the corpus."""
+    fn = {"tv": ett.tv_bridges, "hybrid": ett.hybrid_bridges}[engine]
+    for chunk in ("1", "7", "1000"):
+        monkeypatch.setenv("ETTG_BR_CHUNK", chunk)
+        for gi, (n, edges) in enumerate(bridge_corpus(ett)[:60]):
+            edges = np.asarray(edges, np.int64).reshape(-1, 2)
+            want = ref.bridges("dfs", n, edges)[0]
+            got = fn(ett.EdgeList(n, edges)).is_bridge
+            assert np.array_equal(got, want), (chunk, gi)
+    monkeypatch.setenv("ETTG_BR_CHUNK", "50000")
+    g, truth = ett.planted_bridge_graph(100_000, 600_000, 300, 4)
+    assert np.array_equal(fn(g).is_bridge, truth)
+    bad = g.edges.copy()
+    bad[599_000, 0] = g.n  # in the last chunk
+    with pytest.raises(ett.InvalidArgument, match="out of range"):
+        fn(ett.EdgeList(g.n, bad))
+    with pytest.raises(ett.InvalidArgument, match="disconnected"):
+        fn(ett.EdgeList(2 * g.n, np.concatenate([g.edges, g.edges + g.n])))
+
+
 def test_phase_times_named(ett):
     g, truth = ett.planted_bridge_graph(3000, 20_000, 40, 4)
     times = {}
