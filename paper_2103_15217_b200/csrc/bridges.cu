@@ -717,7 +717,8 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       struct CopyGuard {
         cudaStream_t s;
         cudaEvent_t e;
-        ~CopyGuard() {
+        ~CopyGuard() {  // copies land in the leased arena: never leave one in flight
+          cudaStreamSynchronize(s);
           cudaEventDestroy(e);
           cudaStreamDestroy(s);
         }
