@@ -696,6 +696,19 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   CK(cudaEventRecord(ev[0], st));
   Trace tr("bridges", st);
   CK(cudaMemsetAsync(ws.words, 0, 16 * sizeof(u32), st));
+  // Copies land in the leased arena: the copy stream is drained before the
+  // lease is released (it is declared after the lease, so destroyed first).
+  struct CopyGuard {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e = nullptr;
+    ~CopyGuard() {
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+      if (e) cudaEventDestroy(e);
+    }
+  } copy_guard;
   const uint2* edges;
   bool hooked = false;  // spanning forest hooked while the edge list streamed in
   if (host_i64) {
@@ -710,19 +723,10 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     bool stream_hook = engine != ETTG_BRIDGES_CK && m > 2 * static_cast<u64>(kChunk);
     if (const char* e = std::getenv("ETTG_BR_STREAM")) stream_hook &= std::atoi(e) != 0;
     if (stream_hook) {
-      cudaStream_t cs;
-      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      cudaEvent_t arrived;
-      CK(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming));
-      struct CopyGuard {
-        cudaStream_t s;
-        cudaEvent_t e;
-        ~CopyGuard() {  // copies land in the leased arena: never leave one in flight
-          cudaStreamSynchronize(s);
-          cudaEventDestroy(e);
-          cudaStreamDestroy(s);
-        }
-      } cg{cs, arrived};
+      CK(cudaStreamCreateWithFlags(&copy_guard.s, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&copy_guard.e, cudaEventDisableTiming));
+      cudaStream_t cs = copy_guard.s;
+      cudaEvent_t arrived = copy_guard.e;
       CK(cudaEventRecord(ev[1], st));  // words cleared before the first chunk lands
       CK(cudaStreamWaitEvent(cs, ev[1], 0));
       k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
