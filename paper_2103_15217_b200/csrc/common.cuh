@@ -73,24 +73,45 @@ __device__ __forceinline__ uint2 ldg_rec(const uint2* p) {
   asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
-// 6-B record {inlabel:24, ascendant:24} at byte 6v of a 16-B aligned array:
-// one 16-B load, plus a 4-B load of the next 16 B when the record straddles
-// them (u16 index 6 or 7 within its 16 B: one record in four).
-__device__ __forceinline__ uint2 ldg_rec6(const uint16_t* base, u32 v) {
-  const u64 o = static_cast<u64>(v) * 6;
-  const char* a = reinterpret_cast<const char*>(base) + (o & ~u64(15));
-  const uint4 r = ldg_rec(reinterpret_cast<const uint4*>(a));
-  const u32 k = static_cast<u32>(o & 15) >> 1;  // u16 index of the record's first half-word
-  const u64 lo = r.x | (static_cast<u64>(r.y) << 32), hi = r.z | (static_cast<u64>(r.w) << 32);
-  u64 rec;
-  if (k < 4) {
-    rec = k ? (lo >> (16 * k)) | (hi << (64 - 16 * k)) : lo;
-  } else {
-    rec = hi >> (16 * (k - 4));
-    if (k >= 6) rec |= static_cast<u64>(ldg_u32(reinterpret_cast<const u32*>(a + 16)))
-                       << (16 * (8 - k));
-  }
+// 6-B records {inlabel:24, ascendant:24}, five per 32-B sector (bytes 6k of
+// sector v / 5, k = v % 5; 2 bytes of padding): one 256-bit load
+// (LDG.E.256 on sm_100a) reads a whole sector, so a record never costs a
+// second load or sector.
+constexpr u32 kRec6PerSector = 5;
+__host__ __device__ __forceinline__ u64 rec6_bytes(u64 n) {
+  return (n + kRec6PerSector - 1) / kRec6PerSector * 32;
+}
+struct Sector32 {
+  u32 w[8];
+};
+// Not volatile: the two endpoint gathers of a query must be free to issue
+// back to back (a volatile asm pinned them in order with one register set).
+__device__ __forceinline__ Sector32 ldg_sector(const uint32_t* p) {
+  Sector32 r;
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+        "=r"(r.w[6]), "=r"(r.w[7])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ u32 rec6_sector(u32 v) { return __umulhi(v, 0xCCCCCCCDu) >> 2; }
+// record k = v - 5 * sector starts at u16 3k: words (w[3k/2], w[3k/2 + 1]),
+// shifted right by 16 bits when k is odd
+__device__ __forceinline__ uint2 rec6_extract(const Sector32& x, u32 k) {
+  const u32 p = k == 0 ? x.w[0] : k == 1 ? x.w[1] : k == 2 ? x.w[3] : k == 3 ? x.w[4] : x.w[6];
+  const u32 r = k == 0 ? x.w[1] : k == 1 ? x.w[2] : k == 2 ? x.w[4] : k == 3 ? x.w[5] : x.w[7];
+  const u64 rec = ((static_cast<u64>(r) << 32) | p) >> (16 * (k & 1));
   return make_uint2(static_cast<u32>(rec) & 0xFFFFFFu, static_cast<u32>(rec >> 24) & 0xFFFFFFu);
+}
+// Both endpoint records of a query: the two sector loads issue before either
+// is unpacked.
+__device__ __forceinline__ void ldg_rec6_pair(const uint32_t* base, u32 x, u32 y, uint2& A,
+                                              uint2& B) {
+  const u32 sx = rec6_sector(x), sy = rec6_sector(y);
+  const Sector32 a = ldg_sector(base + 8 * static_cast<u64>(sx));
+  const Sector32 b = ldg_sector(base + 8 * static_cast<u64>(sy));
+  A = rec6_extract(a, x - 5 * sx);
+  B = rec6_extract(b, y - 5 * sy);
 }
 // Streaming loads/stores (read once / write once).
 __device__ __forceinline__ uint2 ld_stream(const uint2* p) {

@@ -315,13 +315,16 @@ __global__ void k_pack_own(const uint2* __restrict__ nodes, const uint2* __restr
 }
 
 // split6 record: {inlabel, ascendant} as 48 bits at byte 6v (n < 2^24).
-__global__ void k_pack6(const uint2* __restrict__ nodes, u32 n, uint16_t* __restrict__ nodes6) {
+__global__ void k_pack6(const uint2* __restrict__ nodes, u32 n, uint32_t* __restrict__ nodes6) {
+  uint16_t* h = reinterpret_cast<uint16_t*>(nodes6);
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const uint2 a = nodes[v];
     const u64 rec = (a.x & 0xFFFFFFu) | (static_cast<u64>(a.y & 0xFFFFFFu) << 24);
-    nodes6[3 * static_cast<u64>(v)] = static_cast<uint16_t>(rec);
-    nodes6[3 * static_cast<u64>(v) + 1] = static_cast<uint16_t>(rec >> 16);
-    nodes6[3 * static_cast<u64>(v) + 2] = static_cast<uint16_t>(rec >> 32);
+    const u32 s = v / kRec6PerSector, k = v % kRec6PerSector;
+    const u64 o = 16 * static_cast<u64>(s) + 3 * k;  // u16 index
+    h[o] = static_cast<uint16_t>(rec);
+    h[o + 1] = static_cast<uint16_t>(rec >> 16);
+    h[o + 2] = static_cast<uint16_t>(rec >> 32);
   }
 }
 
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // gather rate falls off (footprint sweep: 96 MB 151, 128 MB 113 G gathers/s).
 template <class In, class Out>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
-    k_lca_inlabel_split6(const uint16_t* __restrict__ nodes6, const u32* __restrict__ level,
+    k_lca_inlabel_split6(const uint32_t* __restrict__ nodes6, const u32* __restrict__ level,
                         const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
   u32 bad_any = 0;
   for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
@@ -641,7 +644,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     in.get(i, x, y);
     const bool bad = x >= n || y >= n;
     if (bad) x = y = 0;
-    const uint2 A = ldg_rec6(nodes6, x), B = ldg_rec6(nodes6, y);
+    uint2 A, B;
+    ldg_rec6_pair(nodes6, x, y, A, B);
     bool lx = false, ly = false;
     u32 wx = 0, wy = 0;
     if (A.x != B.x) {
@@ -912,7 +916,7 @@ struct ettg_lca {
   char* mem = nullptr;
   uint4* node = nullptr;   // wide layout: {inlabel, ascendant, level, 0}
   uint2* nodes = nullptr;  // split layout: {inlabel, ascendant} ...
-  uint16_t* nodes6 = nullptr;  // split6 layout: the same record in 6 B ...
+  uint32_t* nodes6 = nullptr;  // split6 layout: the same record in 6 B ...
   u32* slevel = nullptr;   // ... + level per node
   uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
   u32* lasc = nullptr;     // ... + ascendant per label
@@ -946,7 +950,7 @@ struct ettg_lca {
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
       }
       if (full || layout == kLayoutSplit) nodes = c.take<uint2>(n);
-      if (full || layout == kLayoutSplit6) nodes6 = c.take<uint16_t>(3 * static_cast<u64>(n) + 32);
+      if (full || layout == kLayoutSplit6) nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
       if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn || layout == kLayoutSplit6))
         slevel = c.take<u32>(n);  // full builds query h->level
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
@@ -1587,7 +1591,7 @@ struct BlobView {
   u32* node4 = nullptr;
   uint4* ltab = nullptr;
   uint2* nodes = nullptr;
-  uint16_t* nodes6 = nullptr;
+  uint32_t* nodes6 = nullptr;
   u32* slevel = nullptr;
   uint2* lab = nullptr;
   size_t bytes = 0;
@@ -1608,7 +1612,7 @@ BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
     b.node4 = c.take<u32>(n);
     b.ltab = c.take<uint4>(labels);
   } else if (layout == kLayoutSplit6) {
-    b.nodes6 = c.take<uint16_t>(3 * static_cast<u64>(n) + 32);
+    b.nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
     b.slevel = c.take<u32>(n);
   } else {
     b.nodes = c.take<uint2>(n);
@@ -1649,7 +1653,8 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
       CK(cudaMemcpyAsync(b.ltab, h->ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     if (b.nodes) CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
-    if (b.nodes6) CK(cudaMemcpyAsync(b.nodes6, h->nodes6, n * 6, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes6)
+      CK(cudaMemcpyAsync(b.nodes6, h->nodes6, rec6_bytes(n), cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(b.slevel, h->slevel, n * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
@@ -1699,7 +1704,8 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
       CK(cudaMemcpyAsync(h->ltab, b.ltab, h->labels * 16, cudaMemcpyDeviceToDevice, st));
     }
     if (b.nodes) CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
-    if (b.nodes6) CK(cudaMemcpyAsync(h->nodes6, b.nodes6, un * 6, cudaMemcpyDeviceToDevice, st));
+    if (b.nodes6)
+      CK(cudaMemcpyAsync(h->nodes6, b.nodes6, rec6_bytes(un), cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(h->slevel, b.slevel, un * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));
