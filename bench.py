@@ -54,7 +54,8 @@ def peaks():
 # (compact) 263.8, 96 MB (split6) 150.7, 128 MB (narrow, split) 113.1, 256 MB
 # (wide) 71.6 G gathers/s.
 L2_GATHER_CEILING = {"compact": 263.8, "narrow": 113.1, "split": 113.1, "wide": 71.6,
-                     "split_own": 71.6, "split6": 150.7}
+                     "split_own": 71.6, "split6": 150.7, "wide9": 92.0}  # wide9: 171 MB,
+# between the 128 MB (113.1) and 192 MB (83.7) points
 
 
 def ncu_traffic(kernel_key: str):
@@ -622,7 +623,7 @@ def main():
         kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
                  "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split",
                  "split_own": "k_lca_inlabel_split_own",
-                 "split6": "k_lca_inlabel_split6"}[layout]
+                 "split6": "k_lca_inlabel_split6", "wide9": "k_lca_inlabel"}[layout]
         q_r = sec["q_rank"]
         if layout == "compact":
             # 12 B streamed + the index read once per launch (node words + label

@@ -76,14 +76,17 @@ extern "C" {
  *           (stars, caterpillars; chosen by a build-time query sample).
  *   SPLIT6  the split record packed into 6 B (n < 2^24): a 16M-node table of
  *           96 MB instead of 128 MB, which B200 gathers from ~1.3x faster.
+ *   WIDE9   the wide record packed into 9 B, three per 32-B sector (n < 2^24):
+ *           171 MB instead of 256 MB at 16M nodes (middle-depth trees).
  * ettg_lca_layout() reports the choice (0 wide, 1 narrow, 2 compact, 3 split,
- * 4 split_own, 5 split6). */
+ * 4 split_own, 5 split6, 6 wide9). */
 #define ETTG_LAYOUT_WIDE 0x100u
 #define ETTG_LAYOUT_NARROW 0x200u
 #define ETTG_LAYOUT_COMPACT 0x400u
 #define ETTG_LAYOUT_SPLIT 0x800u
 #define ETTG_LAYOUT_SPLIT_OWN 0x1000u
 #define ETTG_LAYOUT_SPLIT6 0x2000u
+#define ETTG_LAYOUT_WIDE9 0x4000u
 
 typedef struct ettg_lca ettg_lca;
 

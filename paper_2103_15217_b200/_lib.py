@@ -22,6 +22,7 @@ LAYOUT_COMPACT = 0x400
 LAYOUT_SPLIT = 0x800
 LAYOUT_SPLIT_OWN = 0x1000
 LAYOUT_SPLIT6 = 0x2000
+LAYOUT_WIDE9 = 0x4000
 REDUCE_MIN, REDUCE_MAX, REDUCE_SUM = range(3)  # ettg_segmented_reduce ops
 
 _lock = threading.Lock()

@@ -113,6 +113,24 @@ __device__ __forceinline__ void ldg_rec6_pair(const uint32_t* base, u32 x, u32 y
   A = rec6_extract(a, x - 5 * sx);
   B = rec6_extract(b, y - 5 * sy);
 }
+// 9-B records {inlabel:24, ascendant:24, level:24}, three per 32-B sector
+// (bits 72k of sector v / 3; 5 bytes of padding), one 256-bit load each.
+constexpr u32 kRec9PerSector = 3;
+__host__ __device__ __forceinline__ u64 rec9_bytes(u64 n) {
+  return (n + kRec9PerSector - 1) / kRec9PerSector * 32;
+}
+__device__ __forceinline__ u32 rec9_sector(u32 v) { return __umulhi(v, 0xAAAAAAABu) >> 1; }
+__device__ __forceinline__ uint4 rec9_extract(const Sector32& x, u32 k) {
+  // record k starts at bit 72k = word 2k, bit 8k
+  const u32 v0 = k == 0 ? x.w[0] : k == 1 ? x.w[2] : x.w[4];
+  const u32 v1 = k == 0 ? x.w[1] : k == 1 ? x.w[3] : x.w[5];
+  const u32 v2 = k == 0 ? x.w[2] : k == 1 ? x.w[4] : x.w[6];
+  const u32 sh = 8 * k;
+  const u64 a = (static_cast<u64>(v1) << 32) | v0, b = (static_cast<u64>(v2) << 32) | v1;
+  return make_uint4(static_cast<u32>(a >> sh) & 0xFFFFFFu,
+                    static_cast<u32>(a >> (sh + 24)) & 0xFFFFFFu,
+                    static_cast<u32>(b >> (sh + 16)) & 0xFFFFFFu, 0u);
+}
 // Streaming loads/stores (read once / write once).
 __device__ __forceinline__ uint2 ld_stream(const uint2* p) {
   uint2 r;

@@ -328,6 +328,35 @@ __global__ void k_pack6(const uint2* __restrict__ nodes, u32 n, uint32_t* __rest
   }
 }
 
+// wide9 record: {inlabel, ascendant, level} as 72 bits at bit 72k of sector
+// v / 3, k = v % 3 (n < 2^24: every field fits 24 bits).  One thread per sector.
+__device__ __forceinline__ void put_bits(u64 (&q)[4], u32 off, u64 val) {
+  const u32 i = off / 64, sh = off % 64;
+  q[i] |= val << sh;
+  if (sh > 40) q[i + 1] |= val >> (64 - sh);  // 24-bit fields
+}
+__global__ void k_pack9(const uint4* __restrict__ node, u32 n, uint32_t* __restrict__ nodes9) {
+  const u32 sectors = (n + kRec9PerSector - 1) / kRec9PerSector;
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < sectors; s += gridDim.x * blockDim.x) {
+    u64 q[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (u32 k = 0; k < kRec9PerSector; ++k) {
+      const u32 v = s * kRec9PerSector + k;
+      if (v < n) {
+        const uint4 r = node[v];
+        put_bits(q, 72 * k, r.x & 0xFFFFFFu);
+        put_bits(q, 72 * k + 24, r.y & 0xFFFFFFu);
+        put_bits(q, 72 * k + 48, r.z & 0xFFFFFFu);
+      }
+    }
+    uint4* o = reinterpret_cast<uint4*>(nodes9 + 8 * static_cast<u64>(s));
+    o[0] = make_uint4(static_cast<u32>(q[0]), static_cast<u32>(q[0] >> 32),
+                      static_cast<u32>(q[1]), static_cast<u32>(q[1] >> 32));
+    o[1] = make_uint4(static_cast<u32>(q[2]), static_cast<u32>(q[2] >> 32),
+                      static_cast<u32>(q[3]), static_cast<u32>(q[3] >> 32));
+  }
+}
+
 // ---- RMQ over the tour (block-sparse table, 32-step blocks) ---------------
 // Keys (level << 32 | node) make the minimum's low word the LCA itself.
 __global__ void k_rmq_block(const u64* __restrict__ key, u32 steps, u32 nb,
@@ -434,12 +463,33 @@ constexpr int kQPer = 1;          // queries per thread per loop trip
 constexpr int kQMinBlocks = 8;    // resident CTAs per SM (caps registers at 32)
 constexpr int kQGridPerSM = 64;   // grid = min(ceil(q / 256), 64 x SMs), grid-stride
 
-// inlabel_lca (core/src/lca.cpp:84-109), four queries in flight per thread:
-// two 16-B node-record gathers, then at most two 8-B label-record gathers.
-template <class In, class Out>
+// Node-record sources of the wide kernel: {inlabel, ascendant, level, -}.
+struct WideNodes {  // 16-B records
+  const uint4* p;
+  __device__ __forceinline__ void pair(u32 x, u32 y, uint4& A, uint4& B) const {
+    A = ldg_rec(p + x);
+    B = ldg_rec(p + y);
+  }
+};
+// wide9: the same record in 9 B (n < 2^24), three per 32-B sector read with
+// one 256-bit load: a 16M-node table of 171 MB instead of 256 MB.
+struct Wide9Nodes {
+  const uint32_t* p;
+  __device__ __forceinline__ void pair(u32 x, u32 y, uint4& A, uint4& B) const {
+    const u32 sx = rec9_sector(x), sy = rec9_sector(y);
+    const Sector32 a = ldg_sector(p + 8 * static_cast<u64>(sx));
+    const Sector32 b = ldg_sector(p + 8 * static_cast<u64>(sy));
+    A = rec9_extract(a, x - 3 * sx);
+    B = rec9_extract(b, y - 3 * sy);
+  }
+};
+
+// inlabel_lca (core/src/lca.cpp:84-109): two node-record gathers, then at
+// most two 8-B label-record gathers.
+template <class In, class Out, class Nodes = WideNodes>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
-    k_lca_inlabel(const uint4* __restrict__ node, const uint2* __restrict__ lab, u32 n, In in,
-                  Out out, u64 q, u32* err) {
+    k_lca_inlabel(Nodes node, const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q,
+                  u32* err) {
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
   u32 bad_any = 0;
   for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
@@ -458,8 +508,7 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     uint4 A[kQPer], B[kQPer];
 #pragma unroll
     for (int j = 0; j < kQPer; ++j) {
-      A[j] = ldg_rec(node + x[j]);
-      B[j] = ldg_rec(node + y[j]);
+      node.pair(x[j], y[j], A[j], B[j]);
     }
     u32 ans[kQPer], wx[kQPer], wy[kQPer];
     bool lx[kQPer], ly[kQPer];
@@ -903,7 +952,7 @@ __global__ void __launch_bounds__(kQThreads)
 using namespace ettg;
 
 constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSplit = 3,
-              kLayoutSplitOwn = 4, kLayoutSplit6 = 5;
+              kLayoutSplitOwn = 4, kLayoutSplit6 = 5, kLayoutWide9 = 6;
 
 struct ettg_lca {
   int device = 0;
@@ -917,6 +966,7 @@ struct ettg_lca {
   uint4* node = nullptr;   // wide layout: {inlabel, ascendant, level, 0}
   uint2* nodes = nullptr;  // split layout: {inlabel, ascendant} ...
   uint32_t* nodes6 = nullptr;  // split6 layout: the same record in 6 B ...
+  uint32_t* nodes9 = nullptr;  // wide9 layout: the wide record in 9 B (3 per sector)
   u32* slevel = nullptr;   // ... + level per node
   uint2* node8 = nullptr;  // narrow layout: {inlabel, level} ...
   u32* lasc = nullptr;     // ... + ascendant per label
@@ -951,6 +1001,7 @@ struct ettg_lca {
       }
       if (full || layout == kLayoutSplit) nodes = c.take<uint2>(n);
       if (full || layout == kLayoutSplit6) nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
+      if (full || layout == kLayoutWide9) nodes9 = c.take<uint32_t>(rec9_bytes(n) / 4);
       if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn || layout == kLayoutSplit6))
         slevel = c.take<u32>(n);  // full builds query h->level
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
@@ -1148,6 +1199,10 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, double 
   if (flags == ETTG_LAYOUT_NARROW) return kLayoutNarrow;
   if (flags == ETTG_LAYOUT_SPLIT) return kLayoutSplit;
   if (flags == ETTG_LAYOUT_SPLIT_OWN) return kLayoutSplitOwn;
+  if (flags == ETTG_LAYOUT_WIDE9) {
+    if (n >= (1u << 24)) einval("wide9 layout: needs n < 2^24 (24-bit fields)");
+    return kLayoutWide9;
+  }
   if (flags == ETTG_LAYOUT_SPLIT6) {
     if (n >= (1u << 24)) einval("split6 layout: needs n < 2^24 (24-bit inlabels)");
     return kLayoutSplit6;
@@ -1169,15 +1224,19 @@ u32 choose_layout(u32 n, u64 labels, bool compact_fits, double own_frac, double 
   // grasp(inf) 33.4/55.7, gamma=64 26.9/35.6, 16 20.0/21.4, 8 18.9/18.7,
   // 4 20.4/18.7, 2 24.3/20.2 (level reads per query 0, 0.06, ~0.2, 0.38, ..,
   // 0.99).
-  // split6 (6-B records) once the 8-B table would outgrow the fast-gather
-  // footprint: 16M trees, G q/s split/split6/wide: grasp(inf) 55.6/67.3/-,
-  // gamma=64 35.5/40.1/-, 16 21.4/23.2/-, 8 18.7/20.0/18.9, 4 -/20.0/20.4,
-  // 2 -/21.9/24.3; on 1M-4M trees (tables in L2) split is faster.
+  // Packed records (n < 2^24) once the unpacked table would outgrow the
+  // fast-gather footprint: split6 (6 B) for shallow trees, wide9 (9 B, level
+  // inline) once a level is read for >= 0.3 endpoints per query.  16M trees,
+  // G q/s split / split6 / wide / wide9: grasp(inf) 55.6/67.3/-/42.5,
+  // gamma=64 35.5/40.1/-/31.8, 16 21.4/23.2/-/22.2, 8 18.7/20.0/18.9/20.7,
+  // 4 -/20.0/20.4/22.8, 2 -/21.9/24.3/28.1; on 1M-4M trees (tables in L2) the
+  // unpacked records are as fast or faster.
   if (own_frac > 0.5 && level_per_q < 0.25) return kLayoutSplitOwn;
   const bool six = n < (1u << 24) && static_cast<u64>(n) * 8 > L2 / 2 && split6_enabled();
-  if (six && level_per_q < 0.45) return kLayoutSplit6;
+  if (six && level_per_q < 0.3) return kLayoutSplit6;
   if (level_per_q < 0.25) return kLayoutSplit;
-  return kLayoutWide;
+  const bool nine = n < (1u << 24) && static_cast<u64>(n) * 16 > L2 / 2 && split6_enabled();
+  return nine ? kLayoutWide9 : kLayoutWide;
 }
 
 ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n64,
@@ -1186,7 +1245,8 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   if (n64 >= (int64_t(1) << 31)) einval("tree too large for the 32-bit device index (n >= 2^31)");
   if (root64 < 0 || root64 >= n64) einval("root has no kNone parent entry");
   constexpr unsigned kLayoutMask = ETTG_LAYOUT_WIDE | ETTG_LAYOUT_NARROW | ETTG_LAYOUT_COMPACT |
-                                   ETTG_LAYOUT_SPLIT | ETTG_LAYOUT_SPLIT_OWN | ETTG_LAYOUT_SPLIT6;
+                                   ETTG_LAYOUT_SPLIT | ETTG_LAYOUT_SPLIT_OWN | ETTG_LAYOUT_SPLIT6 |
+                                   ETTG_LAYOUT_WIDE9;
   const unsigned layout_flags = engines & kLayoutMask;
   engines &= ~kLayoutMask;
   if (layout_flags & (layout_flags - 1)) einval("conflicting layout flags");
@@ -1316,6 +1376,10 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
     k_pack_own<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, h->lab, n, h->node);
     CK_LAUNCH();
   }
+  if (h->layout == kLayoutWide9) {
+    k_pack9<<<std::min(g, blocks_for(n / 3 + 1, 256)), 256, 0, st>>>(h->node, n, h->nodes9);
+    CK_LAUNCH();
+  }
   if (h->layout == kLayoutSplit6) {
     k_pack6<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->nodes, n, h->nodes6);
     CK_LAUNCH();
@@ -1389,6 +1453,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     else if (h->layout == kLayoutSplit)
       k_lca_inlabel_split<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab,
                                                                  h->n, in, out, q, err);
+    else if (h->layout == kLayoutWide9)
+      k_lca_inlabel<In, Out, Wide9Nodes><<<blocks, kQThreads, 0, st>>>(
+          Wide9Nodes{h->nodes9}, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit6)
       k_lca_inlabel_split6<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab,
                                                                   h->n, in, out, q, err);
@@ -1396,7 +1463,7 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
       k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
                                                                   in, out, q, err);
     else
-      k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->lab, h->n, in, out, q,
+      k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(WideNodes{h->node}, h->lab, h->n, in, out, q,
                                                            err);
   }
   CK_LAUNCH();
@@ -1592,6 +1659,7 @@ struct BlobView {
   uint4* ltab = nullptr;
   uint2* nodes = nullptr;
   uint32_t* nodes6 = nullptr;
+  uint32_t* nodes9 = nullptr;
   u32* slevel = nullptr;
   uint2* lab = nullptr;
   size_t bytes = 0;
@@ -1611,6 +1679,8 @@ BlobView blob_view(char* base, u32 n, u32 layout, u64 labels) {
   } else if (layout == kLayoutCompact) {
     b.node4 = c.take<u32>(n);
     b.ltab = c.take<uint4>(labels);
+  } else if (layout == kLayoutWide9) {
+    b.nodes9 = c.take<uint32_t>(rec9_bytes(n) / 4);
   } else if (layout == kLayoutSplit6) {
     b.nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
     b.slevel = c.take<u32>(n);
@@ -1655,6 +1725,8 @@ int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream) {
     if (b.nodes) CK(cudaMemcpyAsync(b.nodes, h->nodes, n * 8, cudaMemcpyDeviceToDevice, st));
     if (b.nodes6)
       CK(cudaMemcpyAsync(b.nodes6, h->nodes6, rec6_bytes(n), cudaMemcpyDeviceToDevice, st));
+    if (b.nodes9)
+      CK(cudaMemcpyAsync(b.nodes9, h->nodes9, rec9_bytes(n), cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(b.slevel, h->slevel, n * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(b.lab, h->lab, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
@@ -1673,7 +1745,7 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     u32 head[8];
     CK(cudaMemcpyAsync(head, d_src, sizeof head, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (head[0] != kBlobMagic || head[1] > kLayoutSplit6 || head[2] != static_cast<u32>(n) ||
+    if (head[0] != kBlobMagic || head[1] > kLayoutWide9 || head[2] != static_cast<u32>(n) ||
         head[3] > 32 || head[4] > static_cast<u32>(n))
       einval("not an exported inlabel index of this size");
     auto h = std::make_unique<ettg_lca>();
@@ -1706,6 +1778,8 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device, void* st
     if (b.nodes) CK(cudaMemcpyAsync(h->nodes, b.nodes, un * 8, cudaMemcpyDeviceToDevice, st));
     if (b.nodes6)
       CK(cudaMemcpyAsync(h->nodes6, b.nodes6, rec6_bytes(un), cudaMemcpyDeviceToDevice, st));
+    if (b.nodes9)
+      CK(cudaMemcpyAsync(h->nodes9, b.nodes9, rec9_bytes(un), cudaMemcpyDeviceToDevice, st));
     if (b.slevel)
       CK(cudaMemcpyAsync(h->slevel, b.slevel, un * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(h->lab, b.lab, (un + 1) * 8, cudaMemcpyDeviceToDevice, st));

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (ENGINE_INLABEL, ENGINE_NAIVE, ENGINE_RMQ, LAYOUT_COMPACT, LAYOUT_NARROW, LAYOUT_SPLIT,
-                   LAYOUT_SPLIT_OWN, LAYOUT_SPLIT6,
+                   LAYOUT_SPLIT_OWN, LAYOUT_SPLIT6, LAYOUT_WIDE9,
                    LAYOUT_WIDE,
                    InvalidArgument, OutOfRange, ParseError, check, lib, ptr)
 
@@ -123,7 +123,8 @@ class _LcaHandle:
         """("wide" | "narrow", number of inlabel paths) of the inlabel engine."""
         lay, labels = C.c_int(), C.c_int64()
         check(lib().ettg_lca_layout(self._h, C.byref(lay), C.byref(labels)))
-        return ("wide", "narrow", "compact", "split", "split_own", "split6")[lay.value], labels.value
+        return ("wide", "narrow", "compact", "split", "split_own", "split6",
+                "wide9")[lay.value], labels.value
 
     def index_bytes(self) -> int:
         v = C.c_int64()

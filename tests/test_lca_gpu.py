@@ -239,7 +239,8 @@ def test_naive_errors(ett):
 
 # ------------------------------------------------------- index layouts
 LAYOUTS = [("wide", "LAYOUT_WIDE"), ("narrow", "LAYOUT_NARROW"), ("compact", "LAYOUT_COMPACT"),
-           ("split", "LAYOUT_SPLIT"), ("split_own", "LAYOUT_SPLIT_OWN"), ("split6", "LAYOUT_SPLIT6")]
+           ("split", "LAYOUT_SPLIT"), ("split_own", "LAYOUT_SPLIT_OWN"), ("split6", "LAYOUT_SPLIT6"),
+           ("wide9", "LAYOUT_WIDE9")]
 
 
 def _compact_bits(ref, t):
@@ -287,10 +288,10 @@ def test_forced_layout_medium_trees(ett, ref, name, flag, gamma):
 
 def test_auto_layout_choice_and_replicas(ett):
     """Auto picks compact for a long path (few labels), split for a random tree,
-    wide in between;
+    wide9 in between (6M nodes: the 16-B table would exceed half of L2);
     forced layouts and replicas of each answer identically on the device."""
     import torch
-    for gamma, expect in [(1, "compact"), (GRASP_INF, "split"), (2, "wide")]:
+    for gamma, expect in [(1, "compact"), (GRASP_INF, "split"), (2, "wide9")]:
         t = ett.permute_labels(ett.grasp_tree(6_000_000, gamma, 1), 2)
         idx = ett.inlabel_build(t)
         lay, labels = idx.layout()

@@ -25,7 +25,7 @@ def child():
         n = {"A_1M": 1_000_000, "path_1M": 1_000_000, "g2_1M": 1_000_000, "rand_4M": 4_000_000,
              "path_4M": 4_000_000}.get(name, 16_000_000)
         t = ett.permute_labels(ett.grasp_tree(n, gamma, 1), 2)
-        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW, "compact": ett.LAYOUT_COMPACT, "split": ett.LAYOUT_SPLIT, "split_own": ett.LAYOUT_SPLIT_OWN, "split6": ett.LAYOUT_SPLIT6}.get(os.environ.get("AB_MODE"), 0)
+        flags = {"wide": ett.LAYOUT_WIDE, "narrow": ett.LAYOUT_NARROW, "compact": ett.LAYOUT_COMPACT, "split": ett.LAYOUT_SPLIT, "split_own": ett.LAYOUT_SPLIT_OWN, "split6": ett.LAYOUT_SPLIT6, "wide9": ett.LAYOUT_WIDE9}.get(os.environ.get("AB_MODE"), 0)
         try:
             idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | flags)
         except ett.InvalidArgument as e:
