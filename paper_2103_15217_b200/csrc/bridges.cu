@@ -734,8 +734,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       const auto* src = static_cast<const longlong2*>(edges_in);
       for (u32 lo = 0; lo < m; lo += kChunk) {
         const u32 cnt = std::min(kChunk, m - lo);
-        CK(cudaMemcpyAsync(ws.e64 + lo, src + lo, static_cast<u64>(cnt) * 16,
-                           cudaMemcpyHostToDevice, cs));
+        copy_h2d(ws.e64 + lo, src + lo, static_cast<u64>(cnt) * 16, device, cs);
         CK(cudaEventRecord(arrived, cs));
         CK(cudaStreamWaitEvent(st, arrived, 0));
         k_edges_from_i64<<<std::min(g, blocks_for(cnt, 256)), 256, 0, st>>>(
@@ -746,7 +745,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       }
       hooked = true;
     } else if (m) {
-      CK(cudaMemcpyAsync(ws.e64, edges_in, static_cast<u64>(m) * 16, cudaMemcpyHostToDevice, st));
+      copy_h2d(ws.e64, edges_in, static_cast<u64>(m) * 16, device, st);
       k_edges_from_i64<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.e64, m, n, ws.edges,
                                                                         ws.words);
       CK_LAUNCH();
@@ -887,7 +886,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
     tr.mark("marking");
   }
   CK(cudaEventRecord(ev[3], st));
-  if (h_mask && m) CK(cudaMemcpyAsync(h_mask, d_mask, m, cudaMemcpyDeviceToHost, st));
+  if (h_mask && m) copy_d2h(h_mask, d_mask, m, device, st);
   if (n > 1 && engine != ETTG_BRIDGES_CK)
     CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4, cudaMemcpyDeviceToHost, st));
   u32 w[2] = {0, n - 1};

@@ -1,4 +1,6 @@
 // C-ABI plumbing: error state, device scope, scratch arena, primitives.
+#include <algorithm>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -95,6 +97,163 @@ Lease::~Lease() {
   Arena& a = arena_for(device_);
   cudaEventRecord(a.last, stream_);
   a.mu.unlock();
+}
+
+// ---- pinned staging --------------------------------------------------------
+namespace {
+constexpr size_t kStageChunk = size_t(16) << 20;
+struct Stage {
+  std::mutex mu;
+  char* buf[2] = {nullptr, nullptr};  // pinned, kStageChunk each
+  cudaEvent_t done[2] = {nullptr, nullptr};
+};
+std::mutex g_stage_mu;
+std::map<int, std::unique_ptr<Stage>> g_stages;
+Stage& stage_for(int device) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  auto& s = g_stages[device];
+  if (!s) s = std::make_unique<Stage>();
+  return *s;
+}
+void stage_init(Stage& s) {
+  if (s.buf[0]) return;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&s.buf[i]), kStageChunk, cudaHostAllocPortable));
+    CK(cudaEventCreateWithFlags(&s.done[i], cudaEventDisableTiming));
+  }
+}
+void par_copy_impl(char* dst, const char* src, size_t n) {
+  const size_t kPiece = size_t(1) << 20;
+  const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) if (pieces > 1)
+  for (long i = 0; i < pieces; ++i) {
+    const size_t o = static_cast<size_t>(i) * kPiece;
+    std::memcpy(dst + o, src + o, std::min(kPiece, n - o));
+  }
+}
+}  // namespace
+
+void par_copy(char* dst, const char* src, size_t n) { par_copy_impl(dst, src, n); }
+
+StageLease::StageLease(int device) : s_(&stage_for(device)) {
+  Stage& s = *static_cast<Stage*>(s_);
+  s.mu.lock();
+  try {
+    stage_init(s);
+  } catch (...) {
+    s.mu.unlock();
+    throw;
+  }
+}
+StageLease::~StageLease() { static_cast<Stage*>(s_)->mu.unlock(); }
+char* StageLease::buf(int k) const { return static_cast<Stage*>(s_)->buf[k]; }
+cudaEvent_t StageLease::done(int k) const { return static_cast<Stage*>(s_)->done[k]; }
+size_t StageLease::bytes() { return kStageChunk; }
+
+void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const char* src = static_cast<const char*>(h_src);
+  char* dst = static_cast<char*>(d_dst);
+  int k = 0;
+  for (size_t o = 0; o < bytes; o += kStageChunk, k ^= 1) {
+    const size_t n = std::min(kStageChunk, bytes - o);
+    CK(cudaEventSynchronize(s.done[k]));  // the copy that last read this buffer
+    par_copy(s.buf[k], src + o, n);
+    CK(cudaMemcpyAsync(dst + o, s.buf[k], n, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(s.done[k], st));
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, int device,
+                            cudaStream_t st) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const size_t per = kStageChunk / sizeof(uint2);
+  const size_t chunks = (count + per - 1) / per;
+  auto issue = [&](size_t c) {
+    const size_t lo = c * per, n = std::min(per, count - lo);
+    CK(cudaMemcpyAsync(s.buf[c & 1], d_src + lo, n * sizeof(uint2), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s.done[c & 1], st));
+  };
+  if (chunks) issue(0);
+  for (size_t c = 0; c < chunks; ++c) {
+    if (c + 1 < chunks) issue(c + 1);  // lands while chunk c is widened
+    CK(cudaEventSynchronize(s.done[c & 1]));
+    const size_t lo = c * per, n = std::min(per, count - lo);
+    const uint2* in = reinterpret_cast<const uint2*>(s.buf[c & 1]);
+    int64_t* out = h_dst + 2 * lo;
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (long i = 0; i < static_cast<long>(n); ++i) {
+      out[2 * i] = in[i].x;
+      out[2 * i + 1] = in[i].y;
+    }
+  }
+}
+
+void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  const char* src = static_cast<const char*>(d_src);
+  char* dst = static_cast<char*>(h_dst);
+  auto issue = [&](size_t c) {
+    const size_t o = c * kStageChunk, n = std::min(kStageChunk, bytes - o);
+    CK(cudaMemcpyAsync(s.buf[c & 1], src + o, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s.done[c & 1], st));
+  };
+  if (chunks) issue(0);
+  for (size_t c = 0; c < chunks; ++c) {
+    if (c + 1 < chunks) issue(c + 1);
+    CK(cudaEventSynchronize(s.done[c & 1]));
+    const size_t o = c * kStageChunk, n = std::min(kStageChunk, bytes - o);
+    par_copy(dst + o, s.buf[c & 1], n);
+  }
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st) {
+  if (!bytes) return;
+  if (bytes < (size_t(1) << 20) || is_pinned(h_src))
+    CK(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, st));
+  else
+    staged_h2d(d_dst, h_src, bytes, device, st);
+}
+
+void copy_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st) {
+  if (!bytes) return;
+  if (bytes < (size_t(1) << 20) || is_pinned(h_dst))
+    CK(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
+  else
+    staged_d2h(h_dst, d_src, bytes, device, st);
+}
+
+size_t count_byte(const char* p, size_t len, char c) {
+  const size_t kPiece = size_t(1) << 20;
+  const long pieces = static_cast<long>((len + kPiece - 1) / kPiece);
+  size_t total = 0;
+#pragma omp parallel for schedule(static) reduction(+ : total) if (pieces > 1)
+  for (long i = 0; i < pieces; ++i) {
+    const size_t o = static_cast<size_t>(i) * kPiece;
+    const char* q = p + o;
+    const size_t n = std::min(kPiece, len - o);
+    size_t k = 0;
+    for (size_t j = 0; j < n; ++j) k += q[j] == c;
+    total += k;
+  }
+  return total;
 }
 
 }  // namespace ettg

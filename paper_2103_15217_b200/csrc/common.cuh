@@ -201,6 +201,42 @@ class Lease {
 
 int sm_count(int device);
 
+// Pageable host buffers <-> device through per-device pinned staging (capi.cu):
+// host threads (OpenMP) fill / drain one pinned chunk while the copy engine
+// moves the other.  A plain cudaMemcpy from pageable memory runs ~10 GB/s
+// H2D and, into freshly allocated memory, ~4 GB/s D2H (single-threaded page
+// faults); the staged paths run near the link rate.  Both synchronise `st`.
+void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);
+// D2H of `count` u32 pairs, widened to int64 pairs into h_dst (the reference's
+// i64 ids) by the host threads as the chunks land.
+void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, int device,
+                            cudaStream_t st);
+// The device's two pinned staging buffers, held for a custom pipeline.
+class StageLease {
+ public:
+  explicit StageLease(int device);
+  ~StageLease();
+  char* buf(int k) const;
+  cudaEvent_t done(int k) const;
+  static size_t bytes();  // per buffer
+  StageLease(const StageLease&) = delete;
+  StageLease& operator=(const StageLease&) = delete;
+
+ private:
+  void* s_;
+};
+void par_copy(char* dst, const char* src, size_t n);  // host threads
+// Raw staged D2H into a pageable host buffer (host threads drain the chunks).
+void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st);
+// Page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory) host memory?
+bool is_pinned(const void* p);
+// Host <-> device copies of caller buffers: async when the host side is
+// pinned, staged (and synchronous) when it is pageable.
+void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);
+void copy_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st);
+// Number of `c` bytes in [p, p + len), host threads.
+size_t count_byte(const char* p, size_t len, char c);
+
 // Copy `count` words device->host on `stream` and wait (used for counters
 // and error flags; a handful of bytes).
 inline void read_back(void* host, const void* dev, size_t bytes,

@@ -1140,7 +1140,7 @@ ettg_lca* build_naive_only(const void* parent, bool host_i64, int64_t n64, int64
   CK(cudaMemsetAsync(ws.flags, 0, 8 * sizeof(u32), st));
   const unsigned gb = std::min(g, blocks_for(n, 256));
   if (host_i64) {
-    CK(cudaMemcpyAsync(ws.par64, parent, static_cast<u64>(n) * 8, cudaMemcpyHostToDevice, st));
+    copy_h2d(ws.par64, parent, static_cast<u64>(n) * 8, device, st);
     k_tree_validate<int64_t><<<gb, 256, 0, st>>>(ws.par64, n, root, ws.par, ws.keys, ws.vals,
                                                  ws.flags);
   } else {
@@ -1291,7 +1291,7 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   const unsigned g = sms * 8;
   CK(cudaMemsetAsync(ws.flags, 0, 8 * sizeof(u32), st));
   if (host_i64) {
-    CK(cudaMemcpyAsync(ws.par64, parent, static_cast<u64>(n) * 8, cudaMemcpyHostToDevice, st));
+    copy_h2d(ws.par64, parent, static_cast<u64>(n) * 8, device, st);
     k_tree_validate<int64_t><<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
         ws.par64, n, root, h->par, ws.keys, ws.vals, ws.flags);
   } else {
@@ -1517,6 +1517,44 @@ int ettg_lca_build_ms(const ettg_lca* h, double* ms) {
   });
 }
 
+namespace {
+// Pageable caller buffers (std::vector, numpy): host threads copy each chunk
+// of pairs into a pinned staging buffer and the previous chunk's answers out
+// of the other while the device moves and answers the current one.  A plain
+// cudaMemcpy from / to pageable memory runs at ~10 / ~4 GB/s.
+void query_host_staged(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
+                       int64_t* answers) {
+  StageLease sl(h->device);
+  const u64 per = (StageLease::bytes() / 24) & ~u64(1);  // 16-B pairs + 8-B answers
+  ensure_qbuf(h, per);
+  cudaStream_t st = h->qs[0];
+  CK(cudaMemsetAsync(h->qerr, 0, 8, st));
+  longlong2* dp = reinterpret_cast<longlong2*>(h->qmem);
+  long long* da = reinterpret_cast<long long*>(h->qmem + h->qchunk * 16);
+  const u64 chunks = (q + per - 1) / per;
+  auto drain = [&](u64 c) {  // answers of chunk c: staging -> caller
+    const u64 lo = c * per, cnt = std::min(per, q - lo);
+    CK(cudaEventSynchronize(sl.done(c & 1)));
+    par_copy(reinterpret_cast<char*>(answers + lo), sl.buf(c & 1) + per * 16, cnt * 8);
+  };
+  for (u64 c = 0; c < chunks; ++c) {
+    const int k = c & 1;
+    if (c >= 2) drain(c - 2);  // frees buffer k
+    const u64 lo = c * per, cnt = std::min(per, q - lo);
+    par_copy(sl.buf(k), reinterpret_cast<const char*>(pairs + 2 * lo), cnt * 16);
+    CK(cudaMemcpyAsync(dp, sl.buf(k), cnt * 16, cudaMemcpyHostToDevice, st));
+    launch_query(h, engine, PairsI64{dp}, AnsI64{da}, cnt, h->qerr, st);
+    CK(cudaMemcpyAsync(sl.buf(k) + per * 16, da, cnt * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(sl.done(k), st));
+  }
+  if (chunks >= 2) drain(chunks - 2);
+  drain(chunks - 1);
+  u32 err = 0;
+  read_back(&err, h->qerr, 4, st);
+  if (err) throw Error(ETTG_ERANGE, "query node id out of range");
+}
+}  // namespace
+
 int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pairs, int64_t q,
                           int64_t batch, int64_t* answers) {
   return guard([&] {
@@ -1527,6 +1565,10 @@ int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pa
     if (!pairs || !answers) einval("null argument");
     ettg_lca* h = const_cast<ettg_lca*>(hc);
     DeviceScope ds(h->device);
+    if (q >= (1 << 16) && !(is_pinned(pairs) && is_pinned(answers))) {
+      query_host_staged(h, engine, pairs, static_cast<u64>(q), answers);
+      return;
+    }
     // 1M-query chunks on two streams: H2D of chunk c+1 overlaps the kernel and
     // D2H of chunk c; smaller chunks shorten the unoverlapped fill and drain
     // (config B e2e: 4M chunks 5.36 ms, 1M 5.04 ms, 256K 5.37 ms per 16M).

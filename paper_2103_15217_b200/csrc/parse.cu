@@ -255,13 +255,13 @@ __global__ void k_first_occurrence(const u32* __restrict__ kmin, const u32* __re
   }
 }
 
-struct EdgeOut {  // the reference's i64 pairs, so the host copy is one memcpy
+struct EdgeOut {  // u32 pairs: half the D2H bytes; widened to i64 on the host
   const u32* kmin;
   const u32* kmax;
   u32 cap;
-  longlong2* out;
+  uint2* out;
   __device__ __forceinline__ void operator()(u64 c, u32 r) const {
-    if (r < cap) out[r] = make_longlong2(kmin[c], kmax[c]);
+    if (r < cap) out[r] = make_uint2(kmin[c], kmax[c]);
   }
 };
 
@@ -278,7 +278,7 @@ struct ParseWs {
   u32 *kmin = nullptr, *kmax = nullptr, *iota = nullptr, *k1 = nullptr, *v1 = nullptr,
       *k2 = nullptr, *v2 = nullptr;
   uint8_t* keep = nullptr;
-  longlong2* edges = nullptr;
+  uint2* edges = nullptr;
   unsigned long long* counters = nullptr;
   u32* words = nullptr;
   SortWs sort;
@@ -301,7 +301,7 @@ struct ParseWs {
     k2 = c.take<u32>(L + 1);
     v2 = c.take<u32>(L + 1);
     keep = c.take<uint8_t>(L + 16);
-    edges = c.take<longlong2>(L + 1);
+    edges = c.take<uint2>(L + 1);
     counters = c.take<unsigned long long>(4);
     words = c.take<u32>(8);
     sort.carve(c, L + 1);
@@ -353,10 +353,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   const u64 len = static_cast<u64>(len64);
   // lines = newlines + (1 if the text does not end in '\n'): counted on the
   // host for the workspace size only (memchr pass; the device re-derives it)
-  u64 nnl_host = 0;
-  for (const char* p = text; len && (p = static_cast<const char*>(memchr(p, '\n', text + len - p)));
-       ++p)
-    ++nnl_host;
+  const u64 nnl_host = len ? count_byte(text, len, '\n') : 0;
   const u64 nlines64 = nnl_host + ((len > 0 && text[len - 1] != '\n') ? 1 : 0);
   if (nlines64 >= 0xFFFFFFFFull) throw Error(ETTG_ERANGE, "too many lines");
   const u32 nlines = static_cast<u32>(nlines64);
@@ -379,7 +376,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   Trace tr(dimacs ? "parse_dimacs_gr" : "parse_edge_list", st);
   CK(cudaMemsetAsync(ws.counters, 0, 4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(ws.words, 0xFF, 8 * sizeof(u32), st));
-  if (len) CK(cudaMemcpyAsync(ws.text, text, len, cudaMemcpyHostToDevice, st));
+  if (len) staged_h2d(ws.text, text, len, device, st);
   tr.mark("h2d");
   if (len) {
     k_newlines<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.text, len, ws.flags);
@@ -470,10 +467,7 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
     stats->duplicates_removed = static_cast<int64_t>(C) - m;
   }
   if (static_cast<u64>(cap) < m) throw Error(ETTG_ERANGE, "edge buffer too small (m returned)");
-  if (m) {
-    CK(cudaMemcpyAsync(edges_out, ws.edges, u64(m) * 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  if (m) staged_d2h_widen_pairs(edges_out, ws.edges, m, device, st);
   tr.mark("d2h");
 }
 
