@@ -262,9 +262,21 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
     barrier()
     t = all_max(float(np.mean(times)), device)
     link = host_link_bound(pin_pairs, torch.empty_like(pin_ans).pin_memory(), device)
+    # the same call with pageable numpy buffers (what a std::vector / numpy
+    # caller passes): staged through the library's pinned buffers
+    pg_pairs = np.ascontiguousarray(host)
+    pg_ans = np.empty(hi - lo, np.int64)
+    pg = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        _lib.check(L.ettg_lca_query(idx.handle, pg_pairs.ctypes.data, hi - lo, max(hi - lo, 1),
+                                    pg_ans.ctypes.data))
+        pg.append(time.perf_counter() - t0)
     return {"value": q_total / t, "unit": "queries/s",
             "h2d_bytes_per_step": (hi - lo) * 16, "d2h_bytes_per_step": (hi - lo) * 8,
             "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)",
+            "pageable": {"value": q_total / all_max(min(pg), device), "ms": 1e3 * min(pg),
+                         "what": "same call, numpy (pageable) pairs and answers, best of 3"},
             "link_bound": {"ms": link, "frac": (link / (t * 1e3)) if link else None,
                            "what": "the same H2D + D2H bytes as plain concurrent copies on two "
                                    "streams (no kernel), CUDA events, best of 5; "
