@@ -1000,8 +1000,10 @@ struct ettg_lca {
         lasc = c.take<u32>(static_cast<u64>(n) + 1);
       }
       if (full || layout == kLayoutSplit) nodes = c.take<uint2>(n);
-      if (full || layout == kLayoutSplit6) nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
-      if (full || layout == kLayoutWide9) nodes9 = c.take<uint32_t>(rec9_bytes(n) / 4);
+      // packed records exist only for n < 2^24 (24-bit fields)
+      const bool packable = n < (1u << 24);
+      if ((full && packable) || layout == kLayoutSplit6) nodes6 = c.take<uint32_t>(rec6_bytes(n) / 4);
+      if ((full && packable) || layout == kLayoutWide9) nodes9 = c.take<uint32_t>(rec9_bytes(n) / 4);
       if (!full && (layout == kLayoutSplit || layout == kLayoutSplitOwn || layout == kLayoutSplit6))
         slevel = c.take<u32>(n);  // full builds query h->level
       lab = c.take<uint2>(static_cast<u64>(n) + 1);
