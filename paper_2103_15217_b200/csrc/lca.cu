@@ -1345,15 +1345,17 @@ ettg_lca* build_index(const void* parent, bool host_i64, bool dev_u32, int64_t n
   k_head<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(h->inlabel, h->par, h->level, n,
                                                          h->head, h->lab, ws.up, ws.flags + 1);
   CK_LAUNCH();
+  tr.mark("head");
   for (int t = 31 - __builtin_clz(n); t >= 0; --t) {
     const u32 count = ((n >> t) + 1) >> 1;
     k_asc_level<<<std::min(g, blocks_for(count, 256)), 256, 0, st>>>(ws.up, n, t, h->lasc);
     CK_LAUNCH();
   }
+  tr.mark("asc");
   k_pack<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
       h->inlabel, h->level, h->lasc, h->lab, n, h->node, h->node8, h->nodes, ws.flags + 2);
   CK_LAUNCH();
-  tr.mark("head_asc_pack");
+  tr.mark("pack");
   if (engines & ETTG_ENGINE_RMQ) launch_stats_rmq(h.get(), st, sms);
   tr.mark("rmq");
   if (engines & ETTG_ENGINE_NAIVE) {
