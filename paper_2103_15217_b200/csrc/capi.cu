@@ -1,5 +1,8 @@
 // C-ABI plumbing: error state, device scope, scratch arena, primitives.
+#include <omp.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -115,6 +118,16 @@ Stage& stage_for(int device) {
   if (!s) s = std::make_unique<Stage>();
   return *s;
 }
+// Host threads for staging copies: ETTG_HOST_THREADS, else up to 16 of the
+// visible cores (independent of OMP_NUM_THREADS, which launchers such as
+// torchrun set to 1 per rank).
+int host_threads() {
+  static const int t = [] {
+    if (const char* e = std::getenv("ETTG_HOST_THREADS")) return std::max(1, std::atoi(e));
+    return std::max(1, std::min(16, omp_get_num_procs()));
+  }();
+  return t;
+}
 void stage_init(Stage& s) {
   if (s.buf[0]) return;
   for (int i = 0; i < 2; ++i) {
@@ -125,7 +138,7 @@ void stage_init(Stage& s) {
 void par_copy_impl(char* dst, const char* src, size_t n) {
   const size_t kPiece = size_t(1) << 20;
   const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
-#pragma omp parallel for schedule(static) if (pieces > 1)
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (pieces > 1)
   for (long i = 0; i < pieces; ++i) {
     const size_t o = static_cast<size_t>(i) * kPiece;
     std::memcpy(dst + o, src + o, std::min(kPiece, n - o));
@@ -186,7 +199,7 @@ void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, in
     const size_t lo = c * per, n = std::min(per, count - lo);
     const uint2* in = reinterpret_cast<const uint2*>(s.buf[c & 1]);
     int64_t* out = h_dst + 2 * lo;
-#pragma omp parallel for schedule(static) if (n > 65536)
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (n > 65536)
     for (long i = 0; i < static_cast<long>(n); ++i) {
       out[2 * i] = in[i].x;
       out[2 * i + 1] = in[i].y;
@@ -244,7 +257,8 @@ size_t count_byte(const char* p, size_t len, char c) {
   const size_t kPiece = size_t(1) << 20;
   const long pieces = static_cast<long>((len + kPiece - 1) / kPiece);
   size_t total = 0;
-#pragma omp parallel for schedule(static) reduction(+ : total) if (pieces > 1)
+#pragma omp parallel for schedule(static) reduction(+ : total) num_threads(host_threads()) \
+    if (pieces > 1)
   for (long i = 0; i < pieces; ++i) {
     const size_t o = static_cast<size_t>(i) * kPiece;
     const char* q = p + o;
