@@ -1003,7 +1003,7 @@ int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
     const int sms = sm_count(device);
     CK(cudaMemsetAsync(ws.flags, 0, 32, st));
     if (mm) {
-      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
       k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
           ws.e64, mm, nn, ws.e, ws.flags);
       CK_LAUNCH();
@@ -1012,17 +1012,11 @@ int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
     read_back(&bad, ws.flags, 4, st);
     if (bad) einval("edge endpoint out of range");
     build_csr(ws.e, nn, mm, ws.offs, ws.nbr, ws.eid, ws.csr, st, sms);
-    std::vector<u32> o(static_cast<u64>(nn) + 1), a(2ull * mm), b(2ull * mm);
-    CK(cudaMemcpyAsync(o.data(), ws.offs, o.size() * 4, cudaMemcpyDeviceToHost, st));
+    // values < 2^31: the kNone mapping of the widening never applies
+    staged_d2h_widen_u32(offsets, ws.offs, static_cast<u64>(nn) + 1, device, st);
     if (mm) {
-      CK(cudaMemcpyAsync(a.data(), ws.nbr, a.size() * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(b.data(), ws.eid, b.size() * 4, cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
-    for (u64 i = 0; i < o.size(); ++i) offsets[i] = o[i];
-    for (u64 i = 0; i < a.size(); ++i) {
-      neighbors[i] = a[i];
-      edge_ids[i] = b[i];
+      staged_d2h_widen_u32(neighbors, ws.nbr, 2ull * mm, device, st);
+      staged_d2h_widen_u32(edge_ids, ws.eid, 2ull * mm, device, st);
     }
   });
 }
@@ -1078,7 +1072,7 @@ int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int devic
     CK(cudaMemsetAsync(ws.size, 0, nn * 4ull, st));
     CK(cudaMemsetAsync(ws.best, 0, 8, st));
     if (mm) {
-      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
       k_edges_from_i64<<<std::min(g, blocks_for(mm, 256)), 256, 0, st>>>(ws.e64, mm, nn, ws.e,
                                                                          ws.flags);
       CK_LAUNCH();
@@ -1102,19 +1096,9 @@ int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int devic
                    ws.counts + 1, st);
     u32 cnt[2];
     CK(cudaMemcpyAsync(cnt, ws.counts, sizeof cnt, cudaMemcpyDeviceToHost, st));
-    std::vector<u32> o(nn);
-    CK(cudaMemcpyAsync(o.data(), ws.o2n, nn * 4ull, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    std::vector<uint2> eo(cnt[1]);
-    if (cnt[1]) {
-      CK(cudaMemcpyAsync(eo.data(), ws.eo, cnt[1] * 8ull, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-    }
-    for (u32 v = 0; v < nn; ++v) old_to_new[v] = o[v] == kNone ? int64_t(-1) : int64_t(o[v]);
-    for (u32 i = 0; i < cnt[1]; ++i) {
-      edges_out[2 * i] = eo[i].x;
-      edges_out[2 * i + 1] = eo[i].y;
-    }
+    staged_d2h_widen_u32(old_to_new, ws.o2n, nn, device, st);
+    if (cnt[1]) staged_d2h_widen_pairs(edges_out, ws.eo, cnt[1], device, st);
     *n_out = cnt[0];
     *m_out = cnt[1];
   });
@@ -1162,7 +1146,7 @@ int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root, int 
     CK(cudaMemsetAsync(ws.flags, 0, 32, st));
     CK(cudaMemsetAsync(ws.tree, 0, mm + 16, st));
     if (mm) {
-      CK(cudaMemcpyAsync(ws.e64, edges, static_cast<u64>(mm) * 16, cudaMemcpyHostToDevice, st));
+      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
       k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
           ws.e64, mm, nn, ws.e, ws.flags);
       CK_LAUNCH();
@@ -1174,17 +1158,11 @@ int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root, int 
         run_bfs(ws.e, nn, mm, static_cast<u32>(root), ws.lev, ws.par, ws.pe, ws.tree, ws.bfs, st,
                 sms);
     if (reached != nn) einval("disconnected graph; extract the largest component first");
-    std::vector<u32> l(nn), p(nn), q(nn);
-    CK(cudaMemcpyAsync(l.data(), ws.lev, nn * 4ull, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(p.data(), ws.par, nn * 4ull, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(q.data(), ws.pe, nn * 4ull, cudaMemcpyDeviceToHost, st));
-    if (mm) CK(cudaMemcpyAsync(tree_mask, ws.tree, mm, cudaMemcpyDeviceToHost, st));
+    staged_d2h_widen_u32(level, ws.lev, nn, device, st);
+    staged_d2h_widen_u32(parent, ws.par, nn, device, st);
+    staged_d2h_widen_u32(parent_edge, ws.pe, nn, device, st);
+    if (mm) copy_d2h(tree_mask, ws.tree, mm, device, st);
     CK(cudaStreamSynchronize(st));
-    for (u32 v = 0; v < nn; ++v) {
-      level[v] = l[v] == kNone ? int64_t(-1) : int64_t(l[v]);
-      parent[v] = p[v] == kNone ? int64_t(-1) : int64_t(p[v]);
-      parent_edge[v] = q[v] == kNone ? int64_t(-1) : int64_t(q[v]);
-    }
   });
 }
 

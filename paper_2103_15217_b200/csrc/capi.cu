@@ -228,6 +228,31 @@ void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaSt
   }
 }
 
+void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, int device,
+                          cudaStream_t st) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const size_t per = kStageChunk / sizeof(uint32_t);
+  const size_t chunks = (count + per - 1) / per;
+  auto issue = [&](size_t c) {
+    const size_t lo = c * per, n = std::min(per, count - lo);
+    CK(cudaMemcpyAsync(s.buf[c & 1], d_src + lo, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s.done[c & 1], st));
+  };
+  if (chunks) issue(0);
+  for (size_t c = 0; c < chunks; ++c) {
+    if (c + 1 < chunks) issue(c + 1);
+    CK(cudaEventSynchronize(s.done[c & 1]));
+    const size_t lo = c * per, n = std::min(per, count - lo);
+    const uint32_t* in = reinterpret_cast<const uint32_t*>(s.buf[c & 1]);
+    int64_t* out = h_dst + lo;
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (n > 65536)
+    for (long i = 0; i < static_cast<long>(n); ++i)
+      out[i] = in[i] == 0xFFFFFFFFu ? int64_t(-1) : static_cast<int64_t>(in[i]);
+  }
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

@@ -226,6 +226,10 @@ class StageLease {
   void* s_;
 };
 void par_copy(char* dst, const char* src, size_t n);  // host threads
+// D2H of `count` u32 values widened to int64 (0xFFFFFFFF -> -1, the
+// reference's kNone) by the host threads as the pinned chunks land.
+void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, int device,
+                          cudaStream_t st);
 // Raw staged D2H into a pageable host buffer (host threads drain the chunks).
 void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st);
 // Page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory) host memory?

@@ -1628,10 +1628,9 @@ int ettg_lca_query_dev(const ettg_lca* h, unsigned engine, const uint32_t* d_pai
 namespace {
 void copy_widen(int64_t* dst, const u32* src, u64 count, cudaStream_t st) {
   if (!dst) return;
-  std::vector<u32> tmp(count);
-  CK(cudaMemcpyAsync(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (u64 i = 0; i < count; ++i) dst[i] = tmp[i] == kNone ? -1 : static_cast<int64_t>(tmp[i]);
+  int device = 0;
+  CK(cudaGetDevice(&device));
+  staged_d2h_widen_u32(dst, src, count, device, st);
 }
 }  // namespace
 

@@ -367,7 +367,10 @@ def largest_component(g: EdgeList, device: int = 0) -> ComponentResult:
     nn, mm = C.c_int64(), C.c_int64()
     check(lib().ettg_largest_component(ptr(g.edges), int(g.n), m, device, ptr(o2n), C.byref(nn),
                                        C.byref(mm), ptr(out)))
-    return ComponentResult(EdgeList(nn.value, out[:mm.value].copy()), o2n[:g.n])
+    kept = out[:mm.value]
+    if 2 * mm.value < m:  # release the over-allocation only when it is large
+        kept = kept.copy()
+    return ComponentResult(EdgeList(nn.value, kept), o2n[:g.n])
 
 
 @dataclass
