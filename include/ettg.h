@@ -26,8 +26,12 @@
  *  - Host-buffer calls are synchronous.  *_dev calls enqueue on `stream`
  *    (a cudaStream_t, NULL = legacy default stream) and return immediately
  *    unless documented otherwise.
- *  - A handle may not be used from two host threads at once; distinct
- *    handles are independent.
+ *  - Host-buffer queries on one LCA handle from several host threads are
+ *    serialised by the handle; device-resident (_dev) queries on a shared
+ *    handle need no lock.  Building, exporting or freeing a handle while
+ *    another thread uses it is not allowed.  Distinct handles are
+ *    independent; the scratch arena and pinned staging buffers are shared
+ *    per device and serialised internally.
  *  - Every function returns ETTG_OK or an error code; ettg_last_error()
  *    returns the message of the last failure on the calling thread.
  *    Error codes mirror the reference's exceptions:

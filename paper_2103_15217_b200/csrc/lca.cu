@@ -32,6 +32,7 @@
 // v's first occurrence (rmq tour_nodes, core/src/lca.cpp:135-146).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -955,6 +956,7 @@ constexpr u32 kLayoutWide = 0, kLayoutNarrow = 1, kLayoutCompact = 2, kLayoutSpl
               kLayoutSplitOwn = 4, kLayoutSplit6 = 5, kLayoutWide9 = 6;
 
 struct ettg_lca {
+  std::mutex qmu;  // host-buffer queries share the handle's staging buffers
   int device = 0;
   u32 n = 0;
   u32 root = 0;
@@ -1569,6 +1571,7 @@ int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pa
     if (!pairs || !answers) einval("null argument");
     ettg_lca* h = const_cast<ettg_lca*>(hc);
     DeviceScope ds(h->device);
+    std::lock_guard<std::mutex> qlock(h->qmu);
     if (q >= (1 << 16) && !(is_pinned(pairs) && is_pinned(answers))) {
       query_host_staged(h, engine, pairs, static_cast<u64>(q), answers);
       return;
