@@ -645,7 +645,7 @@ struct BridgeWs {
     head = c.take<u32>(n);
     nxt = c.take<u32>(k + 1);
     tend = c.take<uint2>(n);
-    lr.carve(c, k > 0 ? k : 1);
+    lr.carve(c, k > 0 ? k : 1, true);  // tour ranks only: no down weights
     flags = c.take<u32>(k + 1);
     scan_k = c.take<u64>(scan_ws_words(k + 1));
     pre_of = c.take<u32>(n);

@@ -346,11 +346,11 @@ int ettg_list_rank_dev(const uint32_t* d_succ, int64_t k, int64_t head, uint32_t
     const u32 kk = static_cast<u32>(k);
     ListRankWs ws;
     Carver c;
-    ws.carve(c, kk);
+    ws.carve(c, kk, true);
     u32* pred = c.take<u32>(kk);
     Lease lease(device, st, c.off);
     c = Carver{lease.base()};
-    ws.carve(c, kk);
+    ws.carve(c, kk, true);
     pred = c.take<u32>(kk);
     CK(cudaMemcpyAsync(ws.succ0, d_succ, static_cast<u64>(kk) * 4, cudaMemcpyDeviceToDevice, st));
     const int sms = sm_count(device);

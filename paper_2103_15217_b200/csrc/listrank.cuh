@@ -169,11 +169,15 @@ struct LrCounters {
 // the memory system is already saturated by the resident warps -- so 1.
 constexpr int kLrWalkers = 1;
 
-template <class Down, class H>
+// kNarrow (lists without down weights): 4-B records (local << sid_bits | sid)
+// and sublists capped at cap_step elements (walk micro: -12% vs 8-B records).
+template <class Down, class H, bool kNarrow>
 __global__ void __launch_bounds__(256)
     k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, H head_src, u32 seed,
                u32 mask, const u32* __restrict__ spl, u32* counters, u32 sub_cap,
-               u32* __restrict__ sub_next, u64* __restrict__ sub_w, Down down) {
+               u32* __restrict__ sub_next, u64* __restrict__ sub_w, Down down, u32 cap_step,
+               u32 sid_bits) {
+  u32* rec32 = reinterpret_cast<u32*>(rec);
   const int lane = threadIdx.x & 31;
   const u32 head = head_src.get();
   const u32 lt = lanemask_lt();
@@ -218,7 +222,10 @@ __global__ void __launch_bounds__(256)
     for (int w = 0; w < kLrWalkers; ++w) {
       nxt[w] = kNone;
       if (active[w]) {
-        rec[cur[w]] = (static_cast<u64>(acc[w]) << 32) | sid[w];
+        if (kNarrow)
+          rec32[cur[w]] = ((acc[w] & 0xFFFFu) << sid_bits) | sid[w];
+        else
+          rec[cur[w]] = (static_cast<u64>(acc[w]) << 32) | sid[w];
         nxt[w] = succ[cur[w]];
       }
     }
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(256)
       const u32 nx = nxt[w];
       const bool bad = (nx != kNone && nx >= k) || steps[w] > k;
       const bool stop = bad || nx == kNone || lr_is_splitter(nx, head, seed, mask);
-      if (stop || (acc[w] & 0xFFFFu) == kLrCapStep) {
+      if (stop || (acc[w] & 0xFFFFu) == (kNarrow ? cap_step : kLrCapStep)) {
         sub_next[sid[w]] = bad ? kNone : nx;
         sub_w[sid[w]] = (static_cast<u64>(acc[w] >> 16) << 32) | (acc[w] & 0xFFFFu);
         if (bad) atomicOr(&counters[LrCounters::kErr], kErrStructure);
@@ -333,15 +340,21 @@ __global__ void k_lr_clamp(u32* count, u32 cap, u32* err) {
 template <class H>
 __global__ void k_lr_next_level0(const u64* __restrict__ rec, const u32* __restrict__ sub_next,
                                  const u64* __restrict__ sub_w, const u32* d_S, H head_src,
-                                 u32* __restrict__ succ2, u64* __restrict__ w2, u32* d_head2) {
+                                 u32* __restrict__ succ2, u64* __restrict__ w2, u32* d_head2,
+                                 u32 sid_bits) {
   const u32 S = *d_S;
   const u32 head = head_src.get();
+  const u32* rec32 = reinterpret_cast<const u32*>(rec);
+  const u32 smask = sid_bits ? (1u << sid_bits) - 1u : 0u;
+  auto sid_of = [&](u32 e) {
+    return sid_bits ? (rec32[e] & smask) : static_cast<u32>(rec[e]);
+  };
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const u32 ne = sub_next[i];
-    succ2[i] = ne == kNone ? kNone : static_cast<u32>(rec[ne]);
+    succ2[i] = ne == kNone ? kNone : sid_of(ne);
     w2[i] = sub_w[i];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *d_head2 = static_cast<u32>(rec[head]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_head2 = sid_of(head);
 }
 
 __global__ void k_lr_next_level(const u32* __restrict__ rec_sid, const u32* __restrict__ sub_next,
@@ -535,7 +548,10 @@ struct ListRankWs {
 
   u32 L0 = kLrL0;  // level-0 mean sublist length (power of two); ETTG_LR_L0 overrides
   double wyllie_max = kLrWyllieMax;  // ETTG_LR_WYLLIE overrides (0: smem final only)
-  void carve(Carver& c, u32 k_) {
+  // Narrow level-0 records (weight-free lists, see k_lr_walk0): sid_bits > 0.
+  u32 sid_bits = 0, cap_step = kLrCapStep;
+  // narrow_ok: the caller's lists carry no down weights (NoDown)
+  void carve(Carver& c, u32 k_, bool narrow_ok = false) {
     k = k_;
     if (const char* e = std::getenv("ETTG_LR_L0")) {
       const u32 v = static_cast<u32>(std::atoi(e));
@@ -547,6 +563,21 @@ struct ListRankWs {
     counters = c.take<u32>(64);
     // level 0 caps
     u32 cap1 = next_cap(k, L0) + k / kLrCapStep + 2;
+    sid_bits = 0;
+    cap_step = kLrCapStep;
+    bool narrow = narrow_ok;
+    if (const char* e = std::getenv("ETTG_LR_NARROW")) narrow &= std::atoi(e) != 0;
+    if (narrow) {  // >= 8 local bits: cap splits stay rare (mean sublist 16)
+      const u32 c8 = next_cap(k, L0) + k / 255 + 2;
+      u32 b = 1;
+      while ((u64(1) << b) < c8) ++b;
+      if (b <= 24) {
+        sid_bits = b;
+        cap_step = (1u << (32 - b)) - 1u;
+        if (cap_step > kLrCapStep) cap_step = kLrCapStep;
+        cap1 = next_cap(k, L0) + k / cap_step + 2;
+      }
+    }
     lv[0].cap = k;
     lv[0].spl = c.take<u32>(cap1);
     lv[0].sub_next = c.take<u32>(cap1);
@@ -615,9 +646,14 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
                      cudaMemcpyDeviceToDevice, st));
   tr.mark("splitters0");
   const unsigned walk_blocks = sms * 8;  // 2048 threads / SM resident
-  k_lr_walk0<Down, H><<<walk_blocks, 256, 0, st>>>(ws.succ0, ws.rec0, k, head, seed0, mask0,
-                                                ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
-                                                ws.lv[0].sub_w, down);
+  if (ws.sid_bits)
+    k_lr_walk0<Down, H, true><<<walk_blocks, 256, 0, st>>>(
+        ws.succ0, ws.rec0, k, head, seed0, mask0, ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
+        ws.lv[0].sub_w, down, ws.cap_step, ws.sid_bits);
+  else
+    k_lr_walk0<Down, H, false><<<walk_blocks, 256, 0, st>>>(
+        ws.succ0, ws.rec0, k, head, seed0, mask0, ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
+        ws.lv[0].sub_w, down, ws.cap_step, 0u);
   CK_LAUNCH();
   tr.mark("walk0");
   // level-1 list
@@ -625,7 +661,8 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
   k_lr_clamp<<<1, 1, 0, st>>>(S1, cap1, cnt + LrCounters::kErr);
   u32* head1 = cnt + LrCounters::kLevelBase + 4 * 1 + 2;
   k_lr_next_level0<H><<<blocks_for(cap1, 256), 256, 0, st>>>(
-      ws.rec0, ws.lv[0].sub_next, ws.lv[0].sub_w, S1, head, ws.lv[1].succ, ws.lv[1].w, head1);
+      ws.rec0, ws.lv[0].sub_next, ws.lv[0].sub_w, S1, head, ws.lv[1].succ, ws.lv[1].w, head1,
+      ws.sid_bits);
   CK_LAUNCH();
   // deeper levels
   const u32* S_l = S1;
@@ -711,19 +748,27 @@ struct Lr0View {
   const u64* rec0;
   const u64* prefix1;
   const u32* d_S1;  // number of level-0 sublists (device)
+  u32 sid_bits;     // > 0: narrow 4-B records (no down weights)
   __device__ __forceinline__ void get(u32 e, u32 S1, u32& rank, u32& dsum) const {
-    const u64 r = rec0[e];
-    u32 sid = static_cast<u32>(r);
+    u32 sid, loc;
+    if (sid_bits) {
+      const u32 r = reinterpret_cast<const u32*>(rec0)[e];
+      sid = r & ((1u << sid_bits) - 1u);
+      loc = r >> sid_bits;
+    } else {
+      const u64 r = rec0[e];
+      sid = static_cast<u32>(r);
+      loc = static_cast<u32>(r >> 32);
+    }
     if (sid >= S1) sid = 0;
     const u64 p = prefix1[sid];
-    const u32 loc = static_cast<u32>(r >> 32);
     rank = static_cast<u32>(p) + (loc & 0xFFFFu);
     dsum = static_cast<u32>(p >> 32) + (loc >> 16);
   }
 };
 
 inline Lr0View lr0_view(const ListRankWs& ws) {
-  return Lr0View{ws.rec0, ws.prefix1, ws.counters + LrCounters::kSubTotal0};
+  return Lr0View{ws.rec0, ws.prefix1, ws.counters + LrCounters::kSubTotal0, ws.sid_bits};
 }
 
 __global__ void k_lr_rank_out(Lr0View v, u32 k, u32* __restrict__ rank) {

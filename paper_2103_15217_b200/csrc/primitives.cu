@@ -405,7 +405,7 @@ int ettg_list_scan(const int64_t* succ, const int64_t* values, int64_t k, int64_
     u32 *succ32, *pred, *rank, *err;
     u64* tile_sum;
     auto carve = [&](Carver& c) {
-      ws.carve(c, kk);
+      ws.carve(c, kk, true);
       pred = c.take<u32>(kk);
       d_in = c.take<i64>(kk);
       d_vals = c.take<i64>(kk);
