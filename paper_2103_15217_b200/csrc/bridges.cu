@@ -114,6 +114,20 @@ struct EdgeSubset {
     const u64 full = m / span, rest = m % span;
     return full * kGroup + (rest < kGroup ? rest : kGroup);
   }
+  // phase 1 as (i * magic) >> shift == i / per, exact for i < 2^31
+  // (Granlund-Montgomery; m < 2^31); host side: rest_divider()
+  __device__ __forceinline__ u64 edge_rest(u64 i, u32 magic, u32 shift) const {
+    const u32 span = kGroup * sample, per = span - kGroup, j = static_cast<u32>(i);
+    const u32 q = static_cast<u32>((static_cast<u64>(j) * magic) >> shift);
+    return u64(q) * span + kGroup + (j - q * per);
+  }
+  void rest_divider(u32& magic, u32& shift) const {
+    const u64 per = u64(kGroup) * sample - kGroup;
+    u32 l = 0;
+    while ((u64(1) << l) < per) ++l;
+    shift = 31 + l;
+    magic = static_cast<u32>((u64(1) << shift) / per + 1);
+  }
   __device__ __forceinline__ u64 edge(u64 i) const {
     if (sample <= 1) return i;
     const u64 span = u64(kGroup) * sample;
@@ -148,6 +162,92 @@ __global__ void __launch_bounds__(256, kMinB)
       const u64 i = base + j * stride;
       ok[j] = i < cnt;
       const u64 e = ok[j] ? sub.edge(i) : 0;
+      eidx[j] = e;
+      uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
+      if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
+        bad = 1;
+        ok[j] = false;
+        tree[e] = 0;
+      }
+      if (!ok[j]) uv[j] = make_uint2(0, 0);
+    }
+    u32 a[kHookE], b[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      a[j] = par[uv[j].x];
+      b[j] = par[uv[j].y];
+    }
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      // equal parents => same tree: no find needed (after the compress pass
+      // between the phases this settles most phase-1 edges with two loads)
+      if (a[j] != b[j]) {
+        a[j] = uf_find_from(par, uv[j].x, a[j]);
+        b[j] = uf_find_from(par, uv[j].y, b[j]);
+      }
+      if (a[j] < b[j]) {
+        const u32 tmp = a[j];
+        a[j] = b[j];
+        b[j] = tmp;
+      }
+    }
+    u32 old[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j)
+      old[j] = (ok[j] && a[j] != b[j]) ? atomicCAS(&par[a[j]], a[j], b[j]) : a[j];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      if (!ok[j]) continue;
+      uint8_t t = 0;
+      if (a[j] != b[j]) {
+        if (old[j] == a[j]) {
+          t = 1;
+        } else {  // another thread re-rooted a: retry from what the CAS found
+          u32 x = uf_find(par, old[j]), y = uf_find(par, b[j]);
+          while (x != y) {
+            if (x < y) {
+              const u32 tmp = x;
+              x = y;
+              y = tmp;
+            }
+            const u32 o = atomicCAS(&par[x], x, y);
+            if (o == x) {
+              t = 1;
+              break;
+            }
+            x = uf_find(par, o);
+            y = uf_find(par, y);
+          }
+        }
+      }
+      tree[eidx[j]] = t;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+// Second pass of the sampled hooking (the edges outside the sampled groups):
+// the same body as k_cc_hook with i / per as a multiply-shift instead of an
+// emulated u64 division per edge.  A separate kernel on purpose: changing
+// the shared kernel's index code slowed the sampled pass 2x (see
+// profiles/r1_bridges_tuning.md).
+template <int kHookE, int kMinB>
+__global__ void __launch_bounds__(256, kMinB)
+    k_cc_hook_rest(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
+                   uint8_t* __restrict__ tree, u32* flags, u32 magic, u32 shift) {
+  u32 bad = 0;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  const u64 cnt = sub.count();
+  u64 eidx[kHookE];
+  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
+       base += stride * kHookE) {
+    uint2 uv[kHookE];
+    bool ok[kHookE];
+#pragma unroll
+    for (int j = 0; j < kHookE; ++j) {
+      const u64 i = base + j * stride;
+      ok[j] = i < cnt;
+      const u64 e = ok[j] ? sub.edge_rest(i, magic, shift) : 0;
       eidx[j] = e;
       uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
@@ -573,9 +673,19 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* t
                  int sms, cudaStream_t st) {
   const u64 first = sub.first_count();
   const u64 cnt = sub.sample <= 1 ? sub.m : sub.phase == 0 ? first : sub.m - first;
-  auto kern = k_cc_hook<kEdgesPerThread, 8>;
-  kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
-      edges, sub, n, par, tree, flags);
+  bool rest_kernel = sub.sample > 1 && sub.phase == 1;
+  if (const char* e = std::getenv("ETTG_HOOK_REST")) rest_kernel &= std::atoi(e) != 0;
+  if (rest_kernel) {
+    u32 magic = 0, shift = 0;
+    sub.rest_divider(magic, shift);
+    auto kern = k_cc_hook_rest<kEdgesPerThread, 8>;
+    kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
+        edges, sub, n, par, tree, flags, magic, shift);
+  } else {
+    auto kern = k_cc_hook<kEdgesPerThread, 8>;
+    kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
+        edges, sub, n, par, tree, flags);
+  }
   CK_LAUNCH();
 }
 
