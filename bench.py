@@ -261,7 +261,8 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
         times.append(time.perf_counter() - t0)
     barrier()
     t = all_max(float(np.mean(times)), device)
-    link = host_link_bound(pin_pairs, torch.empty_like(pin_ans).pin_memory(), device)
+    answers = pin_ans.numpy().copy()  # the link test below reuses the pinned buffers
+    link = host_link_bound(pin_pairs, pin_ans, device)
     # the same call with pageable numpy buffers (what a std::vector / numpy
     # caller passes): staged through the library's pinned buffers
     pg_pairs = np.ascontiguousarray(host)
@@ -272,16 +273,18 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
         _lib.check(L.ettg_lca_query(idx.handle, pg_pairs.ctypes.data, hi - lo, max(hi - lo, 1),
                                     pg_ans.ctypes.data))
         pg.append(time.perf_counter() - t0)
+    pg_ok = bool(np.array_equal(pg_ans, answers))
     return {"value": q_total / t, "unit": "queries/s",
             "h2d_bytes_per_step": (hi - lo) * 16, "d2h_bytes_per_step": (hi - lo) * 8,
             "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)",
             "pageable": {"value": q_total / all_max(min(pg), device), "ms": 1e3 * min(pg),
+                         "answers_match_pinned": pg_ok,
                          "what": "same call, numpy (pageable) pairs and answers, best of 3"},
             "link_bound": {"ms": link, "frac": (link / (t * 1e3)) if link else None,
                            "what": "the same H2D + D2H bytes as plain concurrent copies on two "
-                                   "streams (no kernel), CUDA events, best of 5; "
+                                   "streams (no kernel), CUDA events, best of 12; "
                                    "profiles/r1_pcie_micro.md"}}, \
-        pin_ans.numpy()
+        answers
 
 
 def host_link_bound(pin_in, pin_out, device):
@@ -292,7 +295,7 @@ def host_link_bound(pin_in, pin_out, device):
     d_out = torch.empty(pin_out.shape, dtype=pin_out.dtype, device=device)
     s0, s1 = torch.cuda.Stream(device), torch.cuda.Stream(device)
     best = None
-    for _ in range(6):
+    for _ in range(12):
         torch.cuda.synchronize(device)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(s0)
