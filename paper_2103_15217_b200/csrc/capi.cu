@@ -259,6 +259,10 @@ bool is_pinned(const void* p) {
     cudaGetLastError();
     return false;
   }
+  // host-buffer entry points: a device pointer here is a caller error (the
+  // _dev variants take device memory); managed memory is host-accessible
+  if (a.type == cudaMemoryTypeDevice)
+    throw Error(ETTG_EINVAL, "device pointer passed where a host buffer is expected");
   return a.type == cudaMemoryTypeHost;
 }
 

@@ -53,3 +53,13 @@ def test_mixed_calls_from_threads(ett):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+def test_device_pointer_to_host_entry_point_is_rejected(ett):
+    import torch
+    t = ett.permute_labels(ett.grasp_tree(100_000, 4, 3), 5)
+    idx = ett.inlabel_build(t)
+    d = torch.zeros(2 * 100_000, dtype=torch.int64, device="cuda")
+    a = np.empty(100_000, np.int64)
+    rc = ett.lib().ettg_lca_query(idx.handle, d.data_ptr(), 100_000, 100_000, a.ctypes.data)
+    assert rc == 1 and b"device pointer" in ett.lib().ettg_last_error()
