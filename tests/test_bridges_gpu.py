@@ -245,3 +245,19 @@ def test_adversarial_shapes_known_answer(ett, shape):
         fn = ett.tv_bridges if eng == "tv" else ett.hybrid_bridges
         mask = fn(ett.EdgeList(n, e)).is_bridge
         assert np.array_equal(mask, truth), (shape, eng)
+
+
+@pytest.mark.parametrize("order", ["sorted", "reversed", "shuffled"])
+def test_edge_order_independence(ett, order):
+    """Ordered inputs (sorted edge lists are common in files) give the same
+    mask; the second hooking pass links by hashed priority so id-sorted
+    chains stay shallow."""
+    n = 2_000_000
+    path = np.stack([np.arange(n - 1), np.arange(1, n)], 1)
+    cyc = np.concatenate([path, [[n - 1, 0]]])
+    rng = np.random.default_rng(3)
+    for edges, want in ((path, np.ones(n - 1, np.uint8)), (cyc, np.zeros(n, np.uint8))):
+        e = {"sorted": edges, "reversed": edges[::-1].copy(),
+             "shuffled": edges[rng.permutation(len(edges))]}[order]
+        for fn in (ett.tv_bridges, ett.hybrid_bridges):
+            assert np.array_equal(fn(ett.EdgeList(n, e)).is_bridge, want)
