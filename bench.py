@@ -658,13 +658,11 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (reference generators, seeds tree=1 permute=2 "
                                     "queries=3)",
-            "config": {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) "
-                                   "path tree, 16M sample_queries sharded across GPUs",
-                       "n": tree.n, "queries": args.q, "engine": "inlabel",
-                       "index_layout": layout, "inlabel_paths": labels,
-                       "parallelism": f"index replicated, queries sharded x{world}",
-                       "l2": f"flushed (256 MiB write) before every step; index "
-                             f"{idx.index_bytes() / 1e6:.0f} MB"},
+            "config": lca_config_b(tree.n, args.q),
+            "run": {"index_layout": layout, "inlabel_paths": labels,
+                    "parallelism": f"index replicated, queries sharded x{world}",
+                    "l2": f"flushed (256 MiB write) before every step; index "
+                          f"{idx.index_bytes() / 1e6:.0f} MB"},
             "e2e": e2e,
             "gpu_launches": sec["gpu_launches"],
             "build_ms": sec["build_ms"],
@@ -731,43 +729,74 @@ def main():
         dist.destroy_process_group()
 
 
+def lca_config_b(n, q):
+    """The config object both arms print (identical, so the driver can pair
+    them): BASELINE.json configs[1]."""
+    return {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) path tree, "
+                        "16M sample_queries",
+            "n": n, "queries": q, "engine": "inlabel", "seeds": {"tree": 1, "permute": 2,
+                                                                 "queries": 3}}
+
+
+def host_topology():
+    """lscpu-style sockets x cores x threads of this host, plus the cores this
+    process may run on (what the CPU baselines use)."""
+    topo = {"usable_cores": len(os.sched_getaffinity(0))}
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = dict(line.split(":", 1) for line in out.splitlines() if ":" in line)
+        kv = {k.strip(): v.strip() for k, v in kv.items()}
+        topo.update({"model": kv.get("Model name"), "sockets": int(kv.get("Socket(s)", 0)),
+                     "cores_per_socket": int(kv.get("Core(s) per socket", 0)),
+                     "threads_per_core": int(kv.get("Thread(s) per core", 0)),
+                     "cpus": int(kv.get("CPU(s)", 0))})
+    except Exception:
+        pass
+    return topo
+
+
 def reference_arm(args, rank, world):
-    """The reference's own CPU implementation (oracle/_ref = unmodified core/src
-    compiled here) on the same workload, metric and unit.  Rank 0 only."""
+    """The reference's own CPU implementation on the same workload, metric,
+    unit and config as our arm.  Everything here is the unmodified reference
+    (oracle/_ref = core/src compiled from its own sources): the generators
+    grasp_tree / permute_labels / sample_queries (core/src/generators.cpp:21-91),
+    inlabel_build untimed, and each step one answer_batch(inlabel_lca) over
+    all q queries (tools/ett_bench.cpp:136-150), with every host core.
+    Rank 0 only; the other ranks exit without work."""
     if rank != 0:
         return
     from oracle import oracle as orc
-    import paper_2103_15217_b200 as ett
     if not orc.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    cores = os.cpu_count() or 1
+    topo = host_topology()
+    cores = topo["usable_cores"]
     orc.Ref.set_workers(cores)
-    tree = make_tree(ett, args.n, 1)
-    pairs = ett.sample_queries(tree.n, args.q, 3)
-    h = orc.RefInlabel(tree.parent, tree.root)
-    sample = min(len(pairs), 2_000_000)
-    for s in range(args.warmup):
-        h.answer(pairs[:sample])
-    tot_ns = 0
-    for s in range(args.steps):
-        lo = (s * sample) % max(1, len(pairs) - sample + 1)
-        _, ns = h.answer(pairs[lo:lo + sample])
-        tot_ns += ns
-    v = sample * args.steps / (tot_ns / 1e9)
+    par0 = orc.Ref.grasp_tree(args.n, 1, 1)
+    parent, root = orc.Ref.permute_labels(par0, 0, 2)
+    del par0
+    pairs = orc.Ref.sample_queries(args.n, args.q, 3)
+    h = orc.RefInlabel(parent, root)
+    for _ in range(args.warmup):
+        h.answer(pairs)
+    step_ns = []
+    for _ in range(args.steps):
+        _, ns = h.answer(pairs)
+        step_ns.append(ns)
+    ms = float(np.mean(step_ns)) / 1e6
+    v = args.q / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ns / 1e6 / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "i64",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "i64",
             "data": "synthetic (reference generators, seeds tree=1 permute=2 queries=3)",
-            "config": {"workload": "LCA config B: permute_labels(grasp_tree(16M, gamma=1)) "
-                                   "path tree, 16M sample_queries",
-                       "n": tree.n, "queries": args.q, "engine": "inlabel"},
+            "config": lca_config_b(args.n, args.q),
             "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores,
-                             "kind": "reference",
-                             "sample": f"each step: answer_batch(inlabel_lca) over {sample} of "
-                                       f"the 16M queries; inlabel_build "
-                                       f"{h.build_ns / 1e9:.1f} s untimed"},
+                             "kind": "reference", "host": topo,
+                             "sample": f"each step: answer_batch(inlabel_lca) over all {args.q} "
+                                       f"queries (batch = q); inlabel_build "
+                                       f"{h.build_ns / 1e9:.2f} s untimed"},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
