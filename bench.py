@@ -314,24 +314,34 @@ def host_link_bound(pin_in, pin_out, device):
     return best
 
 
-def cpu_lca_baseline(tree, pairs_host, reps=3):
+def cpu_lca_baseline(parent, root, pairs_host, reps=3, one_worker_q=2_000_000, what=""):
     """The reference's own CPU path (oracle/_ref, compiled from the unmodified
-    core/src) on this host, all cores: inlabel_build untimed, answer_batch timed."""
+    core/src) on this host: inlabel_build untimed, answer_batch(inlabel_lca)
+    timed as tools/ett_bench.cpp:141-150 does, with every usable core (best
+    of `reps`) and with one worker on a prefix of `one_worker_q` queries.
+    Returns (baseline dict, reference answers over pairs_host)."""
     from oracle import oracle as orc
     if not orc.have_ref():
         return None, None
-    cores = os.cpu_count() or 1
+    topo = host_topology()
+    cores = topo["usable_cores"]
     orc.Ref.set_workers(cores)
-    h = orc.RefInlabel(tree.parent, tree.root)
+    h = orc.RefInlabel(parent, root)
     best = None
     answers = None
     for _ in range(reps):
         answers, ns = h.answer(pairs_host, len(pairs_host))
         best = ns if best is None else min(best, ns)
+    q1 = min(one_worker_q, len(pairs_host))
+    orc.Ref.set_workers(1)
+    _, ns1 = h.answer(pairs_host[:q1], q1)
+    orc.Ref.set_workers(cores)
     return {"value": len(pairs_host) / (best / 1e9), "unit": "queries/s", "cores": cores,
-            "kind": "reference",
-            "sample": f"answer_batch(inlabel_lca) over {len(pairs_host)} queries of this workload,"
-                      f" best of {reps}; inlabel_build {h.build_ns / 1e9:.1f} s untimed"}, answers
+            "kind": "reference", "host": topo,
+            "sample": f"answer_batch(inlabel_lca) over {len(pairs_host)} queries{what}, "
+                      f"best of {reps}; inlabel_build {h.build_ns / 1e9:.2f} s untimed",
+            "one_worker": {"value": q1 / (ns1 / 1e9), "cores": 1,
+                           "sample": f"the first {q1} of those queries"}}, answers
 
 
 def bridges_section(ett, args, device, peak):
@@ -419,17 +429,25 @@ def bridges_section(ett, args, device, peak):
     if args.cpu_baseline:
         from oracle import oracle as orc
         if orc.have_ref():
-            cores = os.cpu_count() or 1
+            topo = host_topology()
+            cores = topo["usable_cores"]
             orc.Ref.set_workers(cores)
-            Ws = args.cpu_road_side
-            gs, ts = ett.road_like_graph(Ws, Ws, 6, 3, Ws * Ws // 50, 5)
-            mask, ph = orc.Ref.bridges("tv", gs.n, gs.edges)
+            t0 = time.perf_counter()
+            mask, ph = orc.Ref.bridges("tv", n, g.edges)
+            wall = time.perf_counter() - t0
             out["cpu_baseline"] = {
-                "value": gs.m() / (ph[3] / 1e9), "unit": "edges/s", "cores": cores,
-                "kind": "reference",
-                "sample": f"tv_bridges on road-like W=H={Ws} (n={gs.n}, m={gs.m()}), "
-                          f"build_adjacency untimed; phases ns {ph[:3].tolist()}",
-                "parity_vs_truth": bool(np.array_equal(mask, ts))}
+                "value": m / (ph[3] / 1e9), "unit": "edges/s", "cores": cores,
+                "kind": "reference", "host": topo, "ms": ph[3] / 1e6,
+                "sample": f"the whole config D graph (n={n}, m={m}): tv_bridges(adj, &phases) "
+                          f"timed, build_adjacency untimed (tools/ett_bench.cpp:310-317); "
+                          f"phases ns spanning/euler/lowhigh {ph[:3].tolist()}; "
+                          f"{wall:.0f} s wall with build_adjacency",
+                "parity_vs_ours": bool(np.array_equal(mask, d_mask.cpu().numpy())),
+                "parity_vs_truth": bool(np.array_equal(mask, truth)),
+                "one_worker": {"value": None, "cores": 1,
+                               "note": "not run on config D: one worker needs ~15 min "
+                                       "(8 workers take 109 s, SURVEY.md 6); see "
+                                       "bridges_config_C.cpu_baseline.one_worker"}}
     return out
 
 
@@ -466,6 +484,13 @@ def lca_engines_config_a(ett, device):
         out[name] = {"value": q / (ms / 1e3), "ms": ms,
                      "agrees_with_inlabel": bool(torch.equal(ans, ref_ans))}
     out["inlabel_layout"] = idx.layout()[0]
+    from oracle import oracle as orc
+    if orc.have_ref():
+        pairs_host = pairs.cpu().numpy().astype(np.int64).reshape(-1, 2)
+        cb, want = cpu_lca_baseline(t.parent, t.root, pairs_host, reps=5,
+                                    one_worker_q=q, what=" (the whole config)")
+        cb["parity_vs_ours"] = bool(np.array_equal(want, ref_ans.cpu().numpy()))
+        out["cpu_baseline"] = cb
     return out
 
 
@@ -564,14 +589,87 @@ def bridges_config_c(ett, args, device, peak):
     if args.cpu_baseline:
         from oracle import oracle as orc
         if orc.have_ref():
-            cores = os.cpu_count() or 1
+            cores = host_topology()["usable_cores"]
             orc.Ref.set_workers(cores)
             mask, ph = orc.Ref.bridges("tv", n, g.edges)
+            orc.Ref.set_workers(1)
+            _, ph1 = orc.Ref.bridges("tv", n, g.edges)
+            orc.Ref.set_workers(cores)
             out["cpu_baseline"] = {
                 "value": m / (ph[3] / 1e9), "unit": "edges/s", "cores": cores,
-                "kind": "reference", "sample": "full config C, tv_bridges, build_adjacency "
-                                                "untimed (tools/ett_bench.cpp:310-317)",
-                "ms": ph[3] / 1e6, "parity_vs_truth": bool(np.array_equal(mask, truth))}
+                "kind": "reference", "host": host_topology(),
+                "sample": "full config C, tv_bridges, build_adjacency "
+                          "untimed (tools/ett_bench.cpp:310-317)",
+                "ms": ph[3] / 1e6, "parity_vs_truth": bool(np.array_equal(mask, truth)),
+                "parity_vs_ours": bool(np.array_equal(mask, d_mask.cpu().numpy())),
+                "one_worker": {"value": m / (ph1[3] / 1e9), "cores": 1, "ms": ph1[3] / 1e6,
+                               "sample": "the same call with ETT_WORKERS=1"}}
+    return out
+
+
+def config_e_block(ett, args, tree, sec, device, peak, world):
+    """Config E (BASELINE.json configs[4], the north-star 16M-tree scaling
+    config) as a first-class block: throughput, roofline, parity of 16 windows
+    spread over the query stream against the reference's answer_batch, e2e on
+    a bounded prefix through the C-ABI, and the reference CPU baseline."""
+    idx = sec["idx"]
+    layout = idx.layout()[0]
+    q_r = sec["q_rank"]
+    secs = sec["step_ms"] / 1e3
+    sample = ett.sample_queries(tree.n, min(args.e_sample, args.scaling_q), 3)
+    Lbar = lift_mean(idx, sample[:2_000_000])
+    Bq = 12 + 32 * (2 + Lbar)
+    kname = {"split": "k_lca_inlabel_split", "split6": "k_lca_inlabel_split6",
+             "wide": "k_lca_inlabel", "wide9": "k_lca_inlabel"}.get(layout, layout)
+    out = {"workload": "LCA config E: permute_labels(grasp_tree(16M, inf)), 1G sample_queries "
+                       "(counter mode, seed 3) sharded across GPUs",
+           "n": tree.n, "queries": args.scaling_q, "value": sec["value"], "unit": "queries/s",
+           "ms_per_step": sec["step_ms"], "steps": args.scaling_steps, "n_gpus": world,
+           "scaling": "strong", "build_ms": sec["build_ms"], "index_layout": layout,
+           "clocks": sec["clocks"],
+           "roofline": {"bound": "hbm", "achieved": Bq * q_r / secs / 1e9, "peak": peak[0],
+                        "unit": "GB/s", "frac": Bq * q_r / secs / 1e9 / peak[0],
+                        "traffic": ncu_traffic(f"{kname}_E"), "kernel": kname,
+                        "bytes_per_query": Bq, "lifts_per_query": Lbar,
+                        "model": "12 + 32 * (2 + lifts) B per query (SURVEY.md 8(d))",
+                        "note": "the model charges every gather a DRAM sector; the split6 "
+                                "node table (96 MB) is mostly L2-resident",
+                        "l2_gather": {"node_gathers_G_per_s": 2 * q_r / secs / 1e9,
+                                      "ceiling_G_per_s": L2_GATHER_CEILING.get(layout),
+                                      "frac": (2 * q_r / secs / 1e9 / L2_GATHER_CEILING[layout]
+                                               if layout in L2_GATHER_CEILING else None)},
+                        "l1_tag_stage": l1_tag_stage(f"{kname}_E", q_r, secs, sec["clocks"])}}
+    # parity: 16 windows of 1M queries spread across this rank's shard of the
+    # stream, answered by the timed kernel, against the reference answer_batch
+    from oracle import oracle as orc
+    rh = None
+    if orc.have_ref():
+        orc.Ref.set_workers(host_topology()["usable_cores"])
+        rh = orc.RefInlabel(tree.parent, tree.root)
+        win, ok, checked = 1_000_000, True, 0
+        for w in range(16):
+            a = (q_r - win) * w // 15 if q_r > win else 0
+            b = min(a + win, q_r)
+            pairs = sec["pairs"][2 * a:2 * b].cpu().numpy().astype(np.int64).reshape(-1, 2)
+            got = sec["ans"][a:b].cpu().numpy().astype(np.int64)
+            want, _ = rh.answer(pairs)
+            ok &= bool(np.array_equal(got, want))
+            checked += b - a
+        out["parity_vs_reference"] = ok
+        out["parity_sample"] = (f"{checked} queries in 16 windows of {win} spread over stream "
+                                f"positions [{sec['lo']}, {sec['lo'] + q_r}) vs the reference "
+                                f"answer_batch(inlabel_lca)")
+    # e2e on a bounded prefix through the C-ABI with pinned host buffers
+    if world == 1:
+        qe = len(sample)
+        e2e, e2e_ans = e2e_section(ett, idx, tree, qe, 0, qe, device, args.e2e_steps)
+        e2e["sample"] = f"the first {qe} queries of the stream"
+        out["e2e"] = e2e
+        if rh is not None:
+            del e2e_ans
+            cb, _ = cpu_lca_baseline(tree.parent, tree.root, sample, reps=2,
+                                     what=" (a prefix of the 1G-query stream)")
+            out["cpu_baseline"] = cb
     return out
 
 
@@ -586,12 +684,12 @@ def main():
     ap.add_argument("--q", type=int, default=16_000_000)
     ap.add_argument("--scaling-q", type=int, default=1_000_000_000)
     ap.add_argument("--scaling-steps", type=int, default=5)
+    ap.add_argument("--e-sample", type=int, default=64_000_000)
     ap.add_argument("--no-scaling", action="store_true")
     ap.add_argument("--no-bridges", action="store_true")
-    ap.add_argument("--road-side", type=int, default=5600)
-    ap.add_argument("--road-pendant", type=int, default=640_000)
+    ap.add_argument("--road-side", type=int, default=5657)
+    ap.add_argument("--road-pendant", type=int, default=20_761)
     ap.add_argument("--bridge-steps", type=int, default=5)
-    ap.add_argument("--cpu-road-side", type=int, default=1400)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--dist-backend", default="nccl")
@@ -684,7 +782,8 @@ def main():
             "answers_consistent_dev_vs_e2e": consistent,
         }
         if args.cpu_baseline and world == 1:
-            cb, ref_ans = cpu_lca_baseline(tree, pairs_host)
+            cb, ref_ans = cpu_lca_baseline(tree.parent, tree.root, pairs_host,
+                                           what=" (the whole config)")
             if cb is not None:
                 cb["parity_vs_ours"] = bool(np.array_equal(ref_ans, dev_ans))
                 line["cpu_baseline"] = cb
@@ -696,22 +795,7 @@ def main():
         secE = lca_section(ett, args, treeE, args.scaling_q, device, rank, world,
                            args.scaling_steps, 2, "E")
         if rank == 0:
-            line["scaling_config_E"] = {
-                "workload": "permute_labels(grasp_tree(16M, inf)), 1G queries sharded",
-                "value": secE["value"], "unit": "queries/s", "ms_per_step": secE["step_ms"],
-                "steps": args.scaling_steps, "build_ms": secE["build_ms"],
-                "index_layout": secE["idx"].layout()[0],
-                "survey_model_frac_140B": 140 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
-                / peak[0],
-                "l2_gather_frac": (2 * secE["q_rank"] / (secE["step_ms"] / 1e3) / 1e9
-                                   / L2_GATHER_CEILING[secE["idx"].layout()[0]]),
-                "l1_tag_stage": l1_tag_stage(
-                    {"split": "k_lca_inlabel_split_E",
-                     "split6": "k_lca_inlabel_split6_E"}.get(secE["idx"].layout()[0], ""),
-                    secE["q_rank"], secE["step_ms"] / 1e3, secE["clocks"]),
-                "note": "140 B/query assumes every gather is an HBM sector; the split6 "
-                        "layout's 96 MB node table is mostly L2-resident and lifts hit "
-                        "L2, so the survey-model fraction can exceed 1"}
+            line["scaling_config_E"] = config_e_block(ett, args, treeE, secE, device, peak, world)
         del secE
 
     # ---- bridges config D (replicas only: rank 0 of an N=1 run) -------------
