@@ -130,8 +130,10 @@ int ettg_lca_build_dev(const uint32_t* d_parent, int64_t n, int64_t root,
 void ettg_lca_free(ettg_lca* h);
 
 int ettg_lca_size(const ettg_lca* h, int64_t* n);
-/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact, 3 split, 4 split_own) and the number
- * of inlabel paths (distinct labels) in the tree (0 for attached replicas). */
+/* Layout the inlabel engine queries with (0 wide, 1 narrow, 2 compact,
+ * 3 split, 4 split_own, 5 split6, 6 wide9 -- also the layout code in the
+ * blob header written by ettg_lca_index_export_dev) and the number of
+ * inlabel paths (distinct labels) in the tree (0 for attached replicas). */
 int ettg_lca_layout(const ettg_lca* h, int* layout, int64_t* labels);
 /* Device time of the last build (ms), measured with CUDA events. */
 int ettg_lca_build_ms(const ettg_lca* h, double* ms);
@@ -140,7 +142,8 @@ int ettg_lca_build_ms(const ettg_lca* h, double* ms);
  * pairs = x0,y0,x1,y1,... (2q int64), answers = q int64.  batch < 1 ->
  * ETTG_EINVAL; answers do not depend on batch.  Ids outside [0,n) give
  * ETTG_ERANGE (the reference leaves them undefined).  Host copies are
- * pipelined with the query kernel on two streams. */
+ * pipelined with the query kernel on two streams; ids and answers cross
+ * the link as u32 (12 B per query), narrowed and widened by host threads. */
 int ettg_lca_query(const ettg_lca* h, const int64_t* pairs, int64_t q,
                    int64_t batch, int64_t* answers);
 int ettg_lca_query_engine(const ettg_lca* h, unsigned engine,
@@ -183,7 +186,8 @@ int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device,
 /* tv_bridges (core/src/bridges.cpp:311-316) on the undirected simple graph
  * edges = u0,v0,u1,v1,... (2m int64, ids in [0,n)).  is_bridge[m] gets 1
  * for bridges, 0 otherwise, indexed by input edge id.  Disconnected input
- * -> ETTG_EINVAL.  times may be NULL. */
+ * -> ETTG_EINVAL.  times may be NULL.  The ids cross the link narrowed to
+ * u32 by host threads (8 B per edge; ETTG_NARROW=0 ships pinned int64 as is). */
 int ettg_bridges(const int64_t* edges, int64_t n, int64_t m, int device,
                  uint8_t* is_bridge, ettg_phase_times* times);
 /* Device-resident: d_edges = 2m uint32, d_is_bridge = m bytes.  Returns
@@ -199,6 +203,34 @@ int ettg_bridges_dev_engine(const uint32_t* d_edges, int64_t n, int64_t m,
                             int device, int engine, uint8_t* d_is_bridge,
                             void* stream, ettg_phase_times* times);
 
+/* tv_bridges_on_tree (core/src/bridges.cpp:289-309): the TV criterion on a
+ * caller-supplied spanning tree (tree_mask[m], non-zero = tree edge), which
+ * replaces the hooking phase.  A mask that is not a spanning tree fails with
+ * the reference's check_is_tree messages (core/src/euler.cpp:13-33):
+ * ETTG_EINVAL "not a tree: m != n - 1" / "not a tree: disconnected".
+ * The mask cannot change the answer (bridges are a graph property). */
+int ettg_bridges_on_tree(const int64_t* edges, int64_t n, int64_t m, int device,
+                         const uint8_t* tree_mask, uint8_t* is_bridge,
+                         ettg_phase_times* times);
+int ettg_bridges_dev_on_tree(const uint32_t* d_edges, int64_t n, int64_t m,
+                             int device, const uint8_t* d_tree_mask,
+                             uint8_t* d_is_bridge, void* stream,
+                             ettg_phase_times* times);
+
+/* The engines over the reference's own input type, AdjacencyIndex
+ * (core/include/ett/graph.hpp:44-61): offsets[n+1], neighbors[2m],
+ * edge_ids[2m] -- what tv_bridges / ck_bridges / hybrid_bridges(const
+ * AdjacencyIndex&, PhaseTimes*) (core/include/ett/bridges.hpp:55-61) take.
+ * The edge list is recovered on the device by edge id (the slot of the
+ * lower endpoint); the three arrays cross the link narrowed to 4 B.
+ * tree_mask != NULL selects tv_bridges_on_tree (engine must be TV).
+ * A CSR whose slots do not cover every edge id consistently fails with
+ * ETTG_EINVAL "malformed adjacency index". */
+int ettg_bridges_csr(const int64_t* offsets, const int64_t* neighbors,
+                     const int64_t* edge_ids, int64_t n, int64_t m, int device,
+                     int engine, const uint8_t* tree_mask, uint8_t* is_bridge,
+                     ettg_phase_times* times);
+
 /* ---------------------------------------------------------- ingestion -- */
 /* build_adjacency (core/src/graph.cpp:135-173) on the device: offsets[n+1],
  * neighbors[2m], edge_ids[2m], slices sorted by (neighbor, edge id);
@@ -212,6 +244,11 @@ int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
 int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root,
                   int device, uint8_t* tree_mask, int64_t* level,
                   int64_t* parent, int64_t* parent_edge);
+/* bfs_tree(const AdjacencyIndex&, root) (core/include/ett/bridges.hpp:50). */
+int ettg_bfs_tree_csr(const int64_t* offsets, const int64_t* neighbors,
+                      const int64_t* edge_ids, int64_t n, int64_t m, int64_t root,
+                      int device, uint8_t* tree_mask, int64_t* level,
+                      int64_t* parent, int64_t* parent_edge);
 
 /* largest_component (core/src/graph.cpp:219-259): old_to_new[n] (-1 outside),
  * the component's node count in *n_out, and its edges (renumbered, input

@@ -7,8 +7,9 @@
 //   ett::answer_batch(lambda, queries, batch)    -> ettg::answer_batch(idx, queries, batch)
 //   ett::rmq_lca_build / rmq_lca                 -> ettg::rmq_lca_build / answer_batch
 //   ett::node_stats(linearize(...))              -> ettg::node_stats(tree)
-//   ett::tv_bridges(const AdjacencyIndex&, ...)  -> ettg::tv_bridges(const EdgeList&, ...)
-//   ett::ck_bridges / hybrid_bridges             -> ettg::ck_bridges / hybrid_bridges
+//   ett::tv_bridges(const AdjacencyIndex&, PhaseTimes*) -> ettg::tv_bridges (same signature;
+//     also an EdgeList overload), tv_bridges_on_tree, ck_bridges, hybrid_bridges,
+//     dfs_bridges (answered by the device CK engine), PhaseTimes{nanos, add()}
 //   ett::naive_build / naive_lca                 -> ettg::naive_build / answer_batch
 //   ett::ancestor_doubling_levels                -> ettg::ancestor_doubling_levels
 //   ett::build_adjacency / bfs_tree / largest_component -> same names
@@ -74,8 +75,13 @@ struct BridgeMask {
   }
 };
 
+// PhaseTimes (core/include/ett/bridges.hpp:34-38): wall nanoseconds of an
+// engine's phases under the reference's names; here the device time of each
+// phase, measured with CUDA events.
 struct PhaseTimes {
-  std::vector<std::pair<std::string, double>> ms;  // spanning, euler, lowhigh
+  std::vector<std::pair<std::string, i64>> nanos;
+
+  void add(std::string name, i64 ns) { nanos.emplace_back(std::move(name), ns); }
 };
 
 // Owns the device index; movable, not copyable.
@@ -157,40 +163,18 @@ inline NodeStats node_stats(const RootedTree& t, int device = 0) {
   return s;
 }
 
-// tv_bridges (bridges.hpp:55).  Takes the EdgeList the reference builds its
-// AdjacencyIndex from (build_adjacency is not needed on the device).
-inline BridgeMask bridges_engine(const EdgeList& g, int engine, PhaseTimes* times, int device) {
-  std::vector<uint8_t> mask(g.edges.size());
-  ettg_phase_times pt{};
-  check(ettg_bridges_engine(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), device,
-                            engine, mask.data(), &pt));
-  if (times) {  // phase names as the reference records them (bridges.cpp:292-337)
-    times->ms.emplace_back("spanning", pt.spanning_ms);
-    if (engine != ETTG_BRIDGES_CK) times->ms.emplace_back("euler", pt.euler_ms);
-    if (engine == ETTG_BRIDGES_TV) times->ms.emplace_back("lowhigh", pt.lowhigh_ms);
-    else times->ms.emplace_back("marking", pt.marking_ms);
-  }
-  BridgeMask out;
-  out.is_bridge.assign(mask.begin(), mask.end());
-  return out;
-}
-
-inline BridgeMask tv_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
-  return bridges_engine(g, ETTG_BRIDGES_TV, times, device);
-}
-inline BridgeMask ck_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
-  return bridges_engine(g, ETTG_BRIDGES_CK, times, device);
-}
-inline BridgeMask hybrid_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
-  return bridges_engine(g, ETTG_BRIDGES_HYBRID, times, device);
-}
-
-// AdjacencyIndex (graph.hpp:44-61), built on the device.
+// AdjacencyIndex (graph.hpp:44-61), the reference engines' input type.
 struct AdjacencyIndex {
-  i64 n = 0, m = 0;
-  std::vector<i64> offsets, neighbors, edge_ids;
+  i64 n = 0;
+  i64 m = 0;
+  std::vector<i64> offsets;    // n + 1
+  std::vector<i64> neighbors;  // 2m
+  std::vector<i64> edge_ids;   // 2m
+
+  i64 degree(i64 v) const { return offsets[v + 1] - offsets[v]; }
 };
 
+// build_adjacency (graph.hpp:63) on the device; bit-identical CSR.
 inline AdjacencyIndex build_adjacency(const EdgeList& g, int device = 0) {
   AdjacencyIndex a;
   a.n = g.n;
@@ -201,6 +185,95 @@ inline AdjacencyIndex build_adjacency(const EdgeList& g, int device = 0) {
   check(ettg_build_adjacency(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, a.m, device,
                              a.offsets.data(), a.neighbors.data(), a.edge_ids.data()));
   return a;
+}
+
+namespace detail {
+// Phase names as the reference records them (bridges.cpp:292-337).
+inline void phases(PhaseTimes* times, int engine, bool on_tree, const ettg_phase_times& pt) {
+  if (!times) return;
+  auto ns = [](double ms) { return static_cast<i64>(ms * 1e6 + 0.5); };
+  if (!on_tree) times->add("spanning", ns(pt.spanning_ms));
+  if (engine != ETTG_BRIDGES_CK) times->add("euler", ns(pt.euler_ms));
+  if (engine == ETTG_BRIDGES_TV)
+    times->add("lowhigh", ns(pt.lowhigh_ms));
+  else
+    times->add("marking", ns(pt.marking_ms));
+}
+inline BridgeMask mask_of(const std::vector<uint8_t>& m) {
+  BridgeMask out;
+  out.is_bridge.assign(m.begin(), m.end());
+  return out;
+}
+inline BridgeMask bridges_adj(const AdjacencyIndex& g, int engine, const std::vector<char>* tree,
+                              PhaseTimes* times, int device) {
+  std::vector<uint8_t> mask(static_cast<size_t>(g.m));
+  ettg_phase_times pt{};
+  if (tree && static_cast<i64>(tree->size()) != g.m)
+    throw std::invalid_argument("tree mask size mismatch");
+  check(ettg_bridges_csr(g.offsets.data(), g.neighbors.data(), g.edge_ids.data(), g.n, g.m,
+                         device, engine,
+                         tree ? reinterpret_cast<const uint8_t*>(tree->data()) : nullptr,
+                         mask.data(), &pt));
+  phases(times, engine, tree != nullptr, pt);
+  return mask_of(mask);
+}
+inline BridgeMask bridges_edges(const EdgeList& g, int engine, PhaseTimes* times, int device) {
+  std::vector<uint8_t> mask(g.edges.size());
+  ettg_phase_times pt{};
+  check(ettg_bridges_engine(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), device,
+                            engine, mask.data(), &pt));
+  phases(times, engine, false, pt);
+  return mask_of(mask);
+}
+}  // namespace detail
+
+// The engines with the reference's exact signatures (bridges.hpp:55-61), so
+// `using BridgeFn = BridgeMask (*)(const AdjacencyIndex&, PhaseTimes*)`
+// (tools/ett_bench.cpp:111) binds to them; the three-argument overloads pick
+// the device.
+inline BridgeMask tv_bridges(const AdjacencyIndex& g, PhaseTimes* times = nullptr) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_TV, nullptr, times, 0);
+}
+inline BridgeMask ck_bridges(const AdjacencyIndex& g, PhaseTimes* times = nullptr) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_CK, nullptr, times, 0);
+}
+inline BridgeMask hybrid_bridges(const AdjacencyIndex& g, PhaseTimes* times = nullptr) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_HYBRID, nullptr, times, 0);
+}
+// dfs_bridges (bridges.hpp:61) is the reference's sequential verification
+// engine; a depth-first search has no parallel form, so the drop-in answers
+// with the independent device algorithm -- BFS tree + Chaitanya-Kothapalli
+// marking -- which shares no phase with TV.  Same contract: the bridge mask.
+inline BridgeMask dfs_bridges(const AdjacencyIndex& g, PhaseTimes* times = nullptr) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_CK, nullptr, times, 0);
+}
+inline BridgeMask tv_bridges(const AdjacencyIndex& g, PhaseTimes* times, int device) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_TV, nullptr, times, device);
+}
+inline BridgeMask ck_bridges(const AdjacencyIndex& g, PhaseTimes* times, int device) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_CK, nullptr, times, device);
+}
+inline BridgeMask hybrid_bridges(const AdjacencyIndex& g, PhaseTimes* times, int device) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_HYBRID, nullptr, times, device);
+}
+// tv_bridges_on_tree (bridges.hpp:58-60): the caller's spanning tree
+// replaces hooking; a mask that is not a spanning tree throws
+// std::invalid_argument("not a tree: ...") like check_is_tree.
+inline BridgeMask tv_bridges_on_tree(const AdjacencyIndex& g, const std::vector<char>& tree_mask,
+                                     PhaseTimes* times = nullptr, int device = 0) {
+  return detail::bridges_adj(g, ETTG_BRIDGES_TV, &tree_mask, times, device);
+}
+
+// Also straight from the EdgeList the AdjacencyIndex is built from (no CSR
+// needed on the device: 8 B per edge over the link instead of 32).
+inline BridgeMask tv_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return detail::bridges_edges(g, ETTG_BRIDGES_TV, times, device);
+}
+inline BridgeMask ck_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return detail::bridges_edges(g, ETTG_BRIDGES_CK, times, device);
+}
+inline BridgeMask hybrid_bridges(const EdgeList& g, PhaseTimes* times = nullptr, int device = 0) {
+  return detail::bridges_edges(g, ETTG_BRIDGES_HYBRID, times, device);
 }
 
 // SpanningTree fields of bfs_tree (bridges.hpp:12-18, :50).
@@ -217,6 +290,19 @@ inline SpanningTree bfs_tree(const EdgeList& g, i64 root, int device = 0) {
   st.parent_edge.resize(g.n);
   check(ettg_bfs_tree(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(), root, device,
                       mask.data(), st.level.data(), st.parent.data(), st.parent_edge.data()));
+  st.is_tree_edge.assign(mask.begin(), mask.end());
+  return st;
+}
+
+inline SpanningTree bfs_tree(const AdjacencyIndex& g, i64 root, int device = 0) {
+  SpanningTree st;
+  std::vector<uint8_t> mask(static_cast<size_t>(g.m));
+  st.level.resize(g.n);
+  st.parent.resize(g.n);
+  st.parent_edge.resize(g.n);
+  check(ettg_bfs_tree_csr(g.offsets.data(), g.neighbors.data(), g.edge_ids.data(), g.n, g.m, root,
+                          device, mask.data(), st.level.data(), st.parent.data(),
+                          st.parent_edge.data()));
   st.is_tree_edge.assign(mask.begin(), mask.end());
   return st;
 }

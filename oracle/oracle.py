@@ -261,6 +261,17 @@ def ref_largest_component(n, edges):
     return o2n[:n], nn.value, out[:mm.value]
 
 
+def ref_spanning_tree_hooking(n, edges):
+    """The reference's deterministic hooking tree mask (core/src/bridges.cpp:105-158)."""
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    mask = np.empty(max(m, 1), np.uint8)
+    _rc(ref(), ref().ref_spanning_tree_hooking(i64(n), i64(m), _p(edges), _p(mask)),
+        "ref_last_error")
+    return mask[:m]
+
+
+Ref.spanning_tree_hooking = staticmethod(ref_spanning_tree_hooking)
 Ref.build_adjacency = staticmethod(ref_build_adjacency)
 Ref.largest_component = staticmethod(ref_largest_component)
 Ref.bfs_tree = staticmethod(ref_bfs_tree)

@@ -77,6 +77,12 @@ _SIGS = {
     "ettg_build_adjacency": ([p, i64, i64, C.c_int, p, p, p], C.c_int),
     "ettg_largest_component": ([p, i64, i64, C.c_int, p, i64p, i64p, p], C.c_int),
     "ettg_bfs_tree": ([p, i64, i64, i64, C.c_int, p, p, p, p], C.c_int),
+    "ettg_bfs_tree_csr": ([p, p, p, i64, i64, i64, C.c_int, p, p, p, p], C.c_int),
+    "ettg_bridges_on_tree": ([p, i64, i64, C.c_int, p, p, C.POINTER(PhaseTimes)], C.c_int),
+    "ettg_bridges_dev_on_tree": ([p, i64, i64, C.c_int, p, p, p, C.POINTER(PhaseTimes)],
+                                 C.c_int),
+    "ettg_bridges_csr": ([p, p, p, i64, i64, C.c_int, C.c_int, p, p, C.POINTER(PhaseTimes)],
+                         C.c_int),
     "ettg_list_rank_dev": ([p, i64, i64, p, C.c_int, p], C.c_int),
     "ettg_exclusive_scan_dev": ([p, i64, p, C.c_int, p], C.c_int),
     "ettg_sort_pairs_dev": ([p, p, i64, p, p, C.c_int, p], C.c_int),

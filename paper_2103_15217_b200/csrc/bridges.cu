@@ -62,6 +62,40 @@ __global__ void k_iota(u32* __restrict__ a, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
 }
 
+// AdjacencyIndex (core/include/ett/graph.hpp:44-61) -> the COO edge list by
+// edge id.  The slot of vertex v holding neighbour w and edge id e writes
+// edges[e] = (v, w) when v <= w: each edge is written by the slot of its
+// lower endpoint (both slots of a self-loop write the same pair), so the
+// reference's EdgeList is recovered exactly (build_adjacency keeps each
+// edge's (u, v) orientation only up to min/max, which tv_bridges never
+// reads).  Eight lanes per vertex stride over its slots (degree ~16 on the
+// road-like configs).  edges[] must be preset to 0xFF: an id no slot writes
+// stays out of range and fails the endpoint check downstream; decreasing
+// offsets raise flags[0].
+__global__ void k_csr_coo(const u32* __restrict__ off, const u32* __restrict__ nbr,
+                          const u32* __restrict__ eid, u32 n, uint2* __restrict__ edges,
+                          u32* flags) {
+  const u32 sub = threadIdx.x & 7;
+  u32 bad = 0;
+  for (u64 v = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 3; v < n;
+       v += (u64(gridDim.x) * blockDim.x) >> 3) {
+    const u32 a = off[v], b = off[v + 1];
+    bad |= a > b;
+    for (u32 s = a + sub; s < b; s += 8) {
+      const u32 w = nbr[s];
+      if (static_cast<u32>(v) <= w) edges[eid[s]] = make_uint2(static_cast<u32>(v), w);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+// A caller's spanning-tree mask (char per edge, any non-zero = tree edge) as
+// the 0/1 bytes the tree-edge compaction counts.
+__global__ void k_mask01(const uint8_t* __restrict__ in, u32 m, uint8_t* __restrict__ out) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    out[e] = in[e] != 0;
+}
+
 // Second-pass linking by priority: k_cc_hook_rest hooks a root under the
 // root of lower uf_prio (a bijective hash of the id), so the forest stays
 // shallow whatever the edge order.  Hooking the larger id under the smaller
@@ -713,9 +747,84 @@ void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* p
   CK_LAUNCH();
 }
 
+// Input of one bridges call: where the graph lives and in which form.
+struct BridgeIn {
+  enum Kind { kDevU32, kHostI64, kHostCsr } kind = kDevU32;
+  const void* edges = nullptr;  // uint2[m] on the device, or int64[2m] on the host
+  const int64_t *off = nullptr, *nbr = nullptr, *eid = nullptr;  // kHostCsr
+  const uint8_t* tree = nullptr;  // caller spanning tree (tv_bridges_on_tree), or null
+  bool tree_on_host = false;
+  // kHostI64 from pageable memory: narrowed to u32 by host threads while
+  // staging (8 B per edge over the link instead of 16)
+  bool narrow = false;
+};
+
+// Host int64 (u, v) pairs -> device u32 pairs with the reference's endpoint
+// range check (core/src/graph.cpp:141-143); returns true if one is out of
+// range.  Pinned input: one DMA of the int64 pairs and a device narrowing
+// pass (e64 is the landing buffer).  Pageable input: narrowed by the host
+// threads into the pinned stage, so the link carries 8 B per edge.
+bool upload_edges(const int64_t* h, u32 m, u32 n, longlong2* e64, uint2* e, u32* flags,
+                  int device, cudaStream_t st) {
+  if (!m) return false;
+  if (!is_pinned(h) || narrow_enabled()) {
+    return staged_h2d_narrow_u32(reinterpret_cast<u32*>(e), h, 2ull * m, n, false, device, st) !=
+           0;
+  }
+  copy_h2d(e64, h, static_cast<u64>(m) * 16, device, st);
+  k_edges_from_i64<<<std::min<unsigned>(sm_count(device) * 8, blocks_for(m, 256)), 256, 0, st>>>(
+      e64, m, n, e, flags);
+  CK_LAUNCH();
+  u32 bad = 0;
+  read_back(&bad, flags, 4, st);
+  return bad != 0;
+}
+
+// AdjacencyIndex on the host -> device COO edge list (k_csr_coo); the three
+// arrays are narrowed to u32 by the host threads while staging.  Errors are
+// the reference's (bad shape, endpoint range) plus "malformed adjacency
+// index" for ids the slots do not cover consistently.
+struct CsrScratch {
+  u32 *off = nullptr, *nbr = nullptr, *eid = nullptr;
+  void carve(Carver& c, u32 n, u32 m) {
+    off = c.take<u32>(static_cast<u64>(n) + 1);
+    nbr = c.take<u32>(2ull * m + 1);
+    eid = c.take<u32>(2ull * m + 1);
+  }
+};
+void check_csr_shape(const int64_t* off, i64 n, i64 m) {
+  if (!off) einval("null argument");
+  if (off[0] != 0 || off[n] != 2 * m) einval("malformed adjacency index: offsets");
+}
+void upload_csr(const BridgeIn& in, u32 n, u32 m, const CsrScratch& cs, uint2* e, u32* flags,
+                int device, cudaStream_t st) {
+  if (staged_h2d_narrow_u32(cs.off, in.off, static_cast<u64>(n) + 1, 2ull * m + 1, false, device,
+                            st))
+    einval("malformed adjacency index: offsets");
+  if (m) {
+    if (staged_h2d_narrow_u32(cs.nbr, in.nbr, 2ull * m, n, false, device, st))
+      einval("edge endpoint out of range");
+    if (staged_h2d_narrow_u32(cs.eid, in.eid, 2ull * m, m, false, device, st))
+      einval("malformed adjacency index: edge id out of range");
+    CK(cudaMemsetAsync(e, 0xFF, static_cast<u64>(m) * 8, st));
+  }
+  k_csr_coo<<<blocks_for(static_cast<u64>(n) * 8, 256, sm_count(device) * 16), 256, 0, st>>>(
+      cs.off, cs.nbr, cs.eid, n, e, flags);
+  CK_LAUNCH();
+  if (m) {
+    k_cc_range<<<std::min<unsigned>(sm_count(device) * 8, blocks_for(m, 256)), 256, 0, st>>>(
+        e, m, n, flags);
+    CK_LAUNCH();
+  }
+  u32 bad = 0;
+  read_back(&bad, flags, 4, st);
+  if (bad) einval("malformed adjacency index");
+}
+
 struct BridgeWs {
   longlong2* e64 = nullptr;
   uint2* edges = nullptr;
+  CsrScratch csr;
   u32* par = nullptr;
   uint8_t* tree = nullptr;
   u64* scan_m = nullptr;
@@ -741,7 +850,7 @@ struct BridgeWs {
   uint8_t* marked = nullptr;
   u32 *blevel = nullptr, *bparent = nullptr;
   BfsWs bfs;
-  void carve(Carver& c, u32 n, u32 m, bool host_i64, int engine) {
+  void carve(Carver& c, u32 n, u32 m, const BridgeIn& in, int engine) {
     const u32 k = 2 * (n - 1);
     if (engine != ETTG_BRIDGES_TV) {
       rec = c.take<uint2>(n);
@@ -753,10 +862,9 @@ struct BridgeWs {
       bparent = c.take<u32>(n);
       bfs.carve(c, n, m);
     }
-    if (host_i64) {
-      e64 = c.take<longlong2>(m);
-      edges = c.take<uint2>(m);
-    }
+    if (in.kind == BridgeIn::kHostI64 && !in.narrow) e64 = c.take<longlong2>(m);
+    if (in.kind != BridgeIn::kDevU32) edges = c.take<uint2>(m);
+    if (in.kind == BridgeIn::kHostCsr) csr.carve(c, n, m);
     par = c.take<u32>(n);
     tree = c.take<uint8_t>(m + 16);
     scan_m = c.take<u64>(scan_ws_words(m));
@@ -784,14 +892,15 @@ struct BridgeWs {
   }
 };
 
-void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int device,
-                 uint8_t* d_mask_user, uint8_t* h_mask, cudaStream_t st_in,
-                 ettg_phase_times* times, int engine) {
+void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_mask_user,
+                 uint8_t* h_mask, cudaStream_t st_in, ettg_phase_times* times, int engine) {
   if (n64 <= 0) einval("empty graph");
   if (n64 >= (i64(1) << 31) || m64 >= (i64(1) << 31) || m64 < 0)
     einval("graph too large for packed hooking keys");
   if (engine != ETTG_BRIDGES_TV && engine != ETTG_BRIDGES_CK && engine != ETTG_BRIDGES_HYBRID)
     einval("unknown bridges engine");
+  if (in.tree && engine != ETTG_BRIDGES_TV) einval("a caller spanning tree needs the TV engine");
+  const bool on_tree = in.tree != nullptr;
   const u32 n = static_cast<u32>(n64), m = static_cast<u32>(m64);
   const int sms = sm_count(device);
   const unsigned g = sms * 8;
@@ -807,12 +916,12 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
 
   BridgeWs ws;
   Carver c;
-  ws.carve(c, n, m, host_i64, engine);
+  ws.carve(c, n, m, in, engine);
   uint8_t* d_mask = d_mask_user;
   if (!d_mask) d_mask = c.take<uint8_t>(m + 16);
   Lease lease(device, st, c.off);
   c = Carver{lease.base()};
-  ws.carve(c, n, m, host_i64, engine);
+  ws.carve(c, n, m, in, engine);
   if (!d_mask_user) d_mask = c.take<uint8_t>(m + 16);
 
   cudaEvent_t ev[4];
@@ -842,17 +951,37 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   } copy_guard;
   const uint2* edges;
   bool hooked = false;  // spanning forest hooked while the edge list streamed in
-  if (host_i64) {
-    // Host edge lists: the H2D copy dominates an end-to-end call (16 B per
-    // edge over PCIe vs ~35 ps of device work), and union-find hooking is
+  u32 kChunk = 16u << 20;
+  if (const char* e = std::getenv("ETTG_BR_CHUNK")) kChunk = std::max(1, std::atoi(e));
+  bool stream_hook = !on_tree && engine != ETTG_BRIDGES_CK && m > 2 * static_cast<u64>(kChunk);
+  if (const char* e = std::getenv("ETTG_BR_STREAM")) stream_hook &= std::atoi(e) != 0;
+  if (in.kind == BridgeIn::kHostI64 && in.narrow) {
+    // Pageable host edge list: the host threads narrow each chunk to u32
+    // pairs while filling the pinned stage (8 B per edge over the link); the
+    // hooking of a chunk is enqueued behind its copy on the same stream.
+    std::function<void(size_t, size_t)> hook_chunk;
+    if (stream_hook) {
+      k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+      CK_LAUNCH();
+      hook_chunk = [&](size_t lo, size_t cnt) {  // lo, cnt in u32 words (pairs: even)
+        launch_hook(ws.edges + lo / 2, EdgeSubset{static_cast<u32>(cnt / 2), 1, 0}, n, ws.par,
+                    ws.tree + lo / 2, ws.words, sms, st);
+      };
+    }
+    if (m && staged_h2d_narrow_u32(reinterpret_cast<u32*>(ws.edges),
+                                   static_cast<const int64_t*>(in.edges), 2ull * m, n, false,
+                                   device, st, hook_chunk))
+      einval("edge endpoint out of range");
+    hooked = stream_hook;
+    edges = ws.edges;
+  } else if (in.kind == BridgeIn::kHostI64) {
+    // Pinned host edge list: the H2D copy dominates an end-to-end call (16 B
+    // per edge over PCIe vs ~35 ps of device work), and union-find hooking is
     // incremental, so large inputs arrive in 16M-edge chunks on a copy stream
     // while the previous chunk is converted and hooked (all its edges, no
     // sampling: the sampled two-pass order only matters when hooking is on
     // the critical path).  Any spanning forest gives the same bridge mask.
-    u32 kChunk = 16u << 20;
-    if (const char* e = std::getenv("ETTG_BR_CHUNK")) kChunk = std::max(1, std::atoi(e));
-    bool stream_hook = engine != ETTG_BRIDGES_CK && m > 2 * static_cast<u64>(kChunk);
-    if (const char* e = std::getenv("ETTG_BR_STREAM")) stream_hook &= std::atoi(e) != 0;
+    const void* edges_in = in.edges;
     if (stream_hook) {
       CK(cudaStreamCreateWithFlags(&copy_guard.s, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&copy_guard.e, cudaEventDisableTiming));
@@ -882,8 +1011,30 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       CK_LAUNCH();
     }
     edges = ws.edges;
+  } else if (in.kind == BridgeIn::kHostCsr) {
+    upload_csr(in, n, m, ws.csr, ws.edges, ws.words, device, st);
+    edges = ws.edges;
   } else {
-    edges = static_cast<const uint2*>(edges_in);  // range-checked inside k_cc_hook / below
+    edges = static_cast<const uint2*>(in.edges);  // range-checked inside k_cc_hook / below
+  }
+  if (on_tree) {
+    // tv_bridges_on_tree (core/src/bridges.cpp:289-309): the caller's tree
+    // replaces hooking.  Its edge count and acyclicity are checked by the
+    // tour (count = words[1], cover = the list ranking's error flag).
+    if (m) {
+      const uint8_t* src = in.tree;
+      if (in.tree_on_host) {
+        copy_h2d(ws.tree, in.tree, m, device, st);
+        src = ws.tree;
+      }
+      k_mask01<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(src, m, ws.tree);
+      CK_LAUNCH();
+      if (in.kind == BridgeIn::kDevU32) {
+        k_cc_range<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
+        CK_LAUNCH();
+      }
+    }
+    hooked = true;
   }
   if (m) CK(cudaMemsetAsync(d_mask, 0, m, st));
   tr.mark("input");
@@ -893,7 +1044,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   if (engine == ETTG_BRIDGES_CK) {
     // ---- ck_bridges (core/src/bridges.cpp:477-485): BFS tree + marking ----
     // BFS indexes vertices straight from the edge list: check the range first
-    if (!host_i64 && m) {
+    if (in.kind == BridgeIn::kDevU32 && m) {
       k_cc_range<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
       CK_LAUNCH();
     }
@@ -915,6 +1066,7 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
       k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
       CK_LAUNCH();
     }
+    // CK validates endpoints itself; device input to TV / hybrid is checked by k_cc_hook
     if (m && !hooked) {
       // Hook every 4th edge first, compress, then the rest (round-1 A/B on
       // config D: 3.28 vs 4.02 ms for one pass; ETTG_CC_SAMPLE overrides).
@@ -1024,6 +1176,10 @@ void run_bridges(const void* edges_in, bool host_i64, i64 n64, i64 m64, int devi
   if (abort) CK(cudaMemcpyAsync(w, abort, sizeof w, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (w[0]) einval("edge endpoint out of range");
+  if (on_tree) {  // the reference's check_is_tree messages (core/src/euler.cpp:13-33)
+    if (w[1] != n - 1) einval("not a tree: m != n - 1");
+    if (lerr) einval("not a tree: disconnected");
+  }
   if (w[1] != n - 1) einval("disconnected graph; extract the largest component first");
   if (lerr) throw Error(ETTG_EINTERNAL, "bridges: spanning-tree tour ranking failed");
   if (times) {
@@ -1056,7 +1212,12 @@ int ettg_bridges_engine(const int64_t* edges, int64_t n, int64_t m, int device, 
   return guard([&] {
     if ((!edges || !is_bridge) && m > 0) einval("null argument");
     DeviceScope ds(device);
-    run_bridges(edges, true, n, m, device, nullptr, is_bridge, nullptr, times, engine);
+    check_host_ptr(is_bridge);
+    BridgeIn in;
+    in.kind = BridgeIn::kHostI64;
+    in.edges = edges;
+    in.narrow = m > 0 && (!is_pinned(edges) || narrow_enabled());
+    run_bridges(in, n, m, device, nullptr, is_bridge, nullptr, times, engine);
   });
 }
 
@@ -1072,8 +1233,69 @@ int ettg_bridges_dev_engine(const uint32_t* d_edges, int64_t n, int64_t m, int d
   return guard([&] {
     if ((!d_edges || !d_is_bridge) && m > 0) einval("null argument");
     DeviceScope ds(device);
-    run_bridges(d_edges, false, n, m, device, d_is_bridge, nullptr,
-                static_cast<cudaStream_t>(stream), times, engine);
+    BridgeIn in;
+    in.edges = d_edges;
+    run_bridges(in, n, m, device, d_is_bridge, nullptr, static_cast<cudaStream_t>(stream), times,
+                engine);
+  });
+}
+
+int ettg_bridges_on_tree(const int64_t* edges, int64_t n, int64_t m, int device,
+                         const uint8_t* tree_mask, uint8_t* is_bridge, ettg_phase_times* times) {
+  return guard([&] {
+    if ((!edges || !is_bridge || !tree_mask) && m > 0) einval("null argument");
+    DeviceScope ds(device);
+    check_host_ptr(is_bridge);
+    check_host_ptr(tree_mask);
+    BridgeIn in;
+    in.kind = BridgeIn::kHostI64;
+    in.edges = edges;
+    in.narrow = m > 0 && (!is_pinned(edges) || narrow_enabled());
+    static const uint8_t kEmpty = 0;
+    in.tree = m ? tree_mask : &kEmpty;
+    in.tree_on_host = true;
+    run_bridges(in, n, m, device, nullptr, is_bridge, nullptr, times, ETTG_BRIDGES_TV);
+  });
+}
+
+int ettg_bridges_dev_on_tree(const uint32_t* d_edges, int64_t n, int64_t m, int device,
+                             const uint8_t* d_tree_mask, uint8_t* d_is_bridge, void* stream,
+                             ettg_phase_times* times) {
+  return guard([&] {
+    if ((!d_edges || !d_is_bridge || !d_tree_mask) && m > 0) einval("null argument");
+    DeviceScope ds(device);
+    BridgeIn in;
+    in.edges = d_edges;
+    static const uint8_t kEmpty = 0;
+    in.tree = m ? d_tree_mask : &kEmpty;
+    run_bridges(in, n, m, device, d_is_bridge, nullptr, static_cast<cudaStream_t>(stream), times,
+                ETTG_BRIDGES_TV);
+  });
+}
+
+int ettg_bridges_csr(const int64_t* offsets, const int64_t* neighbors, const int64_t* edge_ids,
+                     int64_t n, int64_t m, int device, int engine, const uint8_t* tree_mask,
+                     uint8_t* is_bridge, ettg_phase_times* times) {
+  return guard([&] {
+    if (n <= 0) einval("empty graph");
+    if ((!neighbors || !edge_ids || !is_bridge) && m > 0) einval("null argument");
+    if (n >= (int64_t(1) << 31) || m >= (int64_t(1) << 31) || m < 0)
+      einval("graph too large for packed hooking keys");
+    check_csr_shape(offsets, n, m);
+    DeviceScope ds(device);
+    check_host_ptr(is_bridge);
+    check_host_ptr(tree_mask);
+    BridgeIn in;
+    in.kind = BridgeIn::kHostCsr;
+    in.off = offsets;
+    in.nbr = neighbors;
+    in.eid = edge_ids;
+    static const uint8_t kEmpty = 0;
+    if (tree_mask) {  // tv_bridges_on_tree
+      in.tree = m ? tree_mask : &kEmpty;
+      in.tree_on_host = true;
+    }
+    run_bridges(in, n, m, device, nullptr, is_bridge, nullptr, times, engine);
   });
 }
 
@@ -1121,15 +1343,8 @@ int ettg_build_adjacency(const int64_t* edges, int64_t n, int64_t m, int device,
     ws.carve(c, nn, mm);
     const int sms = sm_count(device);
     CK(cudaMemsetAsync(ws.flags, 0, 32, st));
-    if (mm) {
-      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
-      k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
-          ws.e64, mm, nn, ws.e, ws.flags);
-      CK_LAUNCH();
-    }
-    u32 bad = 0;
-    read_back(&bad, ws.flags, 4, st);
-    if (bad) einval("edge endpoint out of range");
+    if (upload_edges(edges, mm, nn, ws.e64, ws.e, ws.flags, device, st))
+      einval("edge endpoint out of range");
     build_csr(ws.e, nn, mm, ws.offs, ws.nbr, ws.eid, ws.csr, st, sms);
     // values < 2^31: the kNone mapping of the widening never applies
     staged_d2h_widen_u32(offsets, ws.offs, static_cast<u64>(nn) + 1, device, st);
@@ -1190,15 +1405,8 @@ int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int devic
     CK(cudaMemsetAsync(ws.counts, 0, 32, st));
     CK(cudaMemsetAsync(ws.size, 0, nn * 4ull, st));
     CK(cudaMemsetAsync(ws.best, 0, 8, st));
-    if (mm) {
-      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
-      k_edges_from_i64<<<std::min(g, blocks_for(mm, 256)), 256, 0, st>>>(ws.e64, mm, nn, ws.e,
-                                                                         ws.flags);
-      CK_LAUNCH();
-    }
-    u32 bad = 0;
-    read_back(&bad, ws.flags, 4, st);
-    if (bad) einval("edge endpoint out of range");
+    if (upload_edges(edges, mm, nn, ws.e64, ws.e, ws.flags, device, st))
+      einval("edge endpoint out of range");
     k_iota<<<std::min(g, blocks_for(nn, 256)), 256, 0, st>>>(ws.par, nn);
     CK_LAUNCH();
     if (mm) {
@@ -1223,65 +1431,94 @@ int ettg_largest_component(const int64_t* edges, int64_t n, int64_t m, int devic
   });
 }
 
+namespace {
+// bfs_tree (core/src/bridges.cpp:198-249) from an EdgeList or an AdjacencyIndex.
+void bfs_tree_impl(const BridgeIn& in, int64_t n, int64_t m, int64_t root, int device,
+                   uint8_t* tree_mask, int64_t* level, int64_t* parent, int64_t* parent_edge) {
+  if (n <= 0 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 31))
+    einval("graph too large for packed hooking keys");
+  if (root < 0 || root >= n) einval("root out of range");
+  if ((m && !tree_mask) || !level || !parent || !parent_edge) einval("null argument");
+  if (in.kind == BridgeIn::kHostCsr) check_csr_shape(in.off, n, m);
+  DeviceScope ds(device);
+  for (const void* p : {static_cast<const void*>(tree_mask), static_cast<const void*>(level),
+                        static_cast<const void*>(parent), static_cast<const void*>(parent_edge)})
+    check_host_ptr(p);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct SG {
+    cudaStream_t s;
+    ~SG() { cudaStreamDestroy(s); }
+  } sg{st};
+  const u32 nn = static_cast<u32>(n), mm = static_cast<u32>(m);
+  const bool csr = in.kind == BridgeIn::kHostCsr;
+  struct Ws {
+    longlong2* e64;
+    uint2* e;
+    u32 *lev, *par, *pe, *flags;
+    uint8_t* tree;
+    CsrScratch cs;
+    BfsWs bfs;
+    void carve(Carver& c, u32 n, u32 m, bool csr) {
+      e64 = c.take<longlong2>(m + 1);
+      e = c.take<uint2>(m + 1);
+      lev = c.take<u32>(n);
+      par = c.take<u32>(n);
+      pe = c.take<u32>(n);
+      flags = c.take<u32>(8);
+      tree = c.take<uint8_t>(m + 16);
+      if (csr) cs.carve(c, n, m);
+      bfs.carve(c, n, m);
+    }
+  } ws;
+  Carver c;
+  ws.carve(c, nn, mm, csr);
+  Lease lease(device, st, c.off);
+  c = Carver{lease.base()};
+  ws.carve(c, nn, mm, csr);
+  const int sms = sm_count(device);
+  CK(cudaMemsetAsync(ws.flags, 0, 32, st));
+  CK(cudaMemsetAsync(ws.tree, 0, mm + 16, st));
+  if (csr) {
+    upload_csr(in, nn, mm, ws.cs, ws.e, ws.flags, device, st);
+  } else if (upload_edges(static_cast<const int64_t*>(in.edges), mm, nn, ws.e64, ws.e, ws.flags,
+                          device, st)) {
+    einval("edge endpoint out of range");
+  }
+  const u32 reached = run_bfs(ws.e, nn, mm, static_cast<u32>(root), ws.lev, ws.par, ws.pe,
+                              ws.tree, ws.bfs, st, sms);
+  if (reached != nn) einval("disconnected graph; extract the largest component first");
+  staged_d2h_widen_u32(level, ws.lev, nn, device, st);
+  staged_d2h_widen_u32(parent, ws.par, nn, device, st);
+  staged_d2h_widen_u32(parent_edge, ws.pe, nn, device, st);
+  if (mm) copy_d2h(tree_mask, ws.tree, mm, device, st);
+  CK(cudaStreamSynchronize(st));
+}
+}  // namespace
+
 int ettg_bfs_tree(const int64_t* edges, int64_t n, int64_t m, int64_t root, int device,
                   uint8_t* tree_mask, int64_t* level, int64_t* parent, int64_t* parent_edge) {
   return guard([&] {
-    if (n <= 0 || n >= (int64_t(1) << 31) || m < 0 || m >= (int64_t(1) << 31))
-      einval("graph too large for packed hooking keys");
-    if (root < 0 || root >= n) einval("root out of range");
-    if ((!edges && m) || (m && !tree_mask) || !level || !parent || !parent_edge)
-      einval("null argument");
-    DeviceScope ds(device);
-    cudaStream_t st;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct SG {
-      cudaStream_t s;
-      ~SG() { cudaStreamDestroy(s); }
-    } sg{st};
-    const u32 nn = static_cast<u32>(n), mm = static_cast<u32>(m);
-    struct Ws {
-      longlong2* e64;
-      uint2* e;
-      u32 *lev, *par, *pe, *flags;
-      uint8_t* tree;
-      BfsWs bfs;
-      void carve(Carver& c, u32 n, u32 m) {
-        e64 = c.take<longlong2>(m + 1);
-        e = c.take<uint2>(m + 1);
-        lev = c.take<u32>(n);
-        par = c.take<u32>(n);
-        pe = c.take<u32>(n);
-        flags = c.take<u32>(8);
-        tree = c.take<uint8_t>(m + 16);
-        bfs.carve(c, n, m);
-      }
-    } ws;
-    Carver c;
-    ws.carve(c, nn, mm);
-    Lease lease(device, st, c.off);
-    c = Carver{lease.base()};
-    ws.carve(c, nn, mm);
-    const int sms = sm_count(device);
-    CK(cudaMemsetAsync(ws.flags, 0, 32, st));
-    CK(cudaMemsetAsync(ws.tree, 0, mm + 16, st));
-    if (mm) {
-      copy_h2d(ws.e64, edges, static_cast<u64>(mm) * 16, device, st);
-      k_edges_from_i64<<<std::min<unsigned>(sms * 8, blocks_for(mm, 256)), 256, 0, st>>>(
-          ws.e64, mm, nn, ws.e, ws.flags);
-      CK_LAUNCH();
-    }
-    u32 bad = 0;
-    read_back(&bad, ws.flags, 4, st);
-    if (bad) einval("edge endpoint out of range");
-    const u32 reached =
-        run_bfs(ws.e, nn, mm, static_cast<u32>(root), ws.lev, ws.par, ws.pe, ws.tree, ws.bfs, st,
-                sms);
-    if (reached != nn) einval("disconnected graph; extract the largest component first");
-    staged_d2h_widen_u32(level, ws.lev, nn, device, st);
-    staged_d2h_widen_u32(parent, ws.par, nn, device, st);
-    staged_d2h_widen_u32(parent_edge, ws.pe, nn, device, st);
-    if (mm) copy_d2h(tree_mask, ws.tree, mm, device, st);
-    CK(cudaStreamSynchronize(st));
+    if (!edges && m) einval("null argument");
+    BridgeIn in;
+    in.kind = BridgeIn::kHostI64;
+    in.edges = edges;
+    bfs_tree_impl(in, n, m, root, device, tree_mask, level, parent, parent_edge);
+  });
+}
+
+int ettg_bfs_tree_csr(const int64_t* offsets, const int64_t* neighbors, const int64_t* edge_ids,
+                      int64_t n, int64_t m, int64_t root, int device, uint8_t* tree_mask,
+                      int64_t* level, int64_t* parent, int64_t* parent_edge) {
+  return guard([&] {
+    if ((!neighbors || !edge_ids) && m) einval("null argument");
+    if (n <= 0) einval("graph too large for packed hooking keys");
+    BridgeIn in;
+    in.kind = BridgeIn::kHostCsr;
+    in.off = offsets;
+    in.nbr = neighbors;
+    in.eid = edge_ids;
+    bfs_tree_impl(in, n, m, root, device, tree_mask, level, parent, parent_edge);
   });
 }
 

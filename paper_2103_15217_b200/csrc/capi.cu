@@ -147,6 +147,14 @@ void par_copy_impl(char* dst, const char* src, size_t n) {
 }  // namespace
 
 void par_copy(char* dst, const char* src, size_t n) { par_copy_impl(dst, src, n); }
+int host_thread_count() { return host_threads(); }
+bool narrow_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ETTG_NARROW");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 StageLease::StageLease(int device) : s_(&stage_for(device)) {
   Stage& s = *static_cast<Stage*>(s_);
@@ -251,6 +259,43 @@ void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, i
     for (long i = 0; i < static_cast<long>(n); ++i)
       out[i] = in[i] == 0xFFFFFFFFu ? int64_t(-1) : static_cast<int64_t>(in[i]);
   }
+}
+
+u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
+                          bool allow_none, int device, cudaStream_t st,
+                          const std::function<void(size_t, size_t)>& on_chunk) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const size_t per = kStageChunk / sizeof(uint32_t);
+  u64 bad = 0;
+  int k = 0;
+  for (size_t lo = 0; lo < count; lo += per, k ^= 1) {
+    const size_t n = std::min(per, count - lo);
+    CK(cudaEventSynchronize(s.done[k]));  // the copy that last read this buffer
+    uint32_t* out = reinterpret_cast<uint32_t*>(s.buf[k]);
+    const int64_t* in = h_src + lo;
+    u64 b = 0;
+#pragma omp parallel for schedule(static) num_threads(host_threads()) reduction(+ : b) \
+    if (n > 65536)
+    for (long i = 0; i < static_cast<long>(n); ++i) {
+      const uint64_t v = static_cast<uint64_t>(in[i]);
+      const bool ok = v < bound || (allow_none && in[i] == -1);
+      b += !ok;
+      out[i] = ok ? static_cast<uint32_t>(v) : 0xFFFFFFFFu;
+    }
+    bad += b;
+    if (b) break;  // the caller fails the call: skip the rest
+    CK(cudaMemcpyAsync(d_dst + lo, out, n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(s.done[k], st));
+    if (on_chunk) on_chunk(lo, n);
+  }
+  CK(cudaStreamSynchronize(st));
+  return bad;
+}
+
+void check_host_ptr(const void* p) {
+  if (p) (void)is_pinned(p);
 }
 
 bool is_pinned(const void* p) {

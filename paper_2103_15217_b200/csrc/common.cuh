@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <stdexcept>
 #include <string>
 
@@ -226,14 +227,31 @@ class StageLease {
   void* s_;
 };
 void par_copy(char* dst, const char* src, size_t n);  // host threads
+int host_thread_count();  // threads of the host-side staging passes
+// Host int64 ids cross the link narrowed to u32 (default; ETTG_NARROW=0
+// sends pinned int64 buffers as they are, for A/B runs).
+bool narrow_enabled();
 // D2H of `count` u32 values widened to int64 (0xFFFFFFFF -> -1, the
 // reference's kNone) by the host threads as the pinned chunks land.
 void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, int device,
                           cudaStream_t st);
 // Raw staged D2H into a pageable host buffer (host threads drain the chunks).
 void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st);
+// H2D of `count` int64 values narrowed to u32 by the host threads while they
+// fill the pinned stage (the link then carries 4 B per id instead of 8).
+// Values must lie in [0, bound), or be -1 when allow_none (-> 0xFFFFFFFF);
+// the others are stored as 0xFFFFFFFF and counted in the return value (the
+// caller raises its own error).  on_chunk(lo, n), if given, runs after chunk
+// [lo, lo + n) is enqueued on `st` (to enqueue its consumers).  Synchronises st.
+u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
+                          bool allow_none, int device, cudaStream_t st,
+                          const std::function<void(size_t, size_t)>& on_chunk = {});
 // Page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory) host memory?
+// Throws ETTG_EINVAL for a device pointer (host-buffer entry points).
 bool is_pinned(const void* p);
+// is_pinned for its check only: host-buffer entry points call it on every
+// caller buffer, whatever its size or the path it takes.
+void check_host_ptr(const void* p);
 // Host <-> device copies of caller buffers: async when the host side is
 // pinned, staged (and synchronous) when it is pageable.
 void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);

@@ -1541,40 +1541,59 @@ int ettg_lca_build_ms(const ettg_lca* h, double* ms) {
 }
 
 namespace {
-// Pageable caller buffers (std::vector, numpy): host threads copy each chunk
-// of pairs into a pinned staging buffer and the previous chunk's answers out
-// of the other while the device moves and answers the current one.  A plain
-// cudaMemcpy from / to pageable memory runs at ~10 / ~4 GB/s.
-void query_host_staged(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
+// Host int64 pairs -> int64 answers with 12 B per query over the link (u32
+// pairs in, u32 answers out) instead of 24.  The host threads narrow chunk c
+// into pinned stage buffer c & 1 (while the copy engine and the kernel work
+// on chunk c - 1 on the other stream) and widen the answers of chunk c - 2
+// out of it; a B200 host narrows int64 at ~144 GB/s with 16 threads
+// (tools/host_narrow_micro.cpp), faster than PCIe moves the narrowed bytes,
+// so the call runs at the link rate of half the bytes whether the caller's
+// buffers are pinned or pageable.  Ids outside [0, 2^32) are stored as
+// 0xFFFFFFFF, which the kernel's range check rejects (ETTG_ERANGE).
+void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
                        int64_t* answers) {
   StageLease sl(h->device);
-  const u64 per = (StageLease::bytes() / 24) & ~u64(1);  // 16-B pairs + 8-B answers
+  const u64 per = (StageLease::bytes() / 12) & ~u64(7);  // u32 pair + u32 answer per query
   ensure_qbuf(h, per);
-  cudaStream_t st = h->qs[0];
-  CK(cudaMemsetAsync(h->qerr, 0, 8, st));
-  longlong2* dp = reinterpret_cast<longlong2*>(h->qmem);
-  long long* da = reinterpret_cast<long long*>(h->qmem + h->qchunk * 16);
+  CK(cudaMemsetAsync(h->qerr, 0, 8, h->qs[0]));
+  CK(cudaStreamSynchronize(h->qs[0]));
   const u64 chunks = (q + per - 1) / per;
-  auto drain = [&](u64 c) {  // answers of chunk c: staging -> caller
+  const int threads = host_thread_count();
+  auto drain = [&](u64 c) {  // answers of chunk c: stage -> caller, widened
     const u64 lo = c * per, cnt = std::min(per, q - lo);
     CK(cudaEventSynchronize(sl.done(c & 1)));
-    par_copy(reinterpret_cast<char*>(answers + lo), sl.buf(c & 1) + per * 16, cnt * 8);
+    const u32* in = reinterpret_cast<const u32*>(sl.buf(c & 1) + per * 8);
+    int64_t* out = answers + lo;
+#pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 65536)
+    for (long i = 0; i < static_cast<long>(cnt); ++i) out[i] = in[i];
   };
   for (u64 c = 0; c < chunks; ++c) {
     const int k = c & 1;
-    if (c >= 2) drain(c - 2);  // frees buffer k
+    if (c >= 2) drain(c - 2);  // frees stage buffer k
     const u64 lo = c * per, cnt = std::min(per, q - lo);
-    par_copy(sl.buf(k), reinterpret_cast<const char*>(pairs + 2 * lo), cnt * 16);
-    CK(cudaMemcpyAsync(dp, sl.buf(k), cnt * 16, cudaMemcpyHostToDevice, st));
-    launch_query(h, engine, PairsI64{dp}, AnsI64{da}, cnt, h->qerr, st);
-    CK(cudaMemcpyAsync(sl.buf(k) + per * 16, da, cnt * 8, cudaMemcpyDeviceToHost, st));
+    u32* st_pairs = reinterpret_cast<u32*>(sl.buf(k));
+    const int64_t* in = pairs + 2 * lo;
+#pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 32768)
+    for (long i = 0; i < static_cast<long>(2 * cnt); ++i) {
+      const uint64_t v = static_cast<uint64_t>(in[i]);
+      st_pairs[i] = v >> 32 ? kNone : static_cast<u32>(v);
+    }
+    cudaStream_t st = h->qs[k];
+    const u64 qc = h->qchunk;
+    uint2* dp = reinterpret_cast<uint2*>(h->qmem + k * qc * 24);
+    u32* da = reinterpret_cast<u32*>(h->qmem + k * qc * 24 + qc * 8);
+    CK(cudaMemcpyAsync(dp, st_pairs, cnt * 8, cudaMemcpyHostToDevice, st));
+    launch_query(h, engine, PairsU32{dp}, AnsU32{da}, cnt, h->qerr + k, st);
+    CK(cudaMemcpyAsync(sl.buf(k) + per * 8, da, cnt * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(sl.done(k), st));
   }
   if (chunks >= 2) drain(chunks - 2);
   drain(chunks - 1);
-  u32 err = 0;
-  read_back(&err, h->qerr, 4, st);
-  if (err) throw Error(ETTG_ERANGE, "query node id out of range");
+  u32 errs[2] = {0, 0};
+  CK(cudaStreamSynchronize(h->qs[1]));
+  CK(cudaMemcpyAsync(errs, h->qerr, sizeof errs, cudaMemcpyDeviceToHost, h->qs[0]));
+  CK(cudaStreamSynchronize(h->qs[0]));
+  if (errs[0] | errs[1]) throw Error(ETTG_ERANGE, "query node id out of range");
 }
 }  // namespace
 
@@ -1589,8 +1608,10 @@ int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pa
     ettg_lca* h = const_cast<ettg_lca*>(hc);
     DeviceScope ds(h->device);
     std::lock_guard<std::mutex> qlock(h->qmu);
-    if (q >= (1 << 16) && !(is_pinned(pairs) && is_pinned(answers))) {
-      query_host_staged(h, engine, pairs, static_cast<u64>(q), answers);
+    // both checked (a device pointer in either is a caller error, whatever q)
+    const bool pinned = is_pinned(pairs) & is_pinned(answers);
+    if (q >= (1 << 16) && (narrow_enabled() || !pinned)) {
+      query_host_narrow(h, engine, pairs, static_cast<u64>(q), answers);
       return;
     }
     // 1M-query chunks on two streams: H2D of chunk c+1 overlaps the kernel and

@@ -247,39 +247,6 @@ def node_stats(tree: RootedTree, device: int = 0) -> NodeStats:
 
 
 # ------------------------------------------------------------------ bridges
-def _bridges(g: EdgeList, engine: int, device: int, times: dict | None) -> BridgeMask:
-    e = g.edges
-    mask = np.zeros(g.m(), np.uint8)
-    pt = _lib.PhaseTimes()
-    check(lib().ettg_bridges_engine(ptr(e), int(g.n), g.m(), device, engine, ptr(mask),
-                                    C.byref(pt)))
-    if engine == _lib.BRIDGES_TV:
-        phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "lowhigh": pt.lowhigh_ms}
-    elif engine == _lib.BRIDGES_CK:
-        phases = {"spanning": pt.spanning_ms, "marking": pt.marking_ms}
-    else:
-        phases = {"spanning": pt.spanning_ms, "euler": pt.euler_ms, "marking": pt.marking_ms}
-    phases["total"] = pt.total_ms
-    if times is not None:
-        times.update(phases)
-    return BridgeMask(mask, phases)
-
-
-def tv_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
-    """tv_bridges (core/src/bridges.cpp:311-316); times gets spanning/euler/lowhigh ms."""
-    return _bridges(g, _lib.BRIDGES_TV, device, times)
-
-
-def ck_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
-    """ck_bridges (core/src/bridges.cpp:318-325): BFS tree + CK marking."""
-    return _bridges(g, _lib.BRIDGES_CK, device, times)
-
-
-def hybrid_bridges(g: EdgeList, device: int = 0, times: dict | None = None) -> BridgeMask:
-    """hybrid_bridges (core/src/bridges.cpp:327-339): hooking + Euler rooting + CK marking."""
-    return _bridges(g, _lib.BRIDGES_HYBRID, device, times)
-
-
 @dataclass
 class AdjacencyIndex:
     """core/include/ett/graph.hpp:44-63."""
@@ -288,6 +255,71 @@ class AdjacencyIndex:
     offsets: np.ndarray
     neighbors: np.ndarray
     edge_ids: np.ndarray
+
+
+def _phases(engine: int, pt, on_tree: bool = False) -> dict:
+    """Phase names as the reference records them (core/src/bridges.cpp:292-337)."""
+    phases = {} if on_tree else {"spanning": pt.spanning_ms}
+    if engine != _lib.BRIDGES_CK:
+        phases["euler"] = pt.euler_ms
+    if engine == _lib.BRIDGES_TV:
+        phases["lowhigh"] = pt.lowhigh_ms
+    else:
+        phases["marking"] = pt.marking_ms
+    phases["total"] = pt.total_ms
+    return phases
+
+
+def _bridges(g, engine: int, device: int, times: dict | None, tree_mask=None) -> BridgeMask:
+    """g: EdgeList (8 B per edge over the link) or AdjacencyIndex (the
+    reference engines' input type; the edge list is recovered on the device)."""
+    mask = np.zeros(g.m() if isinstance(g, EdgeList) else g.m, np.uint8)
+    pt = _lib.PhaseTimes()
+    tm = None
+    if tree_mask is not None:
+        tm = np.ascontiguousarray(np.asarray(tree_mask) != 0, np.uint8)
+        if len(tm) != len(mask):
+            raise InvalidArgument("tree mask size mismatch")
+    if isinstance(g, AdjacencyIndex):
+        off = np.ascontiguousarray(g.offsets, np.int64)
+        nbr = np.ascontiguousarray(g.neighbors, np.int64)
+        eid = np.ascontiguousarray(g.edge_ids, np.int64)
+        check(lib().ettg_bridges_csr(ptr(off), ptr(nbr), ptr(eid), int(g.n), int(g.m), device,
+                                     engine, ptr(tm) if tm is not None else None, ptr(mask),
+                                     C.byref(pt)))
+    elif tm is not None:
+        check(lib().ettg_bridges_on_tree(ptr(g.edges), int(g.n), g.m(), device, ptr(tm),
+                                         ptr(mask), C.byref(pt)))
+    else:
+        check(lib().ettg_bridges_engine(ptr(g.edges), int(g.n), g.m(), device, engine, ptr(mask),
+                                        C.byref(pt)))
+    phases = _phases(engine, pt, tm is not None)
+    if times is not None:
+        times.update(phases)
+    return BridgeMask(mask, phases)
+
+
+def tv_bridges(g, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """tv_bridges (core/src/bridges.cpp:311-316) on an EdgeList or an
+    AdjacencyIndex; times gets spanning/euler/lowhigh ms."""
+    return _bridges(g, _lib.BRIDGES_TV, device, times)
+
+
+def tv_bridges_on_tree(g, tree_mask, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """tv_bridges_on_tree (core/src/bridges.cpp:289-309): the TV criterion on a
+    caller spanning tree (mask per edge).  Not a spanning tree -> InvalidArgument
+    "not a tree: m != n - 1" / "not a tree: disconnected" (core/src/euler.cpp:13-33)."""
+    return _bridges(g, _lib.BRIDGES_TV, device, times, tree_mask)
+
+
+def ck_bridges(g, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """ck_bridges (core/src/bridges.cpp:318-325): BFS tree + CK marking."""
+    return _bridges(g, _lib.BRIDGES_CK, device, times)
+
+
+def hybrid_bridges(g, device: int = 0, times: dict | None = None) -> BridgeMask:
+    """hybrid_bridges (core/src/bridges.cpp:327-339): hooking + Euler rooting + CK marking."""
+    return _bridges(g, _lib.BRIDGES_HYBRID, device, times)
 
 
 @dataclass
@@ -382,13 +414,21 @@ class SpanningTree:
     parent_edge: np.ndarray
 
 
-def bfs_tree(g: EdgeList, root: int = 0, device: int = 0) -> SpanningTree:
-    """bfs_tree (core/src/bridges.cpp:198-249), bit-identical to the reference."""
-    m = g.m()
+def bfs_tree(g, root: int = 0, device: int = 0) -> SpanningTree:
+    """bfs_tree (core/src/bridges.cpp:198-249) of an EdgeList or an
+    AdjacencyIndex, bit-identical to the reference."""
+    m = g.m() if isinstance(g, EdgeList) else int(g.m)
     mask = np.zeros(max(m, 1), np.uint8)
     lev, par, pe = (np.empty(g.n, np.int64) for _ in range(3))
-    check(lib().ettg_bfs_tree(ptr(g.edges), int(g.n), m, int(root), device, ptr(mask), ptr(lev),
-                              ptr(par), ptr(pe)))
+    if isinstance(g, AdjacencyIndex):
+        off = np.ascontiguousarray(g.offsets, np.int64)
+        nbr = np.ascontiguousarray(g.neighbors, np.int64)
+        eid = np.ascontiguousarray(g.edge_ids, np.int64)
+        check(lib().ettg_bfs_tree_csr(ptr(off), ptr(nbr), ptr(eid), int(g.n), m, int(root),
+                                      device, ptr(mask), ptr(lev), ptr(par), ptr(pe)))
+    else:
+        check(lib().ettg_bfs_tree(ptr(g.edges), int(g.n), m, int(root), device, ptr(mask),
+                                  ptr(lev), ptr(par), ptr(pe)))
     return SpanningTree(mask[:m], lev, par, pe)
 
 

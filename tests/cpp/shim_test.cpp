@@ -43,17 +43,47 @@ int main() {
   ettg::PhaseTimes pt;
   auto mask = ettg::tv_bridges(g, &pt);
   CHECK(mask.is_bridge == std::vector<char>({0, 0, 0, 1}));
-  CHECK(mask.count() == 1 && pt.ms.size() == 3 && pt.ms[0].first == "spanning");
+  CHECK(mask.count() == 1 && pt.nanos.size() == 3 && pt.nanos[0].first == "spanning");
   auto nv = ettg::naive_build(t);
   CHECK(ettg::answer_batch(nv, {{1, 5}, {3, 4}}, 2) == std::vector<ettg::i64>({2, 0}));
   CHECK(ettg::ancestor_doubling_levels(t) == std::vector<ettg::i64>({0, 2, 1, 1, 1, 2}));
   CHECK(ettg::ck_bridges(g).is_bridge == std::vector<char>({0, 0, 0, 1}));
   ettg::PhaseTimes ph;
   CHECK(ettg::hybrid_bridges(g, &ph).is_bridge == std::vector<char>({0, 0, 0, 1}));
-  CHECK(ph.ms.size() == 3 && ph.ms[2].first == "marking");
+  CHECK(ph.nanos.size() == 3 && ph.nanos[2].first == "marking");
   auto adj = ettg::build_adjacency(g);
   CHECK(adj.offsets == std::vector<ettg::i64>({0, 2, 4, 7, 8}));
   CHECK(adj.neighbors == std::vector<ettg::i64>({1, 2, 0, 2, 0, 1, 3, 2}));
+  {  // the reference engines' own input type and signature (bridges.hpp:55-61)
+    using BridgeFn = ettg::BridgeMask (*)(const ettg::AdjacencyIndex&, ettg::PhaseTimes*);
+    const BridgeFn fns[] = {ettg::tv_bridges, ettg::ck_bridges, ettg::hybrid_bridges,
+                            ettg::dfs_bridges};
+    for (BridgeFn f : fns) {
+      ettg::PhaseTimes p;
+      CHECK(f(adj, &p).is_bridge == std::vector<char>({0, 0, 0, 1}));
+      CHECK(!p.nanos.empty() && p.nanos[0].first == "spanning");
+    }
+    // tests/bridges_test.cpp:163-169: the TV criterion does not depend on the tree
+    ettg::PhaseTimes p;
+    auto via_bfs = ettg::tv_bridges_on_tree(adj, ettg::bfs_tree(adj, 0).is_tree_edge, &p);
+    CHECK(via_bfs.is_bridge == ettg::tv_bridges(adj).is_bridge);
+    CHECK(p.nanos.size() == 2 && p.nanos[0].first == "euler" && p.nanos[1].first == "lowhigh");
+    // check_is_tree messages (core/src/euler.cpp:13-33)
+    std::string what;
+    try {
+      ettg::tv_bridges_on_tree(adj, {1, 1, 0, 0});
+    } catch (const std::invalid_argument& e) {
+      what = e.what();
+    }
+    CHECK(what == "not a tree: m != n - 1");
+    what.clear();
+    try {
+      ettg::tv_bridges_on_tree(adj, {1, 1, 1, 0});  // the triangle: a cycle
+    } catch (const std::invalid_argument& e) {
+      what = e.what();
+    }
+    CHECK(what == "not a tree: disconnected");
+  }
   auto bt = ettg::bfs_tree(g, 0);
   CHECK(bt.parent == std::vector<ettg::i64>({-1, 0, 0, 2}));
   auto lc = ettg::largest_component(ettg::EdgeList{6, {{0, 1}, {2, 3}, {3, 4}}});

@@ -448,3 +448,33 @@ def test_star_picks_split_own_and_matches(ett, ref):
     rep = ett.attach_index(buf, n)
     assert rep.layout()[0] == "split_own"
     assert np.array_equal(ett.answer_batch(rep, q, len(q)), want)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_query_narrowed_paths(ett, ref, pinned):
+    """ettg_lca_query ships u32 pairs / answers (12 B per query) whatever the
+    caller's buffers are; answers equal the reference on a multi-chunk batch,
+    every engine; out-of-range ids in a late chunk (>= n, negative, >= 2^32)
+    give OutOfRange, and the handle answers correctly afterwards."""
+    import torch
+    t = ett.permute_labels(ett.grasp_tree(500_000, 16, 21), 22)
+    idx = ett.inlabel_build(t, engines=ett.ENGINE_INLABEL | ett.ENGINE_RMQ | ett.ENGINE_NAIVE)
+    q = ett.sample_queries(t.n, 3_000_000, 23)  # > 2 stage chunks of 1.4M
+    want = ref.lca("inlabel", t.parent, t.root, q)
+    qt = torch.from_numpy(q)
+    if pinned:
+        qt = qt.pin_memory()
+    for eng in (ett.ENGINE_INLABEL, ett.ENGINE_RMQ, ett.ENGINE_NAIVE):
+        out = torch.empty(len(q), dtype=torch.int64)
+        if pinned:
+            out = out.pin_memory()
+        from paper_2103_15217_b200 import _lib
+        _lib.check(_lib.lib().ettg_lca_query_engine(idx.handle, eng, qt.data_ptr(), len(q),
+                                                   len(q), out.data_ptr()))
+        assert np.array_equal(out.numpy(), want), eng
+    for badval in (t.n, -1, 1 << 32, -(1 << 40)):
+        bad = qt.clone()
+        bad[2_900_000, 1] = badval
+        with pytest.raises(ett.OutOfRange):
+            ett.answer_batch(idx, bad.numpy(), len(q))
+    assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
