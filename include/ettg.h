@@ -58,6 +58,7 @@ extern "C" {
 #define ETTG_ENOMEM 4
 #define ETTG_EINTERNAL 5
 #define ETTG_EPARSE 6 /* malformed text input: the reference's std::runtime_error */
+#define ETTG_ENCCL 7  /* NCCL failure while replicating an index across GPUs */
 
 #define ETTG_ENGINE_INLABEL 1u /* Schieber-Vishkin inlabel (core/src/lca.cpp:20-109) */
 #define ETTG_ENGINE_RMQ 2u     /* RMQ over the Euler tour (core/src/lca.cpp:128-157) */
@@ -180,6 +181,37 @@ int ettg_lca_index_bytes(const ettg_lca* h, int64_t* bytes);
 int ettg_lca_index_export_dev(const ettg_lca* h, void* d_dst, void* stream);
 int ettg_lca_index_attach_dev(const void* d_src, int64_t n, int device,
                               void* stream, ettg_lca** out);
+/* The CUDA device a handle's memory lives on. */
+int ettg_lca_device(const ettg_lca* h, int* device);
+
+/* ------------------------------------------------------------ multi-GPU -- */
+/* the index is built once, broadcast with ncclBroadcast
+ * (NVLink 5 / NVSwitch between B200s) and every GPU answers a contiguous
+ * slice of the batch -- answer_batch semantics (core/include/ett/lca.hpp:
+ * 50-65) over several devices, no per-query collective.  NCCL failures give
+ * ETTG_ENCCL. */
+#define ETTG_NCCL_ID_BYTES 128
+/* Contiguous shard [*lo, *hi) of `total` units for rank `rank` of `world`
+ * (sizes differ by at most one, larger first); needs no GPU. */
+int ettg_shard_range(int64_t total, int rank, int world, int64_t* lo, int64_t* hi);
+/* One process, many GPUs: out[i] is a query replica of `src` on devices[i]
+ * (ncclCommInitAll over src's device + the distinct devices; one grouped
+ * ncclBroadcast of the packed index).  Free each with ettg_lca_free. */
+int ettg_lca_replicate(const ettg_lca* src, int ndev, const int* devices, ettg_lca** out);
+/* One process per GPU (torchrun): every rank calls with the same
+ * ETTG_NCCL_ID_BYTES id (made by ettg_nccl_unique_id on one rank and shared
+ * by the caller); rank `root` passes its built index in *h, the others
+ * *h == NULL (or an old replica, which is freed).  On return every rank's *h
+ * answers for the root's tree on `device`. */
+int ettg_nccl_unique_id(void* id);
+int ettg_lca_replicate_rank(ettg_lca** h, int root, const void* id, int rank, int nranks,
+                            int device);
+/* A host batch sharded contiguously across `nrep` replicas (one host thread
+ * each; pairs and answers as in ettg_lca_query_engine); answers in query
+ * order and identical to one replica's. */
+int ettg_lca_query_multi(ettg_lca* const* replicas, int nrep, unsigned engine,
+                         const int64_t* pairs, int64_t q, int64_t batch,
+                         int64_t* answers);
 
 /* ------------------------------------------------------------ bridges -- */
 

@@ -147,6 +147,30 @@ inline std::vector<i64> answer_batch(const LcaIndex& idx,
   return out;
 }
 
+// Multi-GPU: query replicas of an inlabel index on
+// `devices`, one grouped ncclBroadcast of the packed index; and a batch
+// sharded across replicas, answers in query order.
+inline std::vector<LcaIndex> replicate(const LcaIndex& idx, const std::vector<int>& devices) {
+  std::vector<ettg_lca*> out(devices.size(), nullptr);
+  check(ettg_lca_replicate(idx.get(), static_cast<int>(devices.size()), devices.data(),
+                           out.data()));
+  std::vector<LcaIndex> reps;
+  for (ettg_lca* h : out) reps.emplace_back(h, ETTG_ENGINE_INLABEL);
+  return reps;
+}
+
+inline std::vector<i64> answer_batch(const std::vector<LcaIndex>& replicas,
+                                     const std::vector<std::pair<i64, i64>>& queries,
+                                     i64 batch_size) {
+  std::vector<ettg_lca*> hs;
+  for (const auto& r : replicas) hs.push_back(r.get());
+  std::vector<i64> out(queries.size());
+  check(ettg_lca_query_multi(hs.data(), static_cast<int>(hs.size()), ETTG_ENGINE_INLABEL,
+                             reinterpret_cast<const int64_t*>(queries.data()),
+                             static_cast<i64>(queries.size()), batch_size, out.data()));
+  return out;
+}
+
 inline i64 inlabel_lca(const LcaIndex& idx, i64 x, i64 y) {
   return answer_batch(idx, {{x, y}}, 1)[0];
 }

@@ -12,7 +12,8 @@ import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libettg.so")
 
-ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL, ETTG_EPARSE = range(7)
+(ETTG_OK, ETTG_EINVAL, ETTG_ERANGE, ETTG_ECUDA, ETTG_ENOMEM, ETTG_EINTERNAL, ETTG_EPARSE,
+ ETTG_ENCCL) = range(8)
 ENGINE_INLABEL = 1
 ENGINE_RMQ = 2
 ENGINE_NAIVE = 4
@@ -77,6 +78,12 @@ _SIGS = {
     "ettg_build_adjacency": ([p, i64, i64, C.c_int, p, p, p], C.c_int),
     "ettg_largest_component": ([p, i64, i64, C.c_int, p, i64p, i64p, p], C.c_int),
     "ettg_bfs_tree": ([p, i64, i64, i64, C.c_int, p, p, p, p], C.c_int),
+    "ettg_lca_device": ([p, C.POINTER(C.c_int)], C.c_int),
+    "ettg_shard_range": ([i64, C.c_int, C.c_int, i64p, i64p], C.c_int),
+    "ettg_nccl_unique_id": ([p], C.c_int),
+    "ettg_lca_replicate": ([p, C.c_int, p, p], C.c_int),
+    "ettg_lca_replicate_rank": ([C.POINTER(p), C.c_int, p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "ettg_lca_query_multi": ([p, C.c_int, C.c_uint, p, i64, i64, p], C.c_int),
     "ettg_bfs_tree_csr": ([p, p, p, i64, i64, i64, C.c_int, p, p, p, p], C.c_int),
     "ettg_bridges_on_tree": ([p, i64, i64, C.c_int, p, p, C.POINTER(PhaseTimes)], C.c_int),
     "ettg_bridges_dev_on_tree": ([p, i64, i64, C.c_int, p, p, p, C.POINTER(PhaseTimes)],
@@ -121,6 +128,13 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
+            # libettg.so binds NCCL at first use to whatever libnccl.so.2 the
+            # process holds; load torch's (when installed) before anything can
+            # pull in the system copy, which torch's own import would reject.
+            try:
+                import torch  # noqa: F401
+            except ImportError:
+                pass
             if not os.path.exists(LIB_PATH):
                 raise RuntimeError(
                     f"libettg.so not found at {LIB_PATH}; build it with "
@@ -160,8 +174,13 @@ class ParseError(EttgError):
     code = ETTG_EPARSE
 
 
+class NcclError(EttgError):
+    """ETTG_ENCCL: replicating an index across GPUs failed in NCCL."""
+    code = ETTG_ENCCL
+
+
 _EXC = {ETTG_EINVAL: InvalidArgument, ETTG_ERANGE: OutOfRange, ETTG_ECUDA: CudaError,
-        ETTG_EPARSE: ParseError}
+        ETTG_EPARSE: ParseError, ETTG_ENCCL: NcclError}
 
 
 def check(rc: int, gen: bool = False) -> None:

@@ -89,6 +89,29 @@ __global__ void k_csr_coo(const u32* __restrict__ off, const u32* __restrict__ n
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
+// 0/1 mask bytes -> bits (LSB first), one 32-edge word per thread from two
+// 16-B loads; the host-mask D2H then moves m/8 bytes.
+__global__ void k_pack_bits(const uint8_t* __restrict__ mask, u32 m, u32* __restrict__ bits) {
+  const u32 words = (m + 31) / 32;
+  for (u32 w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    const u64 base = u64(w) * 32;
+    u32 x = 0;
+    if (base + 32 <= m) {
+      const uint4 a = reinterpret_cast<const uint4*>(mask + base)[0];
+      const uint4 b = reinterpret_cast<const uint4*>(mask + base)[1];
+      const u32 v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const u32 t = v[i] & 0x01010101u;  // one bit per byte -> 4 bits
+        x |= ((t * 0x10204080u) >> 28) << (4 * i);
+      }
+    } else {
+      for (u64 i = base; i < m; ++i) x |= static_cast<u32>(mask[i] != 0) << (i - base);
+    }
+    bits[w] = x;
+  }
+}
+
 // A caller's spanning-tree mask (char per edge, any non-zero = tree edge) as
 // the 0/1 bytes the tree-edge compaction counts.
 __global__ void k_mask01(const uint8_t* __restrict__ in, u32 m, uint8_t* __restrict__ out) {
@@ -663,6 +686,22 @@ __global__ void k_tv_keys(Lr0View lr, u32 T, const uint2* __restrict__ tend, u32
   }
 }
 
+// tv_bridges_on_tree only: a caller mask of n - 1 edges that is not a
+// spanning tree (a cycle plus an unreached vertex, or a self-loop) can still
+// yield a closed tour the list ranking accepts, when the cyclic part's
+// rotation has a single face.  Then some non-root vertex is the child of no
+// tree edge.  So: every non-root vertex must have a key (key_of preset to
+// kNone) and the ranking must have succeeded; otherwise words[0] |= 4, which
+// stops the later TV kernels (tv_abort) before they index by a bad key.
+__global__ void k_tree_check(const u32* __restrict__ key_of, u32 n, u32 root, const u32* lr_err,
+                             u32* words) {
+  if (tv_abort(words, n)) return;
+  bool bad = blockIdx.x == 0 && threadIdx.x == 0 && *lr_err != 0u;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    bad |= v != root && key_of[v] == kNone;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&words[0], 4u);
+}
+
 __global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
     lh[i] = make_uint2(0xFFFFFFFFu, 0u);
@@ -844,6 +883,7 @@ struct BridgeWs {
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
   u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
+  u32* bits = nullptr;   // the mask packed to bits for a host-mask D2H
   // CK / hybrid
   uint2* rec = nullptr;     // {parent, level} per node
   u32* pedge_of = nullptr;  // parent edge per node
@@ -889,6 +929,7 @@ struct BridgeWs {
     levels = 32 - __builtin_clz(nb);
     sp = c.take<uint2>(static_cast<u64>(levels) * nb);
     words = c.take<u32>(16);
+    bits = c.take<u32>((static_cast<u64>(m) + 31) / 32 + 1);
   }
 };
 
@@ -959,19 +1000,33 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     // Pageable host edge list: the host threads narrow each chunk to u32
     // pairs while filling the pinned stage (8 B per edge over the link); the
     // hooking of a chunk is enqueued behind its copy on the same stream.
+    // The copies run on their own stream so that the hooking of chunk c
+    // overlaps the copy of chunk c + 1.
     std::function<void(size_t, size_t)> hook_chunk;
+    cudaStream_t cs = st;
     if (stream_hook) {
+      CK(cudaStreamCreateWithFlags(&copy_guard.s, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&copy_guard.e, cudaEventDisableTiming));
+      cs = copy_guard.s;
+      CK(cudaEventRecord(ev[1], st));  // the arena lease and words clear come first
+      CK(cudaStreamWaitEvent(cs, ev[1], 0));
       k_iota<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
       CK_LAUNCH();
       hook_chunk = [&](size_t lo, size_t cnt) {  // lo, cnt in u32 words (pairs: even)
+        CK(cudaEventRecord(copy_guard.e, cs));
+        CK(cudaStreamWaitEvent(st, copy_guard.e, 0));
         launch_hook(ws.edges + lo / 2, EdgeSubset{static_cast<u32>(cnt / 2), 1, 0}, n, ws.par,
                     ws.tree + lo / 2, ws.words, sms, st);
       };
     }
     if (m && staged_h2d_narrow_u32(reinterpret_cast<u32*>(ws.edges),
                                    static_cast<const int64_t*>(in.edges), 2ull * m, n, false,
-                                   device, st, hook_chunk))
+                                   device, cs, hook_chunk))
       einval("edge endpoint out of range");
+    if (cs != st) {  // everything after the input reads all of it
+      CK(cudaEventRecord(copy_guard.e, cs));
+      CK(cudaStreamWaitEvent(st, copy_guard.e, 0));
+    }
     hooked = stream_hook;
     edges = ws.edges;
   } else if (in.kind == BridgeIn::kHostI64) {
@@ -1115,9 +1170,15 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
       tr.mark("list_rank");
       const Lr0View lv = lr0_view(ws.lr);
       if (engine == ETTG_BRIDGES_TV) {
+        if (on_tree) CK(cudaMemsetAsync(ws.pre_of, 0xFF, static_cast<u64>(n) * 4, st));
         k_tv_keys<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.tend, 0,
                                                                    ws.pre_of, ws.kt, abort, n);
         CK_LAUNCH();
+        if (on_tree) {
+          k_tree_check<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+              ws.pre_of, n, 0, ws.lr.counters + LrCounters::kErr, ws.words);
+          CK_LAUNCH();
+        }
         tr.mark("keys");
       } else {
         k_tour_flags<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(lv, T, ws.flags);
@@ -1169,16 +1230,21 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     tr.mark("marking");
   }
   CK(cudaEventRecord(ev[3], st));
-  if (h_mask && m) copy_d2h(h_mask, d_mask, m, device, st);
+  if (h_mask && m) {
+    // the mask as bits: m/8 bytes over the link, expanded by host threads
+    k_pack_bits<<<std::min(g, blocks_for((m + 31) / 32, 256)), 256, 0, st>>>(d_mask, m, ws.bits);
+    CK_LAUNCH();
+    staged_d2h_expand_bits(h_mask, ws.bits, m, device, st);
+  }
   if (n > 1 && engine != ETTG_BRIDGES_CK)
     CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4, cudaMemcpyDeviceToHost, st));
   u32 w[2] = {0, n - 1};
   if (abort) CK(cudaMemcpyAsync(w, abort, sizeof w, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (w[0]) einval("edge endpoint out of range");
+  if (w[0] & 1u) einval("edge endpoint out of range");
   if (on_tree) {  // the reference's check_is_tree messages (core/src/euler.cpp:13-33)
     if (w[1] != n - 1) einval("not a tree: m != n - 1");
-    if (lerr) einval("not a tree: disconnected");
+    if (lerr || (w[0] & 4u)) einval("not a tree: disconnected");
   }
   if (w[1] != n - 1) einval("disconnected graph; extract the largest component first");
   if (lerr) throw Error(ETTG_EINTERNAL, "bridges: spanning-tree tour ranking failed");

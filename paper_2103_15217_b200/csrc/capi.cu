@@ -2,6 +2,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -128,6 +129,12 @@ int host_threads() {
   }();
   return t;
 }
+// Per calling thread: a multi-GPU call splits the host threads between the
+// replicas it drives (ScopedHostThreads).
+thread_local int t_host_threads = 0;
+}  // namespace
+int host_thread_count();
+namespace {
 void stage_init(Stage& s) {
   if (s.buf[0]) return;
   for (int i = 0; i < 2; ++i) {
@@ -138,7 +145,7 @@ void stage_init(Stage& s) {
 void par_copy_impl(char* dst, const char* src, size_t n) {
   const size_t kPiece = size_t(1) << 20;
   const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
-#pragma omp parallel for schedule(static) num_threads(host_threads()) if (pieces > 1)
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (pieces > 1)
   for (long i = 0; i < pieces; ++i) {
     const size_t o = static_cast<size_t>(i) * kPiece;
     std::memcpy(dst + o, src + o, std::min(kPiece, n - o));
@@ -147,7 +154,10 @@ void par_copy_impl(char* dst, const char* src, size_t n) {
 }  // namespace
 
 void par_copy(char* dst, const char* src, size_t n) { par_copy_impl(dst, src, n); }
-int host_thread_count() { return host_threads(); }
+int host_thread_count() { return t_host_threads > 0 ? t_host_threads : host_threads(); }
+int host_thread_budget() { return host_threads(); }
+ScopedHostThreads::ScopedHostThreads(int t) : prev_(t_host_threads) { t_host_threads = t; }
+ScopedHostThreads::~ScopedHostThreads() { t_host_threads = prev_; }
 bool narrow_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("ETTG_NARROW");
@@ -207,7 +217,7 @@ void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, in
     const size_t lo = c * per, n = std::min(per, count - lo);
     const uint2* in = reinterpret_cast<const uint2*>(s.buf[c & 1]);
     int64_t* out = h_dst + 2 * lo;
-#pragma omp parallel for schedule(static) num_threads(host_threads()) if (n > 65536)
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 65536)
     for (long i = 0; i < static_cast<long>(n); ++i) {
       out[2 * i] = in[i].x;
       out[2 * i + 1] = in[i].y;
@@ -255,7 +265,7 @@ void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, i
     const size_t lo = c * per, n = std::min(per, count - lo);
     const uint32_t* in = reinterpret_cast<const uint32_t*>(s.buf[c & 1]);
     int64_t* out = h_dst + lo;
-#pragma omp parallel for schedule(static) num_threads(host_threads()) if (n > 65536)
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 65536)
     for (long i = 0; i < static_cast<long>(n); ++i)
       out[i] = in[i] == 0xFFFFFFFFu ? int64_t(-1) : static_cast<int64_t>(in[i]);
   }
@@ -276,7 +286,7 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
     uint32_t* out = reinterpret_cast<uint32_t*>(s.buf[k]);
     const int64_t* in = h_src + lo;
     u64 b = 0;
-#pragma omp parallel for schedule(static) num_threads(host_threads()) reduction(+ : b) \
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) reduction(+ : b) \
     if (n > 65536)
     for (long i = 0; i < static_cast<long>(n); ++i) {
       const uint64_t v = static_cast<uint64_t>(in[i]);
@@ -292,6 +302,47 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
   }
   CK(cudaStreamSynchronize(st));
   return bad;
+}
+
+void staged_d2h_expand_bits(uint8_t* h_dst, const uint32_t* d_bits, size_t count, int device,
+                            cudaStream_t st) {
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  // byte b of a bit word -> 8 mask bytes (0/1), little-endian
+  static const auto table = [] {
+    std::array<uint64_t, 256> t{};
+    for (int b = 0; b < 256; ++b)
+      for (int i = 0; i < 8; ++i) t[b] |= static_cast<uint64_t>((b >> i) & 1) << (8 * i);
+    return t;
+  }();
+  const size_t words = (count + 31) / 32;
+  const size_t per = kStageChunk / 4;  // words per chunk
+  const size_t chunks = (words + per - 1) / per;
+  auto issue = [&](size_t c) {
+    const size_t lo = c * per, n = std::min(per, words - lo);
+    CK(cudaMemcpyAsync(s.buf[c & 1], d_bits + lo, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(s.done[c & 1], st));
+  };
+  if (chunks) issue(0);
+  for (size_t c = 0; c < chunks; ++c) {
+    if (c + 1 < chunks) issue(c + 1);
+    CK(cudaEventSynchronize(s.done[c & 1]));
+    const size_t lo = c * per, n = std::min(per, words - lo);
+    const uint32_t* in = reinterpret_cast<const uint32_t*>(s.buf[c & 1]);
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 16384)
+    for (long w = 0; w < static_cast<long>(n); ++w) {
+      const size_t base = (lo + w) * 32;
+      const uint32_t x = in[w];
+      if (base + 32 <= count) {
+        uint64_t q[4] = {table[x & 0xFF], table[(x >> 8) & 0xFF], table[(x >> 16) & 0xFF],
+                         table[x >> 24]};
+        std::memcpy(h_dst + base, q, 32);
+      } else {
+        for (size_t i = base; i < count; ++i) h_dst[i] = (x >> (i - base)) & 1;
+      }
+    }
+  }
 }
 
 void check_host_ptr(const void* p) {
@@ -331,7 +382,7 @@ size_t count_byte(const char* p, size_t len, char c) {
   const size_t kPiece = size_t(1) << 20;
   const long pieces = static_cast<long>((len + kPiece - 1) / kPiece);
   size_t total = 0;
-#pragma omp parallel for schedule(static) reduction(+ : total) num_threads(host_threads()) \
+#pragma omp parallel for schedule(static) reduction(+ : total) num_threads(host_thread_count()) \
     if (pieces > 1)
   for (long i = 0; i < pieces; ++i) {
     const size_t o = static_cast<size_t>(i) * kPiece;

@@ -227,7 +227,16 @@ class StageLease {
   void* s_;
 };
 void par_copy(char* dst, const char* src, size_t n);  // host threads
-int host_thread_count();  // threads of the host-side staging passes
+int host_thread_count();   // threads of the host-side staging passes (this thread)
+int host_thread_budget();  // all of them (ETTG_HOST_THREADS, else <= 16 cores)
+class ScopedHostThreads {  // caps host_thread_count() on this thread
+ public:
+  explicit ScopedHostThreads(int t);
+  ~ScopedHostThreads();
+
+ private:
+  int prev_;
+};
 // Host int64 ids cross the link narrowed to u32 (default; ETTG_NARROW=0
 // sends pinned int64 buffers as they are, for A/B runs).
 bool narrow_enabled();
@@ -246,6 +255,11 @@ void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaSt
 u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
                           bool allow_none, int device, cudaStream_t st,
                           const std::function<void(size_t, size_t)>& on_chunk = {});
+// D2H of a bit-packed 0/1 mask (`count` bits, LSB first per u32 word) into
+// `count` mask bytes, expanded by the host threads as the chunks land: 1/8
+// of the bytes over the link.
+void staged_d2h_expand_bits(uint8_t* h_dst, const uint32_t* d_bits, size_t count, int device,
+                            cudaStream_t st);
 // Page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory) host memory?
 // Throws ETTG_EINVAL for a device pointer (host-buffer entry points).
 bool is_pinned(const void* p);

@@ -1533,6 +1533,13 @@ int ettg_lca_size(const ettg_lca* h, int64_t* n) {
   });
 }
 
+int ettg_lca_device(const ettg_lca* h, int* device) {
+  return guard([&] {
+    if (!h || !device) einval("null argument");
+    *device = h->device;
+  });
+}
+
 int ettg_lca_build_ms(const ettg_lca* h, double* ms) {
   return guard([&] {
     if (!h || !ms) einval("null argument");
@@ -1551,17 +1558,21 @@ namespace {
 // buffers are pinned or pageable.  Ids outside [0, 2^32) are stored as
 // 0xFFFFFFFF, which the kernel's range check rejects (ETTG_ERANGE).
 void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
-                       int64_t* answers) {
+                       int64_t* answers, bool answers_pinned) {
   StageLease sl(h->device);
-  const u64 per = (StageLease::bytes() / 12) & ~u64(7);  // u32 pair + u32 answer per query
+  // stage bytes per query: the u32 pair, plus the u32 answer when the
+  // caller's answer buffer is pageable (a pinned one takes the int64
+  // answers straight from the device: the D2H direction has room for them)
+  const u64 per = (StageLease::bytes() / (answers_pinned ? 8 : 12)) & ~u64(7);
   ensure_qbuf(h, per);
   CK(cudaMemsetAsync(h->qerr, 0, 8, h->qs[0]));
   CK(cudaStreamSynchronize(h->qs[0]));
   const u64 chunks = (q + per - 1) / per;
   const int threads = host_thread_count();
-  auto drain = [&](u64 c) {  // answers of chunk c: stage -> caller, widened
-    const u64 lo = c * per, cnt = std::min(per, q - lo);
+  auto drain = [&](u64 c) {  // chunk c's stage buffer is free again (pageable: widen answers)
     CK(cudaEventSynchronize(sl.done(c & 1)));
+    if (answers_pinned) return;
+    const u64 lo = c * per, cnt = std::min(per, q - lo);
     const u32* in = reinterpret_cast<const u32*>(sl.buf(c & 1) + per * 8);
     int64_t* out = answers + lo;
 #pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 65536)
@@ -1569,7 +1580,7 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   };
   for (u64 c = 0; c < chunks; ++c) {
     const int k = c & 1;
-    if (c >= 2) drain(c - 2);  // frees stage buffer k
+    if (c >= 2) drain(c - 2);
     const u64 lo = c * per, cnt = std::min(per, q - lo);
     u32* st_pairs = reinterpret_cast<u32*>(sl.buf(k));
     const int64_t* in = pairs + 2 * lo;
@@ -1580,12 +1591,20 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
     }
     cudaStream_t st = h->qs[k];
     const u64 qc = h->qchunk;
-    uint2* dp = reinterpret_cast<uint2*>(h->qmem + k * qc * 24);
-    u32* da = reinterpret_cast<u32*>(h->qmem + k * qc * 24 + qc * 8);
-    CK(cudaMemcpyAsync(dp, st_pairs, cnt * 8, cudaMemcpyHostToDevice, st));
-    launch_query(h, engine, PairsU32{dp}, AnsU32{da}, cnt, h->qerr + k, st);
-    CK(cudaMemcpyAsync(sl.buf(k) + per * 8, da, cnt * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(sl.done(k), st));
+    char* slot = h->qmem + k * qc * 24;  // per stream: 8-B pairs, then 4- or 8-B answers
+    const uint2* dp = reinterpret_cast<const uint2*>(slot);
+    CK(cudaMemcpyAsync(slot, st_pairs, cnt * 8, cudaMemcpyHostToDevice, st));
+    if (answers_pinned) {
+      CK(cudaEventRecord(sl.done(k), st));  // the stage is free once the pairs landed
+      long long* da = reinterpret_cast<long long*>(slot + qc * 8);
+      launch_query(h, engine, PairsU32{dp}, AnsI64{da}, cnt, h->qerr + k, st);
+      CK(cudaMemcpyAsync(answers + lo, da, cnt * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+      u32* da = reinterpret_cast<u32*>(slot + qc * 8);
+      launch_query(h, engine, PairsU32{dp}, AnsU32{da}, cnt, h->qerr + k, st);
+      CK(cudaMemcpyAsync(sl.buf(k) + per * 8, da, cnt * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(sl.done(k), st));
+    }
   }
   if (chunks >= 2) drain(chunks - 2);
   drain(chunks - 1);
@@ -1609,9 +1628,9 @@ int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pa
     DeviceScope ds(h->device);
     std::lock_guard<std::mutex> qlock(h->qmu);
     // both checked (a device pointer in either is a caller error, whatever q)
-    const bool pinned = is_pinned(pairs) & is_pinned(answers);
-    if (q >= (1 << 16) && (narrow_enabled() || !pinned)) {
-      query_host_narrow(h, engine, pairs, static_cast<u64>(q), answers);
+    const bool pairs_pinned = is_pinned(pairs), answers_pinned = is_pinned(answers);
+    if (q >= (1 << 16) && (narrow_enabled() || !(pairs_pinned && answers_pinned))) {
+      query_host_narrow(h, engine, pairs, static_cast<u64>(q), answers, answers_pinned);
       return;
     }
     // 1M-query chunks on two streams: H2D of chunk c+1 overlaps the kernel and

@@ -18,10 +18,10 @@ import torch.distributed as dist
 
 
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous slice [lo, hi) of `total` units owned by `rank`."""
-    base, rem = divmod(total, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
+    """Contiguous slice [lo, hi) of `total` units owned by `rank`
+    (ettg_shard_range, the split ettg_lca_query_multi uses)."""
+    from .ett import shard_range as _c_shard_range
+    return _c_shard_range(total, rank, world)
 
 
 def broadcast_blob(blob: torch.Tensor | None, nbytes: int, device: torch.device,
@@ -38,9 +38,19 @@ def replicate_index(index, n: int, device: torch.device,
                     attach: Callable[[torch.Tensor, int], object] | None = None):
     """Rank 0 passes its built InlabelIndex; every rank returns a usable index.
 
-    The blob size travels first (one int64 broadcast), then the blob itself.
+    Under the NCCL backend the broadcast is the library's own
+    (ettg_lca_replicate_rank: ncclCommInitRank + ncclBroadcast of the packed
+    index, inside libettg.so); torch.distributed only carries the 128-byte
+    NCCL id.  Other backends (gloo, the CPU tests) broadcast the exported blob
+    with torch.distributed: the blob size first, then the blob.
     """
     rank = dist.get_rank()
+    if attach is None and device.type == "cuda" and dist.get_backend() == "nccl":
+        from .ett import nccl_unique_id, replicate_rank
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        return replicate_rank(index if rank == 0 else None, n, 0, box[0], rank,
+                              dist.get_world_size(), device.index or 0)
     size = torch.tensor([index.index_bytes() if rank == 0 else 0], dtype=torch.int64,
                         device=device)
     dist.broadcast(size, src=0)

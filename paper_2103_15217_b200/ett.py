@@ -222,6 +222,55 @@ def attach_index(d_src, n: int, device: int = 0, stream: int | None = None) -> I
     return InlabelIndex(h.value, n, device, ENGINE_INLABEL)
 
 
+# ---------------------------------------------------------------- multi-GPU
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous slice [lo, hi) of `total` units owned by `rank` (ettg_shard_range)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    check(lib().ettg_shard_range(int(total), int(rank), int(world), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def replicate(index: InlabelIndex, devices) -> list[InlabelIndex]:
+    """Query replicas of `index` on `devices` (one process, many GPUs): one
+    grouped ncclBroadcast of the packed index (ettg_lca_replicate)."""
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    out = (C.c_void_p * len(devices))()
+    check(lib().ettg_lca_replicate(index.handle, len(devices), devs, out))
+    return [InlabelIndex(out[i], index.n, int(devices[i]), ENGINE_INLABEL)
+            for i in range(len(devices))]
+
+
+def nccl_unique_id() -> bytes:
+    """An NCCL unique id (128 bytes) to share with the other ranks."""
+    buf = C.create_string_buffer(128)
+    check(lib().ettg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def replicate_rank(index: InlabelIndex | None, n: int, root: int, uid: bytes, rank: int,
+                   nranks: int, device: int) -> InlabelIndex:
+    """One process per GPU: the root passes its built index, the others None;
+    every rank gets an index for the root's tree (ettg_lca_replicate_rank)."""
+    h = C.c_void_p(index.handle.value if index is not None else None)
+    if index is not None:
+        index._h = None  # ownership moves through the call (the root gets it back)
+    check(lib().ettg_lca_replicate_rank(C.byref(h), int(root), C.c_char_p(bytes(uid)), int(rank),
+                                        int(nranks), int(device)))
+    return InlabelIndex(h.value, n, device, ENGINE_INLABEL)
+
+
+def query_multi(replicas: list[InlabelIndex], queries, batch_size: int,
+                engine: int = ENGINE_INLABEL) -> np.ndarray:
+    """answer_batch over several replicas: the batch is split contiguously, one
+    host thread drives each GPU, answers come back in query order."""
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64).reshape(-1, 2))
+    out = np.empty(q.shape[0], np.int64)
+    hs = (C.c_void_p * len(replicas))(*[r.handle.value for r in replicas])
+    check(lib().ettg_lca_query_multi(hs, len(replicas), engine, ptr(q), q.shape[0],
+                                     int(batch_size), ptr(out)))
+    return out
+
+
 def answer_batch(index: _LcaHandle, queries, batch_size: int) -> np.ndarray:
     """answer_batch (core/include/ett/lca.hpp:50-65) for the index's engine."""
     engine = (ENGINE_RMQ if isinstance(index, RmqLcaIndex) else

@@ -21,6 +21,11 @@ int main() {
   CHECK(ettg::inlabel_lca(idx, 3, 4) == 0);
   auto ans = ettg::answer_batch(idx, {{1, 5}, {3, 4}, {5, 5}}, 2);
   CHECK(ans.size() == 3 && ans[0] == 2 && ans[1] == 0 && ans[2] == 5);
+  {  // multi-GPU: replicas (NCCL broadcast) + a sharded batch, same answers
+    auto reps = ettg::replicate(idx, {0, 0});
+    auto multi = ettg::answer_batch(reps, {{1, 5}, {3, 4}, {5, 5}}, 2);
+    CHECK(multi == ans);
+  }
   auto r = ettg::rmq_lca_build(t);
   CHECK(ettg::answer_batch(r, {{1, 5}}, 1)[0] == 2);
   auto st = ettg::node_stats(t);

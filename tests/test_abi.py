@@ -60,3 +60,26 @@ def test_road_like_edge_count_matches_generator(ett):
     g, truth = ett.road_like_graph(W, H, extra, r, pend, 1)
     assert g.m() == m and len(truth) == m
     assert np.all(g.edges[:, 0] != g.edges[:, 1])
+
+
+def test_shard_range_cpu(ett):
+    """ettg_shard_range (the split ettg_lca_query_multi and bench.py use):
+    contiguous, covering, sizes differ by at most one; no GPU needed."""
+    from paper_2103_15217_b200.dist import shard_range
+    for total in (0, 1, 7, 16_000_000, 1_000_000_000, (1 << 40) + 3):
+        for world in (1, 2, 3, 8):
+            cuts = [shard_range(total, r, world) for r in range(world)]
+            assert cuts[0][0] == 0 and cuts[-1][1] == total
+            assert all(cuts[i][1] == cuts[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in cuts]
+            assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+    with pytest.raises(ett.InvalidArgument):
+        shard_range(10, 3, 3)
+
+
+def test_multi_gpu_entry_points_fail_loudly_without_device(ett):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(ett.InvalidArgument):
+        ett.query_multi([], np.zeros((1, 2), np.int64), 1)
