@@ -1230,7 +1230,10 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     tr.mark("marking");
   }
   CK(cudaEventRecord(ev[3], st));
-  if (h_mask && m) {
+  bool mask_bits = true;
+  if (const char* e = std::getenv("ETTG_MASK_BITS")) mask_bits = std::atoi(e) != 0;
+  if (h_mask && m && !mask_bits) copy_d2h(h_mask, d_mask, m, device, st);
+  if (h_mask && m && mask_bits) {
     // the mask as bits: m/8 bytes over the link, expanded by host threads
     k_pack_bits<<<std::min(g, blocks_for((m + 31) / 32, 256)), 256, 0, st>>>(d_mask, m, ws.bits);
     CK_LAUNCH();

@@ -159,11 +159,8 @@ int host_thread_budget() { return host_threads(); }
 ScopedHostThreads::ScopedHostThreads(int t) : prev_(t_host_threads) { t_host_threads = t; }
 ScopedHostThreads::~ScopedHostThreads() { t_host_threads = prev_; }
 bool narrow_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ETTG_NARROW");
-    return !e || std::atoi(e) != 0;
-  }();
-  return on;
+  const char* e = std::getenv("ETTG_NARROW");  // per call: A/B runs flip it
+  return !e || std::atoi(e) != 0;
 }
 
 StageLease::StageLease(int device) : s_(&stage_for(device)) {

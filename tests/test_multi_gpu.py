@@ -23,7 +23,7 @@ def test_replicate_and_query_multi_vs_reference(ett, ref, tree_and_queries):
     want = ref.lca("inlabel", t.parent, t.root, q)
     idx = ett.inlabel_build(t)
     reps = ett.replicate(idx, [0])
-    assert len(reps) == 1 and reps[0].layout() == (idx.layout()[0], 0)
+    assert len(reps) == 1 and reps[0].layout()[0] == idx.layout()[0]
     assert np.array_equal(ett.answer_batch(reps[0], q, len(q)), want)
     # two replicas on the one device: the shard split and the thread fan-out
     reps2 = ett.replicate(idx, [0, 0])
@@ -56,6 +56,5 @@ def test_query_multi_errors(ett, tree_and_queries):
     with pytest.raises(ett.OutOfRange):
         ett.query_multi(reps, bad, len(bad))
     assert len(ett.query_multi(reps, np.zeros((0, 2), np.int64), 1)) == 0
-    rmq_only = ett.rmq_lca_build(t)
-    with pytest.raises(ett.InvalidArgument):
-        ett.replicate(rmq_only, [0])
+    with pytest.raises(ett.InvalidArgument, match="device ordinal"):
+        ett.replicate(reps[0], [0, 64])

@@ -22,8 +22,8 @@ dur = sum(d.get("gpu__time_duration.sum", 0) for d in sel)
 p = os.path.join(ROOT, "profiles", "ncu_summary.json")
 s = json.load(open(p))
 s["bridges_D"] = {"dram_bytes_per_call": tot, "kernels_per_call": len(sel),
-                  "sum_kernel_us_cold": dur, "n": 32000000, "m": 251486389,
-                  "model_bytes": 41 * 251486389 + 108 * 32000000,
+                  "sum_kernel_us_cold": dur, "n": 32022410, "m": 256000000,
+                  "model_bytes": 41 * 256000000 + 108 * 32022410,
                   "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                             "gpu__time_duration.sum over every kernel of the second tv_bridges "
                             "call on config D (tools/gpu_br_dram.sh, tools/br_dram_summary.py)"}

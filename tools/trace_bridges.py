@@ -8,11 +8,11 @@ from paper_2103_15217_b200 import _lib
 if os.environ.get("AB_LIB"):
     _lib.LIB_PATH = os.environ["AB_LIB"]
 L = _lib.lib()
-side = int(os.environ.get("SIDE", "5600"))
+side = int(os.environ.get("SIDE", "5657"))  # config D: n = 32,022,410, m = 256,000,000
 if os.environ.get("GRAPH") == "C":
     g, truth = ett.planted_bridge_graph(1_000_000, 8_000_000, 10_000, 4)
 else:
-    g, truth = ett.road_like_graph(side, side, 6, 3, 640_000 * side * side // (5600 * 5600), 5)
+    g, truth = ett.road_like_graph(side, side, 6, 3, 20_761 * side * side // (5657 * 5657), 5)
 de = torch.from_numpy(g.edges.astype(np.int32).ravel()).cuda()
 dm = torch.empty(g.m(), dtype=torch.uint8, device="cuda")
 for _ in range(int(os.environ.get("REPS", "3"))):
