@@ -9,9 +9,10 @@
 //     classify                 :301-306   bridge iff low >= pre && high < pre + size
 //
 // Device pipeline (input: COO edge list, u32 ids; no CSR of the graph is built):
-//   spanning  k_cc_hook        lock-free union-find (min-id roots, ECL-CC style
-//                              hooking); a successful CAS joins two trees, so
-//                              its edge is a spanning-forest edge
+//   spanning  k_cc_hook        lock-free union-find (ECL-CC style CAS hooking
+//                              of roots in one strict order per pass); a
+//                              successful CAS joins two trees, so its edge is
+//                              a spanning-forest edge
 //   euler     scan             tree-edge compaction (decoupled look-back); the
 //                              count is the connectivity check (n-1 tree edges)
 //             k_tree_rot       per-vertex rotation lists by atomicExch (no sort:
@@ -125,8 +126,13 @@ __global__ void k_mask01(const uint8_t* __restrict__ in, u32 m, uint8_t* __restr
 // everywhere built a chain through every sampled group's root on an
 // id-sorted path (10M-node path, sorted edge list: 5.43 -> 1.91 ms per
 // call); the sampled pass keeps the id rule (config D: priority linking in
-// both passes cost 3%, in the second only ~1%).  Any rule that links two
-// distinct roots keeps the forest acyclic, so the passes may differ.
+// both passes cost 3%, in the second only ~1%).  The streamed chunks of a
+// host edge list (k_cc_hook<.., kPrio = true>) link by priority too.
+// Invariant: every hooking kernel in flight uses ONE strict total order --
+// two concurrent kernels with different orders could CAS two roots under
+// each other and make uf_find loop -- and uf_prio must stay a bijection
+// (mix32 is), so distinct roots never tie.  Kernels on one stream never
+// overlap, so consecutive passes may use different orders.
 __device__ __forceinline__ u32 uf_prio(u32 x) { return mix32(x); }
 
 // Representative of x, starting from an already loaded cur = par[x].  The
@@ -153,9 +159,11 @@ __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(pa
 
 // One pass over the edges, kHookE edges per thread: their parent loads and
 // first CAS attempts are issued together (the kernel is bound by dependent
-// L2 latency, profiles/r1_ncu_bridges.md).  Hooking root a (> b) under b with
-// CAS; on failure retry from the value found.  Each successful CAS unions two
-// distinct trees (a is the minimum of its own tree and b < a), so exactly
+// L2 latency, profiles/r1_ncu_bridges.md).  Each edge hooks the root a of one
+// endpoint under the root b of the other with CAS, a being the later of the
+// two in the kernel's strict total order (ids, or uf_prio with kPrio); on
+// failure it retries from the value found.  A CAS only succeeds on a root
+// (par[a] == a), so each success unions two distinct trees and exactly
 // n - #components edges are marked.  Endpoints are range-checked here (the
 // reference's build_adjacency check, core/src/graph.cpp:141-143) so the edge
 // list is read once.
@@ -211,7 +219,7 @@ __global__ void k_cc_compress(u32* par, u32 n) {
   }
 }
 
-template <int kHookE, int kMinB>
+template <int kHookE, int kMinB, bool kPrio = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               uint8_t* __restrict__ tree, u32* flags) {
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(256, kMinB)
         a[j] = uf_find_from(par, uv[j].x, a[j]);
         b[j] = uf_find_from(par, uv[j].y, b[j]);
       }
-      if (a[j] < b[j]) {
+      if (kPrio ? uf_prio(a[j]) < uf_prio(b[j]) : a[j] < b[j]) {
         const u32 tmp = a[j];
         a[j] = b[j];
         b[j] = tmp;
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(256, kMinB)
         } else {  // another thread re-rooted a: retry from what the CAS found
           u32 x = uf_find(par, old[j]), y = uf_find(par, b[j]);
           while (x != y) {
-            if (x < y) {
+            if (kPrio ? uf_prio(x) < uf_prio(y) : x < y) {
               const u32 tmp = x;
               x = y;
               y = tmp;
@@ -752,7 +760,7 @@ unsigned occ_grid(K kern, u64 work, int sms) {
 }
 
 void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* tree, u32* flags,
-                 int sms, cudaStream_t st) {
+                 int sms, cudaStream_t st, bool prio = false) {
   const u64 first = sub.first_count();
   const u64 cnt = sub.sample <= 1 ? sub.m : sub.phase == 0 ? first : sub.m - first;
   bool rest_kernel = sub.sample > 1 && sub.phase == 1;
@@ -764,7 +772,7 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* t
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tree, flags, magic, shift);
   } else {
-    auto kern = k_cc_hook<kEdgesPerThread, 8>;
+    auto kern = prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>;
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tree, flags);
   }
@@ -1016,7 +1024,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
         CK(cudaEventRecord(copy_guard.e, cs));
         CK(cudaStreamWaitEvent(st, copy_guard.e, 0));
         launch_hook(ws.edges + lo / 2, EdgeSubset{static_cast<u32>(cnt / 2), 1, 0}, n, ws.par,
-                    ws.tree + lo / 2, ws.words, sms, st);
+                    ws.tree + lo / 2, ws.words, sms, st, true);
       };
     }
     if (m && staged_h2d_narrow_u32(reinterpret_cast<u32*>(ws.edges),
@@ -1056,7 +1064,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
             ws.e64 + lo, cnt, n, ws.edges + lo, ws.words);
         CK_LAUNCH();
         launch_hook(ws.edges + lo, EdgeSubset{cnt, 1, 0}, n, ws.par, ws.tree + lo, ws.words, sms,
-                    st);
+                    st, true);
       }
       hooked = true;
     } else if (m) {

@@ -212,7 +212,8 @@ void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaSt
 // i64 ids) by the host threads as the chunks land.
 void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, int device,
                             cudaStream_t st);
-// The device's two pinned staging buffers, held for a custom pipeline.
+// The device's kStageBufs pinned staging buffers, held for a custom pipeline.
+constexpr int kStageBufs = 3;
 class StageLease {
  public:
   explicit StageLease(int device);

@@ -30,6 +30,8 @@
 // root's pair is the virtual start/end of the tour, so the tour list has
 // exactly 2n elements and rank r(down(v)) equals the reference's tour step of
 // v's first occurrence (rmq tour_nodes, core/src/lca.cpp:135-146).
+#include <omp.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -1548,14 +1550,15 @@ int ettg_lca_build_ms(const ettg_lca* h, double* ms) {
 }
 
 namespace {
-// Host int64 pairs -> int64 answers with 12 B per query over the link (u32
-// pairs in, u32 answers out) instead of 24.  The host threads narrow chunk c
-// into pinned stage buffer c & 1 (while the copy engine and the kernel work
-// on chunk c - 1 on the other stream) and widen the answers of chunk c - 2
-// out of it; a B200 host narrows int64 at ~144 GB/s with 16 threads
-// (tools/host_narrow_micro.cpp), faster than PCIe moves the narrowed bytes,
-// so the call runs at the link rate of half the bytes whether the caller's
-// buffers are pinned or pageable.  Ids outside [0, 2^32) are stored as
+// Host int64 pairs -> int64 answers with u32 pairs over the link (8 B per
+// query instead of 16).  The host threads narrow chunk c into pinned stage
+// buffer c % 3 while the copy engines and the kernel work on the chunks
+// before it (two streams).  A pageable answer buffer gets u32 answers (4 B),
+// widened by the host threads out of the stage; a pinned one takes the int64
+// answers straight from the device (the D2H direction has room for them).
+// A B200 host narrows int64 at 70-140 GB/s with 16 threads
+// (tools/host_narrow_micro.cpp, tools/stage_micro.cu): at the 54 GB/s link
+// the narrowed bytes move in about half the time of the int64 ones.  Ids outside [0, 2^32) are stored as
 // 0xFFFFFFFF, which the kernel's range check rejects (ETTG_ERANGE).
 void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
                        int64_t* answers, bool answers_pinned) {
@@ -1569,49 +1572,66 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   CK(cudaStreamSynchronize(h->qs[0]));
   const u64 chunks = (q + per - 1) / per;
   const int threads = host_thread_count();
+  const char* tr = std::getenv("ETTG_TRACE");
+  const bool trace = tr && *tr && *tr != '0';
+  double t_wait = 0, t_narrow = 0, t_widen = 0;
+  const double t_start = trace ? omp_get_wtime() : 0;
   auto drain = [&](u64 c) {  // chunk c's stage buffer is free again (pageable: widen answers)
-    CK(cudaEventSynchronize(sl.done(c & 1)));
+    const double t0 = trace ? omp_get_wtime() : 0;
+    CK(cudaEventSynchronize(sl.done(c % kStageBufs)));
+    if (trace) t_wait += omp_get_wtime() - t0;
     if (answers_pinned) return;
+    const double t1 = trace ? omp_get_wtime() : 0;
     const u64 lo = c * per, cnt = std::min(per, q - lo);
-    const u32* in = reinterpret_cast<const u32*>(sl.buf(c & 1) + per * 8);
+    const u32* in = reinterpret_cast<const u32*>(sl.buf(c % kStageBufs) + per * 8);
     int64_t* out = answers + lo;
 #pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 65536)
     for (long i = 0; i < static_cast<long>(cnt); ++i) out[i] = in[i];
+    if (trace) t_widen += omp_get_wtime() - t1;
   };
   for (u64 c = 0; c < chunks; ++c) {
-    const int k = c & 1;
-    if (c >= 2) drain(c - 2);
+    const int k = c % kStageBufs;  // stage buffer
+    const int s = c & 1;           // stream and device slot
+    if (c >= kStageBufs) drain(c - kStageBufs);
     const u64 lo = c * per, cnt = std::min(per, q - lo);
     u32* st_pairs = reinterpret_cast<u32*>(sl.buf(k));
     const int64_t* in = pairs + 2 * lo;
+    const double t0 = trace ? omp_get_wtime() : 0;
 #pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 32768)
     for (long i = 0; i < static_cast<long>(2 * cnt); ++i) {
       const uint64_t v = static_cast<uint64_t>(in[i]);
       st_pairs[i] = v >> 32 ? kNone : static_cast<u32>(v);
     }
-    cudaStream_t st = h->qs[k];
+    if (trace) t_narrow += omp_get_wtime() - t0;
+    cudaStream_t st = h->qs[s];
     const u64 qc = h->qchunk;
-    char* slot = h->qmem + k * qc * 24;  // per stream: 8-B pairs, then 4- or 8-B answers
+    char* slot = h->qmem + s * qc * 24;  // per stream: 8-B pairs, then 4- or 8-B answers
     const uint2* dp = reinterpret_cast<const uint2*>(slot);
     CK(cudaMemcpyAsync(slot, st_pairs, cnt * 8, cudaMemcpyHostToDevice, st));
     if (answers_pinned) {
       CK(cudaEventRecord(sl.done(k), st));  // the stage is free once the pairs landed
       long long* da = reinterpret_cast<long long*>(slot + qc * 8);
-      launch_query(h, engine, PairsU32{dp}, AnsI64{da}, cnt, h->qerr + k, st);
+      launch_query(h, engine, PairsU32{dp}, AnsI64{da}, cnt, h->qerr + s, st);
       CK(cudaMemcpyAsync(answers + lo, da, cnt * 8, cudaMemcpyDeviceToHost, st));
     } else {
       u32* da = reinterpret_cast<u32*>(slot + qc * 8);
-      launch_query(h, engine, PairsU32{dp}, AnsU32{da}, cnt, h->qerr + k, st);
+      launch_query(h, engine, PairsU32{dp}, AnsU32{da}, cnt, h->qerr + s, st);
       CK(cudaMemcpyAsync(sl.buf(k) + per * 8, da, cnt * 4, cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(sl.done(k), st));
     }
   }
-  if (chunks >= 2) drain(chunks - 2);
-  drain(chunks - 1);
+  for (u64 c = chunks > kStageBufs ? chunks - kStageBufs : 0; c < chunks; ++c) drain(c);
   u32 errs[2] = {0, 0};
   CK(cudaStreamSynchronize(h->qs[1]));
   CK(cudaMemcpyAsync(errs, h->qerr, sizeof errs, cudaMemcpyDeviceToHost, h->qs[0]));
   CK(cudaStreamSynchronize(h->qs[0]));
+  if (trace)
+    std::fprintf(stderr,
+                 "[ettg trace] query_host: q=%llu chunks=%llu per=%llu pinned_answers=%d "
+                 "narrow=%.3f wait=%.3f widen=%.3f wall=%.3f ms\n",
+                 static_cast<unsigned long long>(q), static_cast<unsigned long long>(chunks),
+                 static_cast<unsigned long long>(per), answers_pinned ? 1 : 0, t_narrow * 1e3,
+                 t_wait * 1e3, t_widen * 1e3, (omp_get_wtime() - t_start) * 1e3);
   if (errs[0] | errs[1]) throw Error(ETTG_ERANGE, "query node id out of range");
 }
 }  // namespace
