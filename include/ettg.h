@@ -151,10 +151,14 @@ int ettg_lca_query_engine(const ettg_lca* h, unsigned engine,
                           const int64_t* pairs, int64_t q, int64_t batch,
                           int64_t* answers);
 /* Device-resident batch: d_pairs = 2q uint32, d_answers = q uint32.
- * Out-of-range ids answer 0xFFFFFFFF. */
+ * Out-of-range ids answer 0xFFFFFFFF and raise the handle's sticky error
+ * flag, which ettg_lca_query_dev_error reads (after the work on `stream`)
+ * and clears: *bad = 1 if any _dev query since the last check had an id
+ * outside [0, n). */
 int ettg_lca_query_dev(const ettg_lca* h, unsigned engine,
                        const uint32_t* d_pairs, int64_t q, uint32_t* d_answers,
                        void* stream);
+int ettg_lca_query_dev_error(const ettg_lca* h, void* stream, int* bad);
 
 /* ancestor_doubling_levels (core/src/primitives.cpp:208-241): level[n] by
  * pointer jumping on the device (validates like validate_tree). */

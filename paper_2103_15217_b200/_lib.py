@@ -62,6 +62,7 @@ _SIGS = {
     "ettg_lca_query": ([p, p, i64, i64, p], C.c_int),
     "ettg_lca_query_engine": ([p, C.c_uint, p, i64, i64, p], C.c_int),
     "ettg_lca_query_dev": ([p, C.c_uint, p, i64, p, p], C.c_int),
+    "ettg_lca_query_dev_error": ([p, p, C.POINTER(C.c_int)], C.c_int),
     "ettg_lca_stats": ([p, p, p, p, p], C.c_int),
     "ettg_ancestor_levels": ([p, i64, i64, C.c_int, p], C.c_int),
     "ettg_lca_inlabel_index": ([p, p, p, p, p, p], C.c_int),

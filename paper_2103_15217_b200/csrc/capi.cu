@@ -182,7 +182,10 @@ char* StageLease::buf(int k) const { return static_cast<Stage*>(s_)->buf[k]; }
 cudaEvent_t StageLease::done(int k) const { return static_cast<Stage*>(s_)->done[k]; }
 size_t StageLease::bytes() { return kStageChunk; }
 
+void check_host_ptr(const void* p);
+
 void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st) {
+  check_host_ptr(h_src);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -199,8 +202,44 @@ void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaSt
   CK(cudaStreamSynchronize(st));
 }
 
+size_t staged_h2d_count(void* d_dst, const void* h_src, size_t bytes, char c, int device,
+                        cudaStream_t st) {
+  check_host_ptr(h_src);
+  Stage& s = stage_for(device);
+  std::lock_guard<std::mutex> lk(s.mu);
+  stage_init(s);
+  const char* src = static_cast<const char*>(h_src);
+  char* dst = static_cast<char*>(d_dst);
+  size_t total = 0;
+  int k = 0;
+  for (size_t o = 0; o < bytes; o += kStageChunk, k = (k + 1) % kStageBufs) {
+    const size_t n = std::min(kStageChunk, bytes - o);
+    CK(cudaEventSynchronize(s.done[k]));
+    const size_t kPiece = size_t(1) << 18;
+    const long pieces = static_cast<long>((n + kPiece - 1) / kPiece);
+    char* out = s.buf[k];
+    const char* in = src + o;
+    size_t cnt = 0;
+#pragma omp parallel for schedule(static) num_threads(host_thread_count()) reduction(+ : cnt) \
+    if (pieces > 1)
+    for (long i = 0; i < pieces; ++i) {
+      const size_t a = static_cast<size_t>(i) * kPiece, len = std::min(kPiece, n - a);
+      std::memcpy(out + a, in + a, len);
+      size_t m = 0;
+      for (size_t j = 0; j < len; ++j) m += out[a + j] == c;  // from the just-written (cached) copy
+      cnt += m;
+    }
+    total += cnt;
+    CK(cudaMemcpyAsync(dst + o, s.buf[k], n, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(s.done[k], st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return total;
+}
+
 void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, int device,
                             cudaStream_t st) {
+  check_host_ptr(h_dst);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -227,6 +266,7 @@ void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, in
 }
 
 void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st) {
+  check_host_ptr(h_dst);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -249,6 +289,7 @@ void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaSt
 
 void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, int device,
                           cudaStream_t st) {
+  check_host_ptr(h_dst);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -275,6 +316,7 @@ void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, i
 u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
                           bool allow_none, int device, cudaStream_t st,
                           const std::function<void(size_t, size_t)>& on_chunk) {
+  check_host_ptr(h_src);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -307,6 +349,7 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
 
 void staged_d2h_expand_bits(uint8_t* h_dst, const uint32_t* d_bits, size_t count, int device,
                             cudaStream_t st) {
+  check_host_ptr(h_dst);  // a device pointer here would be written by host threads
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -365,7 +408,7 @@ bool is_pinned(const void* p) {
 
 void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st) {
   if (!bytes) return;
-  if (bytes < (size_t(1) << 20) || is_pinned(h_src))
+  if (is_pinned(h_src) || bytes < (size_t(1) << 20))
     CK(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, st));
   else
     staged_h2d(d_dst, h_src, bytes, device, st);
@@ -373,28 +416,12 @@ void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStre
 
 void copy_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st) {
   if (!bytes) return;
-  if (bytes < (size_t(1) << 20) || is_pinned(h_dst))
+  if (is_pinned(h_dst) || bytes < (size_t(1) << 20))
     CK(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
   else
     staged_d2h(h_dst, d_src, bytes, device, st);
 }
 
-size_t count_byte(const char* p, size_t len, char c) {
-  const size_t kPiece = size_t(1) << 20;
-  const long pieces = static_cast<long>((len + kPiece - 1) / kPiece);
-  size_t total = 0;
-#pragma omp parallel for schedule(static) reduction(+ : total) num_threads(host_thread_count()) \
-    if (pieces > 1)
-  for (long i = 0; i < pieces; ++i) {
-    const size_t o = static_cast<size_t>(i) * kPiece;
-    const char* q = p + o;
-    const size_t n = std::min(kPiece, len - o);
-    size_t k = 0;
-    for (size_t j = 0; j < n; ++j) k += q[j] == c;
-    total += k;
-  }
-  return total;
-}
 
 }  // namespace ettg
 

@@ -208,6 +208,10 @@ int sm_count(int device);
 // H2D and, into freshly allocated memory, ~4 GB/s D2H (single-threaded page
 // faults); the staged paths run near the link rate.  Both synchronise `st`.
 void staged_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);
+// staged_h2d that also counts the bytes equal to `c` (the host threads read
+// every byte while filling the stage anyway).
+size_t staged_h2d_count(void* d_dst, const void* h_src, size_t bytes, char c, int device,
+                        cudaStream_t st);
 // D2H of `count` u32 pairs, widened to int64 pairs into h_dst (the reference's
 // i64 ids) by the host threads as the chunks land.
 void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, int device,
@@ -271,8 +275,6 @@ void check_host_ptr(const void* p);
 // pinned, staged (and synchronous) when it is pageable.
 void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);
 void copy_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaStream_t st);
-// Number of `c` bytes in [p, p + len), host threads.
-size_t count_byte(const char* p, size_t len, char c);
 
 // Copy `count` words device->host on `stream` and wait (used for counters
 // and error flags; a handful of bytes).

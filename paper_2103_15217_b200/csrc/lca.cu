@@ -1007,6 +1007,9 @@ struct ettg_lca {
   char* qmem = nullptr;
   u64 qchunk = 0;
   u32* qerr = nullptr;
+  // device-resident queries: sticky out-of-range flag (ettg_lca_query_dev_error)
+  std::once_flag derr_once;
+  u32* derr = nullptr;
   double build_ms = 0;
 
   void carve(Carver& c) {
@@ -1070,6 +1073,7 @@ struct ettg_lca {
     if (cmem) cudaFree(cmem);
     if (mem) cudaFree(mem);
     if (qmem) cudaFree(qmem);
+    if (derr) cudaFree(derr);
     for (auto s : qs)
       if (s) cudaStreamDestroy(s);
     if (stream) cudaStreamDestroy(stream);
@@ -1696,12 +1700,30 @@ int ettg_lca_query_dev(const ettg_lca* h, unsigned engine, const uint32_t* d_pai
     if (q == 0) return;
     if (!d_pairs || !d_answers) einval("null argument");
     DeviceScope ds(h->device);
-    static thread_local u32* dummy_err[64] = {nullptr};
-    u32*& err = dummy_err[h->device & 63];
-    if (!err) CK(cudaMalloc(&err, 256));
+    ettg_lca* hm = const_cast<ettg_lca*>(h);
+    std::call_once(hm->derr_once, [&] {
+      CK(cudaMalloc(&hm->derr, 256));
+      CK(cudaMemset(hm->derr, 0, 256));
+    });
+    if (!hm->derr) throw Error(ETTG_ECUDA, "query error word allocation failed earlier");
     launch_query(h, engine ? engine : ETTG_ENGINE_INLABEL,
                  PairsU32{reinterpret_cast<const uint2*>(d_pairs)}, AnsU32{d_answers},
-                 static_cast<u64>(q), err, static_cast<cudaStream_t>(stream));
+                 static_cast<u64>(q), hm->derr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ettg_lca_query_dev_error(const ettg_lca* h, void* stream, int* bad) {
+  return guard([&] {
+    if (!h || !bad) einval("null argument");
+    *bad = 0;
+    if (!h->derr) return;
+    DeviceScope ds(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    u32 v = 0;
+    CK(cudaMemcpyAsync(&v, h->derr, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(h->derr, 0, 4, st));
+    CK(cudaStreamSynchronize(st));
+    *bad = v != 0;
   });
 }
 
@@ -1738,11 +1760,15 @@ int ettg_lca_inlabel_index(const ettg_lca* h, int64_t* inlabel, uint64_t* ascend
     copy_widen(level, h->level, h->n, h->stream);
     copy_widen(parent, h->par, h->n, h->stream);
     if (ascendant) {
-      std::vector<uint4> rec(h->n);
-      CK(cudaMemcpyAsync(rec.data(), h->node, static_cast<u64>(h->n) * 16,
-                         cudaMemcpyDeviceToHost, h->stream));
-      CK(cudaStreamSynchronize(h->stream));
-      for (u32 v = 0; v < h->n; ++v) ascendant[v] = rec[v].y;
+      // only the ascendant word of each 16-B node record: a strided D2D copy
+      // into scratch, then the staged D2H (host threads widen to u64; an
+      // ascendant never has all 32 bits set below 2^31 nodes, so the kNone
+      // mapping of the widening cannot apply)
+      Lease lease(h->device, h->stream, static_cast<u64>(h->n) * 4);
+      u32* tmp = reinterpret_cast<u32*>(lease.base());
+      CK(cudaMemcpy2DAsync(tmp, 4, reinterpret_cast<const char*>(h->node) + 4, 16, 4, h->n,
+                           cudaMemcpyDeviceToDevice, h->stream));
+      copy_widen(reinterpret_cast<int64_t*>(ascendant), tmp, h->n, h->stream);
     }
   });
 }

@@ -283,8 +283,7 @@ struct ParseWs {
   u32* words = nullptr;
   SortWs sort;
   void carve(Carver& c, u64 len, u32 maxlines) {
-    const u64 L = maxlines;
-    text = c.take<uint8_t>(len + 16);
+    const u64 L = maxlines;  // `text` is allocated apart (it lands before the count)
     flags = c.take<uint8_t>(std::max<u64>(len, L) + 16);
     scan = c.take<u64>(scan_ws_words(std::max<u64>(len, L) + 1));
     nlpos = c.take<u32>(L + 1);
@@ -351,19 +350,30 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   if (cap < 0 || (cap > 0 && !edges_out)) einval("null edge buffer");
   if (len64 >= (i64(1) << 32)) throw Error(ETTG_ERANGE, "text larger than 4 GiB");
   const u64 len = static_cast<u64>(len64);
-  // lines = newlines + (1 if the text does not end in '\n'): counted on the
-  // host for the workspace size only (memchr pass; the device re-derives it)
-  const u64 nnl_host = len ? count_byte(text, len, '\n') : 0;
-  const u64 nlines64 = nnl_host + ((len > 0 && text[len - 1] != '\n') ? 1 : 0);
-  if (nlines64 >= 0xFFFFFFFFull) throw Error(ETTG_ERANGE, "too many lines");
-  const u32 nlines = static_cast<u32>(nlines64);
-
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct SG {
     cudaStream_t s;
     ~SG() { cudaStreamDestroy(s); }
   } sg{st};
+  // The text goes up first, into its own stream-ordered allocation; the host
+  // threads count the newlines while they fill the pinned stage (the staging
+  // copy reads every byte anyway), which sizes the per-line workspace.
+  // lines = newlines + (1 if the text does not end in '\n'); the device
+  // re-derives the newline positions.
+  struct TextBuf {
+    uint8_t* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~TextBuf() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } tb;
+  tb.s = st;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&tb.p), len + 16, st));
+  const u64 nnl_host = len ? staged_h2d_count(tb.p, text, len, '\n', device, st) : 0;
+  const u64 nlines64 = nnl_host + ((len > 0 && text[len - 1] != '\n') ? 1 : 0);
+  if (nlines64 >= 0xFFFFFFFFull) throw Error(ETTG_ERANGE, "too many lines");
+  const u32 nlines = static_cast<u32>(nlines64);
   const int sms = sm_count(device);
   const unsigned g = sms * 8;
   ParseWs ws;
@@ -372,11 +382,11 @@ void run_parse(const char* text, i64 len64, bool dimacs, int device, int64_t* ed
   Lease lease(device, st, c.off);
   c = Carver{lease.base()};
   ws.carve(c, len, nlines);
+  ws.text = tb.p;
 
   Trace tr(dimacs ? "parse_dimacs_gr" : "parse_edge_list", st);
   CK(cudaMemsetAsync(ws.counters, 0, 4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(ws.words, 0xFF, 8 * sizeof(u32), st));
-  if (len) staged_h2d(ws.text, text, len, device, st);
   tr.mark("h2d");
   if (len) {
     k_newlines<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.text, len, ws.flags);

@@ -114,13 +114,29 @@ class _LcaHandle:
         return out
 
     def query_dev(self, d_pairs, d_answers, engine: int, stream: int | None = None) -> None:
-        """Device-resident batch: uint32/int32 torch tensors (2q) -> (q)."""
+        """Device-resident batch: uint32/int32 torch tensors (2q) -> (q).
+        Out-of-range ids answer 0xFFFFFFFF; query_dev_error() reports them."""
         q = d_answers.numel()
+        ok_types = {"torch.int32", "torch.uint32"}
+        if str(d_pairs.dtype) not in ok_types or str(d_answers.dtype) not in ok_types:
+            raise InvalidArgument("query_dev takes int32 / uint32 tensors")
+        if d_pairs.numel() != 2 * q:
+            raise InvalidArgument("query_dev: d_pairs must hold 2 * d_answers.numel() ids")
+        if not (d_pairs.is_contiguous() and d_answers.is_contiguous()):
+            raise InvalidArgument("query_dev: tensors must be contiguous")
         check(lib().ettg_lca_query_dev(self._h, engine, ptr(d_pairs), q, ptr(d_answers),
                                        stream))
 
+    def query_dev_error(self, stream: int | None = None) -> bool:
+        """True if a query_dev since the last call had an id outside [0, n) (clears)."""
+        bad = C.c_int()
+        check(lib().ettg_lca_query_dev_error(self._h, stream, C.byref(bad)))
+        return bool(bad.value)
+
     def layout(self) -> tuple[str, int]:
-        """("wide" | "narrow", number of inlabel paths) of the inlabel engine."""
+        """(layout, number of inlabel paths) of the inlabel engine; the layout is
+        "wide" | "narrow" | "compact" | "split" | "split_own" | "split6" | "wide9"
+        (codes 0-6 of ettg_lca_layout and of the exported blob header)."""
         lay, labels = C.c_int(), C.c_int64()
         check(lib().ettg_lca_layout(self._h, C.byref(lay), C.byref(labels)))
         return ("wide", "narrow", "compact", "split", "split_own", "split6",
@@ -495,6 +511,10 @@ def list_rank(succ, head: int, device: int = 0) -> np.ndarray:
         return np.zeros(0, np.int64)
     if head < 0 or head >= len(s):
         raise InvalidArgument("list head out of range")
+    if np.any((s < -1) | (s >= len(s))):
+        # narrowing would wrap such a value onto a valid index; the reference
+        # indexes succ with it (undefined), here it is an error
+        raise InvalidArgument("linked list successor out of range")
     d = torch.from_numpy(s.astype(np.uint32)).to(f"cuda:{device}")
     r = torch.empty_like(d)
     check(lib().ettg_list_rank_dev(ptr(d), len(s), int(head), ptr(r), device,

@@ -478,3 +478,27 @@ def test_host_query_narrowed_paths(ett, ref, pinned):
         with pytest.raises(ett.OutOfRange):
             ett.answer_batch(idx, bad.numpy(), len(q))
     assert np.array_equal(ett.answer_batch(idx, q, len(q)), want)
+
+
+def test_query_dev_error_flag_and_argument_checks(ett):
+    import torch
+    t = ett.permute_labels(ett.grasp_tree(10_000, GRASP_INF, 3), 4)
+    idx = ett.inlabel_build(t)
+    q = ett.sample_queries(t.n, 1000, 5)
+    d = torch.from_numpy(q.astype(np.int32).ravel()).cuda()
+    a = torch.empty(1000, dtype=torch.int32, device="cuda")
+    idx.query_dev(d, a, ett.ENGINE_INLABEL)
+    assert not idx.query_dev_error()
+    assert np.array_equal(a.cpu().numpy(), ett.answer_batch(idx, q, 1000))
+    d[7] = t.n  # y of query 3
+    idx.query_dev(d, a, ett.ENGINE_INLABEL)
+    assert idx.query_dev_error()
+    assert a[3].item() == -1  # 0xFFFFFFFF
+    assert not idx.query_dev_error()  # cleared by the read
+    with pytest.raises(ett.InvalidArgument):
+        idx.query_dev(d[:-2], a, ett.ENGINE_INLABEL)
+    with pytest.raises(ett.InvalidArgument):
+        idx.query_dev(d.to(torch.int64), a, ett.ENGINE_INLABEL)
+    st = idx.stats()
+    assert np.array_equal(idx.ascendant, ett.inlabel_build(t).ascendant)  # strided export
+    assert len(st.preorder) == t.n
