@@ -262,7 +262,10 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
     barrier()
     t = all_max(float(np.mean(times)), device)
     answers = pin_ans.numpy().copy()  # the link test below reuses the pinned buffers
-    link = host_link_bound(pin_pairs, pin_ans, device)
+    # the link carries u32 pairs (narrowed by the library's host threads) in
+    # and the int64 answers out: time those bytes as plain copies
+    link = host_link_bound(torch.empty(2 * (hi - lo), dtype=torch.int32).pin_memory(), pin_ans,
+                           device)
     # the same call with pageable numpy buffers (what a std::vector / numpy
     # caller passes): staged through the library's pinned buffers
     pg_pairs = np.ascontiguousarray(host)
@@ -275,8 +278,10 @@ def e2e_section(ett, idx, tree, q_total, lo, hi, device, steps):
         pg.append(time.perf_counter() - t0)
     pg_ok = bool(np.array_equal(pg_ans, answers))
     return {"value": q_total / t, "unit": "queries/s",
-            "h2d_bytes_per_step": (hi - lo) * 16, "d2h_bytes_per_step": (hi - lo) * 8,
-            "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers)",
+            "h2d_bytes_per_step": (hi - lo) * 8, "d2h_bytes_per_step": (hi - lo) * 8,
+            "caller_bytes_per_step": {"in": (hi - lo) * 16, "out": (hi - lo) * 8},
+            "ms_per_step": t * 1e3, "path": "ettg_lca_query (pinned int64 host pairs/answers; "
+                                            "u32 pairs cross the link, narrowed by host threads)",
             "pageable": {"value": q_total / all_max(min(pg), device), "ms": 1e3 * min(pg),
                          "answers_match_pinned": pg_ok,
                          "what": "same call, numpy (pageable) pairs and answers, best of 3"},
@@ -399,32 +404,37 @@ def bridges_section(ett, args, device, peak):
     call_host()
     ok_h = bool(np.array_equal(pin_m.numpy(), truth))
     ts = []
-    for _ in range(2):
+    for _ in range(args.bridge_steps):
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         call_host()
         ts.append(time.perf_counter() - t0)
-    # floor: the edge list's H2D then the mask's D2H (the mask needs every edge)
-    d_e = torch.empty(pin_e.shape, dtype=pin_e.dtype, device=device)
-    d_m = torch.empty(m, dtype=torch.uint8, device=device)
-    spare = torch.empty_like(pin_m).pin_memory()
+    # floor: the narrowed edge list's H2D then the bit mask's D2H (the mask
+    # needs every edge), as plain copies
+    d_e = torch.empty(2 * m, dtype=torch.int32, device=device)
+    src_e = torch.empty(2 * m, dtype=torch.int32).pin_memory()
+    d_m = torch.empty((m + 7) // 8, dtype=torch.uint8, device=device)
+    spare = torch.empty((m + 7) // 8, dtype=torch.uint8).pin_memory()
     copies = []
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        d_e.copy_(pin_e, non_blocking=True)
+        d_e.copy_(src_e, non_blocking=True)
         spare.copy_(d_m, non_blocking=True)
         e1.record()
         e1.synchronize()
         copies.append(e0.elapsed_time(e1))
-    del d_e, d_m, spare
+    del d_e, d_m, spare, src_e
     out["e2e"] = {"value": m / min(ts), "unit": "edges/s", "ms_per_step": 1e3 * min(ts),
-                  "h2d_bytes_per_step": m * 16, "d2h_bytes_per_step": m,
-                  "path": "ettg_bridges (pinned int64 host edge list -> host mask)",
+                  "ms_median": 1e3 * float(np.median(ts)),
+                  "h2d_bytes_per_step": m * 8, "d2h_bytes_per_step": (m + 7) // 8,
+                  "caller_bytes_per_step": {"in": m * 16, "out": m},
+                  "path": "ettg_bridges (pinned int64 host edge list -> host mask; u32 edges "
+                          "cross the link, the mask comes back as bits)",
                   "parity": "bit-exact vs planted truth" if ok_h else "MISMATCH",
                   "link_bound": {"ms": min(copies), "frac": min(copies) / (1e3 * min(ts)),
-                                 "what": "H2D of the edge list then D2H of the mask as plain "
-                                         "copies (no kernel), CUDA events, best of 3"}}
+                                 "what": "H2D of the u32 edge list then D2H of the bit mask "
+                                         "as plain copies (no kernel), CUDA events, best of 3"}}
     del pin_e, pin_m
     if args.cpu_baseline:
         from oracle import oracle as orc

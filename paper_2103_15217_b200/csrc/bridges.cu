@@ -1027,9 +1027,11 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
                     ws.tree + lo / 2, ws.words, sms, st, true);
       };
     }
+    // a pinned edge list sends ~1/3 of its chunks as int64 (narrowed on the
+    // device): host memory bandwidth and the link then balance
     if (m && staged_h2d_narrow_u32(reinterpret_cast<u32*>(ws.edges),
                                    static_cast<const int64_t*>(in.edges), 2ull * m, n, false,
-                                   device, cs, hook_chunk))
+                                   device, cs, hook_chunk, raw_fraction(0.33)))
       einval("edge endpoint out of range");
     if (cs != st) {  // everything after the input reads all of it
       CK(cudaEventRecord(copy_guard.e, cs));

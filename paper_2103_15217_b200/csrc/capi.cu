@@ -313,18 +313,76 @@ void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, i
   }
 }
 
+// Device narrowing of an int64 chunk that crossed the link as is.
+__global__ void k_narrow_u32(const int64_t* __restrict__ in, u64 n, uint64_t bound,
+                             bool allow_none, uint32_t* __restrict__ out, u32* bad) {
+  u32 b = 0;
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n;
+       i += u64(gridDim.x) * blockDim.x) {
+    const int64_t x = in[i];
+    const bool ok = static_cast<uint64_t>(x) < bound || (allow_none && x == -1);
+    b |= !ok;
+    out[i] = ok ? static_cast<uint32_t>(x) : 0xFFFFFFFFu;
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+double raw_fraction(double dflt) {
+  if (const char* e = std::getenv("ETTG_RAW_FRAC")) return std::min(1.0, std::max(0.0, std::atof(e)));
+  return dflt;
+}
+
+bool chunk_is_raw(u64 c, double frac) {
+  return frac > 0 && static_cast<u64>((c + 1) * frac) > static_cast<u64>(c * frac);
+}
+
 u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
                           bool allow_none, int device, cudaStream_t st,
-                          const std::function<void(size_t, size_t)>& on_chunk) {
+                          const std::function<void(size_t, size_t)>& on_chunk,
+                          double raw_frac) {
   check_host_ptr(h_src);  // a device pointer here would be written by host threads
+  if (raw_frac > 0 && !is_pinned(h_src)) raw_frac = 0;  // raw chunks need DMA-able memory
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
   const size_t per = kStageChunk / sizeof(uint32_t);
+  // raw chunks land in one of two int64 scratch buffers (stream-ordered
+  // allocations; reuse is ordered on `st`), plus a device bad-value flag
+  struct Scratch {
+    char* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } sc;
+  int64_t* raw[2] = {nullptr, nullptr};
+  u32* dflag = nullptr;
+  if (raw_frac > 0) {
+    sc.s = st;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&sc.p), 2 * per * 8 + 256, st));
+    raw[0] = reinterpret_cast<int64_t*>(sc.p);
+    raw[1] = raw[0] + per;
+    dflag = reinterpret_cast<u32*>(sc.p + 2 * per * 8);
+    CK(cudaMemsetAsync(dflag, 0, 4, st));
+  }
+  const int sms = sm_count(device);
   u64 bad = 0;
-  int k = 0;
-  for (size_t lo = 0; lo < count; lo += per, k = (k + 1) % kStageBufs) {
+  int k = 0, r = 0;
+  u64 c = 0;
+  for (size_t lo = 0; lo < count; lo += per, ++c) {
     const size_t n = std::min(per, count - lo);
+    if (chunk_is_raw(c, raw_frac)) {
+      // the link carries this chunk as int64 (no host work); the device
+      // narrows it -- host memory bandwidth, not the link, bounds an
+      // all-narrowed upload on the B200 host (e2e)
+      CK(cudaMemcpyAsync(raw[r], h_src + lo, n * 8, cudaMemcpyHostToDevice, st));
+      k_narrow_u32<<<std::min<u64>((n + 255) / 256, u64(sms) * 8), 256, 0, st>>>(
+          raw[r], n, bound, allow_none, d_dst + lo, dflag);
+      CK(cudaGetLastError());
+      r ^= 1;
+      if (on_chunk) on_chunk(lo, n);
+      continue;
+    }
     CK(cudaEventSynchronize(s.done[k]));  // the copy that last read this buffer
     uint32_t* out = reinterpret_cast<uint32_t*>(s.buf[k]);
     const int64_t* in = h_src + lo;
@@ -341,7 +399,14 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
     if (b) break;  // the caller fails the call: skip the rest
     CK(cudaMemcpyAsync(d_dst + lo, out, n * 4, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(s.done[k], st));
+    k = (k + 1) % kStageBufs;
     if (on_chunk) on_chunk(lo, n);
+  }
+  if (dflag) {
+    u32 f = 0;
+    CK(cudaMemcpyAsync(&f, dflag, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bad += f;
   }
   CK(cudaStreamSynchronize(st));
   return bad;

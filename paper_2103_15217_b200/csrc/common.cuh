@@ -257,9 +257,17 @@ void staged_d2h(void* h_dst, const void* d_src, size_t bytes, int device, cudaSt
 // the others are stored as 0xFFFFFFFF and counted in the return value (the
 // caller raises its own error).  on_chunk(lo, n), if given, runs after chunk
 // [lo, lo + n) is enqueued on `st` (to enqueue its consumers).  Synchronises st.
+// raw_frac > 0 (pinned h_src only): that fraction of the chunks crosses the
+// link as int64 and is narrowed on the device instead, trading link bytes
+// for host memory bandwidth (both bind on the B200 host).
 u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
                           bool allow_none, int device, cudaStream_t st,
-                          const std::function<void(size_t, size_t)>& on_chunk = {});
+                          const std::function<void(size_t, size_t)>& on_chunk = {},
+                          double raw_frac = 0);
+// ETTG_RAW_FRAC if set (0..1), else dflt; and whether chunk c of a hybrid
+// upload goes raw (an even spread: floor((c+1) f) > floor(c f)).
+double raw_fraction(double dflt);
+bool chunk_is_raw(u64 c, double frac);
 // D2H of a bit-packed 0/1 mask (`count` bits, LSB first per u32 word) into
 // `count` mask bytes, expanded by the host threads as the chunks land: 1/8
 // of the bytes over the link.

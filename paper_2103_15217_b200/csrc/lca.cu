@@ -1565,7 +1565,7 @@ namespace {
 // the narrowed bytes move in about half the time of the int64 ones.  Ids outside [0, 2^32) are stored as
 // 0xFFFFFFFF, which the kernel's range check rejects (ETTG_ERANGE).
 void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q,
-                       int64_t* answers, bool answers_pinned) {
+                       int64_t* answers, bool pairs_pinned, bool answers_pinned) {
   StageLease sl(h->device);
   // stage bytes per query: the u32 pair, plus the u32 answer when the
   // caller's answer buffer is pageable (a pinned one takes the int64
@@ -1575,6 +1575,12 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   CK(cudaMemsetAsync(h->qerr, 0, 8, h->qs[0]));
   CK(cudaStreamSynchronize(h->qs[0]));
   const u64 chunks = (q + per - 1) / per;
+  // Both buffers pinned: a fraction of the chunks crosses the link as int64
+  // straight from the caller's memory (no host work).  Narrowing costs host
+  // memory bandwidth (read 16 B, write 8 B, DMA-read 8 B per query) on top
+  // of the answers' 8 B; on the B200 host that, not the link, bounds an
+  // all-narrowed call (tools/ab_lca_e2e.py, DESIGN.md e2e).
+  const double raw_frac = pairs_pinned && answers_pinned ? raw_fraction(0.5) : 0.0;
   const int threads = host_thread_count();
   const char* tr = std::getenv("ETTG_TRACE");
   const bool trace = tr && *tr && *tr != '0';
@@ -1593,11 +1599,23 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
     for (long i = 0; i < static_cast<long>(cnt); ++i) out[i] = in[i];
     if (trace) t_widen += omp_get_wtime() - t1;
   };
+  u64 nk = 0;  // narrowed chunks so far (they rotate through the stage)
   for (u64 c = 0; c < chunks; ++c) {
-    const int k = c % kStageBufs;  // stage buffer
-    const int s = c & 1;           // stream and device slot
-    if (c >= kStageBufs) drain(c - kStageBufs);
+    const int s = c & 1;  // stream and device slot
     const u64 lo = c * per, cnt = std::min(per, q - lo);
+    if (chunk_is_raw(c, raw_frac)) {
+      cudaStream_t st = h->qs[s];
+      char* slot = h->qmem + s * h->qchunk * 24;  // int64 pairs, then int64 answers
+      const longlong2* dp = reinterpret_cast<const longlong2*>(slot);
+      long long* da = reinterpret_cast<long long*>(slot + h->qchunk * 16);
+      CK(cudaMemcpyAsync(slot, pairs + 2 * lo, cnt * 16, cudaMemcpyHostToDevice, st));
+      launch_query(h, engine, PairsI64{dp}, AnsI64{da}, cnt, h->qerr + s, st);
+      CK(cudaMemcpyAsync(answers + lo, da, cnt * 8, cudaMemcpyDeviceToHost, st));
+      continue;
+    }
+    const int k = nk % kStageBufs;  // stage buffer
+    if (nk >= kStageBufs) drain(nk - kStageBufs);
+    ++nk;
     u32* st_pairs = reinterpret_cast<u32*>(sl.buf(k));
     const int64_t* in = pairs + 2 * lo;
     const double t0 = trace ? omp_get_wtime() : 0;
@@ -1624,7 +1642,7 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
       CK(cudaEventRecord(sl.done(k), st));
     }
   }
-  for (u64 c = chunks > kStageBufs ? chunks - kStageBufs : 0; c < chunks; ++c) drain(c);
+  for (u64 c = nk > kStageBufs ? nk - kStageBufs : 0; c < nk; ++c) drain(c);
   u32 errs[2] = {0, 0};
   CK(cudaStreamSynchronize(h->qs[1]));
   CK(cudaMemcpyAsync(errs, h->qerr, sizeof errs, cudaMemcpyDeviceToHost, h->qs[0]));
@@ -1654,7 +1672,8 @@ int ettg_lca_query_engine(const ettg_lca* hc, unsigned engine, const int64_t* pa
     // both checked (a device pointer in either is a caller error, whatever q)
     const bool pairs_pinned = is_pinned(pairs), answers_pinned = is_pinned(answers);
     if (q >= (1 << 16) && (narrow_enabled() || !(pairs_pinned && answers_pinned))) {
-      query_host_narrow(h, engine, pairs, static_cast<u64>(q), answers, answers_pinned);
+      query_host_narrow(h, engine, pairs, static_cast<u64>(q), answers, pairs_pinned,
+                        answers_pinned);
       return;
     }
     // 1M-query chunks on two streams: H2D of chunk c+1 overlaps the kernel and
