@@ -1579,8 +1579,9 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   // straight from the caller's memory (no host work).  Narrowing costs host
   // memory bandwidth (read 16 B, write 8 B, DMA-read 8 B per query) on top
   // of the answers' 8 B; on the B200 host that, not the link, bounds an
-  // all-narrowed call (tools/ab_lca_e2e.py, DESIGN.md e2e).
-  const double raw_frac = pairs_pinned && answers_pinned ? raw_fraction(0.5) : 0.0;
+  // all-narrowed call.  Config B, 16M queries (tools/ab_rawfrac.py): raw
+  // share 0 -> 4.92-4.98 ms, 0.375 -> 4.51-4.62, 0.5 -> 4.63-4.66, 1 -> 5.04.
+  const double raw_frac = pairs_pinned && answers_pinned ? raw_fraction(0.375) : 0.0;
   const int threads = host_thread_count();
   const char* tr = std::getenv("ETTG_TRACE");
   const bool trace = tr && *tr && *tr != '0';
