@@ -629,80 +629,6 @@ __global__ void __launch_bounds__(256, kMinB)
   }
 }
 
-// The same updates with the endpoint-u side combined across the warp: edge
-// lists that list each vertex's edges together (CSR-derived lists, the
-// road-like generator, parsed files sorted by source) put runs of equal u in
-// consecutive lanes, and all their u-side updates hit one slot (key(u)).  A
-// segmented min / max over each run (5 shuffle steps) leaves one atomicMin
-// and one atomicMax per run instead of one per edge; the v side stays per
-// edge.  Any edge order gives the same slots (the reduction only merges
-// updates to one address); unsorted lists just form runs of length 1.
-template <int kHookE, int kMinB>
-__global__ void __launch_bounds__(256, kMinB)
-    k_lowhigh_edges_agg(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
-                        const u32* __restrict__ pre_of, uint2* lh, const u32* abort, u32 n) {
-  if (tv_abort(abort, n)) return;
-  u32* w = reinterpret_cast<u32*>(lh);  // slot = key - 1; .x = low, .y = high
-  const int lane = threadIdx.x & 31;
-  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x;
-       base - lane < m;  // warp-uniform: every lane takes part in the shuffles
-       base += stride * kHookE) {
-    uint2 uv[kHookE];
-    bool nt[kHookE];
-#pragma unroll
-    for (int j = 0; j < kHookE; ++j) {
-      const u64 e = base + j * stride;
-      const bool in = e < m;
-      uv[j] = in ? edges[e] : make_uint2(0xFFFFFFFFu, 0u);
-      nt[j] = in && !tree[e];
-    }
-    u32 ku[kHookE], kv[kHookE];
-#pragma unroll
-    for (int j = 0; j < kHookE; ++j) {
-      ku[j] = nt[j] ? __ldg(pre_of + uv[j].x) : 0u;
-      kv[j] = nt[j] ? __ldg(pre_of + uv[j].y) : 0u;
-      nt[j] = nt[j] && ku[j] != kv[j];  // a self-loop changes nothing
-    }
-#pragma unroll
-    for (int j = 0; j < kHookE; ++j) {
-      // u side: low(ku) <- kv if kv < ku, high(ku) <- kv if kv > ku
-      u32 lo = nt[j] && kv[j] < ku[j] ? kv[j] : 0xFFFFFFFFu;
-      u32 hi = nt[j] && kv[j] > ku[j] ? kv[j] : 0u;
-      const u32 prev = __shfl_up_sync(0xffffffffu, uv[j].x, 1);
-      const bool head = lane == 0 || prev != uv[j].x;
-      const u32 heads = __ballot_sync(0xffffffffu, head);
-      // lanes after mine up to the next head belong to my run
-      const u32 after = heads & ~((2u << lane) - 1u);
-      const int end = after ? __ffs(after) - 1 : 32;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const u32 ol = __shfl_down_sync(0xffffffffu, lo, d);
-        const u32 oh = __shfl_down_sync(0xffffffffu, hi, d);
-        if (lane + d < end) {
-          lo = min(lo, ol);
-          hi = max(hi, oh);
-        }
-      }
-      // the run's head owns the u-side update: slot key(u) of the run
-      if (head && (lo != 0xFFFFFFFFu || hi != 0u)) {
-        u32 kh = ku[j];                                // keys are >= 1: 0 = not loaded
-        if (kh == 0u) kh = __ldg(pre_of + uv[j].x);  // the head's own edge is a tree edge
-        if (lo != 0xFFFFFFFFu && w[2 * (kh - 1)] > lo) atomicMin(&w[2 * (kh - 1)], lo);
-        if (hi != 0u && w[2 * (kh - 1) + 1] < hi) atomicMax(&w[2 * (kh - 1) + 1], hi);
-      }
-      // v side, per edge: low(kv) <- ku if ku < kv, high(kv) <- ku if ku > kv
-      if (nt[j]) {
-        if (ku[j] < kv[j]) {
-          if (w[2 * (kv[j] - 1)] > ku[j]) atomicMin(&w[2 * (kv[j] - 1)], ku[j]);
-        } else {
-          if (w[2 * (kv[j] - 1) + 1] < ku[j]) atomicMax(&w[2 * (kv[j] - 1) + 1], ku[j]);
-        }
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
   return make_uint2(min(a.x, b.x), max(a.y, b.y));
 }
@@ -861,11 +787,11 @@ void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* p
   // 0.150 ms), so small slot arrays issue the atomics directly.
   bool check = static_cast<u64>(n) * 16 > (u64(64) << 20);
   if (const char* e = std::getenv("ETTG_LH_CHECK")) check = std::atoi(e) != 0;
-  bool agg = true;
-  if (const char* e = std::getenv("ETTG_LH_AGG")) agg = std::atoi(e) != 0;
-  auto kern = agg     ? k_lowhigh_edges_agg<kEdgesPerThread, 8>
-              : check ? k_lowhigh_edges<kEdgesPerThread, 8, true>
-                      : k_lowhigh_edges<kEdgesPerThread, 8, false>;
+  // (A warp-segmented min/max over runs of equal u, one u-side atomic pair
+  // per run, cut the L2 reductions 254M -> 148M sectors on config D but
+  // doubled the instructions and added reads: 2.37 vs 1.88 ms; round 2.)
+  auto kern = check ? k_lowhigh_edges<kEdgesPerThread, 8, true>
+                    : k_lowhigh_edges<kEdgesPerThread, 8, false>;
   kern<<<occ_grid(kern, (u64(m) + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
       edges, tree, m, pre_of, lh, abort, n);
   CK_LAUNCH();
