@@ -740,7 +740,9 @@ __global__ void __launch_bounds__(256)
     }
     const bool inside = acc.x >= k.x && acc.y < k.y;
     const u32 e = tedge[t];
-    if (e < m) mask[e] = inside ? 1 : 0;
+    // the mask was zeroed before the call: only bridges are stored (a
+    // random byte store per tree edge would read-modify-write 32M sectors)
+    if (inside && e < m) mask[e] = 1;
   }
 }
 

@@ -366,6 +366,10 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
     CK(cudaMemsetAsync(dflag, 0, 4, st));
   }
   const int sms = sm_count(device);
+  const char* tr = std::getenv("ETTG_TRACE");
+  const bool trace = tr && *tr && *tr != '0';
+  double t_wait = 0, t_narrow = 0;
+  const double t_start = trace ? omp_get_wtime() : 0;
   u64 bad = 0;
   int k = 0, r = 0;
   u64 c = 0;
@@ -383,7 +387,13 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
       if (on_chunk) on_chunk(lo, n);
       continue;
     }
+    double t0 = trace ? omp_get_wtime() : 0;
     CK(cudaEventSynchronize(s.done[k]));  // the copy that last read this buffer
+    if (trace) {
+      const double t1 = omp_get_wtime();
+      t_wait += t1 - t0;
+      t0 = t1;
+    }
     uint32_t* out = reinterpret_cast<uint32_t*>(s.buf[k]);
     const int64_t* in = h_src + lo;
     u64 b = 0;
@@ -395,6 +405,7 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
       b += !ok;
       out[i] = ok ? static_cast<uint32_t>(v) : 0xFFFFFFFFu;
     }
+    if (trace) t_narrow += omp_get_wtime() - t0;
     bad += b;
     if (b) break;  // the caller fails the call: skip the rest
     CK(cudaMemcpyAsync(d_dst + lo, out, n * 4, cudaMemcpyHostToDevice, st));
@@ -409,6 +420,12 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
     bad += f;
   }
   CK(cudaStreamSynchronize(st));
+  if (trace)
+    std::fprintf(stderr,
+                 "[ettg trace] h2d_narrow: %llu ids, %llu chunks (raw share %.2f) narrow=%.3f "
+                 "wait=%.3f wall=%.3f ms\n",
+                 static_cast<unsigned long long>(count), static_cast<unsigned long long>(c),
+                 raw_frac, t_narrow * 1e3, t_wait * 1e3, (omp_get_wtime() - t_start) * 1e3);
   return bad;
 }
 

@@ -188,7 +188,7 @@ __global__ void k_ck_classify(const u32* __restrict__ pedge, const uint8_t* __re
                               u32 n, uint8_t* __restrict__ mask, u32 m) {
   for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const u32 e = pedge[v];
-    if (e < m) mask[e] = marked[v] ? 0 : 1;
+    if (e < m && !marked[v]) mask[e] = 1;  // zeroed before the call: bridges only
   }
 }
 
