@@ -1032,12 +1032,11 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
                     ws.tree + lo / 2, ws.words, sms, st, true);
       };
     }
-    // all chunks narrowed on the host by default: sending a share as int64
-    // (ETTG_RAW_FRAC) measured slower and noisier here (0.2: 61.6 vs 65.8 ms
-    // once, 0.33-1.0: 65-105 ms; tools/ab_rawfrac.py, profiles/r2_e2e.md)
+    // pinned: a chunk goes as int64 (narrowed on the device) whenever the
+    // link has caught up with the host narrowing (kRawAdaptive)
     if (m && staged_h2d_narrow_u32(reinterpret_cast<u32*>(ws.edges),
                                    static_cast<const int64_t*>(in.edges), 2ull * m, n, false,
-                                   device, cs, hook_chunk, raw_fraction(0.0)))
+                                   device, cs, hook_chunk, raw_fraction(kRawAdaptive)))
       einval("edge endpoint out of range");
     if (cs != st) {  // everything after the input reads all of it
       CK(cudaEventRecord(copy_guard.e, cs));

@@ -328,7 +328,10 @@ __global__ void k_narrow_u32(const int64_t* __restrict__ in, u64 n, uint64_t bou
 }
 
 double raw_fraction(double dflt) {
-  if (const char* e = std::getenv("ETTG_RAW_FRAC")) return std::min(1.0, std::max(0.0, std::atof(e)));
+  if (const char* e = std::getenv("ETTG_RAW_FRAC")) {
+    if (std::strcmp(e, "auto") == 0) return kRawAdaptive;
+    return std::min(1.0, std::max(0.0, std::atof(e)));
+  }
   return dflt;
 }
 
@@ -336,12 +339,21 @@ bool chunk_is_raw(u64 c, double frac) {
   return frac > 0 && static_cast<u64>((c + 1) * frac) > static_cast<u64>(c * frac);
 }
 
+bool RawPolicy::raw_next(u64 c) const {
+  if (frac == kRawAdaptive) {
+    // the link has drained everything enqueued: the host is the bottleneck
+    // right now, so this chunk goes as is
+    return !last || cudaEventQuery(last) == cudaSuccess;
+  }
+  return chunk_is_raw(c, frac);
+}
+
 u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, uint64_t bound,
                           bool allow_none, int device, cudaStream_t st,
                           const std::function<void(size_t, size_t)>& on_chunk,
                           double raw_frac) {
   check_host_ptr(h_src);  // a device pointer here would be written by host threads
-  if (raw_frac > 0 && !is_pinned(h_src)) raw_frac = 0;  // raw chunks need DMA-able memory
+  if (raw_frac != 0 && !is_pinned(h_src)) raw_frac = 0;  // raw chunks need DMA-able memory
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
@@ -357,7 +369,16 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
   } sc;
   int64_t* raw[2] = {nullptr, nullptr};
   u32* dflag = nullptr;
-  if (raw_frac > 0) {
+  cudaEvent_t raw_ev[2] = {nullptr, nullptr};
+  struct EvFree {
+    cudaEvent_t* e;
+    ~EvFree() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } ev_free{raw_ev};
+  if (raw_frac != 0) {
+    for (auto& e : raw_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     sc.s = st;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&sc.p), 2 * per * 8 + 256, st));
     raw[0] = reinterpret_cast<int64_t*>(sc.p);
@@ -370,12 +391,13 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
   const bool trace = tr && *tr && *tr != '0';
   double t_wait = 0, t_narrow = 0;
   const double t_start = trace ? omp_get_wtime() : 0;
-  u64 bad = 0;
+  u64 bad = 0, nraw = 0;
   int k = 0, r = 0;
   u64 c = 0;
+  RawPolicy pol{raw_frac, nullptr};
   for (size_t lo = 0; lo < count; lo += per, ++c) {
     const size_t n = std::min(per, count - lo);
-    if (chunk_is_raw(c, raw_frac)) {
+    if (raw_frac != 0 && pol.raw_next(c)) {
       // the link carries this chunk as int64 (no host work); the device
       // narrows it -- host memory bandwidth, not the link, bounds an
       // all-narrowed upload on the B200 host (e2e)
@@ -383,7 +405,10 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
       k_narrow_u32<<<std::min<u64>((n + 255) / 256, u64(sms) * 8), 256, 0, st>>>(
           raw[r], n, bound, allow_none, d_dst + lo, dflag);
       CK(cudaGetLastError());
+      CK(cudaEventRecord(raw_ev[r], st));
+      pol.last = raw_ev[r];
       r ^= 1;
+      ++nraw;
       if (on_chunk) on_chunk(lo, n);
       continue;
     }
@@ -410,6 +435,7 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
     if (b) break;  // the caller fails the call: skip the rest
     CK(cudaMemcpyAsync(d_dst + lo, out, n * 4, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(s.done[k], st));
+    pol.last = s.done[k];
     k = (k + 1) % kStageBufs;
     if (on_chunk) on_chunk(lo, n);
   }
@@ -422,10 +448,11 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
   CK(cudaStreamSynchronize(st));
   if (trace)
     std::fprintf(stderr,
-                 "[ettg trace] h2d_narrow: %llu ids, %llu chunks (raw share %.2f) narrow=%.3f "
-                 "wait=%.3f wall=%.3f ms\n",
+                 "[ettg trace] h2d_narrow: %llu ids, %llu chunks, %llu raw (policy %.2f) "
+                 "narrow=%.3f wait=%.3f wall=%.3f ms\n",
                  static_cast<unsigned long long>(count), static_cast<unsigned long long>(c),
-                 raw_frac, t_narrow * 1e3, t_wait * 1e3, (omp_get_wtime() - t_start) * 1e3);
+                 static_cast<unsigned long long>(nraw), raw_frac, t_narrow * 1e3, t_wait * 1e3,
+                 (omp_get_wtime() - t_start) * 1e3);
   return bad;
 }
 

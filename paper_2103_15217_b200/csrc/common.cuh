@@ -264,10 +264,20 @@ u64 staged_h2d_narrow_u32(uint32_t* d_dst, const int64_t* h_src, size_t count, u
                           bool allow_none, int device, cudaStream_t st,
                           const std::function<void(size_t, size_t)>& on_chunk = {},
                           double raw_frac = 0);
-// ETTG_RAW_FRAC if set (0..1), else dflt; and whether chunk c of a hybrid
-// upload goes raw (an even spread: floor((c+1) f) > floor(c f)).
+// ETTG_RAW_FRAC if set (0..1, or "auto"), else dflt; and whether chunk c of
+// a hybrid upload goes raw (an even spread: floor((c+1) f) > floor(c f)).
+// kRawAdaptive: a chunk goes raw whenever the link has drained everything
+// enqueued before it (the host narrowing is then the bottleneck), so the
+// split follows the host's memory bandwidth, which varies from box to box
+// (4 GB narrowed in 33 ms on one B200 host, 72 ms on another).
+constexpr double kRawAdaptive = -1.0;
 double raw_fraction(double dflt);
 bool chunk_is_raw(u64 c, double frac);
+struct RawPolicy {
+  double frac;       // kRawAdaptive, or a static share
+  cudaEvent_t last;  // the last enqueued upload
+  bool raw_next(u64 c) const;
+};
 // D2H of a bit-packed 0/1 mask (`count` bits, LSB first per u32 word) into
 // `count` mask bytes, expanded by the host threads as the chunks land: 1/8
 // of the bytes over the link.

@@ -1579,9 +1579,22 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   // straight from the caller's memory (no host work).  Narrowing costs host
   // memory bandwidth (read 16 B, write 8 B, DMA-read 8 B per query) on top
   // of the answers' 8 B; on the B200 host that, not the link, bounds an
-  // all-narrowed call.  Config B, 16M queries (tools/ab_rawfrac.py): raw
-  // share 0 -> 4.92-4.98 ms, 0.375 -> 4.51-4.62, 0.5 -> 4.63-4.66, 1 -> 5.04.
-  const double raw_frac = pairs_pinned && answers_pinned ? raw_fraction(0.375) : 0.0;
+  // all-narrowed call.  Config B, 16M queries (tools/ab_rawfrac.py): static
+  // raw share 0 -> 4.92-4.98 ms, 0.375 -> 4.51-4.62, 0.5 -> 4.63-4.66, 1 ->
+  // 5.04; the best share depends on the host, so by default a chunk goes raw
+  // whenever the link has drained the uploads before it (kRawAdaptive).
+  const double raw_frac = pairs_pinned && answers_pinned ? raw_fraction(kRawAdaptive) : 0.0;
+  RawPolicy pol{raw_frac, nullptr};
+  cudaEvent_t up_ev[2] = {nullptr, nullptr};  // the last upload on each stream
+  struct EvFree {
+    cudaEvent_t* e;
+    ~EvFree() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } ev_free{up_ev};
+  if (raw_frac != 0)
+    for (auto& e : up_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const int threads = host_thread_count();
   const char* tr = std::getenv("ETTG_TRACE");
   const bool trace = tr && *tr && *tr != '0';
@@ -1604,12 +1617,14 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
   for (u64 c = 0; c < chunks; ++c) {
     const int s = c & 1;  // stream and device slot
     const u64 lo = c * per, cnt = std::min(per, q - lo);
-    if (chunk_is_raw(c, raw_frac)) {
+    if (raw_frac != 0 && pol.raw_next(c)) {
       cudaStream_t st = h->qs[s];
       char* slot = h->qmem + s * h->qchunk * 24;  // int64 pairs, then int64 answers
       const longlong2* dp = reinterpret_cast<const longlong2*>(slot);
       long long* da = reinterpret_cast<long long*>(slot + h->qchunk * 16);
       CK(cudaMemcpyAsync(slot, pairs + 2 * lo, cnt * 16, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(up_ev[s], st));
+      pol.last = up_ev[s];
       launch_query(h, engine, PairsI64{dp}, AnsI64{da}, cnt, h->qerr + s, st);
       CK(cudaMemcpyAsync(answers + lo, da, cnt * 8, cudaMemcpyDeviceToHost, st));
       continue;
@@ -1631,6 +1646,10 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
     char* slot = h->qmem + s * qc * 24;  // per stream: 8-B pairs, then 4- or 8-B answers
     const uint2* dp = reinterpret_cast<const uint2*>(slot);
     CK(cudaMemcpyAsync(slot, st_pairs, cnt * 8, cudaMemcpyHostToDevice, st));
+    if (raw_frac != 0) {
+      CK(cudaEventRecord(up_ev[s], st));
+      pol.last = up_ev[s];
+    }
     if (answers_pinned) {
       CK(cudaEventRecord(sl.done(k), st));  // the stage is free once the pairs landed
       long long* da = reinterpret_cast<long long*>(slot + qc * 8);
