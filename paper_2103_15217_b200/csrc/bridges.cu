@@ -17,7 +17,9 @@
 //                              count is the connectivity check (n-1 tree edges)
 //             k_tree_rot       per-vertex rotation lists by atomicExch (no sort:
 //                              any rotation gives a valid tour)
-//             k_tree_succ      succ(e) = next(twin(e)); cut before first(0)
+//             k_tree_close     rotation lists closed into cycles except the
+//                              root's: succ(e) = nxt[twin(e)] = nxt[e ^ 1],
+//                              read by the list ranking itself
 //             list_rank_core   ranks of the tour rooted at vertex 0
 //             k_tv_keys        node key = tour rank of its down half-edge + 2
 //                              (order-isomorphic to the preorder; a subtree is
@@ -432,7 +434,7 @@ struct TreeOut {
 // half-edge of the root's rotation.
 __device__ __forceinline__ void rot_push(u32 active, u32 x, u32 h, u32 root,
                                          u32* __restrict__ head, u32* __restrict__ nxt,
-                                         u32* last_root) {
+                                         u32* __restrict__ tails, u32* last_root) {
   const int lane = threadIdx.x & 31;
   u32 p;
   bool tail = true;
@@ -451,12 +453,16 @@ __device__ __forceinline__ void rot_push(u32 active, u32 x, u32 h, u32 root,
     p = atomicExch(&head[x], h);
   }
   nxt[h] = p;
-  if (tail && p == kNone && x == root) *last_root = h;
+  if (tail && p == kNone) {
+    tails[x] = h;  // the list's last element: k_tree_close links it to head[x]
+    if (x == root) *last_root = h;
+  }
 }
 
 __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
                            u32 root, u32* __restrict__ head, u32* __restrict__ nxt,
-                           uint2* __restrict__ tend, u32* last_root, const u32* abort, u32 n) {
+                           uint2* __restrict__ tend, u32* __restrict__ tails, u32* last_root,
+                           const u32* abort, u32 n) {
   if (tv_abort(abort, n)) return;
   const u32 stride = gridDim.x * blockDim.x;
   for (u32 base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < T; base += stride) {
@@ -465,29 +471,30 @@ __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restric
     if (t >= T) continue;
     const uint2 uv = edges[tedge[t]];
     tend[t] = uv;
-    rot_push(active, uv.x, 2 * t, root, head, nxt, last_root);
-    rot_push(active, uv.y, 2 * t + 1, root, head, nxt, last_root);
+    rot_push(active, uv.x, 2 * t, root, head, nxt, tails, last_root);
+    rot_push(active, uv.y, 2 * t + 1, root, head, nxt, tails, last_root);
   }
 }
 
-// succ(e) = next(twin(e)) in the cyclic rotation of twin(e)'s source, which
-// is e's destination (core/src/euler.cpp:85-88, :105).  Written as list-rank
-// slots; the cut before head[root] makes the tour a list.
-__global__ void k_tree_succ(const uint2* __restrict__ tend, const u32* __restrict__ head,
-                            const u32* __restrict__ nxt, u32 k, const u32* d_cut,
-                            u32* __restrict__ slot, const u32* abort, u32 n) {
+// Closes every rotation list into a cycle (nxt[tail(x)] = head(x)) except
+// the root's, whose open end is the tour's cut.  Then for every half-edge
+// succ(e) = nxt[e ^ 1] = next(twin(e)) in the cyclic rotation of e's
+// destination (core/src/euler.cpp:85-88, :105), cut before head[root], and
+// the list ranking reads the successor straight from nxt[e ^ 1] -- the same
+// one dependent load per step, with no successor array to build (round 1
+// built it in a separate pass: 0.30 ms and 512 MB of traffic on config D).
+// A bad input (abort) leaves nxt unwritten: every link becomes a tail.
+__global__ void k_tree_close(const u32* __restrict__ head, const u32* __restrict__ tails, u32 root,
+                             u32* __restrict__ nxt, u32 k, const u32* abort, u32 n) {
   const bool off = tv_abort(abort, n);
-  const u32 cut = *d_cut;
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+  const u32 lim = off ? k : n;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
     if (off) {
-      slot[e] = kNone;  // a list of isolated tails: ranked without faults, flagged
-      continue;
+      nxt[i] = kNone;
+    } else if (i != root) {
+      const u32 h = head[i];
+      if (h != kNone) nxt[tails[i]] = h;
     }
-    const u32 tw = e ^ 1u;
-    const uint2 uv = tend[e >> 1];
-    const u32 dst = (e & 1u) ? uv.x : uv.y;
-    const u32 n2 = nxt[tw];
-    slot[e] = e == cut ? kNone : (n2 != kNone ? n2 : head[dst]);
   }
 }
 
@@ -884,6 +891,7 @@ struct BridgeWs {
   u32* head = nullptr;
   u32* nxt = nullptr;
   uint2* tend = nullptr;
+  u32* tails = nullptr;  // last element of each rotation list
   ListRankWs lr;
   u32* flags = nullptr;
   u64* scan_k = nullptr;
@@ -925,6 +933,7 @@ struct BridgeWs {
     head = c.take<u32>(n);
     nxt = c.take<u32>(k + 1);
     tend = c.take<uint2>(n);
+    tails = c.take<u32>(n);
     lr.carve(c, k > 0 ? k : 1, true);  // tour ranks only: no down weights
     flags = c.take<u32>(k + 1);
     scan_k = c.take<u64>(scan_ws_words(k + 1));
@@ -1172,16 +1181,16 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
       CK(cudaMemsetAsync(ws.head, 0xFF, static_cast<u64>(n) * 4, st));
       tr.mark("compact");
       k_tree_rot<<<std::min(g, blocks_for(T, 256)), 256, 0, st>>>(
-          edges, ws.tedge, T, 0, ws.head, ws.nxt, ws.tend, ws.words + 4, abort, n);
+          edges, ws.tedge, T, 0, ws.head, ws.nxt, ws.tend, ws.tails, ws.words + 4, abort, n);
       CK_LAUNCH();
       k_tree_head<<<1, 1, 0, st>>>(ws.head, 0, ws.words + 4, ws.words, abort, n);
       CK_LAUNCH();
       // head and cut stay on the device (words[2], words[3])
-      k_tree_succ<<<std::min(g, blocks_for(k, 256)), 256, 0, st>>>(
-          ws.tend, ws.head, ws.nxt, k, ws.words + 3, ws.lr.succ0, abort, n);
+      k_tree_close<<<std::min(g, blocks_for(std::max(n, k), 256)), 256, 0, st>>>(
+          ws.head, ws.tails, 0, ws.nxt, k, abort, n);
       CK_LAUNCH();
       tr.mark("rotation");
-      list_rank_core_h(k, DevHead{ws.words + 2}, NoDown{}, ws.lr, st, sms);
+      list_rank_core_h(k, DevHead{ws.words + 2}, NoDown{}, ws.lr, st, sms, nullptr, ws.nxt);
       tr.mark("list_rank");
       const Lr0View lv = lr0_view(ws.lr);
       if (engine == ETTG_BRIDGES_TV) {

@@ -206,7 +206,9 @@ constexpr int kLrWalkers = 1;
 
 // kNarrow (lists without down weights): 4-B records (local << sid_bits | sid)
 // and sublists capped at cap_step elements (walk micro: -12% vs 8-B records).
-template <class Down, class H, bool kNarrow>
+// kTwin: the successor of e is succ[e ^ 1] (an Euler tour whose closed
+// rotation lists serve as the successor array, bridges.cu k_tree_close).
+template <class Down, class H, bool kNarrow, bool kTwin = false>
 __global__ void __launch_bounds__(256)
     k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, H head_src, u32 seed,
                u32 mask, const u32* __restrict__ spl, u32* counters, u32 sub_cap,
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(256)
           rec32[cur[w]] = ((acc[w] & 0xFFFFu) << sid_bits) | sid[w];
         else
           rec[cur[w]] = (static_cast<u64>(acc[w]) << 32) | sid[w];
-        nxt[w] = succ[cur[w]];
+        nxt[w] = succ[kTwin ? cur[w] ^ 1u : cur[w]];
       }
     }
 #pragma unroll
@@ -292,6 +294,11 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+}
+
+__global__ void k_twin_succ(const u32* __restrict__ twin_succ, u32 k, u32* __restrict__ succ) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x)
+    succ[e] = twin_succ[e ^ 1u];
 }
 
 // Every element has at most one predecessor and the head has none (checked
@@ -655,9 +662,11 @@ inline u32 lr_seed(int level) { return 0x65746b5fu ^ (0x9e3779b9u * (level + 1))
 // per-element kernel (Lr0View).  `pred` (k words of scratch) enables the
 // injectivity check for caller-supplied lists.  No host synchronisation;
 // errors accumulate in counters[kErr].
+// twin_succ != nullptr: the level-0 successor of e is twin_succ[e ^ 1]
+// instead of ws.succ0[e] (narrow, weight-free lists only).
 template <class Down, class H>
 void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st, int sms,
-                      u32* pred = nullptr) {
+                      u32* pred = nullptr, const u32* twin_succ = nullptr) {
   Trace tr("list_rank", st);
   CK(cudaMemsetAsync(ws.counters, 0, 64 * sizeof(u32), st));
   u32* cnt = ws.counters;
@@ -677,7 +686,16 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
                      cudaMemcpyDeviceToDevice, st));
   tr.mark("splitters0");
   const unsigned walk_blocks = sms * 8;  // 2048 threads / SM resident
-  if (ws.sid_bits)
+  if (twin_succ && !ws.sid_bits) {  // wide records (huge lists): materialise succ0
+    k_twin_succ<<<blocks_for(k, 256), 256, 0, st>>>(twin_succ, k, ws.succ0);
+    CK_LAUNCH();
+    twin_succ = nullptr;
+  }
+  if (twin_succ) {
+    k_lr_walk0<Down, H, true, true><<<walk_blocks, 256, 0, st>>>(
+        twin_succ, ws.rec0, k, head, seed0, mask0, ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
+        ws.lv[0].sub_w, down, ws.cap_step, ws.sid_bits);
+  } else if (ws.sid_bits)
     k_lr_walk0<Down, H, true><<<walk_blocks, 256, 0, st>>>(
         ws.succ0, ws.rec0, k, head, seed0, mask0, ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
         ws.lv[0].sub_w, down, ws.cap_step, ws.sid_bits);
