@@ -1,5 +1,5 @@
-#!/bin/bash
-cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2f; mkdir -p $O
-nvcc -O3 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fopenmp tools/stage_micro.cu -o /tmp/stage_micro && /tmp/stage_micro > $O/stage_micro.txt 2>&1
-ETTG_TRACE=1 timeout 600 python tools/ab_lca_e2e.py > $O/ab_lca.txt 2>&1; echo "lca rc=$?" >> $O/rc.txt
+cd $GRAFT_REPO_ROOT; O=gpurun_out/r2f; mkdir -p $O
+timeout 900 python -m pytest tests/test_bridges_gpu.py tests/test_bridges_dropin_gpu.py -x -q > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+run() { echo "== $*"; env "$@" ETTG_TRACE=1 REPS=4 timeout 300 python tools/trace_bridges.py 2>&1 | grep -E "^bridges|\[ettg trace\] (bridges)|parity" | tail -3; }
+( run ETTG_LH_ID=1; run ETTG_LH_ID=0; run ETTG_LH_ID=1 GRAPH=C; run ETTG_LH_ID=0 GRAPH=C ) > $O/sweep.txt 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:'k_lowhigh_id|k_lh_scatter' -s 2 -c 2 -o $O/prof_lh -f env ETTG_TRACE=0 REPS=2 python tools/trace_bridges.py > $O/ncu.log 2>&1
