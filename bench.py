@@ -88,6 +88,28 @@ def l1_tag_stage(key, queries, secs, clocks):
             "source": "profiles/ncu_summary.json (l1tex__t_sectors ld+st per launch)"}
 
 
+def l2_requests(key, queries, secs, clocks):
+    """The request path from L1 to L2 accepts about one request per SM clock
+    (ncu l1tex__m_l1tex2xbar_req_cycles_active); a random gather is one
+    request, so requests per query -- from the committed ncu capture of the
+    same kernel and config -- times the query rate is the binding unit of the
+    scattered-gather query kernels."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)[key]
+        per_q = s["l2_requests_per_launch"] / s["units_per_launch"]
+    except Exception:
+        return None
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    achieved = per_q * queries / secs / 1e9
+    peak = sms * mhz / 1e3
+    return {"requests_per_query": per_q, "achieved_G_requests_per_s": achieved,
+            "peak_G_requests_per_s": peak, "frac": achieved / peak,
+            "ncu_req_active_pct": s.get("l1_to_l2_req_active_pct"),
+            "source": "profiles/ncu_summary.json (lts__t_requests_srcunit_tex per launch)"}
+
+
 def bridges_traffic(n, m):
     """DRAM bytes per tv_bridges call on config D from the committed ncu sweep
     (all kernels of one call), or None for another graph size."""
@@ -648,7 +670,8 @@ def config_e_block(ett, args, tree, sec, device, peak, world):
                                       "ceiling_G_per_s": L2_GATHER_CEILING.get(layout),
                                       "frac": (2 * q_r / secs / 1e9 / L2_GATHER_CEILING[layout]
                                                if layout in L2_GATHER_CEILING else None)},
-                        "l1_tag_stage": l1_tag_stage(f"{kname}_E", q_r, secs, sec["clocks"])}}
+                        "l1_tag_stage": l1_tag_stage(f"{kname}_E", q_r, secs, sec["clocks"]),
+                        "l1_l2_requests": l2_requests(f"{kname}_E", q_r, secs, sec["clocks"])}}
     # parity: 16 windows of 1M queries spread across this rank's shard of the
     # stream, answered by the timed kernel, against the reference answer_batch
     from oracle import oracle as orc
@@ -784,6 +807,7 @@ def main():
                                           "frac": Bq_survey * q_r / secs / 1e9 / peak[0]},
                          "l1_tag_stage": l1_tag_stage(f"{kname}_B", q_r, secs,
                                                       sec["clocks"]),
+                         "l1_l2_requests": l2_requests(f"{kname}_B", q_r, secs, sec["clocks"]),
                          "l2_gather": {"node_gathers_G_per_s": node_gathers,
                                        "ceiling_G_per_s": L2_GATHER_CEILING.get(layout),
                                        "frac": (node_gathers / L2_GATHER_CEILING[layout]

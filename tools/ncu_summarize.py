@@ -41,6 +41,9 @@ def main():
         "achieved_occupancy_pct": avg("sm__warps_active.avg.pct_of_peak_sustained_active"),
         "l1_tag_sectors_per_launch": (avg("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
                                       + avg("l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum")),
+        "l2_requests_per_launch": avg("lts__t_requests_srcunit_tex.sum"),
+        "l1_to_l2_req_active_pct": avg(
+            "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "launches_averaged": len(sel),
         "source": source,
     }
