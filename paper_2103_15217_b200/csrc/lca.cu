@@ -503,14 +503,17 @@ struct Wide9Nodes {
 
 // inlabel_lca (core/src/lca.cpp:84-109): two node-record gathers, then at
 // most two 8-B label-record gathers.
-template <class In, class Out, class Nodes = WideNodes>
+template <class In, class Out, class Nodes = WideNodes, bool kPf = false>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel(Nodes node, const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q,
                   u32* err) {
+  static_assert(!kPf || kQPer == 1, "pair prefetch is written for one query per thread");
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
   u32 bad_any = 0;
-  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
-       base += stride) {
+  u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x;
+  u32 px = 0, py = 0;
+  if (kPf && base < q) in.get(base, px, py);
+  for (; base < q; base += stride) {
     u32 x[kQPer], y[kQPer];
     bool ok[kQPer], bad[kQPer];
 #pragma unroll
@@ -518,9 +521,18 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
       const u64 i = base + static_cast<u64>(j) * kQThreads;
       ok[j] = i < q;
       x[j] = y[j] = 0;
-      if (ok[j]) in.get(i, x[j], y[j]);
+      if (kPf) {
+        x[j] = px;
+        y[j] = py;
+      } else if (ok[j]) {
+        in.get(i, x[j], y[j]);
+      }
       bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
       if (bad[j]) x[j] = y[j] = 0;
+    }
+    if (kPf) {
+      px = py = 0;
+      if (base + stride < q) in.get(base + stride, px, py);
     }
     uint4 A[kQPer], B[kQPer];
 #pragma unroll
@@ -575,14 +587,17 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // about the size of L2), at the price of a dependent ascendant gather when
 // the inlabels differ.  Pays when few labels are in use (deep, path-like
 // trees: the ascendant and label records stay in L2); see choose_layout().
-template <class In, class Out>
+template <class In, class Out, bool kPf = false>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_narrow(const uint2* __restrict__ node8, const u32* __restrict__ lasc,
                          const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
+  static_assert(!kPf || kQPer == 1, "pair prefetch is written for one query per thread");
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
   u32 bad_any = 0;
-  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
-       base += stride) {
+  u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x;
+  u32 px = 0, py = 0;
+  if (kPf && base < q) in.get(base, px, py);
+  for (; base < q; base += stride) {
     u32 x[kQPer], y[kQPer];
     bool ok[kQPer], bad[kQPer];
 #pragma unroll
@@ -590,9 +605,18 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
       const u64 i = base + static_cast<u64>(j) * kQThreads;
       ok[j] = i < q;
       x[j] = y[j] = 0;
-      if (ok[j]) in.get(i, x[j], y[j]);
+      if (kPf) {
+        x[j] = px;
+        y[j] = py;
+      } else if (ok[j]) {
+        in.get(i, x[j], y[j]);
+      }
       bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
       if (bad[j]) x[j] = y[j] = 0;
+    }
+    if (kPf) {
+      px = py = 0;
+      if (base + stride < q) in.get(base + stride, px, py);
     }
     uint2 A[kQPer], B[kQPer];
 #pragma unroll
@@ -656,15 +680,25 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // inlabels, or an endpoint that is not lifted).  On random trees nearly
 // every query lifts both endpoints, so the hot table is 128 MB instead of
 // the wide layout's 256 MB.
-template <class In, class Out>
+template <class In, class Out, bool kPf = false>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_split(const uint2* __restrict__ nodes, const u32* __restrict__ level,
                         const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
   u32 bad_any = 0;
-  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
-       i += static_cast<u64>(gridDim.x) * kQThreads) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads;
+  u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x;
+  u32 px = 0, py = 0;
+  if (kPf && i < q) in.get(i, px, py);
+  for (; i < q; i += stride) {
     u32 x, y;
-    in.get(i, x, y);
+    if (kPf) {  // this trip's pair was loaded last trip; load the next one now
+      x = px;
+      y = py;
+      px = py = 0;
+      if (i + stride < q) in.get(i + stride, px, py);
+    } else {
+      in.get(i, x, y);
+    }
     const bool bad = x >= n || y >= n;
     if (bad) x = y = 0;
     const uint2 A = ldg_rec(nodes + x), B = ldg_rec(nodes + y);
@@ -699,15 +733,25 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // ascendant are < 2^24 when n < 2^24), so the gathered node table of a 16M
 // tree is 96 MB instead of 128 MB -- under the size at which B200's random
 // gather rate falls off (footprint sweep: 96 MB 151, 128 MB 113 G gathers/s).
-template <class In, class Out>
+template <class In, class Out, bool kPf = false>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_split6(const uint32_t* __restrict__ nodes6, const u32* __restrict__ level,
                         const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
   u32 bad_any = 0;
-  for (u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x; i < q;
-       i += static_cast<u64>(gridDim.x) * kQThreads) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads;
+  u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x;
+  u32 px = 0, py = 0;
+  if (kPf && i < q) in.get(i, px, py);
+  for (; i < q; i += stride) {
     u32 x, y;
-    in.get(i, x, y);
+    if (kPf) {  // this trip's pair was loaded last trip; load the next one now
+      x = px;
+      y = py;
+      px = py = 0;
+      if (i + stride < q) in.get(i + stride, px, py);
+    } else {
+      in.get(i, x, y);
+    }
     const bool bad = x >= n || y >= n;
     if (bad) x = y = 0;
     uint2 A, B;
@@ -796,16 +840,21 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // as in k_lca_inlabel.  On the 16M path tree the node table is 64 MB and the
 // label table holds 7 entries, so every gather is served by L2 after its
 // first touch.
-template <class In, class Out>
+// kPf: the next grid-stride trip's pair is loaded before this trip's gathers
+// (its stream latency overlaps them; kQPer == 1).
+template <class In, class Out, bool kPf = false>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_compact(const u32* __restrict__ node4, const uint4* __restrict__ ltab,
                           const uint2* __restrict__ lab, u32 n, int off_bits, In in, Out out,
                           u64 q, u32* err) {
+  static_assert(!kPf || kQPer == 1, "pair prefetch is written for one query per thread");
   const u64 stride = static_cast<u64>(gridDim.x) * kQThreads * kQPer;
   const u32 omask = off_bits >= 32 ? ~0u : ((1u << off_bits) - 1u);
   u32 bad_any = 0;
-  for (u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x; base < q;
-       base += stride) {
+  u64 base = static_cast<u64>(blockIdx.x) * kQThreads * kQPer + threadIdx.x;
+  u32 px = 0, py = 0;
+  if (kPf && base < q) in.get(base, px, py);
+  for (; base < q; base += stride) {
     u32 x[kQPer], y[kQPer];
     bool ok[kQPer], bad[kQPer];
 #pragma unroll
@@ -813,9 +862,18 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
       const u64 i = base + static_cast<u64>(j) * kQThreads;
       ok[j] = i < q;
       x[j] = y[j] = 0;
-      if (ok[j]) in.get(i, x[j], y[j]);
+      if (kPf) {
+        x[j] = px;
+        y[j] = py;
+      } else if (ok[j]) {
+        in.get(i, x[j], y[j]);
+      }
       bad[j] = ok[j] && (x[j] >= n || y[j] >= n);
       if (bad[j]) x[j] = y[j] = 0;
+    }
+    if (kPf) {
+      px = py = 0;
+      if (base + stride < q) in.get(base + stride, px, py);
     }
     u32 wa[kQPer], wb[kQPer];
 #pragma unroll
@@ -1445,6 +1503,15 @@ void ensure_qbuf(ettg_lca* h, u64 chunk) {
     if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 }
 
+// ETTG_QPF=0 turns the query kernels' pair prefetch off (A/B).
+bool qprefetch() {
+  static const bool v = [] {
+    const char* e = std::getenv("ETTG_QPF");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <class In, class Out>
 void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32* err,
                   cudaStream_t st) {
@@ -1474,26 +1541,29 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     const int grid_per_sm = grid_env ? grid_env : (q <= (u64(1) << 21) ? kQMinBlocks : kQGridPerSM);
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * grid_per_sm);
     if (h->layout == kLayoutCompact)
-      k_lca_inlabel_compact<In, Out><<<blocks, kQThreads, 0, st>>>(
-          h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q, err);
+      (qprefetch() ? k_lca_inlabel_compact<In, Out, true> : k_lca_inlabel_compact<In, Out, false>)
+          <<<blocks, kQThreads, 0, st>>>(h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q,
+                                         err);
     else if (h->layout == kLayoutSplitOwn)
       k_lca_inlabel_split_own<In, Out><<<blocks, kQThreads, 0, st>>>(h->node, h->slevel, h->lab,
                                                                      h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit)
-      k_lca_inlabel_split<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab,
-                                                                 h->n, in, out, q, err);
+      (qprefetch() ? k_lca_inlabel_split<In, Out, true> : k_lca_inlabel_split<In, Out, false>)
+          <<<blocks, kQThreads, 0, st>>>(h->nodes, h->slevel, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutWide9)
-      k_lca_inlabel<In, Out, Wide9Nodes><<<blocks, kQThreads, 0, st>>>(
+      (qprefetch() ? k_lca_inlabel<In, Out, Wide9Nodes, true>
+                   : k_lca_inlabel<In, Out, Wide9Nodes, false>)<<<blocks, kQThreads, 0, st>>>(
           Wide9Nodes{h->nodes9}, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit6)
-      k_lca_inlabel_split6<In, Out><<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab,
-                                                                  h->n, in, out, q, err);
+      (qprefetch() ? k_lca_inlabel_split6<In, Out, true> : k_lca_inlabel_split6<In, Out, false>)
+          <<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutNarrow)
-      k_lca_inlabel_narrow<In, Out><<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n,
-                                                                  in, out, q, err);
+      (qprefetch() ? k_lca_inlabel_narrow<In, Out, true> : k_lca_inlabel_narrow<In, Out, false>)
+          <<<blocks, kQThreads, 0, st>>>(h->node8, h->lasc, h->lab, h->n, in, out, q, err);
     else
-      k_lca_inlabel<In, Out><<<blocks, kQThreads, 0, st>>>(WideNodes{h->node}, h->lab, h->n, in, out, q,
-                                                           err);
+      (qprefetch() ? k_lca_inlabel<In, Out, WideNodes, true>
+                   : k_lca_inlabel<In, Out, WideNodes, false>)<<<blocks, kQThreads, 0, st>>>(
+          WideNodes{h->node}, h->lab, h->n, in, out, q, err);
   }
   CK_LAUNCH();
 }

@@ -1,7 +1,8 @@
 #!/bin/bash
-cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2k; mkdir -p $O
-timeout 900 python -m pytest tests/test_bridges_gpu.py tests/test_bridges_dropin_gpu.py tests/test_cpp_shim.py -x -q > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/rc.txt
-run() { echo "== $*"; env "$@" ETTG_TRACE=1 REPS=4 timeout 300 python tools/trace_bridges.py 2>&1 | grep -E "^bridges|\[ettg trace\] bridges|parity" | tail -3; }
-( run ETTG_LH_AGG=1; run ETTG_LH_AGG=0; run GRAPH=C ETTG_LH_AGG=1; run GRAPH=C ETTG_LH_AGG=0 ) > $O/sweep.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_lowhigh_edges" -c 1 -o $O/lh env REPS=1 python tools/trace_bridges.py > $O/ncu.log 2>&1; echo "ncu rc=$?" >> $O/rc.txt
+cd $GRAFT_REPO_ROOT; O=gpurun_out/r2k; mkdir -p $O
+timeout 600 python -m pytest tests/test_lca_gpu.py -x -q > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+for r in 1 2; do
+for v in "ETTG_QPF=0" "ETTG_QPF=1" "ETTG_QPF=1 ETTG_QGRID=8" "ETTG_QPF=1 ETTG_QGRID=16" "ETTG_QPF=0 ETTG_QGRID=8"; do
+  echo "== $v" >> $O/ab.txt
+  env $v AB_ONLY=B_path,path_4M,path_1M timeout 300 python tools/ab_lca.py auto >> $O/ab.txt 2>&1
+done; done

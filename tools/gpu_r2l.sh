@@ -1,7 +1,8 @@
 #!/bin/bash
-cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2l; mkdir -p $O
-timeout 900 python -m pytest tests/test_bridges_gpu.py tests/test_bridges_dropin_gpu.py -x -q > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/rc.txt
-run() { echo "== $*"; env "$@" ETTG_TRACE=1 REPS=4 timeout 300 python tools/trace_bridges.py 2>&1 | grep -E "^bridges|\[ettg trace\] bridges|parity" | tail -3; }
-( run X=D; run GRAPH=C ) > $O/sweep.txt 2>&1
-timeout 600 python tools/ab_bridges_e2e_trace.py > $O/e2e.txt 2>&1
+cd $GRAFT_REPO_ROOT; O=gpurun_out/r2l2; mkdir -p $O
+timeout 600 python -m pytest tests/test_lca_gpu.py tests/test_multi_gpu.py -x -q > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/rc.txt
+for r in 1 2; do
+for v in "ETTG_QPF=0" "ETTG_QPF=1"; do
+  echo "== $v" >> $O/ab.txt
+  env $v AB_ONLY=B_path,E_rand,g2,g8,g64,rand_4M timeout 300 python tools/ab_lca.py auto >> $O/ab.txt 2>&1
+done; done
