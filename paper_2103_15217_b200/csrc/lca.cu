@@ -937,6 +937,83 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
   if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
 }
 
+// Compact layout, two-stage software pipeline (ETTG_QPF=2): at the top of
+// each trip the node words of the next trip's endpoints are gathered and
+// the pair after that is loaded, then this trip's query finishes from the
+// words gathered one trip earlier -- so each thread keeps its next gathers
+// in flight while it works (the kernel is bound by L1 -> L2 requests,
+// DESIGN.md section 4).
+template <class In, class Out>
+__global__ void __launch_bounds__(kQThreads, kQMinBlocks)
+    k_lca_inlabel_compact_pipe(const u32* __restrict__ node4, const uint4* __restrict__ ltab,
+                               const uint2* __restrict__ lab, u32 n, int off_bits, In in, Out out,
+                               u64 q, u32* err) {
+  const u64 stride = static_cast<u64>(gridDim.x) * kQThreads;
+  const u32 omask = off_bits >= 32 ? ~0u : ((1u << off_bits) - 1u);
+  u32 bad_any = 0;
+  u64 i = static_cast<u64>(blockIdx.x) * kQThreads + threadIdx.x;
+  // stage 0: pair of trip i; stage 1: words of trip i, pair of trip i + stride
+  u32 x = 0, y = 0, wa = 0, wb = 0, nx = 0, ny = 0;
+  bool bad = false;
+  if (i < q) {
+    in.get(i, x, y);
+    bad = x >= n || y >= n;
+    if (bad) x = y = 0;
+    wa = ldg_u32(node4 + x);
+    wb = ldg_u32(node4 + y);
+  }
+  if (i + stride < q) in.get(i + stride, nx, ny);
+  for (; i < q; i += stride) {
+    // next trip: its words and the pair after it
+    const u64 i1 = i + stride;
+    bool nbad = false;
+    u32 nwa = 0, nwb = 0, cx = nx, cy = ny;
+    if (i1 < q) {
+      nbad = cx >= n || cy >= n;
+      if (nbad) cx = cy = 0;
+      nwa = ldg_u32(node4 + cx);
+      nwb = ldg_u32(node4 + cy);
+      nx = ny = 0;
+      if (i1 + stride < q) in.get(i1 + stride, nx, ny);
+    }
+    // this trip
+    const u32 la = off_bits >= 32 ? 0u : wa >> off_bits;
+    const u32 lb = off_bits >= 32 ? 0u : wb >> off_bits;
+    uint4 A = make_uint4(0u, 0u, 0u, 0u), B = A;
+    if (la != lb) {
+      A = ldg_rec(ltab + la);
+      B = ldg_rec(ltab + lb);
+    }
+    const u32 ox = wa & omask, oy = wb & omask;
+    u32 ans = ox <= oy ? x : y;
+    if ((wa ^ wb) > omask) {  // different label indices
+      const int hbit = hb32(A.x ^ B.x);
+      const u32 common = A.y & B.y & ~((1u << hbit) - 1u);
+      const int jb = tz32(common);
+      const u32 target = (A.x & ~((2u << jb) - 1u)) | (1u << jb);
+      const u32 lowmask = (1u << jb) - 1u;
+      uint2 LX = make_uint2(x, A.z + ox), LY = make_uint2(y, B.z + oy);
+      if (A.x != target) {
+        const int kx = hb32(A.y & lowmask);
+        LX = ldg_rec(lab + min((A.x & ~((2u << kx) - 1u)) | (1u << kx), n));
+      }
+      if (B.x != target) {
+        const int ky = hb32(B.y & lowmask);
+        LY = ldg_rec(lab + min((B.x & ~((2u << ky) - 1u)) | (1u << ky), n));
+      }
+      ans = LX.y <= LY.y ? LX.x : LY.x;
+    }
+    out.put(i, bad ? kNone : ans);
+    bad_any |= bad;
+    x = cx;
+    y = cy;
+    wa = nwa;
+    wb = nwb;
+    bad = nbad;
+  }
+  if (__any_sync(0xffffffffu, bad_any) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 // naive_lca (core/src/lca.cpp:118-126): walk the deeper node up, then both.
 // One query per thread; cost is the x-y tree distance (the paper's baseline).
 template <class In, class Out>
@@ -1503,14 +1580,16 @@ void ensure_qbuf(ettg_lca* h, u64 chunk) {
     if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 }
 
-// ETTG_QPF=0 turns the query kernels' pair prefetch off (A/B).
-bool qprefetch() {
-  static const bool v = [] {
+// ETTG_QPF=0 turns the query kernels' pair prefetch off, 1 uses it without the
+// compact layout's two-stage pipeline, 2 (default) with it (A/B).
+int qprefetch_mode() {
+  static const int v = [] {
     const char* e = std::getenv("ETTG_QPF");
-    return !e || std::atoi(e) != 0;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
+bool qprefetch() { return qprefetch_mode() != 0; }
 
 template <class In, class Out>
 void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32* err,
@@ -1541,7 +1620,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     const int grid_per_sm = grid_env ? grid_env : (q <= (u64(1) << 21) ? kQMinBlocks : kQGridPerSM);
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * grid_per_sm);
     if (h->layout == kLayoutCompact)
-      (qprefetch() ? k_lca_inlabel_compact<In, Out, true> : k_lca_inlabel_compact<In, Out, false>)
+      (qprefetch_mode() == 2   ? k_lca_inlabel_compact_pipe<In, Out>
+       : qprefetch_mode() == 1 ? k_lca_inlabel_compact<In, Out, true>
+                               : k_lca_inlabel_compact<In, Out, false>)
           <<<blocks, kQThreads, 0, st>>>(h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q,
                                          err);
     else if (h->layout == kLayoutSplitOwn)
