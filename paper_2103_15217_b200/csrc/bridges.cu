@@ -636,6 +636,96 @@ __global__ void __launch_bounds__(256, kMinB)
   }
 }
 
+// The same updates with runs of equal first endpoint combined.  Each thread
+// takes kE consecutive edges; edges that share their first endpoint u (a
+// source-grouped list: CSR-derived inputs, road-graph files, config D's
+// generator) fold their u-side updates -- low(u) from neighbours with smaller
+// keys, high(u) from larger ones -- into one filtered read and at most one
+// atomic per run, while the v-side update stays per edge.  On inputs without
+// runs every edge is its own run (the same work as k_lowhigh_edges).
+template <int kE>
+__global__ void __launch_bounds__(256, 4)
+    k_lowhigh_runs(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
+                   const u32* __restrict__ key_of, uint2* lh, const u32* abort, u32 n) {
+  static_assert(kE == 8, "vector loads are written for 8 edges per thread");
+  if (tv_abort(abort, n)) return;
+  u32* w = reinterpret_cast<u32*>(lh);  // slot = key - 1; [2s] = low, [2s + 1] = high
+  const u64 nchunk = (static_cast<u64>(m) + kE - 1) / kE;
+  for (u64 c = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunk;
+       c += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 e0 = c * kE;
+    uint2 uv[kE];
+    bool nt[kE];
+    if (e0 + kE <= m) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(edges + e0);
+#pragma unroll
+      for (int j = 0; j < kE / 2; ++j) {
+        const uint4 v = __ldg(e4 + j);
+        uv[2 * j] = make_uint2(v.x, v.y);
+        uv[2 * j + 1] = make_uint2(v.z, v.w);
+      }
+      const uint2 f = __ldg(reinterpret_cast<const uint2*>(tree + e0));
+#pragma unroll
+      for (int j = 0; j < kE; ++j) nt[j] = ((j < 4 ? f.x >> (8 * j) : f.y >> (8 * (j - 4))) & 0xFF) == 0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kE; ++j) {
+        const bool in = e0 + j < m;
+        uv[j] = in ? edges[e0 + j] : make_uint2(0, 0);
+        nt[j] = in && !tree[e0 + j];
+      }
+    }
+    u32 ku[kE], kv[kE];
+#pragma unroll
+    for (int j = 0; j < kE; ++j) {
+      ku[j] = __ldg(key_of + uv[j].x);
+      kv[j] = nt[j] ? __ldg(key_of + uv[j].y) : 0u;
+    }
+    // per edge the v-side update (slot word va, value = the key of u); after
+    // the last edge of a run, the run's low and high for u (unfiltered:
+    // a run's aggregate usually improves its slot)
+    u32 va[kE], lv[kE], hv[kE];
+    u32 accL = 0xFFFFFFFFu, accH = 0u;
+#pragma unroll
+    for (int j = 0; j < kE; ++j) {
+      va[j] = 0xFFFFFFFFu;
+      if (nt[j] && ku[j] != kv[j]) {
+        if (kv[j] < ku[j]) {  // low(u) <- kv, high(v) <- ku
+          accL = min(accL, kv[j]);
+          va[j] = 2 * (kv[j] - 1) + 1;
+        } else {              // high(u) <- kv, low(v) <- ku
+          accH = max(accH, kv[j]);
+          va[j] = 2 * (kv[j] - 1);
+        }
+      }
+      const bool last = j == kE - 1 || uv[j + 1 < kE ? j + 1 : j].x != uv[j].x;
+      lv[j] = last ? accL : 0xFFFFFFFFu;
+      hv[j] = last ? accH : 0u;
+      if (last) {
+        accL = 0xFFFFFFFFu;
+        accH = 0u;
+      }
+    }
+    // v-side filter reads (low only falls, high only rises: a stale value
+    // only lets an unneeded atomic through), then the atomics
+    u32 cv[kE];
+#pragma unroll
+    for (int j = 0; j < kE; ++j) cv[j] = va[j] != 0xFFFFFFFFu ? w[va[j]] : 0u;
+#pragma unroll
+    for (int j = 0; j < kE; ++j) {
+      if (va[j] != 0xFFFFFFFFu) {
+        if (va[j] & 1u) {
+          if (cv[j] < ku[j]) atomicMax(&w[va[j]], ku[j]);
+        } else {
+          if (cv[j] > ku[j]) atomicMin(&w[va[j]], ku[j]);
+        }
+      }
+      if (lv[j] != 0xFFFFFFFFu) atomicMin(&w[2 * (ku[j] - 1)], lv[j]);
+      if (hv[j] != 0u) atomicMax(&w[2 * (ku[j] - 1) + 1], hv[j]);
+    }
+  }
+}
+
 __device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
   return make_uint2(min(a.x, b.x), max(a.y, b.y));
 }
@@ -799,6 +889,17 @@ void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* p
   // (A warp-segmented min/max over runs of equal u, one u-side atomic pair
   // per run, cut the L2 reductions 254M -> 148M sectors on config D but
   // doubled the instructions and added reads: 2.37 vs 1.88 ms; round 2.)
+  static const bool runs = [] {
+    const char* e = std::getenv("ETTG_LH_RUNS");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (runs && check && reinterpret_cast<uintptr_t>(tree) % 8 == 0 &&
+      reinterpret_cast<uintptr_t>(edges) % 16 == 0) {
+    auto kr = k_lowhigh_runs<8>;
+    kr<<<occ_grid(kr, (u64(m) + 7) / 8, sms), 256, 0, st>>>(edges, tree, m, pre_of, lh, abort, n);
+    CK_LAUNCH();
+    return;
+  }
   auto kern = check ? k_lowhigh_edges<kEdgesPerThread, 8, true>
                     : k_lowhigh_edges<kEdgesPerThread, 8, false>;
   kern<<<occ_grid(kern, (u64(m) + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
