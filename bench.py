@@ -767,7 +767,7 @@ def main():
         Bq_survey = 12 + 32 * (2 + Lbar)  # one 32-B sector per gather
         layout, labels = idx.layout()
         kname = {"wide": "k_lca_inlabel", "narrow": "k_lca_inlabel_narrow",
-                 "compact": "k_lca_inlabel_compact", "split": "k_lca_inlabel_split",
+                 "compact": "k_lca_inlabel_compact_pipe", "split": "k_lca_inlabel_split",
                  "split_own": "k_lca_inlabel_split_own",
                  "split6": "k_lca_inlabel_split6", "wide9": "k_lca_inlabel"}[layout]
         q_r = sec["q_rank"]
