@@ -155,16 +155,21 @@ constexpr u32 kCompactTile = kScanThreads * 16 * kCompactVec;  // 16384 flags
 
 __device__ __forceinline__ u32 byte_sum4(u32 w) { return (w * 0x01010101u) >> 24; }
 
-template <class Out>
+// kMode 0: one pass, the tile prefix from the decoupled look-back; 1: only
+// store the tile's count in cnt[tile]; 2: write with the tile prefix taken
+// from cnt[tile] (k_tile_scan's exclusive prefix of the mode-1 counts).
+template <class Out, int kMode = 0>
 __global__ void __launch_bounds__(kScanThreads)
     k_compact_u8(const uint8_t* __restrict__ flags, u64 n, Out out, u64* status, u32* ticket,
-                 u32* total) {
+                 u32* total, u32* cnt = nullptr) {
   __shared__ u32 s_warp[kScanThreads / 32];
   __shared__ u32 s_tile, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const u32 tile = s_tile;
+  if (kMode == 0) {
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+  }
+  const u32 tile = kMode == 0 ? s_tile : blockIdx.x;
   const u64 tbase = static_cast<u64>(tile) * kCompactTile;
   uint4 v[kCompactVec];
 #pragma unroll
@@ -205,12 +210,17 @@ __global__ void __launch_bounds__(kScanThreads)
       if (lane < kScanThreads / 32) s_round[k][lane] = carry + wi - w;
       carry += __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
     }
-    const u32 pre = tile_lookback(status, tile, carry);
-    if (lane == 0) {
-      s_prefix = pre;
-      if (total && static_cast<u64>(tile + 1) * kCompactTile >= n) *total = pre + carry;
+    if (kMode == 1) {
+      if (lane == 0) cnt[tile] = carry;
+    } else {
+      const u32 pre = kMode == 0 ? tile_lookback(status, tile, carry) : cnt[tile];
+      if (lane == 0) {
+        s_prefix = pre;
+        if (total && static_cast<u64>(tile + 1) * kCompactTile >= n) *total = pre + carry;
+      }
     }
   }
+  if (kMode == 1) return;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kCompactVec; ++k) {
@@ -225,6 +235,35 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// Exclusive scan of per-tile counts in place, one CTA.
+__global__ void __launch_bounds__(1024) k_tile_scan(u32* cnt, u32 tiles) {
+  __shared__ u32 s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 per = (tiles + 1023) / 1024, a = min(tiles, tid * per), b = min(tiles, a + per);
+  u32 local = 0;
+  for (u32 i = a; i < b; ++i) local += cnt[i];
+  const u32 incl = warp_incl_scan(local);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 w = s_warp[lane];
+    const u32 wi = warp_incl_scan(w);
+    s_warp[lane] = wi - w;
+  }
+  __syncthreads();
+  u32 run = s_warp[warp] + incl - local;
+  for (u32 i = a; i < b; ++i) {
+    const u32 v = cnt[i];
+    cnt[i] = run;
+    run += v;
+  }
+}
+
+// Two passes over the flags (count per tile, one-CTA scan of the tile counts,
+// write) instead of one pass with a look-back chain: the flags are read twice
+// but no tile waits on its predecessor.  Config D (256M flags, 16K tiles):
+// the one-pass kernel streamed at 0.9 TB/s, bound by the look-back chain.
+// ETTG_COMPACT_2PASS=0 selects the one-pass kernel (A/B).
 template <class Out>
 void compact_u8(const uint8_t* flags, u64 n, Out out, u64* status, u32* total, cudaStream_t st) {
   if (n == 0) {
@@ -232,6 +271,20 @@ void compact_u8(const uint8_t* flags, u64 n, Out out, u64* status, u32* total, c
     return;
   }
   const u64 tiles = (n + kCompactTile - 1) / kCompactTile;
+  static const bool two_pass = [] {
+    const char* e = std::getenv("ETTG_COMPACT_2PASS");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (two_pass && tiles > 1) {
+    u32* cnt = reinterpret_cast<u32*>(status);  // tiles words (status holds >= 2 per tile)
+    k_compact_u8<Out, 1><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(
+        flags, n, out, nullptr, nullptr, nullptr, cnt);
+    k_tile_scan<<<1, 1024, 0, st>>>(cnt, static_cast<u32>(tiles));
+    k_compact_u8<Out, 2><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(
+        flags, n, out, nullptr, nullptr, total, cnt);
+    CK_LAUNCH();
+    return;
+  }
   CK(cudaMemsetAsync(status, 0, (tiles + 1) * sizeof(u64), st));
   u32* ticket = reinterpret_cast<u32*>(status + tiles);
   k_compact_u8<Out><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(flags, n, out, status,
