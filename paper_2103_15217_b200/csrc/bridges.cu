@@ -178,27 +178,37 @@ __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(pa
 // every sample-th single edge touched every sector twice (ncu, config D:
 // 2.6 GB DRAM read in each phase).
 constexpr u32 kGroup = 4;
+// goff: the group of each span phase 0 takes; lead: the leading groups of
+// each span that earlier phase-0 rounds took, so phase 1 takes the others
+// (ETTG_CC_ROUNDS: one sampled group per round, a compress after each).
 struct EdgeSubset {
-  u32 m, sample, phase;
-  __device__ __forceinline__ u64 count() const {
-    if (sample <= 1) return m;
-    const u64 first = first_count();
-    return phase == 0 ? first : m - first;
-  }
-  __host__ __device__ __forceinline__ u64 first_count() const {
-    const u64 span = u64(kGroup) * sample;  // one sampled group per span
+  u32 m, sample, phase, goff = 0, lead = 1;
+  u32 total = 0;  // count(), filled in by launch_hook so the kernels do not loop
+  // edges of group g summed over all spans
+  __host__ __device__ __forceinline__ u64 group_count(u32 g) const {
+    const u64 span = u64(kGroup) * sample;
     const u64 full = m / span, rest = m % span;
-    return full * kGroup + (rest < kGroup ? rest : kGroup);
+    const u64 lo = u64(g) * kGroup;
+    const u64 part = rest > lo ? (rest - lo < kGroup ? rest - lo : kGroup) : 0;
+    return full * kGroup + part;
+  }
+  __host__ __device__ __forceinline__ u64 count() const {
+    if (sample <= 1) return m;
+    if (phase == 0) return group_count(goff);
+    u64 c = m;
+    for (u32 g = 0; g < lead; ++g) c -= group_count(g);
+    return c;
   }
   // phase 1 as (i * magic) >> shift == i / per, exact for i < 2^31
   // (Granlund-Montgomery; m < 2^31); host side: rest_divider()
   __device__ __forceinline__ u64 edge_rest(u64 i, u32 magic, u32 shift) const {
-    const u32 span = kGroup * sample, per = span - kGroup, j = static_cast<u32>(i);
+    const u32 span = kGroup * sample, skip = kGroup * lead, per = span - skip,
+              j = static_cast<u32>(i);
     const u32 q = static_cast<u32>((static_cast<u64>(j) * magic) >> shift);
-    return u64(q) * span + kGroup + (j - q * per);
+    return u64(q) * span + skip + (j - q * per);
   }
   void rest_divider(u32& magic, u32& shift) const {
-    const u64 per = u64(kGroup) * sample - kGroup;
+    const u64 per = u64(kGroup) * (sample - lead);
     u32 l = 0;
     while ((u64(1) << l) < per) ++l;
     shift = 31 + l;
@@ -207,9 +217,9 @@ struct EdgeSubset {
   __device__ __forceinline__ u64 edge(u64 i) const {
     if (sample <= 1) return i;
     const u64 span = u64(kGroup) * sample;
-    if (phase == 0) return (i / kGroup) * span + (i % kGroup);
-    const u64 per = span - kGroup;  // edges of one span left for phase 1
-    return (i / per) * span + kGroup + (i % per);
+    if (phase == 0) return (i / kGroup) * span + u64(goff) * kGroup + (i % kGroup);
+    const u64 skip = u64(kGroup) * lead, per = span - skip;  // edges of one span left for phase 1
+    return (i / per) * span + skip + (i % per);
   }
 };
 
@@ -221,13 +231,20 @@ __global__ void k_cc_compress(u32* par, u32 n) {
   }
 }
 
-template <int kHookE, int kMinB, bool kPrio = false>
+// kCs: the edge stream is loaded with the evict-first (.cs) policy so that it
+// does not push the union-find parents out of L2 (ETTG_BR_CS bit 0).
+template <class T>
+__device__ __forceinline__ T ld_edge(const T* p, bool cs) {
+  return cs ? __ldcs(p) : *p;
+}
+
+template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               uint8_t* __restrict__ tree, u32* flags) {
   u32 bad = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  const u64 cnt = sub.count();
+  const u64 cnt = sub.total;
   u64 eidx[kHookE];
   for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
        base += stride * kHookE) {
@@ -239,7 +256,7 @@ __global__ void __launch_bounds__(256, kMinB)
       ok[j] = i < cnt;
       const u64 e = ok[j] ? sub.edge(i) : 0;
       eidx[j] = e;
-      uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
+      uv[j] = ok[j] ? ld_edge(edges + e, kCs) : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
         bad = 1;
         ok[j] = false;
@@ -307,13 +324,13 @@ __global__ void __launch_bounds__(256, kMinB)
 // emulated u64 division per edge.  A separate kernel on purpose: changing
 // the shared kernel's index code slowed the sampled pass 2x (see
 // profiles/r1_bridges_tuning.md).
-template <int kHookE, int kMinB>
+template <int kHookE, int kMinB, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook_rest(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
                    uint8_t* __restrict__ tree, u32* flags, u32 magic, u32 shift) {
   u32 bad = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  const u64 cnt = sub.count();
+  const u64 cnt = sub.total;
   u64 eidx[kHookE];
   for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
        base += stride * kHookE) {
@@ -325,7 +342,7 @@ __global__ void __launch_bounds__(256, kMinB)
       ok[j] = i < cnt;
       const u64 e = ok[j] ? sub.edge_rest(i, magic, shift) : 0;
       eidx[j] = e;
-      uv[j] = ok[j] ? edges[e] : make_uint2(0, 0);
+      uv[j] = ok[j] ? ld_edge(edges + e, kCs) : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
         bad = 1;
         ok[j] = false;
@@ -643,7 +660,7 @@ __global__ void __launch_bounds__(256, kMinB)
 // keys, high(u) from larger ones -- into one filtered read and at most one
 // atomic per run, while the v-side update stays per edge.  On inputs without
 // runs every edge is its own run (the same work as k_lowhigh_edges).
-template <int kE>
+template <int kE, bool kCs = false>
 __global__ void __launch_bounds__(256, 4)
     k_lowhigh_runs(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
                    const u32* __restrict__ key_of, uint2* lh, const u32* abort, u32 n) {
@@ -660,11 +677,12 @@ __global__ void __launch_bounds__(256, 4)
       const uint4* e4 = reinterpret_cast<const uint4*>(edges + e0);
 #pragma unroll
       for (int j = 0; j < kE / 2; ++j) {
-        const uint4 v = __ldg(e4 + j);
+        const uint4 v = kCs ? __ldcs(e4 + j) : __ldg(e4 + j);
         uv[2 * j] = make_uint2(v.x, v.y);
         uv[2 * j + 1] = make_uint2(v.z, v.w);
       }
-      const uint2 f = __ldg(reinterpret_cast<const uint2*>(tree + e0));
+      const uint2 f = kCs ? __ldcs(reinterpret_cast<const uint2*>(tree + e0))
+                          : __ldg(reinterpret_cast<const uint2*>(tree + e0));
 #pragma unroll
       for (int j = 0; j < kE; ++j) nt[j] = ((j < 4 ? f.x >> (8 * j) : f.y >> (8 * (j - 4))) & 0xFF) == 0;
     } else {
@@ -858,20 +876,35 @@ unsigned occ_grid(K kern, u64 work, int sms) {
       std::min<u64>(blocks_for(work, 256, ~0u), u64(sms) * std::max(per, 1)));
 }
 
+// Streamed-edge cache policy: bit 0 hooking, bit 1 low/high.  A/B on config
+// D (profiles/r2_cache_hints.md): hooking 2.06 -> 2.00-2.02 ms with bit 0;
+// bit 1 changes nothing, so the default is 1.
+int br_cs() {
+  static const int v = [] {
+    const char* e = std::getenv("ETTG_BR_CS");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* tree, u32* flags,
                  int sms, cudaStream_t st, bool prio = false) {
-  const u64 first = sub.first_count();
-  const u64 cnt = sub.sample <= 1 ? sub.m : sub.phase == 0 ? first : sub.m - first;
+  sub.total = static_cast<u32>(sub.count());
+  const u64 cnt = sub.total;
   bool rest_kernel = sub.sample > 1 && sub.phase == 1;
   if (const char* e = std::getenv("ETTG_HOOK_REST")) rest_kernel &= std::atoi(e) != 0;
   if (rest_kernel) {
     u32 magic = 0, shift = 0;
     sub.rest_divider(magic, shift);
-    auto kern = k_cc_hook_rest<kEdgesPerThread, 8>;
+    auto kern = br_cs() & 1 ? k_cc_hook_rest<kEdgesPerThread, 8, true>
+                            : k_cc_hook_rest<kEdgesPerThread, 8, false>;
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tree, flags, magic, shift);
   } else {
-    auto kern = prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>;
+    auto kern = br_cs() & 1
+                    ? (prio ? k_cc_hook<kEdgesPerThread, 8, true, true>
+                            : k_cc_hook<kEdgesPerThread, 8, false, true>)
+                    : (prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>);
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tree, flags);
   }
@@ -895,7 +928,7 @@ void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* p
   }();
   if (runs && check && reinterpret_cast<uintptr_t>(tree) % 8 == 0 &&
       reinterpret_cast<uintptr_t>(edges) % 16 == 0) {
-    auto kr = k_lowhigh_runs<8>;
+    auto kr = br_cs() & 2 ? k_lowhigh_runs<8, true> : k_lowhigh_runs<8, false>;
     kr<<<occ_grid(kr, (u64(m) + 7) / 8, sms), 256, 0, st>>>(edges, tree, m, pre_of, lh, abort, n);
     CK_LAUNCH();
     return;
@@ -1250,15 +1283,21 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     if (m && !hooked) {
       // Hook every 4th edge first, compress, then the rest (round-1 A/B on
       // config D: 3.28 vs 4.02 ms for one pass; ETTG_CC_SAMPLE overrides).
-      u32 sample = 4;
+      u32 sample = 4, rounds = 1;
       if (const char* ev = std::getenv("ETTG_CC_SAMPLE")) sample = std::max(1, std::atoi(ev));
+      if (const char* ev = std::getenv("ETTG_CC_ROUNDS")) rounds = std::max(1, std::atoi(ev));
       if (sample <= 1) {
         launch_hook(edges, EdgeSubset{m, 1, 0}, n, ws.par, ws.tree, ws.words, sms, st);
       } else {
-        launch_hook(edges, EdgeSubset{m, sample, 0}, n, ws.par, ws.tree, ws.words, sms, st);
-        k_cc_compress<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
-        CK_LAUNCH();
-        launch_hook(edges, EdgeSubset{m, sample, 1}, n, ws.par, ws.tree, ws.words, sms, st);
+        rounds = std::min(rounds, sample - 1);
+        for (u32 r = 0; r < rounds; ++r) {
+          launch_hook(edges, EdgeSubset{m, sample, 0, r, 1}, n, ws.par, ws.tree, ws.words, sms,
+                      st);
+          k_cc_compress<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
+          CK_LAUNCH();
+        }
+        launch_hook(edges, EdgeSubset{m, sample, 1, 0, rounds}, n, ws.par, ws.tree, ws.words, sms,
+                    st);
       }
       tr.mark("cc_hook");
     }

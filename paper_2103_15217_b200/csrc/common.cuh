@@ -95,6 +95,34 @@ __device__ __forceinline__ Sector32 ldg_sector(const uint32_t* p) {
       : "l"(p));
   return r;
 }
+// L2 eviction-priority variants of the index gathers: the policy word comes
+// from createpolicy once per thread; evict_last keeps the gathered table's
+// lines ahead of the streamed pairs and answers (which load/store with .cs).
+__device__ __forceinline__ u64 l2_policy_evict_last() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ Sector32 ldg_sector_l2(const uint32_t* p, u64 pol) {
+  Sector32 r;
+  asm("ld.global.nc.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+        "=r"(r.w[6]), "=r"(r.w[7])
+      : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ u32 ldg_u32_l2(const u32* p, u64 pol) {
+  u32 r;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_rec_l2(const uint2* p, u64 pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ u32 rec6_sector(u32 v) { return __umulhi(v, 0xCCCCCCCDu) >> 2; }
 // record k = v - 5 * sector starts at u16 3k: words (w[3k/2], w[3k/2 + 1]),
 // shifted right by 16 bits when k is odd
@@ -111,6 +139,14 @@ __device__ __forceinline__ void ldg_rec6_pair(const uint32_t* base, u32 x, u32 y
   const u32 sx = rec6_sector(x), sy = rec6_sector(y);
   const Sector32 a = ldg_sector(base + 8 * static_cast<u64>(sx));
   const Sector32 b = ldg_sector(base + 8 * static_cast<u64>(sy));
+  A = rec6_extract(a, x - 5 * sx);
+  B = rec6_extract(b, y - 5 * sy);
+}
+__device__ __forceinline__ void ldg_rec6_pair_l2(const uint32_t* base, u32 x, u32 y, uint2& A,
+                                                 uint2& B, u64 pol) {
+  const u32 sx = rec6_sector(x), sy = rec6_sector(y);
+  const Sector32 a = ldg_sector_l2(base + 8 * static_cast<u64>(sx), pol);
+  const Sector32 b = ldg_sector_l2(base + 8 * static_cast<u64>(sy), pol);
   A = rec6_extract(a, x - 5 * sx);
   B = rec6_extract(b, y - 5 * sy);
 }

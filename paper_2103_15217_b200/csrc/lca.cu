@@ -733,7 +733,9 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // ascendant are < 2^24 when n < 2^24), so the gathered node table of a 16M
 // tree is 96 MB instead of 128 MB -- under the size at which B200's random
 // gather rate falls off (footprint sweep: 96 MB 151, 128 MB 113 G gathers/s).
-template <class In, class Out, bool kPf = false>
+// kL2: 1 = node-sector gathers with an L2 evict_last policy, 2 = the label
+// and level gathers too (ETTG_L2HINT A/B).
+template <class In, class Out, bool kPf = false, int kL2 = 0>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_split6(const uint32_t* __restrict__ nodes6, const u32* __restrict__ level,
                         const uint2* __restrict__ lab, u32 n, In in, Out out, u64 q, u32* err) {
@@ -755,7 +757,12 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     const bool bad = x >= n || y >= n;
     if (bad) x = y = 0;
     uint2 A, B;
-    ldg_rec6_pair(nodes6, x, y, A, B);
+    // the policy word is made per trip: holding it across the loop spills at 32 registers
+    const u64 pol = kL2 ? l2_policy_evict_last() : 0;
+    if (kL2)
+      ldg_rec6_pair_l2(nodes6, x, y, A, B, pol);
+    else
+      ldg_rec6_pair(nodes6, x, y, A, B);
     bool lx = false, ly = false;
     u32 wx = 0, wy = 0;
     if (A.x != B.x) {
@@ -775,8 +782,14 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
         ly = true;
       }
     }
-    const uint2 LX = lx ? ldg_rec(lab + wx) : make_uint2(x, ldg_u32(level + x));
-    const uint2 LY = ly ? ldg_rec(lab + wy) : make_uint2(y, ldg_u32(level + y));
+    uint2 LX, LY;
+    if (kL2 == 2) {
+      LX = lx ? ldg_rec_l2(lab + wx, pol) : make_uint2(x, ldg_u32_l2(level + x, pol));
+      LY = ly ? ldg_rec_l2(lab + wy, pol) : make_uint2(y, ldg_u32_l2(level + y, pol));
+    } else {
+      LX = lx ? ldg_rec(lab + wx) : make_uint2(x, ldg_u32(level + x));
+      LY = ly ? ldg_rec(lab + wy) : make_uint2(y, ldg_u32(level + y));
+    }
     out.put(i, bad ? kNone : (LX.y <= LY.y ? LX.x : LY.x));
     bad_any |= bad;
   }
@@ -943,7 +956,7 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
 // words gathered one trip earlier -- so each thread keeps its next gathers
 // in flight while it works (the kernel is bound by L1 -> L2 requests,
 // DESIGN.md section 4).
-template <class In, class Out>
+template <class In, class Out, int kL2 = 0>
 __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     k_lca_inlabel_compact_pipe(const u32* __restrict__ node4, const uint4* __restrict__ ltab,
                                const uint2* __restrict__ lab, u32 n, int off_bits, In in, Out out,
@@ -959,20 +972,22 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     in.get(i, x, y);
     bad = x >= n || y >= n;
     if (bad) x = y = 0;
-    wa = ldg_u32(node4 + x);
-    wb = ldg_u32(node4 + y);
+    const u64 pol = kL2 ? l2_policy_evict_last() : 0;
+    wa = (kL2 ? ldg_u32_l2(node4 + x, pol) : ldg_u32(node4 + x));
+    wb = (kL2 ? ldg_u32_l2(node4 + y, pol) : ldg_u32(node4 + y));
   }
   if (i + stride < q) in.get(i + stride, nx, ny);
   for (; i < q; i += stride) {
     // next trip: its words and the pair after it
     const u64 i1 = i + stride;
+    const u64 pol = kL2 ? l2_policy_evict_last() : 0;  // per trip: see split6
     bool nbad = false;
     u32 nwa = 0, nwb = 0, cx = nx, cy = ny;
     if (i1 < q) {
       nbad = cx >= n || cy >= n;
       if (nbad) cx = cy = 0;
-      nwa = ldg_u32(node4 + cx);
-      nwb = ldg_u32(node4 + cy);
+      nwa = (kL2 ? ldg_u32_l2(node4 + cx, pol) : ldg_u32(node4 + cx));
+      nwb = (kL2 ? ldg_u32_l2(node4 + cy, pol) : ldg_u32(node4 + cy));
       nx = ny = 0;
       if (i1 + stride < q) in.get(i1 + stride, nx, ny);
     }
@@ -1590,6 +1605,17 @@ int qprefetch_mode() {
   return v;
 }
 bool qprefetch() { return qprefetch_mode() != 0; }
+// L2 eviction hints on the index gathers (k_lca_inlabel_split6 /
+// k_lca_inlabel_compact_pipe kL2): 0 off, 1 node table, 2 all index tables.
+// A/B (profiles/r2_cache_hints.md): config B 101.5 -> 102.8 G q/s with 1,
+// config E unchanged with 1 and 2% slower with 2; default 1.
+int l2hint_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("ETTG_L2HINT");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
 
 template <class In, class Out>
 void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32* err,
@@ -1620,7 +1646,8 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     const int grid_per_sm = grid_env ? grid_env : (q <= (u64(1) << 21) ? kQMinBlocks : kQGridPerSM);
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * grid_per_sm);
     if (h->layout == kLayoutCompact)
-      (qprefetch_mode() == 2   ? k_lca_inlabel_compact_pipe<In, Out>
+      (qprefetch_mode() == 2   ? (l2hint_mode() ? k_lca_inlabel_compact_pipe<In, Out, 1>
+                                                : k_lca_inlabel_compact_pipe<In, Out, 0>)
        : qprefetch_mode() == 1 ? k_lca_inlabel_compact<In, Out, true>
                                : k_lca_inlabel_compact<In, Out, false>)
           <<<blocks, kQThreads, 0, st>>>(h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q,
@@ -1636,7 +1663,10 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
                    : k_lca_inlabel<In, Out, Wide9Nodes, false>)<<<blocks, kQThreads, 0, st>>>(
           Wide9Nodes{h->nodes9}, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit6)
-      (qprefetch() ? k_lca_inlabel_split6<In, Out, true> : k_lca_inlabel_split6<In, Out, false>)
+      (!qprefetch()          ? k_lca_inlabel_split6<In, Out, false>
+       : l2hint_mode() == 1 ? k_lca_inlabel_split6<In, Out, true, 1>
+       : l2hint_mode() == 2 ? k_lca_inlabel_split6<In, Out, true, 2>
+                            : k_lca_inlabel_split6<In, Out, true, 0>)
           <<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutNarrow)
       (qprefetch() ? k_lca_inlabel_narrow<In, Out, true> : k_lca_inlabel_narrow<In, Out, false>)
