@@ -116,10 +116,15 @@ __global__ void k_pack_bits(const uint8_t* __restrict__ mask, u32 m, u32* __rest
 }
 
 // A caller's spanning-tree mask (char per edge, any non-zero = tree edge) as
-// the 0/1 bytes the tree-edge compaction counts.
-__global__ void k_mask01(const uint8_t* __restrict__ in, u32 m, uint8_t* __restrict__ out) {
-  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
-    out[e] = in[e] != 0;
+// the tree bits the compaction counts: one 32-edge word per thread.
+__global__ void k_mask_bits(const uint8_t* __restrict__ in, u32 m, u32* __restrict__ bits) {
+  const u32 words = (m + 31) / 32;
+  for (u32 w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    const u64 base = u64(w) * 32;
+    u32 x = 0;
+    for (u32 i = 0; i < 32 && base + i < m; ++i) x |= static_cast<u32>(in[base + i] != 0) << i;
+    bits[w] = x;
+  }
 }
 
 // Second-pass linking by priority: k_cc_hook_rest hooks a root under the
@@ -184,6 +189,7 @@ constexpr u32 kGroup = 4;
 struct EdgeSubset {
   u32 m, sample, phase, goff = 0, lead = 1;
   u32 total = 0;  // count(), filled in by launch_hook so the kernels do not loop
+  u32 ebase = 0;  // index of edges[0] in the tree bit array (streamed chunks)
   // edges of group g summed over all spans
   __host__ __device__ __forceinline__ u64 group_count(u32 g) const {
     const u64 span = u64(kGroup) * sample;
@@ -241,7 +247,7 @@ __device__ __forceinline__ T ld_edge(const T* p, bool cs) {
 template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
-              uint8_t* __restrict__ tree, u32* flags) {
+              u32* __restrict__ tbits, u32* flags) {
   u32 bad = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   const u64 cnt = sub.total;
@@ -260,7 +266,6 @@ __global__ void __launch_bounds__(256, kMinB)
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
         bad = 1;
         ok[j] = false;
-        tree[e] = 0;
       }
       if (!ok[j]) uv[j] = make_uint2(0, 0);
     }
@@ -290,11 +295,10 @@ __global__ void __launch_bounds__(256, kMinB)
       old[j] = (ok[j] && a[j] != b[j]) ? atomicCAS(&par[a[j]], a[j], b[j]) : a[j];
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      if (!ok[j]) continue;
-      uint8_t t = 0;
-      if (a[j] != b[j]) {
+      bool t = false;
+      if (ok[j] && a[j] != b[j]) {
         if (old[j] == a[j]) {
-          t = 1;
+          t = true;
         } else {  // another thread re-rooted a: retry from what the CAS found
           u32 x = uf_find(par, old[j]), y = uf_find(par, b[j]);
           while (x != y) {
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(256, kMinB)
             }
             const u32 o = atomicCAS(&par[x], x, y);
             if (o == x) {
-              t = 1;
+              t = true;
               break;
             }
             x = uf_find(par, o);
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(256, kMinB)
           }
         }
       }
-      tree[eidx[j]] = t;
+      if (t) set_bit(tbits, sub.ebase + eidx[j]);
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(256, kMinB)
 template <int kHookE, int kMinB, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook_rest(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
-                   uint8_t* __restrict__ tree, u32* flags, u32 magic, u32 shift) {
+                   u32* __restrict__ tbits, u32* flags, u32 magic, u32 shift) {
   u32 bad = 0;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   const u64 cnt = sub.total;
@@ -346,7 +350,6 @@ __global__ void __launch_bounds__(256, kMinB)
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
         bad = 1;
         ok[j] = false;
-        tree[e] = 0;
       }
       if (!ok[j]) uv[j] = make_uint2(0, 0);
     }
@@ -376,11 +379,10 @@ __global__ void __launch_bounds__(256, kMinB)
       old[j] = (ok[j] && a[j] != b[j]) ? atomicCAS(&par[a[j]], a[j], b[j]) : a[j];
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      if (!ok[j]) continue;
-      uint8_t t = 0;
-      if (a[j] != b[j]) {
+      bool t = false;
+      if (ok[j] && a[j] != b[j]) {
         if (old[j] == a[j]) {
-          t = 1;
+          t = true;
         } else {  // another thread re-rooted a: retry from what the CAS found
           u32 x = uf_find(par, old[j]), y = uf_find(par, b[j]);
           while (x != y) {
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(256, kMinB)
             }
             const u32 o = atomicCAS(&par[x], x, y);
             if (o == x) {
-              t = 1;
+              t = true;
               break;
             }
             x = uf_find(par, o);
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(256, kMinB)
           }
         }
       }
-      tree[eidx[j]] = t;
+      if (t) set_bit(tbits, sub.ebase + eidx[j]);
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
@@ -607,7 +609,7 @@ __global__ void k_root_stats(u32 root, u32 n, u32* pre_of, u32* size_by_pre, u32
 // an atomic is issued only when it can change the slot.
 template <int kHookE, int kMinB, bool kCheck = true>
 __global__ void __launch_bounds__(256, kMinB)
-    k_lowhigh_edges(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
+    k_lowhigh_edges(const uint2* __restrict__ edges, const u32* __restrict__ tbits, u32 m,
                     const u32* __restrict__ pre_of, uint2* lh, const u32* abort, u32 n) {
   if (tv_abort(abort, n)) return;
   u32* w = reinterpret_cast<u32*>(lh);  // slot = preorder - 1; .x = low, .y = high
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(256, kMinB)
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
       const u64 e = base + j * stride;
-      nt[j] = e < m && !tree[e];
+      nt[j] = e < m && !test_bit(tbits, e);
       uv[j] = nt[j] ? edges[e] : make_uint2(0, 0);
     }
     u32 pa[kHookE], pb[kHookE];
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(256, kMinB)
 // runs every edge is its own run (the same work as k_lowhigh_edges).
 template <int kE, bool kCs = false>
 __global__ void __launch_bounds__(256, 4)
-    k_lowhigh_runs(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree, u32 m,
+    k_lowhigh_runs(const uint2* __restrict__ edges, const u32* __restrict__ tbits, u32 m,
                    const u32* __restrict__ key_of, uint2* lh, const u32* abort, u32 n) {
   static_assert(kE == 8, "vector loads are written for 8 edges per thread");
   if (tv_abort(abort, n)) return;
@@ -681,16 +683,16 @@ __global__ void __launch_bounds__(256, 4)
         uv[2 * j] = make_uint2(v.x, v.y);
         uv[2 * j + 1] = make_uint2(v.z, v.w);
       }
-      const uint2 f = kCs ? __ldcs(reinterpret_cast<const uint2*>(tree + e0))
-                          : __ldg(reinterpret_cast<const uint2*>(tree + e0));
+      // the 8 tree bits of this chunk: byte (e0 & 31) / 8 of its word
+      const u32 f = __ldg(tbits + (e0 >> 5)) >> (e0 & 31);
 #pragma unroll
-      for (int j = 0; j < kE; ++j) nt[j] = ((j < 4 ? f.x >> (8 * j) : f.y >> (8 * (j - 4))) & 0xFF) == 0;
+      for (int j = 0; j < kE; ++j) nt[j] = ((f >> j) & 1u) == 0;
     } else {
 #pragma unroll
       for (int j = 0; j < kE; ++j) {
         const bool in = e0 + j < m;
         uv[j] = in ? edges[e0 + j] : make_uint2(0, 0);
-        nt[j] = in && !tree[e0 + j];
+        nt[j] = in && !test_bit(tbits, e0 + j);
       }
     }
     u32 ku[kE], kv[kE];
@@ -832,7 +834,8 @@ __global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
 
 __global__ void __launch_bounds__(256)
     k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ pre,
-                    const uint2* __restrict__ suf, const uint2* __restrict__ sp, u32 nb, u32 len,
+                    const uint2* __restrict__ suf, const uint2* __restrict__ sp, u32 nb,
+                    const uint2* __restrict__ sps, u32 nsb, u32 len,
                     const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
                     uint8_t* __restrict__ mask, u32 m, const u32* abort, u32 n) {
   if (tv_abort(abort, n)) return;
@@ -847,10 +850,24 @@ __global__ void __launch_bounds__(256)
     } else {
       acc = lh_merge(__ldg(suf + a), __ldg(pre + b));
       if (lb > la + 1) {
+        constexpr int kTop = st_tile_log<uint2>();  // widest row kept with a superblock table
         const u32 cnt = lb - la - 1;
         const int kk = hb32(cnt);
-        const uint2* row = sp + static_cast<u64>(kk) * nb;
-        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kk)]));
+        if (kk <= kTop || !sps) {
+          const uint2* row = sp + static_cast<u64>(kk) * nb;
+          acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kk)]));
+        } else {
+          // first and last 2^kTop blocks from the top row, whole superblocks
+          // strictly between theirs from the superblock table
+          const uint2* row = sp + static_cast<u64>(kTop) * nb;
+          acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kTop)]));
+          const u32 s1 = ((la + 1) >> kTop) + 1, s2e = (lb - 1) >> kTop;  // [s1, s2e)
+          if (s1 < s2e) {
+            const int k2 = hb32(s2e - s1);
+            const uint2* srow = sps + static_cast<u64>(k2) * nsb;
+            acc = lh_merge(acc, lh_merge(srow[s1], srow[s2e - (1u << k2)]));
+          }
+        }
       }
     }
     const bool inside = acc.x >= k.x && acc.y < k.y;
@@ -887,7 +904,7 @@ int br_cs() {
   return v;
 }
 
-void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* tree, u32* flags,
+void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, u32* tbits, u32* flags,
                  int sms, cudaStream_t st, bool prio = false) {
   sub.total = static_cast<u32>(sub.count());
   const u64 cnt = sub.total;
@@ -899,19 +916,19 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, uint8_t* t
     auto kern = br_cs() & 1 ? k_cc_hook_rest<kEdgesPerThread, 8, true>
                             : k_cc_hook_rest<kEdgesPerThread, 8, false>;
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
-        edges, sub, n, par, tree, flags, magic, shift);
+        edges, sub, n, par, tbits, flags, magic, shift);
   } else {
     auto kern = br_cs() & 1
                     ? (prio ? k_cc_hook<kEdgesPerThread, 8, true, true>
                             : k_cc_hook<kEdgesPerThread, 8, false, true>)
                     : (prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>);
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
-        edges, sub, n, par, tree, flags);
+        edges, sub, n, par, tbits, flags);
   }
   CK_LAUNCH();
 }
 
-void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* pre_of, uint2* lh,
+void launch_lowhigh(const uint2* edges, const u32* tbits, u32 m, const u32* pre_of, uint2* lh,
                     const u32* abort, u32 n, int sms, cudaStream_t st) {
   // Read-before-atomic filter: on config D (512 MB of key slots) it skips most
   // atomics (low/high 2.72 -> 1.96 ms); when the slots sit in L2 (config C,
@@ -926,17 +943,16 @@ void launch_lowhigh(const uint2* edges, const uint8_t* tree, u32 m, const u32* p
     const char* e = std::getenv("ETTG_LH_RUNS");
     return !e || std::atoi(e) != 0;
   }();
-  if (runs && check && reinterpret_cast<uintptr_t>(tree) % 8 == 0 &&
-      reinterpret_cast<uintptr_t>(edges) % 16 == 0) {
+  if (runs && check && reinterpret_cast<uintptr_t>(edges) % 16 == 0) {
     auto kr = br_cs() & 2 ? k_lowhigh_runs<8, true> : k_lowhigh_runs<8, false>;
-    kr<<<occ_grid(kr, (u64(m) + 7) / 8, sms), 256, 0, st>>>(edges, tree, m, pre_of, lh, abort, n);
+    kr<<<occ_grid(kr, (u64(m) + 7) / 8, sms), 256, 0, st>>>(edges, tbits, m, pre_of, lh, abort, n);
     CK_LAUNCH();
     return;
   }
   auto kern = check ? k_lowhigh_edges<kEdgesPerThread, 8, true>
                     : k_lowhigh_edges<kEdgesPerThread, 8, false>;
   kern<<<occ_grid(kern, (u64(m) + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
-      edges, tree, m, pre_of, lh, abort, n);
+      edges, tbits, m, pre_of, lh, abort, n);
   CK_LAUNCH();
 }
 
@@ -1019,7 +1035,8 @@ struct BridgeWs {
   uint2* edges = nullptr;
   CsrScratch csr;
   u32* par = nullptr;
-  uint8_t* tree = nullptr;
+  u32* tbits = nullptr;  // spanning-forest flag per input edge, one bit each
+  u64 tbits_bytes = 0;
   u64* scan_m = nullptr;
   u32* tedge = nullptr;
   u32* head = nullptr;
@@ -1037,6 +1054,8 @@ struct BridgeWs {
   uint2 *lh_pre = nullptr, *lh_suf = nullptr;  // TV: in-block prefix / suffix extrema
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
+  uint2* sps = nullptr;  // TV: superblock table (build_sparse_rows_super), or null
+  u32 nsb = 0, slev = 0;
   u32* words = nullptr;  // [0] edge-range flag, [1] tree-edge count, [2] head
   u32* bits = nullptr;   // the mask packed to bits for a host-mask D2H
   // CK / hybrid
@@ -1061,7 +1080,10 @@ struct BridgeWs {
     if (in.kind != BridgeIn::kDevU32) edges = c.take<uint2>(m);
     if (in.kind == BridgeIn::kHostCsr) csr.carve(c, n, m);
     par = c.take<u32>(n);
-    tree = c.take<uint8_t>(m + 16);
+    // bits (32 MB on config D, L2-resident) instead of one byte per edge:
+    // written by hooking, read by the compaction and low/high
+    tbits_bytes = ((static_cast<u64>(m) + 31) / 32 + 4) * 4;
+    tbits = c.take<u32>(tbits_bytes / 4);
     scan_m = c.take<u64>(scan_ws_words(m));
     tedge = c.take<u32>(n);
     head = c.take<u32>(n);
@@ -1083,7 +1105,18 @@ struct BridgeWs {
     }
     nb = (lh_len + 31) / 32;
     levels = 32 - __builtin_clz(nb);
-    sp = c.take<uint2>(static_cast<u64>(levels) * nb);
+    u32 rows = levels;
+    nsb = slev = 0;
+    if (engine == ETTG_BRIDGES_TV) {
+      st_super_shape<uint2>(nb, nsb, slev);
+      if (nsb <= kStSuperMax) {
+        rows = std::min<u32>(levels, st_tile_log<uint2>() + 1);
+        if (nsb) sps = c.take<uint2>(static_cast<u64>(slev) * nsb);
+      } else {
+        nsb = slev = 0;
+      }
+    }
+    sp = c.take<uint2>(static_cast<u64>(rows) * nb);
     words = c.take<u32>(16);
     bits = c.take<u32>((static_cast<u64>(m) + 31) / 32 + 1);
   }
@@ -1133,6 +1166,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
   CK(cudaEventRecord(ev[0], st));
   Trace tr("bridges", st);
   CK(cudaMemsetAsync(ws.words, 0, 16 * sizeof(u32), st));
+  CK(cudaMemsetAsync(ws.tbits, 0, ws.tbits_bytes, st));
   // Copies land in the leased arena: the copy stream is drained before the
   // lease is released (it is declared after the lease, so destroyed first).
   struct CopyGuard {
@@ -1171,8 +1205,9 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
       hook_chunk = [&](size_t lo, size_t cnt) {  // lo, cnt in u32 words (pairs: even)
         CK(cudaEventRecord(copy_guard.e, cs));
         CK(cudaStreamWaitEvent(st, copy_guard.e, 0));
-        launch_hook(ws.edges + lo / 2, EdgeSubset{static_cast<u32>(cnt / 2), 1, 0}, n, ws.par,
-                    ws.tree + lo / 2, ws.words, sms, st, true);
+        launch_hook(ws.edges + lo / 2,
+                    EdgeSubset{static_cast<u32>(cnt / 2), 1, 0, 0, 1, 0, static_cast<u32>(lo / 2)},
+                    n, ws.par, ws.tbits, ws.words, sms, st, true);
       };
     }
     // pinned: a chunk goes as int64 (narrowed on the device) whenever the
@@ -1213,8 +1248,8 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
         k_edges_from_i64<<<std::min(g, blocks_for(cnt, 256)), 256, 0, st>>>(
             ws.e64 + lo, cnt, n, ws.edges + lo, ws.words);
         CK_LAUNCH();
-        launch_hook(ws.edges + lo, EdgeSubset{cnt, 1, 0}, n, ws.par, ws.tree + lo, ws.words, sms,
-                    st, true);
+        launch_hook(ws.edges + lo, EdgeSubset{cnt, 1, 0, 0, 1, 0, lo}, n, ws.par, ws.tbits,
+                    ws.words, sms, st, true);
       }
       hooked = true;
     } else if (m) {
@@ -1236,11 +1271,11 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     // tour (count = words[1], cover = the list ranking's error flag).
     if (m) {
       const uint8_t* src = in.tree;
-      if (in.tree_on_host) {
-        copy_h2d(ws.tree, in.tree, m, device, st);
-        src = ws.tree;
+      if (in.tree_on_host) {  // d_mask is cleared below, after the conversion
+        copy_h2d(d_mask, in.tree, m, device, st);
+        src = d_mask;
       }
-      k_mask01<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(src, m, ws.tree);
+      k_mask_bits<<<std::min(g, blocks_for((m + 31) / 32, 256)), 256, 0, st>>>(src, m, ws.tbits);
       CK_LAUNCH();
       if (in.kind == BridgeIn::kDevU32) {
         k_cc_range<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, m, n, ws.words);
@@ -1264,8 +1299,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     u32 bad = 0;
     read_back(&bad, ws.words, 4, st);
     if (bad) einval("edge endpoint out of range");
-    if (m) CK(cudaMemsetAsync(ws.tree, 0, m, st));
-    const u32 reached = run_bfs(edges, n, m, 0, ws.blevel, ws.bparent, ws.pedge_of, ws.tree,
+    const u32 reached = run_bfs(edges, n, m, 0, ws.blevel, ws.bparent, ws.pedge_of, ws.tbits,
                                 ws.bfs, st, sms);
     if (reached != n) einval("disconnected graph; extract the largest component first");
     tr.mark("bfs");
@@ -1287,16 +1321,16 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
       if (const char* ev = std::getenv("ETTG_CC_SAMPLE")) sample = std::max(1, std::atoi(ev));
       if (const char* ev = std::getenv("ETTG_CC_ROUNDS")) rounds = std::max(1, std::atoi(ev));
       if (sample <= 1) {
-        launch_hook(edges, EdgeSubset{m, 1, 0}, n, ws.par, ws.tree, ws.words, sms, st);
+        launch_hook(edges, EdgeSubset{m, 1, 0}, n, ws.par, ws.tbits, ws.words, sms, st);
       } else {
         rounds = std::min(rounds, sample - 1);
         for (u32 r = 0; r < rounds; ++r) {
-          launch_hook(edges, EdgeSubset{m, sample, 0, r, 1}, n, ws.par, ws.tree, ws.words, sms,
+          launch_hook(edges, EdgeSubset{m, sample, 0, r, 1}, n, ws.par, ws.tbits, ws.words, sms,
                       st);
           k_cc_compress<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.par, n);
           CK_LAUNCH();
         }
-        launch_hook(edges, EdgeSubset{m, sample, 1, 0, rounds}, n, ws.par, ws.tree, ws.words, sms,
+        launch_hook(edges, EdgeSubset{m, sample, 1, 0, rounds}, n, ws.par, ws.tbits, ws.words, sms,
                     st);
       }
       tr.mark("cc_hook");
@@ -1304,7 +1338,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     CK(cudaEventRecord(ev[1], st));
 
     // ---- Euler tour of the forest, rooted at 0 ---------------------------
-    compact_u8(ws.tree, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
+    compact_bits(ws.tbits, m, TreeOut{ws.tedge, n}, ws.scan_m, ws.words + 1, st);
     const bool tv = engine == ETTG_BRIDGES_TV;
     if (!tv) {
       u32 w[2];
@@ -1367,15 +1401,17 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     const u32 len = 2 * n;  // slots key - 1, keys in [1, 2n - 1]
     k_lh_neutral<<<std::min(g, blocks_for(len, 256)), 256, 0, st>>>(ws.lh, len);
     CK_LAUNCH();
-    if (m && n > 1) launch_lowhigh(edges, ws.tree, m, ws.pre_of, ws.lh, abort, n, sms, st);
+    if (m && n > 1) launch_lowhigh(edges, ws.tbits, m, ws.pre_of, ws.lh, abort, n, sms, st);
     tr.mark("lowhigh_edges");
     k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
         ws.lh, len, ws.nb, ws.sp, ws.lh_pre, ws.lh_suf);
     CK_LAUNCH();
-    build_sparse_rows(ws.sp, ws.nb, ws.levels, LhMerge{}, g, st);
+    if (!build_sparse_rows_super(ws.sp, ws.nb, ws.levels, ws.sps, LhMerge{}, st))
+      build_sparse_rows(ws.sp, ws.nb, ws.levels, LhMerge{}, g, st);
     if (n > 1) {
       k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
-          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, len, ws.kt, ws.tedge, n - 1, d_mask, m,
+          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, ws.sps, ws.nsb, len, ws.kt, ws.tedge, n - 1,
+          d_mask, m,
           abort, n);
       CK_LAUNCH();
     }
@@ -1384,7 +1420,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     // ---- CK marking (core/src/bridges.cpp:40-76) -------------------------
     CK(cudaMemsetAsync(ws.marked, 0, n, st));
     if (m) {
-      k_ck_mark<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tree, m, ws.rec,
+      k_ck_mark<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(edges, ws.tbits, m, ws.rec,
                                                                  ws.marked);
       CK_LAUNCH();
     }
@@ -1689,7 +1725,7 @@ void bfs_tree_impl(const BridgeIn& in, int64_t n, int64_t m, int64_t root, int d
     longlong2* e64;
     uint2* e;
     u32 *lev, *par, *pe, *flags;
-    uint8_t* tree;
+    u32* tbits;
     CsrScratch cs;
     BfsWs bfs;
     void carve(Carver& c, u32 n, u32 m, bool csr) {
@@ -1699,7 +1735,7 @@ void bfs_tree_impl(const BridgeIn& in, int64_t n, int64_t m, int64_t root, int d
       par = c.take<u32>(n);
       pe = c.take<u32>(n);
       flags = c.take<u32>(8);
-      tree = c.take<uint8_t>(m + 16);
+      tbits = c.take<u32>((static_cast<u64>(m) + 31) / 32 + 4);
       if (csr) cs.carve(c, n, m);
       bfs.carve(c, n, m);
     }
@@ -1711,7 +1747,7 @@ void bfs_tree_impl(const BridgeIn& in, int64_t n, int64_t m, int64_t root, int d
   ws.carve(c, nn, mm, csr);
   const int sms = sm_count(device);
   CK(cudaMemsetAsync(ws.flags, 0, 32, st));
-  CK(cudaMemsetAsync(ws.tree, 0, mm + 16, st));
+  CK(cudaMemsetAsync(ws.tbits, 0, ((static_cast<u64>(mm) + 31) / 32 + 4) * 4, st));
   if (csr) {
     upload_csr(in, nn, mm, ws.cs, ws.e, ws.flags, device, st);
   } else if (upload_edges(static_cast<const int64_t*>(in.edges), mm, nn, ws.e64, ws.e, ws.flags,
@@ -1719,12 +1755,12 @@ void bfs_tree_impl(const BridgeIn& in, int64_t n, int64_t m, int64_t root, int d
     einval("edge endpoint out of range");
   }
   const u32 reached = run_bfs(ws.e, nn, mm, static_cast<u32>(root), ws.lev, ws.par, ws.pe,
-                              ws.tree, ws.bfs, st, sms);
+                              ws.tbits, ws.bfs, st, sms);
   if (reached != nn) einval("disconnected graph; extract the largest component first");
   staged_d2h_widen_u32(level, ws.lev, nn, device, st);
   staged_d2h_widen_u32(parent, ws.par, nn, device, st);
   staged_d2h_widen_u32(parent_edge, ws.pe, nn, device, st);
-  if (mm) copy_d2h(tree_mask, ws.tree, mm, device, st);
+  if (mm) staged_d2h_expand_bits(tree_mask, ws.tbits, mm, device, st);
   CK(cudaStreamSynchronize(st));
 }
 }  // namespace

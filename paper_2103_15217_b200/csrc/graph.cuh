@@ -106,7 +106,7 @@ struct BfsState {
   u32* level;
   u32* parent;
   u32* pedge;
-  uint8_t* tree;
+  u32* tbits;  // tree-edge bit per input edge
 };
 
 // expand: every unvisited neighbour w of a frontier vertex u keeps the
@@ -143,7 +143,7 @@ __global__ void k_bfs_commit(BfsState s, int p, const u32* __restrict__ offs,
       if (atomicCAS(&s.level[w], kNone, lu + 1) != kNone) continue;
       s.parent[w] = u;
       s.pedge[w] = static_cast<u32>(c);
-      s.tree[static_cast<u32>(c)] = 1;
+      atomicOr(&s.tbits[static_cast<u32>(c) >> 5], 1u << (static_cast<u32>(c) & 31));
       s.front[1 - p][atomicAdd(&s.size[1 - p], 1u)] = w;
       ++added;
     }
@@ -154,10 +154,10 @@ __global__ void k_bfs_commit(BfsState s, int p, const u32* __restrict__ offs,
 // ---- CK marking ---------------------------------------------------------------
 // rec[v] = {parent, level}.  Racy duplicate stores of 1 are idempotent
 // (core/src/bridges.cpp:40-41).
-__global__ void k_ck_mark(const uint2* __restrict__ edges, const uint8_t* __restrict__ tree,
+__global__ void k_ck_mark(const uint2* __restrict__ edges, const u32* __restrict__ tbits,
                           u32 m, const uint2* __restrict__ rec, uint8_t* marked) {
   for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    if (tree[e]) continue;
+    if (test_bit(tbits, e)) continue;
     const uint2 uv = edges[e];
     u32 a = uv.x, b = uv.y;
     if (a == b) continue;
@@ -236,13 +236,13 @@ __global__ void k_bfs_init(BfsState s, u32 n, u32 root) {
 
 constexpr int kBfsChunk = 16;  // levels per CUDA-graph replay
 
-// Returns the number of vertices reached.  tree[m] must be zeroed by the caller.
+// Returns the number of vertices reached.  tbits[(m + 31) / 32] must be zeroed by the caller.
 inline u32 run_bfs(const uint2* edges, u32 n, u32 m, u32 root, u32* level, u32* parent,
-                   u32* pedge, uint8_t* tree, const BfsWs& ws, cudaStream_t st, int sms) {
+                   u32* pedge, u32* tbits, const BfsWs& ws, cudaStream_t st, int sms) {
   Trace tr("bfs", st);
   build_csr(edges, n, m, ws.offs, ws.nbr, ws.eid, ws.csr, st, sms);
   tr.mark("csr");
-  BfsState s{{ws.front0, ws.front1}, ws.size, ws.cand, level, parent, pedge, tree};
+  BfsState s{{ws.front0, ws.front1}, ws.size, ws.cand, level, parent, pedge, tbits};
   const unsigned g = std::min<unsigned>(sms * 8, blocks_for(n, 256));
   k_bfs_init<<<g, 256, 0, st>>>(s, n, root);
   CK_LAUNCH();

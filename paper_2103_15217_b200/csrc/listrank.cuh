@@ -208,7 +208,9 @@ constexpr int kLrWalkers = 1;
 // and sublists capped at cap_step elements (walk micro: -12% vs 8-B records).
 // kTwin: the successor of e is succ[e ^ 1] (an Euler tour whose closed
 // rotation lists serve as the successor array, bridges.cu k_tree_close).
-template <class Down, class H, bool kNarrow, bool kTwin = false>
+// kHint (ETTG_LR_HINT A/B): bit 0 = record stores evict-first (.cs), bit 1 =
+// successor loads with an L2 evict_last policy.
+template <class Down, class H, bool kNarrow, bool kTwin = false, int kHint = 0>
 __global__ void __launch_bounds__(256)
     k_lr_walk0(const u32* __restrict__ succ, u64* __restrict__ rec, u32 k, H head_src, u32 seed,
                u32 mask, const u32* __restrict__ spl, u32* counters, u32 sub_cap,
@@ -257,11 +259,17 @@ __global__ void __launch_bounds__(256)
     for (int w = 0; w < kLrWalkers; ++w) {
       nxt[w] = kNone;
       if (active[w]) {
-        if (kNarrow)
-          rec32[cur[w]] = ((acc[w] & 0xFFFFu) << sid_bits) | sid[w];
-        else
+        if (kNarrow) {
+          const u32 r = ((acc[w] & 0xFFFFu) << sid_bits) | sid[w];
+          if (kHint & 1)
+            __stcs(rec32 + cur[w], r);
+          else
+            rec32[cur[w]] = r;
+        } else {
           rec[cur[w]] = (static_cast<u64>(acc[w]) << 32) | sid[w];
-        nxt[w] = succ[kTwin ? cur[w] ^ 1u : cur[w]];
+        }
+        const u32* sp = succ + (kTwin ? cur[w] ^ 1u : cur[w]);
+        nxt[w] = (kHint & 2) ? ldg_u32_l2(sp, l2_policy_evict_last()) : *sp;
       }
     }
 #pragma unroll
@@ -692,7 +700,15 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
     twin_succ = nullptr;
   }
   if (twin_succ) {
-    k_lr_walk0<Down, H, true, true><<<walk_blocks, 256, 0, st>>>(
+    static const int hint = [] {
+      const char* e = std::getenv("ETTG_LR_HINT");
+      return e ? std::atoi(e) & 3 : 0;
+    }();
+    auto kern = hint == 1   ? k_lr_walk0<Down, H, true, true, 1>
+                : hint == 2 ? k_lr_walk0<Down, H, true, true, 2>
+                : hint == 3 ? k_lr_walk0<Down, H, true, true, 3>
+                            : k_lr_walk0<Down, H, true, true, 0>;
+    kern<<<walk_blocks, 256, 0, st>>>(
         twin_succ, ws.rec0, k, head, seed0, mask0, ws.lv[0].spl, cnt, cap1, ws.lv[0].sub_next,
         ws.lv[0].sub_w, down, ws.cap_step, ws.sid_bits);
   } else if (ws.sid_bits)

@@ -292,6 +292,84 @@ void compact_u8(const uint8_t* flags, u64 n, Out out, u64* status, u32* total, c
   CK_LAUNCH();
 }
 
+// ---- bit-flag compaction ----------------------------------------------------
+// The same two passes over a bit array (flag i = bit i & 31 of word i >> 5,
+// bits past n zero): 64K flags per tile, 8 rounds of one word (32 flags) per
+// thread, ranks in flag order.  A warp's outputs of one round are contiguous,
+// so they are staged in shared memory and stored coalesced (per-lane runs of
+// ranks stored directly made the write pass slower than the byte-flag one).
+constexpr int kCompactBitRounds = 8;
+constexpr u32 kCompactBitTile = kScanThreads * 32 * kCompactBitRounds;  // 65536 flags
+
+template <class Out, int kMode>
+__global__ void __launch_bounds__(kScanThreads)
+    k_compact_bits(const u32* __restrict__ words, u64 n, Out out, u32* total, u32* cnt) {
+  __shared__ u32 s_round[kCompactBitRounds][kScanThreads / 32];
+  __shared__ u32 s_prefix;
+  __shared__ u32 s_buf[kScanThreads / 32][32 * 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 tile = blockIdx.x;
+  const u64 tbase = static_cast<u64>(tile) * kCompactBitTile;
+  const u64 nw = (n + 31) / 32;
+  u32 v[kCompactBitRounds], inclk[kCompactBitRounds];
+#pragma unroll
+  for (int k = 0; k < kCompactBitRounds; ++k) {
+    const u64 w = tbase / 32 + static_cast<u64>(k) * kScanThreads + tid;
+    v[k] = w < nw ? words[w] : 0u;
+    inclk[k] = warp_incl_scan(static_cast<u32>(__popc(v[k])));
+    if (lane == 31) s_round[k][warp] = inclk[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    u32 carry = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactBitRounds; ++k) {
+      const u32 w = lane < kScanThreads / 32 ? s_round[k][lane] : 0u;
+      const u32 wi = warp_incl_scan(w);
+      if (lane < kScanThreads / 32) s_round[k][lane] = carry + wi - w;
+      carry += __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    }
+    if (kMode == 1) {
+      if (lane == 0) cnt[tile] = carry;
+    } else if (lane == 0) {
+      const u32 pre = cnt[tile];
+      s_prefix = pre;
+      if (total && static_cast<u64>(tile + 1) * kCompactBitTile >= n) *total = pre + carry;
+    }
+  }
+  if (kMode == 1) return;
+  __syncthreads();
+  u32* buf = s_buf[warp];
+#pragma unroll
+  for (int k = 0; k < kCompactBitRounds; ++k) {
+    const u32 wtot = __shfl_sync(0xffffffffu, inclk[k], 31);
+    if (wtot == 0) continue;  // warp-uniform
+    const u32 local = (static_cast<u32>(k) * kScanThreads + tid) * 32;  // flag offset in the tile
+    u32 off = inclk[k] - __popc(v[k]);
+    for (u32 b = v[k]; b; b &= b - 1) buf[off++] = local + (__ffs(b) - 1);
+    __syncwarp();
+    const u32 r0 = s_prefix + s_round[k][warp];
+    for (u32 j = lane; j < wtot; j += 32) out(tbase + buf[j], r0 + j);
+    __syncwarp();
+  }
+}
+
+template <class Out>
+void compact_bits(const u32* words, u64 n, Out out, u64* status, u32* total, cudaStream_t st) {
+  if (n == 0) {
+    if (total) CK(cudaMemsetAsync(total, 0, sizeof(u32), st));
+    return;
+  }
+  const u64 tiles = (n + kCompactBitTile - 1) / kCompactBitTile;
+  u32* cnt = reinterpret_cast<u32*>(status);  // tiles words
+  k_compact_bits<Out, 1><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(words, n, out,
+                                                                               nullptr, cnt);
+  k_tile_scan<<<1, 1024, 0, st>>>(cnt, static_cast<u32>(tiles));
+  k_compact_bits<Out, 2><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(words, n, out,
+                                                                               total, cnt);
+  CK_LAUNCH();
+}
+
 // status must hold scan_ws_words(n) u64 words (last one doubles as ticket).
 template <class In, class Out>
 void scan_exclusive(In in, Out out, u64 n, u64* status, u32* total,
