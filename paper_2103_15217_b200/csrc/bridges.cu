@@ -151,6 +151,7 @@ __device__ __forceinline__ u32 uf_prio(u32 x) { return mix32(x); }
 // read-only walk was fastest on C (0.18 ms) but let lattice chains grow on
 // road graphs (config D 3.80 vs 2.31 ms); profiles/r1_bridges_tuning.md.
 constexpr int kShortcutHops = 8;
+template <int kHops = kShortcutHops>
 __device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
   if (cur == x) return x;
   u32 next;
@@ -159,7 +160,7 @@ __device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
     cur = next;
     ++hops;
   }
-  if (hops >= kShortcutHops) par[x] = cur;
+  if (hops >= kHops) par[x] = cur;
   return cur;
 }
 __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(par, x, par[x]); }
@@ -244,7 +245,7 @@ __device__ __forceinline__ T ld_edge(const T* p, bool cs) {
   return cs ? __ldcs(p) : *p;
 }
 
-template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false>
+template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false, int kSc = kShortcutHops>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               u32* __restrict__ tbits, u32* flags) {
@@ -280,8 +281,8 @@ __global__ void __launch_bounds__(256, kMinB)
       // equal parents => same tree: no find needed (after the compress pass
       // between the phases this settles most phase-1 edges with two loads)
       if (a[j] != b[j]) {
-        a[j] = uf_find_from(par, uv[j].x, a[j]);
-        b[j] = uf_find_from(par, uv[j].y, b[j]);
+        a[j] = uf_find_from<kSc>(par, uv[j].x, a[j]);
+        b[j] = uf_find_from<kSc>(par, uv[j].y, b[j]);
       }
       if (kPrio ? uf_prio(a[j]) < uf_prio(b[j]) : a[j] < b[j]) {
         const u32 tmp = a[j];
@@ -478,6 +479,8 @@ __device__ __forceinline__ void rot_push(u32 active, u32 x, u32 h, u32 root,
   }
 }
 
+// (Fetching the next trip's endpoints before this trip's atomics made the
+// rotation slower on config D: 0.76-0.77 vs 0.74 ms, gpurun_out/r2aa.)
 __global__ void k_tree_rot(const uint2* __restrict__ edges, const u32* __restrict__ tedge, u32 T,
                            u32 root, u32* __restrict__ head, u32* __restrict__ nxt,
                            uint2* __restrict__ tend, u32* __restrict__ tails, u32* last_root,
@@ -662,24 +665,33 @@ __global__ void __launch_bounds__(256, kMinB)
 // keys, high(u) from larger ones -- into one filtered read and at most one
 // atomic per run, while the v-side update stays per edge.  On inputs without
 // runs every edge is its own run (the same work as k_lowhigh_edges).
-template <int kE, bool kCs = false>
-__global__ void __launch_bounds__(256, 4)
+template <int kE, bool kCs = false, int kMinB = 5>
+__global__ void __launch_bounds__(256, kMinB)
     k_lowhigh_runs(const uint2* __restrict__ edges, const u32* __restrict__ tbits, u32 m,
                    const u32* __restrict__ key_of, uint2* lh, const u32* abort, u32 n) {
   static_assert(kE == 8, "vector loads are written for 8 edges per thread");
   if (tv_abort(abort, n)) return;
   u32* w = reinterpret_cast<u32*>(lh);  // slot = key - 1; [2s] = low, [2s + 1] = high
   const u64 nchunk = (static_cast<u64>(m) + kE - 1) / kE;
+  const u64 gstride = static_cast<u64>(gridDim.x) * blockDim.x;
+  auto load_chunk = [&](u64 cc, uint4* dst) {
+    if ((cc + 1) * kE <= m) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(edges + cc * kE);
+#pragma unroll
+      for (int j = 0; j < kE / 2; ++j) dst[j] = kCs ? __ldcs(e4 + j) : __ldg(e4 + j);
+    }
+  };
   for (u64 c = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunk;
-       c += static_cast<u64>(gridDim.x) * blockDim.x) {
+       c += gstride) {
     const u64 e0 = c * kE;
     uint2 uv[kE];
     bool nt[kE];
     if (e0 + kE <= m) {
-      const uint4* e4 = reinterpret_cast<const uint4*>(edges + e0);
+      uint4 cv[kE / 2];
+      load_chunk(c, cv);
 #pragma unroll
       for (int j = 0; j < kE / 2; ++j) {
-        const uint4 v = kCs ? __ldcs(e4 + j) : __ldg(e4 + j);
+        const uint4 v = cv[j];
         uv[2 * j] = make_uint2(v.x, v.y);
         uv[2 * j + 1] = make_uint2(v.z, v.w);
       }
@@ -752,10 +764,17 @@ __device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
 
 // Level 0 plus in-block prefix and suffix extrema (32-entry blocks), so a
 // range that crosses a block boundary costs two gathers plus the sparse
-// table instead of a scan of its partial blocks.
+// table instead of a scan of its partial blocks.  One array holds both: a
+// key range [a, b] starts at a vertex's own slot a and ends at the slot b
+// of its up half-edge, which never receives an update (neutral), so ps[i]
+// is the suffix from i where lh[i] is set and the prefix up to i where it
+// is neutral; nmask[block] has a bit per neutral slot.  A range starting at
+// a neutral vertex slot takes the suffix from the next set slot of its
+// block (k_classify_tour).  Half the stores of separate prefix and suffix
+// arrays.
 __global__ void k_lh_block_ps(const uint2* __restrict__ lh, u32 n, u32 nb,
-                              uint2* __restrict__ sp0, uint2* __restrict__ pre,
-                              uint2* __restrict__ suf) {
+                              uint2* __restrict__ sp0, uint2* __restrict__ ps,
+                              u32* __restrict__ nmask) {
   const u32 lane = threadIdx.x & 31;
   const u32 warps = (gridDim.x * blockDim.x) >> 5;
   for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
@@ -772,11 +791,11 @@ __global__ void k_lh_block_ps(const uint2* __restrict__ lh, u32 n, u32 nb,
       o.y = __shfl_down_sync(0xffffffffu, g.y, d);
       if (lane + d < 32) g = lh_merge(g, o);
     }
-    if (i < n) {
-      pre[i] = f;
-      suf[i] = g;
-    }
+    const bool neutral = v.x == 0xFFFFFFFFu && v.y == 0u;
+    const u32 nm = __ballot_sync(0xffffffffu, neutral);
+    if (i < n) ps[i] = neutral ? f : g;
     if (lane == 31) sp0[b] = f;
+    if (lane == 0) nmask[b] = nm;
   }
 }
 
@@ -833,8 +852,8 @@ __global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
 }
 
 __global__ void __launch_bounds__(256)
-    k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ pre,
-                    const uint2* __restrict__ suf, const uint2* __restrict__ sp, u32 nb,
+    k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ ps,
+                    const u32* __restrict__ nmask, const uint2* __restrict__ sp, u32 nb,
                     const uint2* __restrict__ sps, u32 nsb, u32 len,
                     const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
                     uint8_t* __restrict__ mask, u32 m, const u32* abort, u32 n) {
@@ -848,7 +867,12 @@ __global__ void __launch_bounds__(256)
       acc = lh[a];
       for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
     } else {
-      acc = lh_merge(__ldg(suf + a), __ldg(pre + b));
+      // suffix of block la from a: ps[a], or from the next slot when a's
+      // own slot is neutral (then ps[a] is a prefix); prefix of block lb
+      // up to b: ps[b] (b is an up slot, always neutral)
+      const u32 set = ~__ldg(nmask + la) & (0xFFFFFFFFu << (a & 31u));
+      const uint2 sa = set ? __ldg(ps + (la << 5) + (__ffs(set) - 1)) : make_uint2(0xFFFFFFFFu, 0u);
+      acc = lh_merge(sa, __ldg(ps + b));
       if (lb > la + 1) {
         constexpr int kTop = st_tile_log<uint2>();  // widest row kept with a superblock table
         const u32 cnt = lb - la - 1;
@@ -913,14 +937,24 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, u32* tbits
   if (rest_kernel) {
     u32 magic = 0, shift = 0;
     sub.rest_divider(magic, shift);
+    // (Loading the next trip's edges before this trip's finds -- 1 or 2
+    // edges per thread, 6 or 8 CTAs/SM -- did not help: 1.88-2.09 vs 1.89 ms.)
     auto kern = br_cs() & 1 ? k_cc_hook_rest<kEdgesPerThread, 8, true>
                             : k_cc_hook_rest<kEdgesPerThread, 8, false>;
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tbits, flags, magic, shift);
   } else {
+    static const int sc = [] {
+      const char* e = std::getenv("ETTG_HOOK_SC");
+      return e ? std::atoi(e) : 8;
+    }();
     auto kern = br_cs() & 1
-                    ? (prio ? k_cc_hook<kEdgesPerThread, 8, true, true>
-                            : k_cc_hook<kEdgesPerThread, 8, false, true>)
+                    ? (prio      ? k_cc_hook<kEdgesPerThread, 8, true, true>
+                       : sc == 2  ? k_cc_hook<kEdgesPerThread, 8, false, true, 2>
+                       : sc == 4  ? k_cc_hook<kEdgesPerThread, 8, false, true, 4>
+                       : sc == 16 ? k_cc_hook<kEdgesPerThread, 8, false, true, 16>
+                       : sc == 99 ? k_cc_hook<kEdgesPerThread, 8, false, true, 1 << 30>
+                                  : k_cc_hook<kEdgesPerThread, 8, false, true>)
                     : (prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>);
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tbits, flags);
@@ -944,6 +978,8 @@ void launch_lowhigh(const uint2* edges, const u32* tbits, u32 m, const u32* pre_
     return !e || std::atoi(e) != 0;
   }();
   if (runs && check && reinterpret_cast<uintptr_t>(edges) % 16 == 0) {
+    // 5 CTAs/SM (48 registers): 1.76 -> 1.67 ms on config D vs 4 at 64
+    // registers; 6 spills (profiles/r2_bridges_notes.md)
     auto kr = br_cs() & 2 ? k_lowhigh_runs<8, true> : k_lowhigh_runs<8, false>;
     kr<<<occ_grid(kr, (u64(m) + 7) / 8, sms), 256, 0, st>>>(edges, tbits, m, pre_of, lh, abort, n);
     CK_LAUNCH();
@@ -1051,7 +1087,8 @@ struct BridgeWs {
   u32* pedge_by_pre = nullptr;
   uint2* lh = nullptr;
   uint2* kt = nullptr;  // TV: (key, up key) per tree edge
-  uint2 *lh_pre = nullptr, *lh_suf = nullptr;  // TV: in-block prefix / suffix extrema
+  uint2* lh_ps = nullptr;  // TV: in-block suffix (set slots) / prefix (neutral slots) extrema
+  u32* lh_nmask = nullptr;  // TV: neutral-slot bits per 32-slot block
   uint2* sp = nullptr;
   u32 nb = 0, levels = 0;
   uint2* sps = nullptr;  // TV: superblock table (build_sparse_rows_super), or null
@@ -1090,7 +1127,12 @@ struct BridgeWs {
     nxt = c.take<u32>(k + 1);
     tend = c.take<uint2>(n);
     tails = c.take<u32>(n);
-    lr.carve(c, k > 0 ? k : 1, true);  // tour ranks only: no down weights
+    // Tour ranks only (no down weights).  Level means 8 / 4 instead of 16 / 16:
+    // the level-0 walk of a lattice spanning tree's tour is bound by its
+    // tail (the longest sublist, ~L0 ln(k / L0) dependent steps) -- config D
+    // walk0 1.19 -> 0.70 ms, list ranking 1.67 -> 1.46 ms
+    // (profiles/r2_bridges_notes.md); random trees (the LCA build) keep 16 / 16.
+    lr.carve(c, k > 0 ? k : 1, true, 8, 4);
     flags = c.take<u32>(k + 1);
     scan_k = c.take<u64>(scan_ws_words(k + 1));
     pre_of = c.take<u32>(n);
@@ -1100,8 +1142,8 @@ struct BridgeWs {
     lh = c.take<uint2>(lh_len);
     if (engine == ETTG_BRIDGES_TV) {
       kt = c.take<uint2>(n);
-      lh_pre = c.take<uint2>(lh_len);
-      lh_suf = c.take<uint2>(lh_len);
+      lh_ps = c.take<uint2>(lh_len);
+      lh_nmask = c.take<u32>((lh_len + 31) / 32);
     }
     nb = (lh_len + 31) / 32;
     levels = 32 - __builtin_clz(nb);
@@ -1404,13 +1446,13 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     if (m && n > 1) launch_lowhigh(edges, ws.tbits, m, ws.pre_of, ws.lh, abort, n, sms, st);
     tr.mark("lowhigh_edges");
     k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
-        ws.lh, len, ws.nb, ws.sp, ws.lh_pre, ws.lh_suf);
+        ws.lh, len, ws.nb, ws.sp, ws.lh_ps, ws.lh_nmask);
     CK_LAUNCH();
     if (!build_sparse_rows_super(ws.sp, ws.nb, ws.levels, ws.sps, LhMerge{}, st))
       build_sparse_rows(ws.sp, ws.nb, ws.levels, LhMerge{}, g, st);
     if (n > 1) {
       k_classify_tour<<<std::min(g, blocks_for(n - 1, 256)), 256, 0, st>>>(
-          ws.lh, ws.lh_pre, ws.lh_suf, ws.sp, ws.nb, ws.sps, ws.nsb, len, ws.kt, ws.tedge, n - 1,
+          ws.lh, ws.lh_ps, ws.lh_nmask, ws.sp, ws.nb, ws.sps, ws.nsb, len, ws.kt, ws.tedge, n - 1,
           d_mask, m,
           abort, n);
       CK_LAUNCH();

@@ -593,15 +593,23 @@ struct ListRankWs {
   }
 
   u32 L0 = kLrL0;  // level-0 mean sublist length (power of two); ETTG_LR_L0 overrides
+  u32 Ld = kLrL;   // deeper levels; ETTG_LR_L overrides
   double wyllie_max = kLrWyllieMax;  // ETTG_LR_WYLLIE overrides (0: smem final only)
   // Narrow level-0 records (weight-free lists, see k_lr_walk0): sid_bits > 0.
   u32 sid_bits = 0, cap_step = kLrCapStep;
   // narrow_ok: the caller's lists carry no down weights (NoDown)
-  void carve(Carver& c, u32 k_, bool narrow_ok = false) {
+  // l0 / ld: default level means for this caller (powers of two)
+  void carve(Carver& c, u32 k_, bool narrow_ok = false, u32 l0 = kLrL0, u32 ld = kLrL) {
     k = k_;
+    L0 = l0;
+    Ld = ld;
     if (const char* e = std::getenv("ETTG_LR_L0")) {
       const u32 v = static_cast<u32>(std::atoi(e));
       if (v >= 2 && v <= 1024 && (v & (v - 1)) == 0) L0 = v;
+    }
+    if (const char* e = std::getenv("ETTG_LR_L")) {
+      const u32 v = static_cast<u32>(std::atoi(e));
+      if (v >= 2 && v <= 1024 && (v & (v - 1)) == 0) Ld = v;
     }
     if (const char* e = std::getenv("ETTG_LR_WYLLIE")) wyllie_max = std::atof(e);
     succ0 = c.take<u32>(k);
@@ -648,13 +656,13 @@ struct ListRankWs {
       }
       L.rec_sid = c.take<u32>(cap);
       L.rec_loc = c.take<u64>(cap);
-      u32 capn = next_cap(cap, kLrL);
+      u32 capn = next_cap(cap, Ld);
       L.spl = c.take<u32>(capn);
       L.sub_next = c.take<u32>(capn);
       L.sub_w = c.take<u64>(capn);
       L.scan_status = c.take<u64>(scan_ws_words(cap));
       cap = capn;
-      expect /= kLrL;
+      expect /= Ld;
       ++l;
     }
     levels = l;  // walk levels 0..l-1, Wyllie on level l
@@ -738,7 +746,7 @@ void list_rank_core_h(u32 k, H head, Down down, ListRankWs& ws, cudaStream_t st,
     u32* nspl = cnt + LrCounters::kLevelBase + 4 * l + 1;
     u32* hd = cnt + LrCounters::kLevelBase + 4 * l + 2;
     u32* hd_next = cnt + LrCounters::kLevelBase + 4 * (l + 1) + 2;
-    const u32 seed = lr_seed(l), mask = kLrL - 1;
+    const u32 seed = lr_seed(l), mask = ws.Ld - 1;
     spl_compact(SplInDev{hd, S_l, seed, mask}, L.cap, L.spl, N.cap, nspl,
                 cnt + LrCounters::kErr, st);
     k_lr_clamp<<<1, 1, 0, st>>>(nspl, N.cap, cnt + LrCounters::kErr);
