@@ -151,7 +151,6 @@ __device__ __forceinline__ u32 uf_prio(u32 x) { return mix32(x); }
 // read-only walk was fastest on C (0.18 ms) but let lattice chains grow on
 // road graphs (config D 3.80 vs 2.31 ms); profiles/r1_bridges_tuning.md.
 constexpr int kShortcutHops = 8;
-template <int kHops = kShortcutHops>
 __device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
   if (cur == x) return x;
   u32 next;
@@ -160,7 +159,7 @@ __device__ __forceinline__ u32 uf_find_from(u32* par, u32 x, u32 cur) {
     cur = next;
     ++hops;
   }
-  if (hops >= kHops) par[x] = cur;
+  if (hops >= kShortcutHops) par[x] = cur;
   return cur;
 }
 __device__ __forceinline__ u32 uf_find(u32* par, u32 x) { return uf_find_from(par, x, par[x]); }
@@ -245,7 +244,7 @@ __device__ __forceinline__ T ld_edge(const T* p, bool cs) {
   return cs ? __ldcs(p) : *p;
 }
 
-template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false, int kSc = kShortcutHops>
+template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               u32* __restrict__ tbits, u32* flags) {
@@ -281,8 +280,8 @@ __global__ void __launch_bounds__(256, kMinB)
       // equal parents => same tree: no find needed (after the compress pass
       // between the phases this settles most phase-1 edges with two loads)
       if (a[j] != b[j]) {
-        a[j] = uf_find_from<kSc>(par, uv[j].x, a[j]);
-        b[j] = uf_find_from<kSc>(par, uv[j].y, b[j]);
+        a[j] = uf_find_from(par, uv[j].x, a[j]);
+        b[j] = uf_find_from(par, uv[j].y, b[j]);
       }
       if (kPrio ? uf_prio(a[j]) < uf_prio(b[j]) : a[j] < b[j]) {
         const u32 tmp = a[j];
@@ -858,8 +857,12 @@ __global__ void __launch_bounds__(256)
                     const uint2* __restrict__ kt, const u32* __restrict__ tedge, u32 T,
                     uint8_t* __restrict__ mask, u32 m, const u32* abort, u32 n) {
   if (tv_abort(abort, n)) return;
-  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
-    const uint2 k = kt[t];
+  const u32 stride = gridDim.x * blockDim.x;
+  u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+  uint2 knext = t < T ? kt[t] : make_uint2(1, 1);
+  for (; t < T; t += stride) {
+    const uint2 k = knext;  // this trip's key range, loaded one trip ahead
+    if (static_cast<u64>(t) + stride < T) knext = kt[t + stride];
     const u32 a = k.x - 1, b = min(k.y - 1, len - 1);
     const u32 la = a >> 5, lb = b >> 5;
     uint2 acc;
@@ -894,11 +897,13 @@ __global__ void __launch_bounds__(256)
         }
       }
     }
-    const bool inside = acc.x >= k.x && acc.y < k.y;
-    const u32 e = tedge[t];
     // the mask was zeroed before the call: only bridges are stored (a
-    // random byte store per tree edge would read-modify-write 32M sectors)
-    if (inside && e < m) mask[e] = 1;
+    // random byte store per tree edge would read-modify-write 32M sectors),
+    // and only a bridge reads its input edge id
+    if (acc.x >= k.x && acc.y < k.y) {
+      const u32 e = tedge[t];
+      if (e < m) mask[e] = 1;
+    }
   }
 }
 
@@ -944,17 +949,12 @@ void launch_hook(const uint2* edges, EdgeSubset sub, u32 n, u32* par, u32* tbits
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tbits, flags, magic, shift);
   } else {
-    static const int sc = [] {
-      const char* e = std::getenv("ETTG_HOOK_SC");
-      return e ? std::atoi(e) : 8;
-    }();
+    // (Sampled-pass shortcut after 2 / 4 / 16 / no hops instead of 8: config D
+    // hooking 1.90 / 1.88 / 2.03 / 2.09 vs 1.91 ms, config C 0.20 / 0.18 /
+    // 0.17 / 0.17 vs 0.17 ms; 8 kept, gpurun_out/r2bb.)
     auto kern = br_cs() & 1
-                    ? (prio      ? k_cc_hook<kEdgesPerThread, 8, true, true>
-                       : sc == 2  ? k_cc_hook<kEdgesPerThread, 8, false, true, 2>
-                       : sc == 4  ? k_cc_hook<kEdgesPerThread, 8, false, true, 4>
-                       : sc == 16 ? k_cc_hook<kEdgesPerThread, 8, false, true, 16>
-                       : sc == 99 ? k_cc_hook<kEdgesPerThread, 8, false, true, 1 << 30>
-                                  : k_cc_hook<kEdgesPerThread, 8, false, true>)
+                    ? (prio ? k_cc_hook<kEdgesPerThread, 8, true, true>
+                            : k_cc_hook<kEdgesPerThread, 8, false, true>)
                     : (prio ? k_cc_hook<kEdgesPerThread, 8, true> : k_cc_hook<kEdgesPerThread, 8, false>);
     kern<<<occ_grid(kern, (cnt + kEdgesPerThread - 1) / kEdgesPerThread, sms), 256, 0, st>>>(
         edges, sub, n, par, tbits, flags);
