@@ -771,30 +771,83 @@ __device__ __forceinline__ uint2 lh_merge(uint2 a, uint2 b) {
 // a neutral vertex slot takes the suffix from the next set slot of its
 // block (k_classify_tour).  Half the stores of separate prefix and suffix
 // arrays.
+// Four slots per lane (one 32-B load / store), eight lanes per 32-slot
+// block: in-lane prefix / suffix, then 3-step segmented shuffles across the
+// block's lanes (12 shuffles per lane for 4 slots; one slot per lane needed
+// 20 per slot and made the kernel L1/MIO-bound, 0.28 ms on config D).
 __global__ void k_lh_block_ps(const uint2* __restrict__ lh, u32 n, u32 nb,
                               uint2* __restrict__ sp0, uint2* __restrict__ ps,
                               u32* __restrict__ nmask) {
-  const u32 lane = threadIdx.x & 31;
+  const u32 lane = threadIdx.x & 31, sub = lane & 7;  // lane within its block
   const u32 warps = (gridDim.x * blockDim.x) >> 5;
-  for (u32 b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
-    const u32 i = b * 32 + lane;
-    const uint2 v = i < n ? lh[i] : make_uint2(0xFFFFFFFFu, 0u);
-    uint2 f = v, g = v;
+  const uint2 kNeutral = make_uint2(0xFFFFFFFFu, 0u);
+  // a warp covers 4 blocks (128 slots)
+  for (u32 w4 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w4 * 4 < nb; w4 += warps) {
+    const u32 i0 = w4 * 128 + lane * 4;  // first of this lane's 4 slots
+    uint2 v[4];
+    if (i0 + 4 <= n) {
+      const uint4 p = reinterpret_cast<const uint4*>(lh + i0)[0];
+      const uint4 q = reinterpret_cast<const uint4*>(lh + i0)[1];
+      v[0] = make_uint2(p.x, p.y);
+      v[1] = make_uint2(p.z, p.w);
+      v[2] = make_uint2(q.x, q.y);
+      v[3] = make_uint2(q.z, q.w);
+    } else {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint2 o;
-      o.x = __shfl_up_sync(0xffffffffu, f.x, d);
-      o.y = __shfl_up_sync(0xffffffffu, f.y, d);
-      if (lane >= static_cast<u32>(d)) f = lh_merge(f, o);
-      o.x = __shfl_down_sync(0xffffffffu, g.x, d);
-      o.y = __shfl_down_sync(0xffffffffu, g.y, d);
-      if (lane + d < 32) g = lh_merge(g, o);
+      for (int j = 0; j < 4; ++j) v[j] = i0 + j < n ? lh[i0 + j] : kNeutral;
     }
-    const bool neutral = v.x == 0xFFFFFFFFu && v.y == 0u;
-    const u32 nm = __ballot_sync(0xffffffffu, neutral);
-    if (i < n) ps[i] = neutral ? f : g;
-    if (lane == 31) sp0[b] = f;
-    if (lane == 0) nmask[b] = nm;
+    // in-lane inclusive prefix / suffix
+    uint2 pf[4], sf[4];
+    pf[0] = v[0];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) pf[j] = lh_merge(pf[j - 1], v[j]);
+    sf[3] = v[3];
+#pragma unroll
+    for (int j = 2; j >= 0; --j) sf[j] = lh_merge(sf[j + 1], v[j]);
+    // exclusive prefix / suffix of the lane aggregates within the block's 8 lanes
+    uint2 ip = pf[3], is = sf[0];  // inclusive over lanes, built by shuffles
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      uint2 o;
+      o.x = __shfl_up_sync(0xffffffffu, ip.x, d);
+      o.y = __shfl_up_sync(0xffffffffu, ip.y, d);
+      if (sub >= static_cast<u32>(d)) ip = lh_merge(ip, o);
+      o.x = __shfl_down_sync(0xffffffffu, is.x, d);
+      o.y = __shfl_down_sync(0xffffffffu, is.y, d);
+      if (sub + d < 8) is = lh_merge(is, o);
+    }
+    uint2 ep, es;  // exclusive: lanes before / after this one in the block
+    ep.x = __shfl_up_sync(0xffffffffu, ip.x, 1);
+    ep.y = __shfl_up_sync(0xffffffffu, ip.y, 1);
+    es.x = __shfl_down_sync(0xffffffffu, is.x, 1);
+    es.y = __shfl_down_sync(0xffffffffu, is.y, 1);
+    if (sub == 0) ep = kNeutral;
+    if (sub == 7) es = kNeutral;
+    u32 nib = 0;
+    uint2 o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool neutral = v[j].x == 0xFFFFFFFFu && v[j].y == 0u;
+      nib |= static_cast<u32>(neutral) << j;
+      o[j] = neutral ? lh_merge(ep, pf[j]) : lh_merge(es, sf[j]);
+    }
+    if (i0 + 4 <= n) {
+      reinterpret_cast<uint4*>(ps + i0)[0] = make_uint4(o[0].x, o[0].y, o[1].x, o[1].y);
+      reinterpret_cast<uint4*>(ps + i0)[1] = make_uint4(o[2].x, o[2].y, o[3].x, o[3].y);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j < n) ps[i0 + j] = o[j];
+    }
+    // block word: nibble of lane sub at bits 4 * sub (OR over the 8 lanes)
+    u32 word = nib << (4 * sub);
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, d);
+    const u32 b = w4 * 4 + (lane >> 3);
+    if (sub == 7 && b < nb) {
+      sp0[b] = ip;  // block aggregate
+      nmask[b] = word;
+    }
   }
 }
 
@@ -1445,7 +1498,7 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
     CK_LAUNCH();
     if (m && n > 1) launch_lowhigh(edges, ws.tbits, m, ws.pre_of, ws.lh, abort, n, sms, st);
     tr.mark("lowhigh_edges");
-    k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 32, 256), 256, 0, st>>>(
+    k_lh_block_ps<<<blocks_for(static_cast<u64>(ws.nb) * 8, 256), 256, 0, st>>>(
         ws.lh, len, ws.nb, ws.sp, ws.lh_ps, ws.lh_nmask);
     CK_LAUNCH();
     if (!build_sparse_rows_super(ws.sp, ws.nb, ws.levels, ws.sps, LhMerge{}, st))

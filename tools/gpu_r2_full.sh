@@ -22,8 +22,8 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
    --clock-control none --csv --log-file $O/br_dram.csv \
    env ETTG_TRACE=0 REPS=2 python tools/trace_bridges.py > $O/ncu_br.log 2>&1; echo "br dram rc=$?" >> $O/rc.txt
 timeout 1200 ncu --set full --clock-control none --import-source on \
-   -k regex:'k_cc_hook|k_lowhigh|k_lr_walk0|k_tree_rot|k_classify_tour|k_lh_block_ps|k_tv_keys' \
-   -s 8 -c 8 -o $O/prof_br -f env ETTG_TRACE=0 REPS=2 python tools/trace_bridges.py > $O/ncu_br2.log 2>&1; echo "br full rc=$?" >> $O/rc.txt
+   -k regex:'k_cc_hook|k_lowhigh|k_lr_walk0|k_tree_rot|k_classify_tour|k_lh_block_ps|k_tv_keys|k_compact_bits|k_tree_close' \
+   -s 10 -c 11 -o $O/prof_br -f env ETTG_TRACE=0 REPS=2 python tools/trace_bridges.py > $O/ncu_br2.log 2>&1; echo "br full rc=$?" >> $O/rc.txt
 ETTG_TRACE=1 REPS=4 timeout 300 python tools/trace_bridges.py > $O/trace_br.log 2>&1
 fi
 du -sh $O
