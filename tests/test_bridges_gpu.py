@@ -261,3 +261,26 @@ def test_edge_order_independence(ett, order):
              "shuffled": edges[rng.permutation(len(edges))]}[order]
         for fn in (ett.tv_bridges, ett.hybrid_bridges):
             assert np.array_equal(fn(ett.EdgeList(n, e)).is_bridge, want)
+
+
+@pytest.mark.parametrize("gamma,seed", [(2, 11), (64, 12), (0, 13)])
+def test_tree_plus_few_chords_vs_reference(ett, ref, gamma, seed):
+    """A random tree plus a few chords: most vertices carry no non-tree edge,
+    so most low/high key slots stay neutral and many key ranges start at a
+    neutral slot or cross block boundaries -- the cases the combined in-block
+    suffix/prefix array and its neutral-slot masks handle (k_lh_block_ps,
+    k_classify_tour).  Odd sizes leave partial 4-slot groups and blocks."""
+    rng = np.random.default_rng(seed)
+    n = 300_007
+    t = ett.permute_labels(ett.grasp_tree(n, gamma if gamma else ett.K_GRASP_INFINITY, seed), seed)
+    par = np.asarray(t.parent, np.int64)
+    child = np.flatnonzero(par >= 0)
+    tree = np.stack([child, par[child]], 1)
+    chords = rng.integers(0, n, size=(1_501, 2))
+    e = np.concatenate([tree, chords])
+    e = e[rng.permutation(len(e))]
+    got = ett.tv_bridges(ett.EdgeList(n, e)).is_bridge
+    want, _ = ref.bridges("dfs", n, e)
+    assert 0 < int(want.sum()) < len(e)
+    assert np.array_equal(got, want)
+    assert np.array_equal(ett.hybrid_bridges(ett.EdgeList(n, e)).is_bridge, want)
