@@ -195,15 +195,6 @@ __device__ __forceinline__ u32 ld_volatile_u32(const u32* p) {
   return v;
 }
 
-// Sets bit i (of a bit array) for the lanes with set = true; lanes that hit
-// the same 32-bit word are merged into one atomicOr.  Every lane of the warp
-// must call it (the caller's loop is warp-uniform).
-__device__ __forceinline__ void warp_set_bit(u32* words, u64 i, bool set) {
-  const u32 w = set ? static_cast<u32>(i >> 5) : kNone;
-  const u32 peers = __match_any_sync(0xffffffffu, w);
-  const u32 v = __reduce_or_sync(peers, set ? 1u << (i & 31) : 0u);
-  if (set && static_cast<int>(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(words + w, v);
-}
 // One lane, one bit (a RED.OR: nothing waits on it).
 __device__ __forceinline__ void set_bit(u32* words, u64 i) {
   atomicOr(words + (i >> 5), 1u << (i & 31));
