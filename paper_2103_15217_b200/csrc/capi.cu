@@ -255,13 +255,9 @@ void staged_d2h_widen_pairs(int64_t* h_dst, const uint2* d_src, size_t count, in
     if (c + 1 < chunks) issue(c + 1);  // lands while chunk c is widened
     CK(cudaEventSynchronize(s.done[c & 1]));
     const size_t lo = c * per, n = std::min(per, count - lo);
-    const uint2* in = reinterpret_cast<const uint2*>(s.buf[c & 1]);
-    int64_t* out = h_dst + 2 * lo;
-#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 65536)
-    for (long i = 0; i < static_cast<long>(n); ++i) {
-      out[2 * i] = in[i].x;
-      out[2 * i + 1] = in[i].y;
-    }
+    // pairs are 2n consecutive u32 ids: zero-extended with streaming stores
+    host_widen_u32(h_dst + 2 * lo, reinterpret_cast<const uint32_t*>(s.buf[c & 1]), 2 * n, false,
+                   host_thread_count());
   }
 }
 
@@ -306,10 +302,7 @@ void staged_d2h_widen_u32(int64_t* h_dst, const uint32_t* d_src, size_t count, i
     CK(cudaEventSynchronize(s.done[c & 1]));
     const size_t lo = c * per, n = std::min(per, count - lo);
     const uint32_t* in = reinterpret_cast<const uint32_t*>(s.buf[c & 1]);
-    int64_t* out = h_dst + lo;
-#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 65536)
-    for (long i = 0; i < static_cast<long>(n); ++i)
-      out[i] = in[i] == 0xFFFFFFFFu ? int64_t(-1) : static_cast<int64_t>(in[i]);
+    host_widen_u32(h_dst + lo, in, n, true, host_thread_count());  // streaming stores
   }
 }
 
@@ -462,13 +455,6 @@ void staged_d2h_expand_bits(uint8_t* h_dst, const uint32_t* d_bits, size_t count
   Stage& s = stage_for(device);
   std::lock_guard<std::mutex> lk(s.mu);
   stage_init(s);
-  // byte b of a bit word -> 8 mask bytes (0/1), little-endian
-  static const auto table = [] {
-    std::array<uint64_t, 256> t{};
-    for (int b = 0; b < 256; ++b)
-      for (int i = 0; i < 8; ++i) t[b] |= static_cast<uint64_t>((b >> i) & 1) << (8 * i);
-    return t;
-  }();
   const size_t words = (count + 31) / 32;
   const size_t per = kStageChunk / 4;  // words per chunk
   const size_t chunks = (words + per - 1) / per;
@@ -483,18 +469,7 @@ void staged_d2h_expand_bits(uint8_t* h_dst, const uint32_t* d_bits, size_t count
     CK(cudaEventSynchronize(s.done[c & 1]));
     const size_t lo = c * per, n = std::min(per, words - lo);
     const uint32_t* in = reinterpret_cast<const uint32_t*>(s.buf[c & 1]);
-#pragma omp parallel for schedule(static) num_threads(host_thread_count()) if (n > 16384)
-    for (long w = 0; w < static_cast<long>(n); ++w) {
-      const size_t base = (lo + w) * 32;
-      const uint32_t x = in[w];
-      if (base + 32 <= count) {
-        uint64_t q[4] = {table[x & 0xFF], table[(x >> 8) & 0xFF], table[(x >> 16) & 0xFF],
-                         table[x >> 24]};
-        std::memcpy(h_dst + base, q, 32);
-      } else {
-        for (size_t i = base; i < count; ++i) h_dst[i] = (x >> (i - base)) & 1;
-      }
-    }
+    host_expand_bits(h_dst, in, lo, lo + n, count, host_thread_count());  // streaming stores
   }
 }
 

@@ -333,6 +333,10 @@ bool is_pinned(const void* p);
 // is_pinned for its check only: host-buffer entry points call it on every
 // caller buffer, whatever its size or the path it takes.
 void check_host_ptr(const void* p);
+// hostcopy.cpp: stage -> caller memory with streaming stores
+void host_widen_u32(int64_t* dst, const uint32_t* src, size_t n, bool none_to_minus1, int threads);
+void host_expand_bits(uint8_t* dst, const uint32_t* in, size_t w0, size_t w1, size_t count,
+                      int threads);
 // Host <-> device copies of caller buffers: async when the host side is
 // pinned, staged (and synchronous) when it is pageable.
 void copy_h2d(void* d_dst, const void* h_src, size_t bytes, int device, cudaStream_t st);

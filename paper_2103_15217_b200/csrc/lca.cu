@@ -1789,9 +1789,7 @@ void query_host_narrow(ettg_lca* h, unsigned engine, const int64_t* pairs, u64 q
     const double t1 = trace ? omp_get_wtime() : 0;
     const u64 lo = c * per, cnt = std::min(per, q - lo);
     const u32* in = reinterpret_cast<const u32*>(sl.buf(c % kStageBufs) + per * 8);
-    int64_t* out = answers + lo;
-#pragma omp parallel for schedule(static) num_threads(threads) if (cnt > 65536)
-    for (long i = 0; i < static_cast<long>(cnt); ++i) out[i] = in[i];
+    host_widen_u32(answers + lo, in, cnt, false, threads);  // streaming stores: no RFO
     if (trace) t_widen += omp_get_wtime() - t1;
   };
   u64 nk = 0;  // narrowed chunks so far (they rotate through the stage)
