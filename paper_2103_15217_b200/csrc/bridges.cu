@@ -282,11 +282,11 @@ __global__ void __launch_bounds__(256, kMinB)
       if (a[j] != b[j]) {
         a[j] = uf_find_from(par, uv[j].x, a[j]);
         b[j] = uf_find_from(par, uv[j].y, b[j]);
-      }
-      if (kPrio ? uf_prio(a[j]) < uf_prio(b[j]) : a[j] < b[j]) {
-        const u32 tmp = a[j];
-        a[j] = b[j];
-        b[j] = tmp;
+        if (kPrio ? uf_prio(a[j]) < uf_prio(b[j]) : a[j] < b[j]) {
+          const u32 tmp = a[j];
+          a[j] = b[j];
+          b[j] = tmp;
+        }
       }
     }
     u32 old[kHookE];
@@ -366,11 +366,13 @@ __global__ void __launch_bounds__(256, kMinB)
       if (a[j] != b[j]) {
         a[j] = uf_find_from(par, uv[j].x, a[j]);
         b[j] = uf_find_from(par, uv[j].y, b[j]);
-      }
-      if (uf_prio(a[j]) < uf_prio(b[j])) {  // hook the higher priority value under the lower
-        const u32 tmp = a[j];
-        a[j] = b[j];
-        b[j] = tmp;
+        // hook the higher priority value under the lower (the hash only when
+        // the parents differ: most second-pass edges stop at equal parents)
+        if (uf_prio(a[j]) < uf_prio(b[j])) {
+          const u32 tmp = a[j];
+          a[j] = b[j];
+          b[j] = tmp;
+        }
       }
     }
     u32 old[kHookE];
@@ -664,6 +666,9 @@ __global__ void __launch_bounds__(256, kMinB)
 // keys, high(u) from larger ones -- into one filtered read and at most one
 // atomic per run, while the v-side update stays per edge.  On inputs without
 // runs every edge is its own run (the same work as k_lowhigh_edges).
+// (Folding a run that continues into the next lane's chunk into this lane's
+// u-side update -- two shuffles per chunk, one atomic pair instead of two --
+// spilled at 48 registers and was no faster: 1.68 vs 1.66 ms on config D.)
 template <int kE, bool kCs = false, int kMinB = 5>
 __global__ void __launch_bounds__(256, kMinB)
     k_lowhigh_runs(const uint2* __restrict__ edges, const u32* __restrict__ tbits, u32 m,
