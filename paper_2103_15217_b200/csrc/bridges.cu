@@ -332,19 +332,22 @@ template <int kHookE, int kMinB, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook_rest(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
                    u32* __restrict__ tbits, u32* flags, u32 magic, u32 shift) {
+  // 32-bit indices (m < 2^31; the grid is a few waves of resident CTAs): the
+  // 64-bit index arithmetic was a large share of this pass's instructions
   u32 bad = 0;
-  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  const u64 cnt = sub.total;
-  u64 eidx[kHookE];
-  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
-       base += stride * kHookE) {
+  const u32 stride = gridDim.x * blockDim.x;
+  const u32 cnt = sub.total;
+  const u32 span = kGroup * sub.sample, skip = kGroup * sub.lead, per = span - skip;
+  u32 eidx[kHookE];
+  for (u32 base = blockIdx.x * blockDim.x + threadIdx.x; base < cnt; base += stride * kHookE) {
     uint2 uv[kHookE];
     bool ok[kHookE];
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      const u64 i = base + j * stride;
+      const u32 i = base + j * stride;
       ok[j] = i < cnt;
-      const u64 e = ok[j] ? sub.edge_rest(i, magic, shift) : 0;
+      const u32 q = static_cast<u32>((static_cast<u64>(i) * magic) >> shift);  // i / per
+      const u32 e = ok[j] ? q * span + skip + (i - q * per) : 0u;
       eidx[j] = e;
       uv[j] = ok[j] ? ld_edge(edges + e, kCs) : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
