@@ -248,19 +248,25 @@ template <int kHookE, int kMinB, bool kPrio = false, bool kCs = false>
 __global__ void __launch_bounds__(256, kMinB)
     k_cc_hook(const uint2* __restrict__ edges, EdgeSubset sub, u32 n, u32* par,
               u32* __restrict__ tbits, u32* flags) {
+  // 32-bit indices as in k_cc_hook_rest (m < 2^31)
   u32 bad = 0;
-  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  const u64 cnt = sub.total;
-  u64 eidx[kHookE];
-  for (u64 base = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; base < cnt;
-       base += stride * kHookE) {
+  const u32 stride = gridDim.x * blockDim.x;
+  const u32 cnt = sub.total;
+  const u32 span = kGroup * sub.sample, goff = kGroup * sub.goff;
+  const bool sampled0 = sub.sample > 1 && sub.phase == 0;
+  u32 eidx[kHookE];
+  for (u32 base = blockIdx.x * blockDim.x + threadIdx.x; base < cnt; base += stride * kHookE) {
     uint2 uv[kHookE];
     bool ok[kHookE];
 #pragma unroll
     for (int j = 0; j < kHookE; ++j) {
-      const u64 i = base + j * stride;
+      const u32 i = base + j * stride;
       ok[j] = i < cnt;
-      const u64 e = ok[j] ? sub.edge(i) : 0;
+      u32 e = 0;
+      if (ok[j])
+        e = sub.sample <= 1 ? i
+            : sampled0      ? (i / kGroup) * span + goff + (i % kGroup)
+                            : static_cast<u32>(sub.edge(i));  // phase 1 (ETTG_HOOK_REST=0 only)
       eidx[j] = e;
       uv[j] = ok[j] ? ld_edge(edges + e, kCs) : make_uint2(0, 0);
       if (ok[j] && (uv[j].x >= n || uv[j].y >= n)) {
