@@ -1253,7 +1253,9 @@ struct BuildWs {
     sort.carve(c, m + 1);
     crange = c.take<uint2>(n);
     jj = c.take<u32>(n);
-    lr.carve(c, 2 * n);
+    // level means 32 / 8 (vs 16 / 16): 16M random tree build 5.02 -> 4.87 ms,
+    // 16M path 4.40 -> 4.35 ms (profiles/r2_bridges_notes.md, gpurun_out/r2ab2)
+    lr.carve(c, 2 * n, false, 32, 8);
     up = c.take<u32>(static_cast<u64>(n) + 1);
     hrec = c.take<uint4>(static_cast<u64>(n) + 1);
     scan = c.take<u64>(scan_ws_words(static_cast<u64>(n) + 1));
