@@ -502,3 +502,46 @@ def test_query_dev_error_flag_and_argument_checks(ett):
     st = idx.stats()
     assert np.array_equal(idx.ascendant, ett.inlabel_build(t).ascendant)  # strided export
     assert len(st.preorder) == t.n
+
+
+def test_host_answers_unaligned_and_odd(ett, ref):
+    """ettg_lca_query into caller buffers whose start is not 32-B aligned and
+    whose length is odd: the host widening's scalar head / tail around its
+    streaming stores (csrc/hostcopy.cpp), for pageable and pinned answers."""
+    import ctypes
+    import torch
+    from paper_2103_15217_b200 import _lib
+    t = ett.permute_labels(ett.grasp_tree(300_000, GRASP_INF, 9), 10)
+    idx = ett.inlabel_build(t)
+    want = None
+    for q, off in ((1_000_003, 1), (999_999, 3), (5, 1), (70_001, 2)):
+        qs = np.ascontiguousarray(ett.sample_queries(t.n, q, 11))
+        want = ref.lca("inlabel", t.parent, t.root, qs)
+        buf = np.full(q + 8, -7, np.int64)  # 8-B aligned, start moved by `off` elements
+        _lib.check(_lib.lib().ettg_lca_query(idx.handle, qs.ctypes.data, q, q,
+                                             buf[off:].ctypes.data))
+        assert np.array_equal(buf[off:off + q], want), (q, off)
+        assert (buf[:off] == -7).all() and (buf[off + q:] == -7).all()
+        pin = torch.full((q + 8,), -7, dtype=torch.int64).pin_memory()
+        pq = torch.from_numpy(qs).pin_memory()
+        _lib.check(_lib.lib().ettg_lca_query(idx.handle, pq.data_ptr(), q, q,
+                                             pin.data_ptr() + 8 * off))
+        got = pin.numpy()
+        assert np.array_equal(got[off:off + q], want), (q, off, "pinned")
+        assert (got[:off] == -7).all() and (got[off + q:] == -7).all()
+
+
+def test_host_mask_unaligned(ett):
+    """tv_bridges into a host mask that starts one byte past an aligned address
+    (the bit expansion's unaligned-store path) and has an odd length."""
+    import torch
+    from paper_2103_15217_b200 import _lib
+    g, truth = ett.planted_bridge_graph(200_003, 1_200_007, 301, 8)
+    e = np.ascontiguousarray(g.edges, dtype=np.int64)
+    m = len(e)
+    for pinned in (False, True):
+        buf = (torch.full((m + 64,), 7, dtype=torch.uint8).pin_memory().numpy() if pinned
+               else np.full(m + 64, 7, np.uint8))
+        _lib.check(_lib.lib().ettg_bridges(e.ctypes.data, g.n, m, 0, buf[1:].ctypes.data, None))
+        assert np.array_equal(buf[1:1 + m], truth), pinned
+        assert buf[0] == 7 and (buf[1 + m:] == 7).all()
