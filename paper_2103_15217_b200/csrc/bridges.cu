@@ -10,11 +10,13 @@
 //
 // Device pipeline (input: COO edge list, u32 ids; no CSR of the graph is built):
 //   spanning  k_cc_hook        lock-free union-find (ECL-CC style CAS hooking
-//                              of roots in one strict order per pass); a
-//                              successful CAS joins two trees, so its edge is
-//                              a spanning-forest edge
-//   euler     scan             tree-edge compaction (decoupled look-back); the
-//                              count is the connectivity check (n-1 tree edges)
+//             k_cc_hook_rest   of roots in one strict order per pass: a sampled
+//                              pass, a compress, the rest); a successful CAS
+//                              joins two trees, so its edge is a spanning-forest
+//                              edge and sets the edge's forest bit
+//   euler     k_compact_bits   forest bits -> tree-edge ids (tile counts, one-CTA
+//                              scan, write); the count is the connectivity check
+//                              (n - 1 tree edges)
 //             k_tree_rot       per-vertex rotation lists by atomicExch (no sort:
 //                              any rotation gives a valid tour)
 //             k_tree_close     rotation lists closed into cycles except the
@@ -26,11 +28,13 @@
 //                              the key range up to its up half-edge), so TV
 //                              needs no "#downs before" scan (CK / hybrid still
 //                              use k_tour_flags + the StatsOut scan for levels)
-//   lowhigh   k_lh_neutral / k_lowhigh_edges (one atomicMin + one atomicMax
-//             per non-tree edge into the slots of the endpoints' keys; the
-//             reference's other two updates, and its own-preorder seeds, never
-//             change the test), block-sparse min/max table over the 2n key
-//             slots, k_classify_tour writes the bridge mask by input edge id.
+//   lowhigh   k_lh_neutral / k_lowhigh_runs (one atomicMin / atomicMax per
+//             non-tree edge into the slots of the endpoints' keys, runs of equal
+//             first endpoint folded; the reference's other two updates, and its
+//             own-preorder seeds, never change the test), k_lh_block_ps (block
+//             extrema, one in-block suffix/prefix array, neutral-slot masks),
+//             block and superblock sparse tables over the 2n key slots,
+//             k_classify_tour writes the bridge mask by input edge id.
 //
 // The spanning forest may differ from the reference's; bridges are a graph
 // property, so the mask cannot (core/include/ett/bridges.hpp:56-58).
