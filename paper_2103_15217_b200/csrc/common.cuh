@@ -111,9 +111,24 @@ __device__ __forceinline__ Sector32 ldg_sector_l2(const uint32_t* p, u64 pol) {
       : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ Sector32 ldg_sector_l2_na(const uint32_t* p, u64 pol) {
+  Sector32 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+        "=r"(r.w[6]), "=r"(r.w[7])
+      : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ u32 ldg_u32_l2(const u32* p, u64 pol) {
   u32 r;
   asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ u32 ldg_u32_l2_na(const u32* p, u64 pol) {  // L1::no_allocate too
+  u32 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(r)
+               : "l"(p), "l"(pol));
   return r;
 }
 __device__ __forceinline__ uint2 ldg_rec_l2(const uint2* p, u64 pol) {
@@ -142,11 +157,14 @@ __device__ __forceinline__ void ldg_rec6_pair(const uint32_t* base, u32 x, u32 y
   A = rec6_extract(a, x - 5 * sx);
   B = rec6_extract(b, y - 5 * sy);
 }
+template <bool kNoAlloc = false>
 __device__ __forceinline__ void ldg_rec6_pair_l2(const uint32_t* base, u32 x, u32 y, uint2& A,
                                                  uint2& B, u64 pol) {
   const u32 sx = rec6_sector(x), sy = rec6_sector(y);
-  const Sector32 a = ldg_sector_l2(base + 8 * static_cast<u64>(sx), pol);
-  const Sector32 b = ldg_sector_l2(base + 8 * static_cast<u64>(sy), pol);
+  const Sector32 a = kNoAlloc ? ldg_sector_l2_na(base + 8 * static_cast<u64>(sx), pol)
+                              : ldg_sector_l2(base + 8 * static_cast<u64>(sx), pol);
+  const Sector32 b = kNoAlloc ? ldg_sector_l2_na(base + 8 * static_cast<u64>(sy), pol)
+                              : ldg_sector_l2(base + 8 * static_cast<u64>(sy), pol);
   A = rec6_extract(a, x - 5 * sx);
   B = rec6_extract(b, y - 5 * sy);
 }

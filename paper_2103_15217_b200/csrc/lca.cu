@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     // the policy word is made per trip: holding it across the loop spills at 32 registers
     const u64 pol = kL2 ? l2_policy_evict_last() : 0;
     if (kL2)
-      ldg_rec6_pair_l2(nodes6, x, y, A, B, pol);
+      ldg_rec6_pair_l2<kL2 == 4>(nodes6, x, y, A, B, pol);
     else
       ldg_rec6_pair(nodes6, x, y, A, B);
     bool lx = false, ly = false;
@@ -973,8 +973,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     bad = x >= n || y >= n;
     if (bad) x = y = 0;
     const u64 pol = kL2 ? l2_policy_evict_last() : 0;
-    wa = (kL2 ? ldg_u32_l2(node4 + x, pol) : ldg_u32(node4 + x));
-    wb = (kL2 ? ldg_u32_l2(node4 + y, pol) : ldg_u32(node4 + y));
+    wa = (kL2 == 3 ? ldg_u32_l2_na(node4 + x, pol) : kL2 ? ldg_u32_l2(node4 + x, pol) : ldg_u32(node4 + x));
+    wb = (kL2 == 3 ? ldg_u32_l2_na(node4 + y, pol) : kL2 ? ldg_u32_l2(node4 + y, pol) : ldg_u32(node4 + y));
   }
   if (i + stride < q) in.get(i + stride, nx, ny);
   for (; i < q; i += stride) {
@@ -986,8 +986,8 @@ __global__ void __launch_bounds__(kQThreads, kQMinBlocks)
     if (i1 < q) {
       nbad = cx >= n || cy >= n;
       if (nbad) cx = cy = 0;
-      nwa = (kL2 ? ldg_u32_l2(node4 + cx, pol) : ldg_u32(node4 + cx));
-      nwb = (kL2 ? ldg_u32_l2(node4 + cy, pol) : ldg_u32(node4 + cy));
+      nwa = (kL2 == 3 ? ldg_u32_l2_na(node4 + cx, pol) : kL2 ? ldg_u32_l2(node4 + cx, pol) : ldg_u32(node4 + cx));
+      nwb = (kL2 == 3 ? ldg_u32_l2_na(node4 + cy, pol) : kL2 ? ldg_u32_l2(node4 + cy, pol) : ldg_u32(node4 + cy));
       nx = ny = 0;
       if (i1 + stride < q) in.get(i1 + stride, nx, ny);
     }
@@ -1607,14 +1607,16 @@ int qprefetch_mode() {
   return v;
 }
 bool qprefetch() { return qprefetch_mode() != 0; }
-// L2 eviction hints on the index gathers (k_lca_inlabel_split6 /
-// k_lca_inlabel_compact_pipe kL2): 0 off, 1 node table, 2 all index tables.
-// A/B (profiles/r2_cache_hints.md): config B 101.5 -> 102.8 G q/s with 1,
-// config E unchanged with 1 and 2% slower with 2; default 1.
+// Cache hints on the index gathers (k_lca_inlabel_split6 /
+// k_lca_inlabel_compact_pipe kL2): 0 off, 1 L2 evict_last on the node table,
+// 2 on all index tables, 3 = 1 plus L1::no_allocate on the compact words,
+// 4 = 3 plus L1::no_allocate on the split6 sectors.  A/B
+// (profiles/r2_cache_hints.md): config B 101.5 -> 102.8 (1) -> 104.1-104.9
+// G q/s (4), config E 68.8 -> 69.4, grasp(64) 41.1 -> 42.1; default 4.
 int l2hint_mode() {
   static const int v = [] {
     const char* e = std::getenv("ETTG_L2HINT");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 4;
   }();
   return v;
 }
@@ -1648,8 +1650,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
     const int grid_per_sm = grid_env ? grid_env : (q <= (u64(1) << 21) ? kQMinBlocks : kQGridPerSM);
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * grid_per_sm);
     if (h->layout == kLayoutCompact)
-      (qprefetch_mode() == 2   ? (l2hint_mode() ? k_lca_inlabel_compact_pipe<In, Out, 1>
-                                                : k_lca_inlabel_compact_pipe<In, Out, 0>)
+      (qprefetch_mode() == 2   ? (l2hint_mode() >= 3 ? k_lca_inlabel_compact_pipe<In, Out, 3>
+                                  : l2hint_mode()    ? k_lca_inlabel_compact_pipe<In, Out, 1>
+                                                     : k_lca_inlabel_compact_pipe<In, Out, 0>)
        : qprefetch_mode() == 1 ? k_lca_inlabel_compact<In, Out, true>
                                : k_lca_inlabel_compact<In, Out, false>)
           <<<blocks, kQThreads, 0, st>>>(h->node4, h->ltab, h->lab, h->n, h->off_bits, in, out, q,
@@ -1666,8 +1669,9 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
           Wide9Nodes{h->nodes9}, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutSplit6)
       (!qprefetch()          ? k_lca_inlabel_split6<In, Out, false>
-       : l2hint_mode() == 1 ? k_lca_inlabel_split6<In, Out, true, 1>
        : l2hint_mode() == 2 ? k_lca_inlabel_split6<In, Out, true, 2>
+       : l2hint_mode() == 4 ? k_lca_inlabel_split6<In, Out, true, 4>
+       : l2hint_mode()      ? k_lca_inlabel_split6<In, Out, true, 1>
                             : k_lca_inlabel_split6<In, Out, true, 0>)
           <<<blocks, kQThreads, 0, st>>>(h->nodes6, h->slevel, h->lab, h->n, in, out, q, err);
     else if (h->layout == kLayoutNarrow)
