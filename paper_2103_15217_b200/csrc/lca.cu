@@ -1647,7 +1647,13 @@ void launch_query(const ettg_lca* h, unsigned engine, In in, Out out, u64 q, u32
       const char* e = std::getenv("ETTG_QGRID");
       return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    const int grid_per_sm = grid_env ? grid_env : (q <= (u64(1) << 21) ? kQMinBlocks : kQGridPerSM);
+    // split6 (sector gathers, DRAM-bound) keeps more CTAs in the grid: 16M
+    // grasp(inf) tree, 1G queries 71.2 -> 72.6 G q/s at 128 vs 64 per SM; the
+    // other layouts are best at 64 (gpurun_out/r2ak, r2al)
+    const int grid_per_sm =
+        grid_env ? grid_env
+                 : q <= (u64(1) << 21) ? kQMinBlocks
+                 : h->layout == kLayoutSplit6 ? 2 * kQGridPerSM : kQGridPerSM;
     unsigned blocks = std::min<u64>((q + per - 1) / per, u64(sms) * grid_per_sm);
     if (h->layout == kLayoutCompact)
       (qprefetch_mode() == 2   ? (l2hint_mode() >= 3 ? k_lca_inlabel_compact_pipe<In, Out, 3>
