@@ -253,6 +253,19 @@ int ettg_bridges_dev_on_tree(const uint32_t* d_edges, int64_t n, int64_t m,
                              uint8_t* d_is_bridge, void* stream,
                              ettg_phase_times* times);
 
+/* low_high (core/src/bridges.cpp:251-287) as the TV engine computes it, for
+ * checking the intermediate (diagnostic; not a timed path).  The spanning
+ * tree is tree_mask (as ettg_bridges_on_tree) or, when tree_mask is NULL,
+ * the engine's own hooking tree, returned in tree_out[m] (0/1) if non-NULL.
+ * Per node, rooted at 0: preorder[v] (1-based, the Euler-tour order the
+ * engine walks), low[v] / high[v] = the minimum / maximum preorder over v's
+ * subtree and the non-tree neighbours of its subtree -- the reference's
+ * LowHigh over that preorder (its test oracle recursive_low_high,
+ * tests/oracles.hpp:166-201).  Errors as ettg_bridges / ettg_bridges_on_tree. */
+int ettg_bridges_low_high(const int64_t* edges, int64_t n, int64_t m, int device,
+                          const uint8_t* tree_mask, uint8_t* tree_out,
+                          int64_t* preorder, int64_t* low, int64_t* high);
+
 /* The engines over the reference's own input type, AdjacencyIndex
  * (core/include/ett/graph.hpp:44-61): offsets[n+1], neighbors[2m],
  * edge_ids[2m] -- what tv_bridges / ck_bridges / hybrid_bridges(const

@@ -271,7 +271,36 @@ def ref_spanning_tree_hooking(n, edges):
     return mask[:m]
 
 
+def ref_low_high(n, edges, tree_mask):
+    """The reference's low_high (core/src/bridges.cpp:251-287) on its own
+    euler_root_tree(tree_mask, root 0): (preorder, parent, low, high)."""
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    tm = np.ascontiguousarray(tree_mask, np.uint8)
+    out = [np.empty(n, np.int64) for _ in range(4)]
+    _rc(ref(), ref().ref_low_high(i64(n), i64(m), _p(edges), _p(tm), *[_p(a) for a in out]),
+        "ref_last_error")
+    return tuple(out)
+
+
+def ref_recursive_low_high(n, edges, tree_mask, parent, root, preorder):
+    """recursive_low_high (reference tests/oracles.hpp:166-201) over any rooted
+    tree and preorder: (low, high)."""
+    edges = np.ascontiguousarray(edges, np.int64).reshape(-1, 2)
+    m = edges.shape[0]
+    tm = np.ascontiguousarray(tree_mask, np.uint8)
+    par = np.ascontiguousarray(parent, np.int64)
+    pre = np.ascontiguousarray(preorder, np.int64)
+    low, high = np.empty(n, np.int64), np.empty(n, np.int64)
+    _rc(ref(), ref().ref_recursive_low_high(i64(n), i64(m), _p(edges), _p(tm), _p(par),
+                                            i64(root), _p(pre), _p(low), _p(high)),
+        "ref_last_error")
+    return low, high
+
+
 Ref.spanning_tree_hooking = staticmethod(ref_spanning_tree_hooking)
+Ref.low_high = staticmethod(ref_low_high)
+Ref.recursive_low_high = staticmethod(ref_recursive_low_high)
 Ref.build_adjacency = staticmethod(ref_build_adjacency)
 Ref.largest_component = staticmethod(ref_largest_component)
 Ref.bfs_tree = staticmethod(ref_bfs_tree)

@@ -24,6 +24,8 @@
 #include "ett/graph.hpp"
 #include "ett/lca.hpp"
 #include "ett/primitives.hpp"
+#include "oracles.hpp"  // tests/oracles.hpp (recursive_low_high)
+#include <pthread.h>
 
 using namespace ett;
 
@@ -325,6 +327,59 @@ int ref_spanning_tree_hooking(int64_t n, int64_t m, const int64_t* edges,
     AdjacencyIndex adj = build_adjacency(make_edges(n, m, edges));
     auto mask = spanning_tree_hooking(adj);
     for (int64_t i = 0; i < m; ++i) tree_mask[i] = mask[i] ? 1 : 0;
+  });
+}
+
+// low_high (core/src/bridges.cpp:251-287) on the reference's own rooting of
+// `tree_mask` (euler_root_tree, root 0): preorder, parent, low, high per node.
+int ref_low_high(int64_t n, int64_t m, const int64_t* edges, const uint8_t* tree_mask,
+                 int64_t* preorder, int64_t* parent, int64_t* low, int64_t* high) {
+  return guard([&] {
+    AdjacencyIndex adj = build_adjacency(make_edges(n, m, edges));
+    std::vector<char> mask(tree_mask, tree_mask + m);
+    SpanningTree st = euler_root_tree(adj, mask, 0);
+    LowHigh lh = low_high(adj, st, *st.stats);
+    for (int64_t v = 0; v < n; ++v) {
+      preorder[v] = st.stats->preorder[v];
+      parent[v] = st.rooted.parent[v];
+      low[v] = lh.low[v];
+      high[v] = lh.high[v];
+    }
+  });
+}
+
+// recursive_low_high (tests/oracles.hpp:166-201) over a caller rooted tree and
+// preorder.  Its recursion is as deep as the tree, so it runs on a thread
+// with a 1 GB stack.
+int ref_recursive_low_high(int64_t n, int64_t m, const int64_t* edges,
+                           const uint8_t* tree_mask, const int64_t* parent, int64_t root,
+                           const int64_t* preorder, int64_t* low, int64_t* high) {
+  return guard([&] {
+    struct Job {
+      EdgeList g;
+      std::vector<char> mask;
+      std::vector<i64> parent, pre;
+      i64 root;
+      oracle::LowHighOracle out;
+    } job{make_edges(n, m, edges), std::vector<char>(tree_mask, tree_mask + m),
+          std::vector<i64>(parent, parent + n), std::vector<i64>(preorder, preorder + n), root,
+          {}};
+    auto body = [](void* p) -> void* {
+      auto* j = static_cast<Job*>(p);
+      j->out = oracle::recursive_low_high(j->g, j->mask, j->parent, j->root, j->pre);
+      return nullptr;
+    };
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, size_t(1) << 30);
+    pthread_t th;
+    if (pthread_create(&th, &attr, body, &job) != 0) throw std::runtime_error("pthread_create");
+    pthread_join(th, nullptr);
+    pthread_attr_destroy(&attr);
+    for (int64_t v = 0; v < n; ++v) {
+      low[v] = job.out.low[v];
+      high[v] = job.out.high[v];
+    }
   });
 }
 

@@ -89,6 +89,7 @@ _SIGS = {
     "ettg_bridges_on_tree": ([p, i64, i64, C.c_int, p, p, C.POINTER(PhaseTimes)], C.c_int),
     "ettg_bridges_dev_on_tree": ([p, i64, i64, C.c_int, p, p, p, C.POINTER(PhaseTimes)],
                                  C.c_int),
+    "ettg_bridges_low_high": ([p, i64, i64, C.c_int, p, p, p, p, p], C.c_int),
     "ettg_bridges_csr": ([p, p, p, i64, i64, C.c_int, C.c_int, p, p, C.POINTER(PhaseTimes)],
                          C.c_int),
     "ettg_list_rank_dev": ([p, i64, i64, p, C.c_int, p], C.c_int),

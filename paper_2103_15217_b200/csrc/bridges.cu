@@ -921,6 +921,50 @@ __global__ void k_lh_neutral(uint2* __restrict__ lh, u32 len) {
     lh[i] = make_uint2(0xFFFFFFFFu, 0u);
 }
 
+// Extrema of the low/high slots [a, b] (b an up slot, so neutral), from the
+// per-slot values, the in-block prefix / suffix array, the block sparse table
+// and, for the widest rows, the superblock table.
+__device__ __forceinline__ uint2 lh_range(const uint2* __restrict__ lh,
+                                          const uint2* __restrict__ ps,
+                                          const u32* __restrict__ nmask,
+                                          const uint2* __restrict__ sp, u32 nb,
+                                          const uint2* __restrict__ sps, u32 nsb, u32 a, u32 b) {
+  const u32 la = a >> 5, lb = b >> 5;
+  uint2 acc;
+  if (la == lb) {
+    acc = lh[a];
+    for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
+  } else {
+    // suffix of block la from a: ps[a], or from the next slot when a's
+    // own slot is neutral (then ps[a] is a prefix); prefix of block lb
+    // up to b: ps[b] (b is an up slot, always neutral)
+    const u32 set = ~__ldg(nmask + la) & (0xFFFFFFFFu << (a & 31u));
+    const uint2 sa = set ? __ldg(ps + (la << 5) + (__ffs(set) - 1)) : make_uint2(0xFFFFFFFFu, 0u);
+    acc = lh_merge(sa, __ldg(ps + b));
+    if (lb > la + 1) {
+      constexpr int kTop = st_tile_log<uint2>();  // widest row kept with a superblock table
+      const u32 cnt = lb - la - 1;
+      const int kk = hb32(cnt);
+      if (kk <= kTop || !sps) {
+        const uint2* row = sp + static_cast<u64>(kk) * nb;
+        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kk)]));
+      } else {
+        // first and last 2^kTop blocks from the top row, whole superblocks
+        // strictly between theirs from the superblock table
+        const uint2* row = sp + static_cast<u64>(kTop) * nb;
+        acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kTop)]));
+        const u32 s1 = ((la + 1) >> kTop) + 1, s2e = (lb - 1) >> kTop;  // [s1, s2e)
+        if (s1 < s2e) {
+          const int k2 = hb32(s2e - s1);
+          const uint2* srow = sps + static_cast<u64>(k2) * nsb;
+          acc = lh_merge(acc, lh_merge(srow[s1], srow[s2e - (1u << k2)]));
+        }
+      }
+    }
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(256)
     k_classify_tour(const uint2* __restrict__ lh, const uint2* __restrict__ ps,
                     const u32* __restrict__ nmask, const uint2* __restrict__ sp, u32 nb,
@@ -934,40 +978,7 @@ __global__ void __launch_bounds__(256)
   for (; t < T; t += stride) {
     const uint2 k = knext;  // this trip's key range, loaded one trip ahead
     if (static_cast<u64>(t) + stride < T) knext = kt[t + stride];
-    const u32 a = k.x - 1, b = min(k.y - 1, len - 1);
-    const u32 la = a >> 5, lb = b >> 5;
-    uint2 acc;
-    if (la == lb) {
-      acc = lh[a];
-      for (u32 j = a + 1; j <= b; ++j) acc = lh_merge(acc, __ldg(lh + j));
-    } else {
-      // suffix of block la from a: ps[a], or from the next slot when a's
-      // own slot is neutral (then ps[a] is a prefix); prefix of block lb
-      // up to b: ps[b] (b is an up slot, always neutral)
-      const u32 set = ~__ldg(nmask + la) & (0xFFFFFFFFu << (a & 31u));
-      const uint2 sa = set ? __ldg(ps + (la << 5) + (__ffs(set) - 1)) : make_uint2(0xFFFFFFFFu, 0u);
-      acc = lh_merge(sa, __ldg(ps + b));
-      if (lb > la + 1) {
-        constexpr int kTop = st_tile_log<uint2>();  // widest row kept with a superblock table
-        const u32 cnt = lb - la - 1;
-        const int kk = hb32(cnt);
-        if (kk <= kTop || !sps) {
-          const uint2* row = sp + static_cast<u64>(kk) * nb;
-          acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kk)]));
-        } else {
-          // first and last 2^kTop blocks from the top row, whole superblocks
-          // strictly between theirs from the superblock table
-          const uint2* row = sp + static_cast<u64>(kTop) * nb;
-          acc = lh_merge(acc, lh_merge(row[la + 1], row[lb - (1u << kTop)]));
-          const u32 s1 = ((la + 1) >> kTop) + 1, s2e = (lb - 1) >> kTop;  // [s1, s2e)
-          if (s1 < s2e) {
-            const int k2 = hb32(s2e - s1);
-            const uint2* srow = sps + static_cast<u64>(k2) * nsb;
-            acc = lh_merge(acc, lh_merge(srow[s1], srow[s2e - (1u << k2)]));
-          }
-        }
-      }
-    }
+    const uint2 acc = lh_range(lh, ps, nmask, sp, nb, sps, nsb, k.x - 1, min(k.y - 1, len - 1));
     // the mask was zeroed before the call: only bridges are stored (a
     // random byte store per tree edge would read-modify-write 32M sectors),
     // and only a bridge reads its input edge id
@@ -976,6 +987,59 @@ __global__ void __launch_bounds__(256)
       if (e < m) mask[e] = 1;
     }
   }
+}
+
+// ettg_bridges_low_high (diagnostic, not on the timed path): the reference's
+// low_high values (core/src/bridges.cpp:251-287) in preorder numbers.  cnt is
+// the exclusive count of used key slots (cnt[K - 1] + 1 = preorder of the
+// node with key K); a node's subtree holds the keys [K, U), so
+// size = cnt[U - 1] - cnt[K - 1].  The slots hold only the updates that can
+// move the TV test (k_lowhigh_runs); the reference's remaining ones are the
+// node's own preorder, min'd / max'd in here: low = min(pre, slots),
+// high = max(pre + size - 1, slots).  Thread T handles the root.
+__global__ void k_lh_export(const uint2* __restrict__ lh, const uint2* __restrict__ ps,
+                            const u32* __restrict__ nmask, const uint2* __restrict__ sp, u32 nb,
+                            const uint2* __restrict__ sps, u32 nsb, u32 len,
+                            const uint2* __restrict__ kt, const uint2* __restrict__ tend,
+                            const u32* __restrict__ key_of, const u32* __restrict__ cnt, u32 T,
+                            u32 root, int64_t* __restrict__ pre_out,
+                            int64_t* __restrict__ low_out, int64_t* __restrict__ high_out,
+                            const u32* abort, u32 n) {
+  if (tv_abort(abort, n)) return;
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) {
+    uint2 k;
+    u32 node, pre, size;
+    if (t < T) {
+      k = kt[t];
+      const uint2 uv = tend[t];
+      node = key_of[uv.y] == k.x ? uv.y : uv.x;
+      pre = cnt[k.x - 1] + 1;
+      size = cnt[k.y - 1] - cnt[k.x - 1];
+    } else {
+      k = make_uint2(1u, len);
+      node = root;
+      pre = 1;
+      size = n;
+    }
+    const uint2 acc = lh_range(lh, ps, nmask, sp, nb, sps, nsb, k.x - 1, min(k.y - 1, len - 1));
+    const u32 lo = acc.x == 0xFFFFFFFFu ? pre : min(pre, cnt[acc.x - 1] + 1);
+    const u32 hi = acc.y == 0u ? pre + size - 1 : max(pre + size - 1, cnt[acc.y - 1] + 1);
+    pre_out[node] = pre;
+    low_out[node] = lo;
+    high_out[node] = hi;
+  }
+}
+
+__global__ void k_key_used(const u32* __restrict__ key_of, u32 n, u32* __restrict__ used,
+                           const u32* abort) {
+  if (tv_abort(abort, n)) return;
+  for (u32 v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (key_of[v] - 1 < 2 * n - 1) used[key_of[v] - 1] = 1u;
+}
+
+__global__ void k_bits_to_bytes(const u32* __restrict__ bits, u32 m, uint8_t* __restrict__ out) {
+  for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    out[e] = (bits[e >> 5] >> (e & 31)) & 1u;
 }
 
 // Edge-kernel launch shape: 2 edges per thread at 8 CTAs/SM (<= 32 regs),
@@ -1073,6 +1137,9 @@ struct BridgeIn {
   // kHostI64 from pageable memory: narrowed to u32 by host threads while
   // staging (8 B per edge over the link instead of 16)
   bool narrow = false;
+  // ettg_bridges_low_high: host outputs (TV engine; tree_out may be null)
+  int64_t *x_pre = nullptr, *x_low = nullptr, *x_high = nullptr;
+  uint8_t* x_tree = nullptr;
 };
 
 // Host int64 (u, v) pairs -> device u32 pairs with the reference's endpoint
@@ -1172,6 +1239,8 @@ struct BridgeWs {
   uint8_t* marked = nullptr;
   u32 *blevel = nullptr, *bparent = nullptr;
   BfsWs bfs;
+  int64_t* x3 = nullptr;      // ettg_bridges_low_high: preorder, low, high
+  uint8_t* xtree = nullptr;   // ettg_bridges_low_high: tree mask bytes
   void carve(Carver& c, u32 n, u32 m, const BridgeIn& in, int engine) {
     const u32 k = 2 * (n - 1);
     if (engine != ETTG_BRIDGES_TV) {
@@ -1232,6 +1301,10 @@ struct BridgeWs {
     sp = c.take<uint2>(static_cast<u64>(rows) * nb);
     words = c.take<u32>(16);
     bits = c.take<u32>((static_cast<u64>(m) + 31) / 32 + 1);
+    if (in.x_pre) {
+      x3 = c.take<int64_t>(3 * static_cast<u64>(n));
+      xtree = c.take<uint8_t>(m + 16);
+    }
   }
 };
 
@@ -1529,6 +1602,22 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
       CK_LAUNCH();
     }
     tr.mark("rmq_classify");
+    if (in.x_pre) {  // ettg_bridges_low_high (untimed diagnostic)
+      CK(cudaMemsetAsync(ws.flags, 0, (2 * static_cast<u64>(n) - 1) * 4, st));
+      k_key_used<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(ws.pre_of, n, ws.flags, abort);
+      CK_LAUNCH();
+      scan_exclusive(ArrayIn{ws.flags}, ArrayOut{ws.flags}, 2 * static_cast<u64>(n) - 1,
+                     ws.scan_k, nullptr, st);
+      int64_t* xp = ws.x3;
+      k_lh_export<<<std::min(g, blocks_for(n, 256)), 256, 0, st>>>(
+          ws.lh, ws.lh_ps, ws.lh_nmask, ws.sp, ws.nb, ws.sps, ws.nsb, len, ws.kt, ws.tend,
+          ws.pre_of, ws.flags, n - 1, 0, xp, xp + n, xp + 2 * static_cast<u64>(n), abort, n);
+      CK_LAUNCH();
+      if (m) {
+        k_bits_to_bytes<<<std::min(g, blocks_for(m, 256)), 256, 0, st>>>(ws.tbits, m, ws.xtree);
+        CK_LAUNCH();
+      }
+    }
   } else {
     // ---- CK marking (core/src/bridges.cpp:40-76) -------------------------
     CK(cudaMemsetAsync(ws.marked, 0, n, st));
@@ -1554,6 +1643,14 @@ void run_bridges(const BridgeIn& in, i64 n64, i64 m64, int device, uint8_t* d_ma
   }
   if (n > 1 && engine != ETTG_BRIDGES_CK)
     CK(cudaMemcpyAsync(&lerr, ws.lr.counters + LrCounters::kErr, 4, cudaMemcpyDeviceToHost, st));
+  if (in.x_pre) {
+    const u64 nb8 = static_cast<u64>(n) * 8;
+    CK(cudaMemcpyAsync(in.x_pre, ws.x3, nb8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(in.x_low, ws.x3 + n, nb8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(in.x_high, ws.x3 + 2 * static_cast<u64>(n), nb8, cudaMemcpyDeviceToHost,
+                       st));
+    if (in.x_tree && m) CK(cudaMemcpyAsync(in.x_tree, ws.xtree, m, cudaMemcpyDeviceToHost, st));
+  }
   u32 w[2] = {0, n - 1};
   if (abort) CK(cudaMemcpyAsync(w, abort, sizeof w, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1637,6 +1734,30 @@ int ettg_bridges_on_tree(const int64_t* edges, int64_t n, int64_t m, int device,
     in.tree = m ? tree_mask : &kEmpty;
     in.tree_on_host = true;
     run_bridges(in, n, m, device, nullptr, is_bridge, nullptr, times, ETTG_BRIDGES_TV);
+  });
+}
+
+int ettg_bridges_low_high(const int64_t* edges, int64_t n, int64_t m, int device,
+                          const uint8_t* tree_mask, uint8_t* tree_out, int64_t* preorder,
+                          int64_t* low, int64_t* high) {
+  return guard([&] {
+    if ((!edges && m > 0) || !preorder || !low || !high) einval("null argument");
+    DeviceScope ds(device);
+    BridgeIn in;
+    in.kind = BridgeIn::kHostI64;
+    in.edges = edges;
+    in.narrow = m > 0 && (!is_pinned(edges) || narrow_enabled());
+    static const uint8_t kEmpty = 0;
+    if (tree_mask) {
+      check_host_ptr(tree_mask);
+      in.tree = m ? tree_mask : &kEmpty;
+      in.tree_on_host = true;
+    }
+    in.x_pre = preorder;
+    in.x_low = low;
+    in.x_high = high;
+    in.x_tree = tree_out;
+    run_bridges(in, n, m, device, nullptr, nullptr, nullptr, nullptr, ETTG_BRIDGES_TV);
   });
 }
 

@@ -377,6 +377,35 @@ def tv_bridges_on_tree(g, tree_mask, device: int = 0, times: dict | None = None)
     return _bridges(g, _lib.BRIDGES_TV, device, times, tree_mask)
 
 
+@dataclass
+class LowHigh:
+    """core/include/ett/bridges.hpp LowHigh, plus the preorder it is numbered
+    in and the spanning tree it was computed on."""
+    preorder: np.ndarray
+    low: np.ndarray
+    high: np.ndarray
+    tree_mask: np.ndarray
+
+
+def low_high(g: EdgeList, tree_mask=None, device: int = 0) -> LowHigh:
+    """The TV engine's low/high intermediate (core/src/bridges.cpp:251-287)
+    on tree_mask, or on its own hooking tree when tree_mask is None: per node
+    the preorder (root 0, the engine's Euler-tour order) and the min / max
+    preorder over the subtree and its non-tree neighbours.  Diagnostic."""
+    n, m = int(g.n), g.m()
+    tm = None
+    if tree_mask is not None:
+        tm = np.ascontiguousarray(np.asarray(tree_mask) != 0, np.uint8)
+        if len(tm) != m:
+            raise InvalidArgument("tree mask size mismatch")
+    tree = np.zeros(max(m, 1), np.uint8)
+    pre, low, high = (np.empty(max(n, 1), np.int64) for _ in range(3))
+    check(lib().ettg_bridges_low_high(ptr(g.edges), n, m, device,
+                                      ptr(tm) if tm is not None else None, ptr(tree),
+                                      ptr(pre), ptr(low), ptr(high)))
+    return LowHigh(pre[:n], low[:n], high[:n], tree[:m] if tm is None else tm)
+
+
 def ck_bridges(g, device: int = 0, times: dict | None = None) -> BridgeMask:
     """ck_bridges (core/src/bridges.cpp:318-325): BFS tree + CK marking."""
     return _bridges(g, _lib.BRIDGES_CK, device, times)
