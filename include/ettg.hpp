@@ -300,6 +300,36 @@ inline BridgeMask hybrid_bridges(const EdgeList& g, PhaseTimes* times = nullptr,
   return detail::bridges_edges(g, ETTG_BRIDGES_HYBRID, times, device);
 }
 
+// LowHigh (bridges.hpp) as the TV engine computes it, with the preorder it is
+// numbered in (root 0) and the spanning tree used: tree_mask, or the engine's
+// own hooking tree when null.  A diagnostic for checking the intermediate
+// against the reference's low_high (core/src/bridges.cpp:251-287).
+struct LowHigh {
+  std::vector<i64> low, high, preorder;
+  std::vector<char> tree_mask;
+};
+inline LowHigh low_high(const EdgeList& g, const std::vector<char>* tree_mask = nullptr,
+                        int device = 0) {
+  if (tree_mask && static_cast<i64>(tree_mask->size()) != g.m())
+    throw std::invalid_argument("tree mask size mismatch");
+  LowHigh out;
+  out.low.resize(static_cast<size_t>(g.n));
+  out.high.resize(static_cast<size_t>(g.n));
+  out.preorder.resize(static_cast<size_t>(g.n));
+  std::vector<uint8_t> tree(g.edges.size());
+  check(ettg_bridges_low_high(reinterpret_cast<const int64_t*>(g.edges.data()), g.n, g.m(),
+                              device,
+                              tree_mask ? reinterpret_cast<const uint8_t*>(tree_mask->data())
+                                        : nullptr,
+                              tree.data(), out.preorder.data(), out.low.data(),
+                              out.high.data()));
+  if (tree_mask)
+    out.tree_mask = *tree_mask;
+  else
+    out.tree_mask.assign(tree.begin(), tree.end());
+  return out;
+}
+
 // SpanningTree fields of bfs_tree (bridges.hpp:12-18, :50).
 struct SpanningTree {
   std::vector<char> is_tree_edge;

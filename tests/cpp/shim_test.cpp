@@ -1,5 +1,6 @@
 // C++ caller through include/ettg.hpp, written like the reference's own tests
 // (tests/lca_test.cpp:47-74, tests/bridges_test.cpp): exits non-zero on failure.
+#include <algorithm>
 #include <cstdio>
 #include <sstream>
 #include <stdexcept>
@@ -88,6 +89,17 @@ int main() {
       what = e.what();
     }
     CHECK(what == "not a tree: disconnected");
+  }
+  {  // low/high intermediate (bridges.cpp:251-287) on the BFS tree {01, 02, 23}:
+     // 3 is a leaf without non-tree edges; 1 and 2 see each other's preorder
+    auto bfs = ettg::bfs_tree(g, 0).is_tree_edge;
+    auto lh = ettg::low_high(g, &bfs);
+    const auto& pre = lh.preorder;
+    CHECK(pre[0] == 1 && lh.low[0] == 1 && lh.high[0] == 4);
+    CHECK(lh.low[3] == pre[3] && lh.high[3] == pre[3]);
+    CHECK(lh.low[1] == std::min(pre[1], pre[2]) && lh.low[2] == std::min(pre[1], pre[2]));
+    CHECK(lh.high[1] == std::max(pre[1], pre[2]));
+    CHECK(ettg::low_high(g).tree_mask.size() == g.edges.size());
   }
   auto bt = ettg::bfs_tree(g, 0);
   CHECK(bt.parent == std::vector<ettg::i64>({-1, 0, 0, 2}));
